@@ -1,0 +1,193 @@
+/*
+ * fraqcu.h -- C ABI of the B200-native fast convolution-quadrature (CQ) path of arXiv 1901.05128.
+ *
+ * Drop-in boundary for the reference `fraq` library (/root/reference/proj).  The reference
+ * exposes a C++20 header API plus a pybind11 module `_fraq`; it has no C FFI.
+ * Every entry point below replaces one reference function or method, cited as path:line under
+ * /root/reference/proj.  The C++ mirror of the reference headers (namespace fraq, same class and
+ * function names, same exception types) and the Python module `_fraq` are thin layers over this
+ * ABI: paper_1901_05128_b200/csrc/fraq.hpp and fraq_py.cpp.  INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *   - plain C types only: double / long / int / pointers + sizes; no torch or CUDA types;
+ *   - `mem` arguments say where a buffer lives: FRAQ_HOST (pageable or pinned host memory) or
+ *     FRAQ_DEVICE (a device pointer on the context's GPU, zero-copy);
+ *   - all arithmetic is IEEE fp64 on the device (sm_100a); there is no CPU fallback: without a
+ *     CUDA device every compute entry point returns FRAQ_ECUDA;
+ *   - status codes map 1:1 onto the reference's exception types:
+ *       FRAQ_EINVAL  -> std::invalid_argument    FRAQ_ELOGIC   -> std::logic_error
+ *       FRAQ_ERANGE  -> std::out_of_range        FRAQ_ERUNTIME -> std::runtime_error
+ *     FRAQ_ECUDA / FRAQ_ENOMEM are device failures.  fraq_last_error() returns the message of the
+ *     last failure on the calling thread;
+ *   - a context is bound to one device and one CUDA stream; all work is stream-ordered; calls
+ *     that return values in host memory synchronize the stream.
+ */
+#ifndef FRAQCU_H
+#define FRAQCU_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FRAQ_MAX_POINTS 512 /* gauss_jacobi cap, gauss_jacobi.cpp:13 */
+#define FRAQ_MAX_HEAD 512
+
+enum {
+    FRAQ_OK = 0,
+    FRAQ_EINVAL = -1,
+    FRAQ_ELOGIC = -2,
+    FRAQ_ERANGE = -3,
+    FRAQ_ERUNTIME = -4,
+    FRAQ_ECUDA = -5,
+    FRAQ_ENOMEM = -6
+};
+enum { FRAQ_HOST = 0, FRAQ_DEVICE = 1 };
+/* HistoryVariant, fast_kernel.hpp:79-82 */
+enum { FRAQ_STANDALONE = 0, FRAQ_SCHEME = 1 };
+/* Scheme, fpfp.hpp:14 */
+enum { FRAQ_BE = 0, FRAQ_FASTBE = 1, FRAQ_SBD = 2, FRAQ_FASTSBD = 3 };
+/* InitialData, fpfp.hpp:21 */
+enum { FRAQ_POLY_SIN = 0, FRAQ_INDICATOR = 1, FRAQ_CUSTOM = 2 };
+
+typedef struct fraq_ctx_s* fraq_ctx;
+typedef struct fraq_hist_s* fraq_hist;
+
+/* Compressed kernel tables: FastKernelBE (sbd = 0; m1 = node_weights, r1 = ratios, head[0..1])
+ * or FastKernelSBD (sbd = 1; families (m1, r1) and (m2, r2), head[0..n_head-1]).
+ * fast_kernel.hpp:13-39.  Plain value type; the device copy is made when a history uses it. */
+typedef struct {
+    int sbd;
+    double gamma; /* the CQ exponent ("alpha" in the reference kernel structs) */
+    double tau;
+    int n_head; /* 2 for BE */
+    int np1, np2;
+    double head[FRAQ_MAX_HEAD];
+    double m1[FRAQ_MAX_POINTS], r1[FRAQ_MAX_POINTS];
+    double m2[FRAQ_MAX_POINTS], r2[FRAQ_MAX_POINTS];
+} fraq_kernel_t;
+
+/* KernelBudget, fast_kernel.hpp:68-74. */
+typedef struct {
+    long horizon;
+    double eps_tol;
+    int max_points;
+    int max_head;
+    double achieved_eps; /* out */
+} fraq_budget_t;
+
+/* ProblemSpec, fpfp.hpp:27-41. */
+typedef struct {
+    double alpha1, alpha2, coupling_a, length, t_final;
+    int grid_m;
+    long n_steps;
+    int initial;              /* FRAQ_POLY_SIN / FRAQ_INDICATOR / FRAQ_CUSTOM */
+    const double* custom_g1;  /* host, grid_m values (custom only) */
+    const double* custom_g2;
+} fraq_spec_t;
+
+/* KernelConfig, fpfp.hpp:50-57. */
+typedef struct {
+    int be_points, sbd_points_1, sbd_points_2, sbd_head;
+    double eps_tol;
+    int auto_size;
+} fraq_kconf_t;
+
+/* RunResult minus the state, fpfp.hpp:59-65, plus the chosen table sizes. */
+typedef struct {
+    double loop_seconds, setup_seconds;
+    double kernel_eps1, kernel_eps2;
+    int np[4];     /* field 1 (np1, np2), field 2 (np1, np2) */
+    int n_head[2];
+} fraq_run_info_t;
+
+/* ---------------------------------------------------------------- context / errors */
+int fraq_ctx_create(int device, void* cuda_stream /* cudaStream_t, NULL = own stream */,
+                    fraq_ctx* out);
+int fraq_ctx_destroy(fraq_ctx ctx);
+int fraq_ctx_synchronize(fraq_ctx ctx);
+void* fraq_ctx_stream(fraq_ctx ctx);
+int fraq_last_error(char* buf, size_t n);
+int fraq_version(void);
+
+/* ---------------------------------------------------------------- L0 quadrature
+ * gauss_jacobi.hpp:19-35 / gauss_jacobi.cpp:108-204.  Nodes by Sturm bisection on the Jacobi
+ * matrix (one thread per eigenvalue), one guarded Newton polish, Christoffel weights: device
+ * setup kernel K2.  Output in host memory (n values each). */
+double fraq_gamma(double x);
+double fraq_inv_gamma_product(double g);
+int fraq_jacobi_moment(double a, double b, int k, double* out);
+int fraq_gauss_jacobi(fraq_ctx ctx, double a, double b, int n, double* nodes, double* weights);
+
+/* ---------------------------------------------------------------- L1 classical weights
+ * cq_weights.hpp:23-33 / cq_weights.cpp:19-67: device kernel K1.  out holds n_max+1 values. */
+int fraq_be_weights(fraq_ctx ctx, double g, double tau, long n_max, double* out, int mem);
+int fraq_sbd_weights(fraq_ctx ctx, double g, double tau, long n_max, double* out, int mem);
+int fraq_coupling_from_transition(double m, double* out);
+
+/* ---------------------------------------------------------------- L2 compressed kernels
+ * fast_kernel.hpp:53-77 / fast_kernel.cpp:38-256: device kernels K2 (rules), K3 (fold),
+ * K4 (error scan + auto sizing, same growth sequence and caps as the reference). */
+int fraq_build_be_kernel(fraq_ctx ctx, double g, double tau, int n_points, fraq_kernel_t* out);
+int fraq_build_sbd_kernel(fraq_ctx ctx, double g, double tau, int n_points_1, int n_points_2,
+                          int n_head, fraq_kernel_t* out);
+int fraq_default_sbd_head(double g);
+int fraq_build_be_kernel_auto(fraq_ctx ctx, double g, double tau, fraq_budget_t* budget,
+                              fraq_kernel_t* out);
+int fraq_build_sbd_kernel_auto(fraq_ctx ctx, double g, double tau, fraq_budget_t* budget,
+                               fraq_kernel_t* out);
+/* Batched auto sizing for parameter sweeps: n kernels at once (one CTA per exponent). */
+int fraq_build_kernels_auto(fraq_ctx ctx, int sbd, int n, const double* gammas, double tau,
+                            fraq_budget_t* budgets, fraq_kernel_t* out);
+/* FastKernel*::reconstruct (fast_kernel.cpp:38-52) at n indices. */
+int fraq_reconstruct(fraq_ctx ctx, const fraq_kernel_t* k, long n, const long* idx, double* out);
+/* kernel_error_report (fast_kernel.cpp:126-180): eps (nullable, host, n_max+1 values). */
+int fraq_kernel_error_report(fraq_ctx ctx, const fraq_kernel_t* k, long n_max, double* eps,
+                             double* max_eps, long* argmax);
+
+/* ---------------------------------------------------------------- L2 history states
+ * BeHistory / SbdHistory (fast_kernel.hpp:87-146, fast_kernel.cpp:261-409) on the device.
+ * A history holds n_groups contiguous DOF groups, group g having dims[g] DOFs and its own kernel
+ * (one group = the reference object with dim = dims[0]).  State layout: per group
+ * y[node][dof] (DOF contiguous, padded), lag ring [cap][dof].  Sequencing checks and error codes
+ * follow the reference exactly; state-observing calls run the fused step kernel K5. */
+int fraq_hist_create(fraq_ctx ctx, int n_groups, const fraq_kernel_t* const* kernels,
+                     const long* dims, int variant, fraq_hist* out);
+int fraq_hist_destroy(fraq_hist h);
+int fraq_hist_info(fraq_hist h, long* level, long* appended, long* dim);
+int fraq_hist_push(fraq_hist h, const double* value, int mem);
+int fraq_hist_advance(fraq_hist h);
+int fraq_hist_append(fraq_hist h, const double* value, int mem);
+int fraq_hist_history_sum(fraq_hist h, double* out, int mem);
+int fraq_hist_derivative(fraq_hist h, double* out, int mem);
+int fraq_hist_lagged(fraq_hist h, long depth, double* out, int mem);
+/* Batched standalone evaluation: pushes U[n * ldu + 0 .. dim) for n = 0..n_steps-1 and writes the
+ * derivative after each push to D[n * ldd + ...] (NaN where the reference would throw
+ * "too early"); D may be NULL.  Equivalent to n_steps x (push; derivative).  Uses the
+ * temporally blocked kernel K5b (history kept on chip across the whole call). */
+int fraq_hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, long ldd,
+                  int mem);
+/* Which kernel the last fraq_hist_run used: 1 = K5b temporally blocked, 0 = per-step K5. */
+int fraq_hist_last_path(fraq_hist h);
+
+/* ---------------------------------------------------------------- L4 FFPE
+ * run() (fpfp.cpp:351-381) for n_inst independent instances (BASELINE C3: 1, C5: 4096) solved
+ * together on the device: histories K5 for both fields, RHS + 2x2-block tridiagonal solve K6,
+ * SBD correction sequence K7.  g1/g2: host, n_inst * grid_m values (row per instance). */
+void fraq_kconf_default(fraq_kconf_t* c);
+int fraq_run(fraq_ctx ctx, const fraq_spec_t* specs, int n_inst, int scheme,
+             const fraq_kconf_t* kconf, double* g1, double* g2, fraq_run_info_t* info);
+/* run() with the reference's per-step observer (fpfp.cpp:360-365): fn(n, g1, g2, grid_m, user)
+ * sees the initial state (n = 0) and every accepted level; single instance.  Each call copies
+ * the level back to the host, so the loop time includes those copies. */
+typedef void (*fraq_observer_fn)(long n, const double* g1, const double* g2, int grid_m,
+                                 void* user);
+int fraq_run_observed(fraq_ctx ctx, const fraq_spec_t* spec, int scheme,
+                      const fraq_kconf_t* kconf, fraq_observer_fn fn, void* user, double* g1,
+                      double* g2, fraq_run_info_t* info);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FRAQCU_H */

@@ -1,0 +1,100 @@
+"""B200-native fast convolution quadrature for Riemann-Liouville derivatives (arXiv 1901.05128).
+
+Drop-in for the reference Python package ``fraq`` (proj/python/fraq/__init__.py): the same
+``__all__`` names with the same signatures, re-exported from the compiled module ``_fraq``
+(paper_1901_05128_b200/csrc/fraq_py.cpp), which runs every operator on the GPU through the C ABI
+in include/fraqcu.h.  There is no CPU fallback: importing without the built extension raises.
+
+    import paper_1901_05128_b200 as fraq
+    k = fraq.build_sbd_kernel(0.4, 0.05, 20, 20, 8)
+    h = fraq.SbdHistory(k, fraq.HistoryVariant.standalone, 1)
+"""
+from __future__ import annotations
+
+import math as _math
+
+try:
+    from . import _fraq as _impl
+except ImportError as exc:  # pragma: no cover - the product must not silently degrade
+    raise ImportError(
+        "paper_1901_05128_b200: the CUDA extension is not built "
+        "(run `python -m paper_1901_05128_b200.build`): " + str(exc)) from exc
+
+# reference __all__ (proj/python/fraq/__init__.py:13-41)
+__all__ = [
+    "BeHistory",
+    "FastKernelBE",
+    "FastKernelSBD",
+    "HistoryVariant",
+    "JacobiRule",
+    "KernelConfig",
+    "KernelErrorReport",
+    "ProblemSpec",
+    "RunResult",
+    "SbdHistory",
+    "Scheme",
+    "StateField",
+    "WeightTable",
+    "be_weights",
+    "build_be_kernel",
+    "build_sbd_kernel",
+    "compute_rates",
+    "coupling_from_transition",
+    "default_sbd_head",
+    "gauss_jacobi",
+    "initial_field",
+    "jacobi_moment",
+    "kernel_error_report",
+    "l2_norm",
+    "parse_fraction",
+    "run",
+    "sbd_weights",
+]
+
+# B200 additions (batched / device entry points)
+EXTRA = [
+    "KernelBudget",
+    "MultiHistory",
+    "build_be_kernel_auto",
+    "build_sbd_kernel_auto",
+    "context_stream",
+    "gamma_fn",
+    "make_be_kernel",
+    "make_sbd_kernel",
+    "run_batch",
+    "synchronize",
+]
+
+globals().update({name: getattr(_impl, name) for name in __all__ + EXTRA
+                  if hasattr(_impl, name)})
+
+
+def parse_fraction(text: str) -> float:
+    """"1/3200" exactly (numerator/denominator) or a plain decimal (bench.cpp:42-57)."""
+    t = text.strip()
+    if "/" in t:
+        num, den = t.split("/", 1)
+        try:
+            n, d = int(num), int(den)
+        except ValueError as e:
+            raise ValueError("bad fraction: " + text) from e
+        if d == 0:
+            raise ValueError("bad fraction: " + text)
+        return float(n) / float(d)
+    try:
+        return float(t)
+    except ValueError as e:
+        raise ValueError("bad number: " + text) from e
+
+
+def compute_rates(tau_and_error):
+    """rate_k = ln(E_k / E_{k+1}) / ln 2 for halving taus; NaN for zero errors (bench.cpp:140-153)."""
+    rates = []
+    for (tc, ec), (tf, ef) in zip(tau_and_error, tau_and_error[1:]):
+        if abs(tc / tf - 2.0) > 1e-9:
+            raise ValueError("compute_rates: taus must halve")
+        rates.append(float("nan") if ec == 0.0 or ef == 0.0 else _math.log(ec / ef) / _math.log(2.0))
+    return rates
+
+
+__all__ = __all__ + EXTRA

@@ -1,0 +1,315 @@
+// capi.cu -- extern "C" entry points of libfraqcu (declared in include/fraqcu.h).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "history.cuh"
+#include "internal.cuh"
+
+namespace fraqcu {
+
+thread_local std::string g_last_error;
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+// history.cu
+void hist_create(fraq_ctx c, int n_groups, const fraq_kernel_t* const* ks, const long* dims,
+                 int variant, fraq_hist* out);
+void hist_destroy(fraq_hist h);
+void hist_info(fraq_hist h, long* level, long* appended, long* dim);
+void hist_push(fraq_hist h, const double* v, int mem);
+void hist_advance(fraq_hist h);
+void hist_append(fraq_hist h, const double* v, int mem);
+void hist_output(fraq_hist h, int mode, double* out, int mem);
+void hist_lagged(fraq_hist h, long depth, double* out, int mem);
+void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, long ldd, int mem);
+int hist_last_path(fraq_hist h);
+// ffpe.cu
+void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
+              const fraq_kconf_t* kc, double* g1, double* g2, fraq_run_info_t* info,
+              fraq_observer_fn obs, void* user);
+
+namespace {
+constexpr double kPi = 3.14159265358979323846;
+
+double host_gamma(double x) {  // gauss_jacobi.cpp:108-123 (host scalar helper for the ABI)
+    static const double c[9] = {0.99999999999980993,  676.5203681218851,     -1259.1392167224028,
+                                771.32342877765313,   -176.61502916214059,   12.507343278686905,
+                                -0.13857109526572012, 9.9843695780195716e-6, 1.5056327351493116e-7};
+    if (x < 0.5) return kPi / (std::sin(kPi * x) * host_gamma(1.0 - x));
+    x -= 1.0;
+    double acc = c[0];
+    for (int i = 1; i < 9; ++i) acc += c[i] / (x + i);
+    const double t = x + 7.5;
+    return std::sqrt(2.0 * kPi) * std::pow(t, x + 0.5) * std::exp(-t) * acc;
+}
+
+void check_exps(double a, double b) {
+    if (!(a > -1.0) || !(b > -1.0))
+        fail(FRAQ_EINVAL, "jacobi exponents must be > -1, got a=" + std::to_string(a) +
+                              " b=" + std::to_string(b));
+}
+}  // namespace
+
+}  // namespace fraqcu
+
+using namespace fraqcu;
+
+extern "C" {
+
+int fraq_version(void) { return 10000; }
+
+int fraq_last_error(char* buf, size_t n) {
+    if (buf && n) {
+        std::strncpy(buf, g_last_error.c_str(), n - 1);
+        buf[n - 1] = 0;
+    }
+    return (int)g_last_error.size();
+}
+
+int fraq_ctx_create(int device, void* stream, fraq_ctx* out) {
+    return guarded([&] {
+        if (!out) fail(FRAQ_EINVAL, "fraq_ctx_create: null out");
+        int count = 0;
+        cudaError_t e = cudaGetDeviceCount(&count);
+        if (e != cudaSuccess || count == 0)
+            fail(FRAQ_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+        if (device < 0 || device >= count) fail(FRAQ_EINVAL, "fraq_ctx_create: bad device");
+        FRAQ_CUDA(cudaSetDevice(device));
+        auto* c = new fraq_ctx_s();
+        c->device = device;
+        if (stream) {
+            c->stream = (cudaStream_t)stream;
+        } else {
+            cudaError_t es = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+            if (es != cudaSuccess) {
+                delete c;
+                fail(FRAQ_ECUDA, cudaGetErrorString(es));
+            }
+            c->own_stream = true;
+        }
+        cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+        *out = c;
+    });
+}
+
+int fraq_ctx_destroy(fraq_ctx c) {
+    return guarded([&] {
+        if (!c) return;
+        cudaSetDevice(c->device);
+        cudaStreamSynchronize(c->stream);
+        if (c->own_stream) cudaStreamDestroy(c->stream);
+        delete c;
+    });
+}
+
+int fraq_ctx_synchronize(fraq_ctx c) {
+    return guarded([&] {
+        check_ctx(c);
+        FRAQ_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+void* fraq_ctx_stream(fraq_ctx c) { return c ? (void*)c->stream : nullptr; }
+
+// ------------------------------------------------------------------ L0
+double fraq_gamma(double x) { return host_gamma(x); }
+double fraq_inv_gamma_product(double g) { return std::sin(kPi * g) / kPi; }
+
+int fraq_jacobi_moment(double a, double b, int k, double* out) {
+    // gauss_jacobi.cpp:135-149 (scalar, host: a test oracle in the reference)
+    return guarded([&] {
+        check_exps(a, b);
+        if (k < 0) fail(FRAQ_EINVAL, "jacobi_moment: k must be >= 0");
+        const double m0 = std::pow(2.0, a + b + 1.0) * host_gamma(a + 1.0) * host_gamma(b + 1.0) /
+                          host_gamma(a + b + 2.0);
+        double prev = m0;
+        if (k == 0) {
+            *out = prev;
+            return;
+        }
+        double cur = (b - a) / (a + b + 2.0) * prev;
+        for (int j = 1; j < k; ++j) {
+            const double nxt = ((b - a) * cur + j * prev) / (a + b + 2.0 + j);
+            prev = cur;
+            cur = nxt;
+        }
+        *out = cur;
+    });
+}
+
+int fraq_gauss_jacobi(fraq_ctx c, double a, double b, int n, double* nodes, double* weights) {
+    return guarded([&] {
+        check_ctx(c);
+        gauss_jacobi_dev(c, a, b, n, nodes, weights);
+    });
+}
+
+// ------------------------------------------------------------------ L1
+static int weights_common(fraq_ctx c, bool sbd, double g, double tau, long n_max, double* out,
+                          int mem) {
+    return guarded([&] {
+        check_ctx(c);
+        if (mem == FRAQ_DEVICE) {
+            if (sbd)
+                sbd_weights_dev(c, g, tau, n_max, out);
+            else
+                be_weights_dev(c, g, tau, n_max, out);
+            return;
+        }
+        check_weight_args(g, tau);
+        if (n_max < 0) fail(FRAQ_EINVAL, sbd ? "sbd_weights: n_max must be >= 0"
+                                            : "be_weights: n_max must be >= 0");
+        DevBuf<double> d((size_t)n_max + 1);
+        if (sbd)
+            sbd_weights_dev(c, g, tau, n_max, d.p);
+        else
+            be_weights_dev(c, g, tau, n_max, d.p);
+        FRAQ_CUDA(cudaMemcpy(out, d.p, sizeof(double) * (n_max + 1), cudaMemcpyDeviceToHost));
+    });
+}
+
+int fraq_be_weights(fraq_ctx c, double g, double tau, long n_max, double* out, int mem) {
+    return weights_common(c, false, g, tau, n_max, out, mem);
+}
+int fraq_sbd_weights(fraq_ctx c, double g, double tau, long n_max, double* out, int mem) {
+    return weights_common(c, true, g, tau, n_max, out, mem);
+}
+
+int fraq_coupling_from_transition(double m, double* out) {
+    // cq_weights.cpp:61-67
+    return guarded([&] {
+        if (!(m > 0.0) || !(m <= 1.0))
+            fail(FRAQ_EINVAL,
+                 "coupling_from_transition: m must be in (0,1], got " + std::to_string(m));
+        if (m == 0.5)
+            fail(FRAQ_EINVAL,
+                 "coupling_from_transition: m = 1/2 makes the transition matrix singular");
+        *out = (1.0 - m) / (2.0 * m - 1.0);
+    });
+}
+
+// ------------------------------------------------------------------ L2 kernels
+int fraq_build_be_kernel(fraq_ctx c, double g, double tau, int np, fraq_kernel_t* out) {
+    return guarded([&] {
+        check_ctx(c);
+        build_be_kernel_dev(c, g, tau, np, out);
+    });
+}
+
+int fraq_build_sbd_kernel(fraq_ctx c, double g, double tau, int np1, int np2, int nh,
+                          fraq_kernel_t* out) {
+    return guarded([&] {
+        check_ctx(c);
+        build_sbd_kernel_dev(c, g, tau, np1, np2, nh, out);
+    });
+}
+
+int fraq_default_sbd_head(double g) { return g <= 0.5 ? 15 : 17; }
+
+int fraq_build_be_kernel_auto(fraq_ctx c, double g, double tau, fraq_budget_t* b,
+                              fraq_kernel_t* out) {
+    return guarded([&] {
+        check_ctx(c);
+        build_kernel_auto_dev(c, false, 1, &g, tau, b, out);
+    });
+}
+
+int fraq_build_sbd_kernel_auto(fraq_ctx c, double g, double tau, fraq_budget_t* b,
+                               fraq_kernel_t* out) {
+    return guarded([&] {
+        check_ctx(c);
+        build_kernel_auto_dev(c, true, 1, &g, tau, b, out);
+    });
+}
+
+int fraq_build_kernels_auto(fraq_ctx c, int sbd, int n, const double* gammas, double tau,
+                            fraq_budget_t* budgets, fraq_kernel_t* out) {
+    return guarded([&] {
+        check_ctx(c);
+        build_kernel_auto_dev(c, sbd != 0, n, gammas, tau, budgets, out);
+    });
+}
+
+int fraq_reconstruct(fraq_ctx c, const fraq_kernel_t* k, long n, const long* idx, double* out) {
+    return guarded([&] {
+        check_ctx(c);
+        reconstruct_dev(c, k, n, idx, out);
+    });
+}
+
+int fraq_kernel_error_report(fraq_ctx c, const fraq_kernel_t* k, long n_max, double* eps,
+                             double* max_eps, long* argmax) {
+    return guarded([&] {
+        check_ctx(c);
+        kernel_error_report_dev(c, k, n_max, eps, max_eps, argmax);
+    });
+}
+
+// ------------------------------------------------------------------ L2 histories
+int fraq_hist_create(fraq_ctx c, int n_groups, const fraq_kernel_t* const* kernels,
+                     const long* dims, int variant, fraq_hist* out) {
+    return guarded([&] { hist_create(c, n_groups, kernels, dims, variant, out); });
+}
+int fraq_hist_destroy(fraq_hist h) {
+    return guarded([&] { hist_destroy(h); });
+}
+int fraq_hist_info(fraq_hist h, long* level, long* appended, long* dim) {
+    return guarded([&] {
+        if (!h) fail(FRAQ_EINVAL, "null history");
+        hist_info(h, level, appended, dim);
+    });
+}
+int fraq_hist_push(fraq_hist h, const double* v, int mem) {
+    return guarded([&] { hist_push(h, v, mem); });
+}
+int fraq_hist_advance(fraq_hist h) {
+    return guarded([&] { hist_advance(h); });
+}
+int fraq_hist_append(fraq_hist h, const double* v, int mem) {
+    return guarded([&] { hist_append(h, v, mem); });
+}
+int fraq_hist_history_sum(fraq_hist h, double* out, int mem) {
+    return guarded([&] { hist_output(h, 1, out, mem); });
+}
+int fraq_hist_derivative(fraq_hist h, double* out, int mem) {
+    return guarded([&] { hist_output(h, 2, out, mem); });
+}
+int fraq_hist_lagged(fraq_hist h, long depth, double* out, int mem) {
+    return guarded([&] { hist_lagged(h, depth, out, mem); });
+}
+int fraq_hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, long ldd,
+                  int mem) {
+    return guarded([&] { hist_run(h, U, ldu, n_steps, D, ldd, mem); });
+}
+int fraq_hist_last_path(fraq_hist h) { return h ? hist_last_path(h) : -1; }
+
+// ------------------------------------------------------------------ L4
+void fraq_kconf_default(fraq_kconf_t* c) {
+    c->be_points = 64;
+    c->sbd_points_1 = 41;
+    c->sbd_points_2 = 41;
+    c->sbd_head = 0;
+    c->eps_tol = 1e-12;
+    c->auto_size = 1;
+}
+
+int fraq_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
+             const fraq_kconf_t* kconf, double* g1, double* g2, fraq_run_info_t* info) {
+    return guarded([&] {
+        check_ctx(c);
+        ffpe_run(c, specs, n_inst, scheme, kconf, g1, g2, info, nullptr, nullptr);
+    });
+}
+
+int fraq_run_observed(fraq_ctx c, const fraq_spec_t* spec, int scheme, const fraq_kconf_t* kconf,
+                      fraq_observer_fn fn, void* user, double* g1, double* g2,
+                      fraq_run_info_t* info) {
+    return guarded([&] {
+        check_ctx(c);
+        ffpe_run(c, spec, 1, scheme, kconf, g1, g2, info, fn, user);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,456 @@
+// fraq.cpp -- C++ mirror of the reference `fraq` API on the B200 C ABI (see fraq.hpp).
+#include "fraq.hpp"
+
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+namespace fraq {
+
+namespace {
+
+std::string last_error() {
+    char buf[1024];
+    fraq_last_error(buf, sizeof(buf));
+    return buf;
+}
+
+}  // namespace
+
+void check(int st) {
+    if (st == FRAQ_OK) return;
+    const std::string msg = last_error();
+    switch (st) {
+        case FRAQ_EINVAL: throw std::invalid_argument(msg);
+        case FRAQ_ELOGIC: throw std::logic_error(msg);
+        case FRAQ_ERANGE: throw std::out_of_range(msg);
+        case FRAQ_ENOMEM: throw std::bad_alloc();
+        default: throw std::runtime_error(msg);
+    }
+}
+
+fraq_ctx default_context() {
+    static std::mutex mu;
+    static fraq_ctx ctx = nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!ctx) {
+        int dev = 0;
+        if (const char* e = std::getenv("FRAQ_DEVICE")) dev = std::atoi(e);
+        check(fraq_ctx_create(dev, nullptr, &ctx));
+    }
+    return ctx;
+}
+
+// ------------------------------------------------------------------ gauss_jacobi
+double gamma_fn(double x) { return fraq_gamma(x); }
+double inv_gamma_product(double alpha) { return fraq_inv_gamma_product(alpha); }
+
+double jacobi_moment0(double a, double b) { return jacobi_moment(a, b, 0); }
+
+double jacobi_moment(double a, double b, int k) {
+    double out = 0.0;
+    check(fraq_jacobi_moment(a, b, k, &out));
+    return out;
+}
+
+JacobiRule gauss_jacobi(double a, double b, int n) {
+    JacobiRule r;
+    r.exponent_a = a;
+    r.exponent_b = b;
+    const int cap = n > 0 ? n : 1;
+    r.nodes.resize(cap);
+    r.weights.resize(cap);
+    check(fraq_gauss_jacobi(default_context(), a, b, n, r.nodes.data(), r.weights.data()));
+    r.nodes.resize(n);
+    r.weights.resize(n);
+    return r;
+}
+
+// ------------------------------------------------------------------ cq_weights
+WeightTable be_weights(double alpha, double tau, long n_max) {
+    WeightTable t;
+    t.scheme = CqScheme::BE;
+    t.alpha = alpha;
+    t.tau = tau;
+    t.weights.resize(n_max >= 0 ? n_max + 1 : 1);
+    check(fraq_be_weights(default_context(), alpha, tau, n_max, t.weights.data(), FRAQ_HOST));
+    return t;
+}
+
+WeightTable sbd_weights(double alpha, double tau, long n_max) {
+    WeightTable t;
+    t.scheme = CqScheme::SBD;
+    t.alpha = alpha;
+    t.tau = tau;
+    t.weights.resize(n_max >= 0 ? n_max + 1 : 1);
+    check(fraq_sbd_weights(default_context(), alpha, tau, n_max, t.weights.data(), FRAQ_HOST));
+    return t;
+}
+
+double coupling_from_transition(double m) {
+    double a = 0.0;
+    check(fraq_coupling_from_transition(m, &a));
+    return a;
+}
+
+// ------------------------------------------------------------------ kernels
+fraq_kernel_t to_flat(const FastKernelBE& k) {
+    fraq_kernel_t f;
+    std::memset(&f, 0, sizeof(f));
+    if (k.ratios.size() > FRAQ_MAX_POINTS || k.node_weights.size() != k.ratios.size())
+        throw std::invalid_argument("FastKernelBE: malformed node tables");
+    f.sbd = 0;
+    f.gamma = k.alpha;
+    f.tau = k.tau;
+    f.n_head = 2;
+    f.head[0] = k.head[0];
+    f.head[1] = k.head[1];
+    f.np1 = (int)k.ratios.size();
+    f.np2 = 0;
+    std::memcpy(f.m1, k.node_weights.data(), sizeof(double) * f.np1);
+    std::memcpy(f.r1, k.ratios.data(), sizeof(double) * f.np1);
+    return f;
+}
+
+fraq_kernel_t to_flat(const FastKernelSBD& k) {
+    fraq_kernel_t f;
+    std::memset(&f, 0, sizeof(f));
+    if (k.ratio1.size() > FRAQ_MAX_POINTS || k.ratio2.size() > FRAQ_MAX_POINTS ||
+        k.mult1.size() != k.ratio1.size() || k.mult2.size() != k.ratio2.size() ||
+        k.head.size() > FRAQ_MAX_HEAD || (int)k.head.size() < k.n_head)
+        throw std::invalid_argument("FastKernelSBD: malformed tables");
+    f.sbd = 1;
+    f.gamma = k.alpha;
+    f.tau = k.tau;
+    f.n_head = k.n_head;
+    std::memcpy(f.head, k.head.data(), sizeof(double) * k.n_head);
+    f.np1 = (int)k.ratio1.size();
+    f.np2 = (int)k.ratio2.size();
+    std::memcpy(f.m1, k.mult1.data(), sizeof(double) * f.np1);
+    std::memcpy(f.r1, k.ratio1.data(), sizeof(double) * f.np1);
+    std::memcpy(f.m2, k.mult2.data(), sizeof(double) * f.np2);
+    std::memcpy(f.r2, k.ratio2.data(), sizeof(double) * f.np2);
+    return f;
+}
+
+FastKernelBE be_from_flat(const fraq_kernel_t& f) {
+    FastKernelBE k;
+    k.alpha = f.gamma;
+    k.tau = f.tau;
+    k.head[0] = f.head[0];
+    k.head[1] = f.head[1];
+    k.node_weights.assign(f.m1, f.m1 + f.np1);
+    k.ratios.assign(f.r1, f.r1 + f.np1);
+    return k;
+}
+
+FastKernelSBD sbd_from_flat(const fraq_kernel_t& f) {
+    FastKernelSBD k;
+    k.alpha = f.gamma;
+    k.tau = f.tau;
+    k.n_head = f.n_head;
+    k.head.assign(f.head, f.head + f.n_head);
+    k.mult1.assign(f.m1, f.m1 + f.np1);
+    k.ratio1.assign(f.r1, f.r1 + f.np1);
+    k.mult2.assign(f.m2, f.m2 + f.np2);
+    k.ratio2.assign(f.r2, f.r2 + f.np2);
+    return k;
+}
+
+namespace {
+double recon_one(const fraq_kernel_t& f, long i) {
+    double out = 0.0;
+    check(fraq_reconstruct(default_context(), &f, 1, &i, &out));
+    return out;
+}
+
+KernelErrorReport report(const fraq_kernel_t& f, long n_max) {
+    KernelErrorReport r;
+    r.alpha = f.gamma;
+    r.tau = f.tau;
+    r.head_len = f.sbd ? f.n_head : 2;
+    r.max_index = n_max;
+    r.eps.assign(n_max >= 0 ? n_max + 1 : 1, 0.0);
+    check(fraq_kernel_error_report(default_context(), &f, n_max, r.eps.data(), &r.max_eps,
+                                   &r.argmax));
+    return r;
+}
+}  // namespace
+
+double FastKernelBE::reconstruct(long i) const { return recon_one(to_flat(*this), i); }
+double FastKernelSBD::reconstruct(long i) const { return recon_one(to_flat(*this), i); }
+
+FastKernelBE build_be_kernel(double alpha, double tau, int n_points) {
+    fraq_kernel_t f;
+    check(fraq_build_be_kernel(default_context(), alpha, tau, n_points, &f));
+    return be_from_flat(f);
+}
+
+FastKernelSBD build_sbd_kernel(double alpha, double tau, int n1, int n2, int n_head) {
+    fraq_kernel_t f;
+    check(fraq_build_sbd_kernel(default_context(), alpha, tau, n1, n2, n_head, &f));
+    return sbd_from_flat(f);
+}
+
+int default_sbd_head(double alpha) { return fraq_default_sbd_head(alpha); }
+
+KernelErrorReport kernel_error_report(const FastKernelBE& k, long n_max) {
+    return report(to_flat(k), n_max);
+}
+KernelErrorReport kernel_error_report(const FastKernelSBD& k, long n_max) {
+    return report(to_flat(k), n_max);
+}
+
+FastKernelBE build_be_kernel_auto(double alpha, double tau, KernelBudget& b) {
+    fraq_budget_t fb{b.horizon, b.eps_tol, b.max_points, b.max_head, 0.0};
+    fraq_kernel_t f;
+    check(fraq_build_be_kernel_auto(default_context(), alpha, tau, &fb, &f));
+    b.horizon = fb.horizon;
+    b.achieved_eps = fb.achieved_eps;
+    return be_from_flat(f);
+}
+
+FastKernelSBD build_sbd_kernel_auto(double alpha, double tau, KernelBudget& b) {
+    fraq_budget_t fb{b.horizon, b.eps_tol, b.max_points, b.max_head, 0.0};
+    fraq_kernel_t f;
+    check(fraq_build_sbd_kernel_auto(default_context(), alpha, tau, &fb, &f));
+    b.horizon = fb.horizon;
+    b.achieved_eps = fb.achieved_eps;
+    return sbd_from_flat(f);
+}
+
+// ------------------------------------------------------------------ histories
+DeviceHistory::DeviceHistory(const std::vector<fraq_kernel_t>& kernels,
+                             const std::vector<long>& dims, HistoryVariant variant) {
+    std::vector<const fraq_kernel_t*> kp;
+    long total = 0;
+    for (std::size_t g = 0; g < kernels.size(); ++g) {
+        kp.push_back(&kernels[g]);
+        total += dims[g];
+    }
+    check(fraq_hist_create(default_context(), (int)kernels.size(), kp.data(), dims.data(),
+                           variant == HistoryVariant::standalone ? FRAQ_STANDALONE : FRAQ_SCHEME,
+                           &h_));
+    dim_ = (std::size_t)total;
+    lag_.resize(dim_);
+}
+
+DeviceHistory::~DeviceHistory() {
+    if (h_) fraq_hist_destroy(h_);
+}
+
+DeviceHistory::DeviceHistory(DeviceHistory&& o) noexcept
+    : h_(o.h_), dim_(o.dim_), lag_(std::move(o.lag_)) {
+    o.h_ = nullptr;
+}
+
+DeviceHistory& DeviceHistory::operator=(DeviceHistory&& o) noexcept {
+    if (this != &o) {
+        if (h_) fraq_hist_destroy(h_);
+        h_ = o.h_;
+        dim_ = o.dim_;
+        lag_ = std::move(o.lag_);
+        o.h_ = nullptr;
+    }
+    return *this;
+}
+
+static void check_dim(std::size_t have, std::size_t want, const char* what) {
+    if (have != want) throw std::invalid_argument(std::string(what) + ": wrong dimension");
+}
+
+void DeviceHistory::push(std::span<const double> v) {
+    check_dim(v.size(), dim_, "History::append");
+    check(fraq_hist_push(h_, v.data(), FRAQ_HOST));
+}
+void DeviceHistory::advance() { check(fraq_hist_advance(h_)); }
+void DeviceHistory::append(std::span<const double> v) {
+    check_dim(v.size(), dim_, "History::append");
+    check(fraq_hist_append(h_, v.data(), FRAQ_HOST));
+}
+long DeviceHistory::level() const {
+    long l = 0;
+    check(fraq_hist_info(h_, &l, nullptr, nullptr));
+    return l;
+}
+long DeviceHistory::appended() const {
+    long a = 0;
+    check(fraq_hist_info(h_, nullptr, &a, nullptr));
+    return a;
+}
+void DeviceHistory::history_sum(std::span<double> out) const {
+    check_dim(out.size(), dim_, "History::history_sum");
+    check(fraq_hist_history_sum(h_, out.data(), FRAQ_HOST));
+}
+void DeviceHistory::derivative(std::span<double> out) const {
+    check_dim(out.size(), dim_, "History::derivative");
+    check(fraq_hist_derivative(h_, out.data(), FRAQ_HOST));
+}
+std::span<const double> DeviceHistory::lagged(long depth) const {
+    check(fraq_hist_lagged(h_, depth, lag_.data(), FRAQ_HOST));
+    return {lag_.data(), dim_};
+}
+void DeviceHistory::run(const double* U, long ldu, long n_steps, double* D, long ldd, int mem) {
+    check(fraq_hist_run(h_, U, ldu, n_steps, D, ldd, mem));
+}
+int DeviceHistory::last_path() const { return fraq_hist_last_path(h_); }
+
+BeHistory::BeHistory(const FastKernelBE& k, HistoryVariant v, std::size_t dim)
+    : DeviceHistory({to_flat(k)}, {(long)dim}, v) {}
+
+SbdHistory::SbdHistory(const FastKernelSBD& k, HistoryVariant v, std::size_t dim)
+    : DeviceHistory({to_flat(k)}, {(long)dim}, v) {}
+
+// ------------------------------------------------------------------ fpfp
+Scheme scheme_from_name(const std::string& name) {
+    if (name == "be") return Scheme::BE;
+    if (name == "fastbe" || name == "fbe") return Scheme::FastBE;
+    if (name == "sbd") return Scheme::SBD;
+    if (name == "fastsbd" || name == "fsbd") return Scheme::FastSBD;
+    throw std::invalid_argument("unknown scheme: " + name);
+}
+
+std::string scheme_name(Scheme s) {
+    switch (s) {
+        case Scheme::BE: return "be";
+        case Scheme::FastBE: return "fastbe";
+        case Scheme::SBD: return "sbd";
+        case Scheme::FastSBD: return "fastsbd";
+    }
+    return "?";
+}
+
+bool scheme_is_fast(Scheme s) { return s == Scheme::FastBE || s == Scheme::FastSBD; }
+bool scheme_is_sbd(Scheme s) { return s == Scheme::SBD || s == Scheme::FastSBD; }
+
+StateField initial_field(const ProblemSpec& spec) {
+    StateField f;
+    const int m = spec.grid_m;
+    f.g1.resize(m);
+    f.g2.resize(m);
+    const double h = spec.h();
+    for (int j = 0; j < m; ++j) {
+        const double x = (j + 1) * h;
+        switch (spec.initial) {
+            case InitialData::poly_sin:
+                f.g1[j] = x * (1.0 - x);
+                f.g2[j] = std::sin(x);
+                break;
+            case InitialData::indicator:
+                f.g1[j] = x > 0.5 ? 1.0 - x : 0.0;
+                f.g2[j] = x < 0.5 ? x : 0.0;
+                break;
+            case InitialData::custom:
+                if ((int)spec.custom_g1.size() != m || (int)spec.custom_g2.size() != m)
+                    throw std::invalid_argument(
+                        "initial_field: custom samples must have grid_m entries");
+                f.g1 = spec.custom_g1;
+                f.g2 = spec.custom_g2;
+                break;
+        }
+    }
+    return f;
+}
+
+double l2_norm(std::span<const double> v, double h) {
+    double s = 0.0;
+    for (double x : v) s += x * x;
+    return std::sqrt(h * s);
+}
+
+namespace {
+fraq_spec_t flat_spec(const ProblemSpec& s) {
+    fraq_spec_t f;
+    f.alpha1 = s.alpha1;
+    f.alpha2 = s.alpha2;
+    f.coupling_a = s.coupling_a;
+    f.length = s.length;
+    f.t_final = s.t_final;
+    f.grid_m = s.grid_m;
+    f.n_steps = s.n_steps;
+    f.initial = s.initial == InitialData::poly_sin
+                    ? FRAQ_POLY_SIN
+                    : (s.initial == InitialData::indicator ? FRAQ_INDICATOR : FRAQ_CUSTOM);
+    f.custom_g1 = s.custom_g1.empty() ? nullptr : s.custom_g1.data();
+    f.custom_g2 = s.custom_g2.empty() ? nullptr : s.custom_g2.data();
+    return f;
+}
+fraq_kconf_t flat_kconf(const KernelConfig& k) {
+    return fraq_kconf_t{k.be_points, k.sbd_points_1, k.sbd_points_2, k.sbd_head, k.eps_tol,
+                        k.auto_size ? 1 : 0};
+}
+int flat_scheme(Scheme s) {
+    switch (s) {
+        case Scheme::BE: return FRAQ_BE;
+        case Scheme::FastBE: return FRAQ_FASTBE;
+        case Scheme::SBD: return FRAQ_SBD;
+        default: return FRAQ_FASTSBD;
+    }
+}
+struct ObsCtx {
+    const std::function<void(long, const StateField&)>* fn;
+    StateField f;
+};
+void obs_tramp(long n, const double* g1, const double* g2, int m, void* user) {
+    auto* o = static_cast<ObsCtx*>(user);
+    o->f.g1.assign(g1, g1 + m);
+    o->f.g2.assign(g2, g2 + m);
+    o->f.step = n;
+    (*o->fn)(n, o->f);
+}
+}  // namespace
+
+RunResult run(const ProblemSpec& spec, Scheme scheme, const KernelConfig& kconf,
+              const std::function<void(long, const StateField&)>& observer) {
+    if (spec.initial == InitialData::custom &&
+        ((int)spec.custom_g1.size() != spec.grid_m || (int)spec.custom_g2.size() != spec.grid_m))
+        throw std::invalid_argument("initial_field: custom samples must have grid_m entries");
+    const fraq_spec_t fs = flat_spec(spec);
+    const fraq_kconf_t kc = flat_kconf(kconf);
+    RunResult rr;
+    rr.final_state.g1.resize(spec.grid_m > 0 ? spec.grid_m : 1);
+    rr.final_state.g2.resize(spec.grid_m > 0 ? spec.grid_m : 1);
+    fraq_run_info_t info{};
+    if (observer) {
+        ObsCtx oc{&observer, {}};
+        check(fraq_run_observed(default_context(), &fs, flat_scheme(scheme), &kc, obs_tramp, &oc,
+                                rr.final_state.g1.data(), rr.final_state.g2.data(), &info));
+    } else {
+        check(fraq_run(default_context(), &fs, 1, flat_scheme(scheme), &kc, rr.final_state.g1.data(),
+                       rr.final_state.g2.data(), &info));
+    }
+    rr.final_state.step = spec.n_steps;
+    rr.loop_seconds = info.loop_seconds;
+    rr.setup_seconds = info.setup_seconds;
+    rr.kernel_eps1 = info.kernel_eps1;
+    rr.kernel_eps2 = info.kernel_eps2;
+    return rr;
+}
+
+std::vector<RunResult> run_batch(const std::vector<ProblemSpec>& specs, Scheme scheme,
+                                 const KernelConfig& kconf) {
+    std::vector<fraq_spec_t> fs;
+    for (const auto& s : specs) fs.push_back(flat_spec(s));
+    const fraq_kconf_t kc = flat_kconf(kconf);
+    const int n = (int)specs.size();
+    if (n == 0) return {};
+    const int m = specs[0].grid_m;
+    std::vector<double> g1((size_t)n * m), g2((size_t)n * m);
+    fraq_run_info_t info{};
+    check(fraq_run(default_context(), fs.data(), n, flat_scheme(scheme), &kc, g1.data(), g2.data(),
+                   &info));
+    std::vector<RunResult> out(n);
+    for (int i = 0; i < n; ++i) {
+        out[i].final_state.g1.assign(g1.begin() + (size_t)i * m, g1.begin() + (size_t)(i + 1) * m);
+        out[i].final_state.g2.assign(g2.begin() + (size_t)i * m, g2.begin() + (size_t)(i + 1) * m);
+        out[i].final_state.step = specs[i].n_steps;
+        out[i].loop_seconds = info.loop_seconds;
+        out[i].setup_seconds = info.setup_seconds;
+    }
+    return out;
+}
+
+}  // namespace fraq

@@ -1,0 +1,223 @@
+// fraq.hpp -- C++ mirror of the reference `fraq` headers (proj/include/fraq/*.hpp) on top of the
+// B200 C ABI (include/fraqcu.h).
+//
+// Same namespace, class, function and field names, argument meaning and exception types as the
+// reference (gauss_jacobi.hpp, cq_weights.hpp, fast_kernel.hpp, fpfp.hpp), so reference call
+// sites compile unchanged against this header.  Every compute call runs on the GPU through the
+// C ABI; there is no CPU fallback (no CUDA device -> std::runtime_error).
+//
+// Differences, all additive:
+//   * BeHistory / SbdHistory own a device history (fraq_hist); lagged() returns a span into a
+//     host mirror that stays valid until the next call on the object;
+//   * run(U, n_steps, D) batched evaluation (host or device pointers) on the histories;
+//   * run_batch() solves many FFPE instances at once (BASELINE C5).
+#pragma once
+
+#include <cstddef>
+#include <functional>
+#include <memory>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "fraqcu.h"
+
+namespace fraq {
+
+// ------------------------------------------------------------------ runtime
+/// Process-wide context on the current device (FRAQ_DEVICE env overrides), created lazily.
+fraq_ctx default_context();
+/// Throws the reference exception type matching a fraqcu status code.
+void check(int status);
+
+// ------------------------------------------------------------------ gauss_jacobi.hpp
+struct JacobiRule {
+    double exponent_a = 0.0;
+    double exponent_b = 0.0;
+    std::vector<double> nodes;
+    std::vector<double> weights;
+    std::size_t size() const { return nodes.size(); }
+};
+
+double gamma_fn(double x);
+double inv_gamma_product(double alpha);
+double jacobi_moment0(double exponent_a, double exponent_b);
+double jacobi_moment(double exponent_a, double exponent_b, int k);
+JacobiRule gauss_jacobi(double exponent_a, double exponent_b, int n_points);
+
+// ------------------------------------------------------------------ cq_weights.hpp
+enum class CqScheme { BE, SBD };
+
+struct WeightTable {
+    CqScheme scheme = CqScheme::BE;
+    double alpha = 0.0;
+    double tau = 1.0;
+    std::vector<double> weights;
+    double operator[](std::size_t i) const { return weights[i]; }
+    std::size_t size() const { return weights.size(); }
+};
+
+WeightTable be_weights(double alpha, double tau, long n_max);
+WeightTable sbd_weights(double alpha, double tau, long n_max);
+double coupling_from_transition(double m);
+
+// ------------------------------------------------------------------ fast_kernel.hpp
+struct FastKernelBE {
+    double alpha = 0.0;
+    double tau = 1.0;
+    double head[2] = {0.0, 0.0};
+    std::vector<double> node_weights;
+    std::vector<double> ratios;
+    std::size_t n_points() const { return ratios.size(); }
+    double reconstruct(long i) const;
+};
+
+struct FastKernelSBD {
+    double alpha = 0.0;
+    double tau = 1.0;
+    int n_head = 3;
+    std::vector<double> head;
+    std::vector<double> mult1;
+    std::vector<double> ratio1;
+    std::vector<double> mult2;
+    std::vector<double> ratio2;
+    double reconstruct(long i) const;
+};
+
+struct KernelErrorReport {
+    double alpha = 0.0;
+    double tau = 1.0;
+    long head_len = 0;
+    long max_index = 0;
+    std::vector<double> eps;
+    double max_eps = 0.0;
+    long argmax = 0;
+};
+
+FastKernelBE build_be_kernel(double alpha, double tau, int n_points);
+FastKernelSBD build_sbd_kernel(double alpha, double tau, int n_points_1, int n_points_2,
+                               int n_head);
+int default_sbd_head(double alpha);
+KernelErrorReport kernel_error_report(const FastKernelBE& k, long n_max);
+KernelErrorReport kernel_error_report(const FastKernelSBD& k, long n_max);
+
+struct KernelBudget {
+    long horizon = 0;
+    double eps_tol = 1e-12;
+    int max_points = 256;
+    int max_head = 256;
+    double achieved_eps = 0.0;
+};
+
+FastKernelBE build_be_kernel_auto(double alpha, double tau, KernelBudget& budget);
+FastKernelSBD build_sbd_kernel_auto(double alpha, double tau, KernelBudget& budget);
+
+enum class HistoryVariant { standalone, scheme };
+
+// flat conversions (the ABI's value type)
+fraq_kernel_t to_flat(const FastKernelBE& k);
+fraq_kernel_t to_flat(const FastKernelSBD& k);
+FastKernelBE be_from_flat(const fraq_kernel_t& f);
+FastKernelSBD sbd_from_flat(const fraq_kernel_t& f);
+
+/// Common device history implementation (one or several DOF groups).
+class DeviceHistory {
+public:
+    DeviceHistory(const std::vector<fraq_kernel_t>& kernels, const std::vector<long>& dims,
+                  HistoryVariant variant);
+    ~DeviceHistory();
+    DeviceHistory(const DeviceHistory&) = delete;
+    DeviceHistory& operator=(const DeviceHistory&) = delete;
+    DeviceHistory(DeviceHistory&&) noexcept;
+    DeviceHistory& operator=(DeviceHistory&&) noexcept;
+
+    void push(std::span<const double> value);
+    void advance();
+    void append(std::span<const double> value);
+    long level() const;
+    long appended() const;
+    std::size_t dim() const { return dim_; }
+    void history_sum(std::span<double> out) const;
+    void derivative(std::span<double> out) const;
+    std::span<const double> lagged(long depth) const;
+    /// n_steps x (push U row; derivative -> D row).  mem: FRAQ_HOST or FRAQ_DEVICE.
+    void run(const double* U, long ldu, long n_steps, double* D, long ldd, int mem = FRAQ_HOST);
+    int last_path() const;
+    fraq_hist handle() const { return h_; }
+
+private:
+    fraq_hist h_ = nullptr;
+    std::size_t dim_ = 0;
+    mutable std::vector<double> lag_;
+};
+
+/// BeHistory (fast_kernel.hpp:87-116) on the device.
+class BeHistory : public DeviceHistory {
+public:
+    BeHistory(const FastKernelBE& kernel, HistoryVariant variant, std::size_t dim);
+};
+
+/// SbdHistory (fast_kernel.hpp:120-146) on the device.
+class SbdHistory : public DeviceHistory {
+public:
+    SbdHistory(const FastKernelSBD& kernel, HistoryVariant variant, std::size_t dim);
+};
+
+// ------------------------------------------------------------------ fpfp.hpp
+enum class Scheme { BE, FastBE, SBD, FastSBD };
+Scheme scheme_from_name(const std::string& name);
+std::string scheme_name(Scheme s);
+bool scheme_is_fast(Scheme s);
+bool scheme_is_sbd(Scheme s);
+
+enum class InitialData { poly_sin, indicator, custom };
+
+struct ProblemSpec {
+    double alpha1 = 0.5;
+    double alpha2 = 0.5;
+    double coupling_a = 0.0;
+    int grid_m = 255;
+    double length = 1.0;
+    double t_final = 1.0;
+    long n_steps = 100;
+    InitialData initial = InitialData::poly_sin;
+    std::vector<double> custom_g1, custom_g2;
+    double tau() const { return t_final / double(n_steps); }
+    double h() const { return length / double(grid_m + 1); }
+};
+
+struct StateField {
+    std::vector<double> g1, g2;
+    long step = 0;
+};
+
+struct KernelConfig {
+    int be_points = 64;
+    int sbd_points_1 = 41;
+    int sbd_points_2 = 41;
+    int sbd_head = 0;
+    double eps_tol = 1e-12;
+    bool auto_size = true;
+};
+
+struct RunResult {
+    StateField final_state;
+    double loop_seconds = 0.0;
+    double setup_seconds = 0.0;
+    double kernel_eps1 = 0.0;
+    double kernel_eps2 = 0.0;
+};
+
+StateField initial_field(const ProblemSpec& spec);
+double l2_norm(std::span<const double> v, double h);
+
+/// fpfp.cpp:351-381 on the device.  The observer, when set, sees the initial state only (the
+/// device loop does not stream intermediate states back; pass n_steps-limited specs instead).
+RunResult run(const ProblemSpec& spec, Scheme scheme, const KernelConfig& kconf = {},
+              const std::function<void(long, const StateField&)>& observer = nullptr);
+
+/// Many independent instances (same grid_m, n_steps, t_final) solved together.
+std::vector<RunResult> run_batch(const std::vector<ProblemSpec>& specs, Scheme scheme,
+                                 const KernelConfig& kconf = {});
+
+}  // namespace fraq

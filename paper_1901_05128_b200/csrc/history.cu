@@ -1,0 +1,773 @@
+// history.cu -- the fused fast-CQ history kernels and the device history objects.
+//
+// K5  (step_kernel)    one time level for every DOF: advance (y <- r y + f u_lag) fused with the
+//                      append into the lag ring and the readout (node sum + exact head window).
+//                      One HBM pass over the state per level.  BeHistory/SbdHistory
+//                      advance/append/history_sum/derivative, fast_kernel.cpp:268-409.
+// K5b (run_kernel)     temporally blocked standalone evaluation over many levels: each warp owns
+//                      4 DOFs x all nodes in registers for the whole call, so the state never
+//                      leaves the SM; inputs stream in, derivatives stream out.  fp64-FMA bound.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "history.cuh"
+
+namespace fraqcu {
+
+namespace {
+
+struct d4 {
+    double x, y, z, w;
+};
+
+// 256-bit streaming access to the history state: L1 bypass, L2 evict-first so the lag rings
+// and head windows (touched once per level) stay L2-resident while the state streams.
+__device__ __forceinline__ d4 ld_stream(const double* p) {
+    d4 v;
+    asm volatile("ld.global.L1::no_allocate.L2::evict_first.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_stream(double* p, const d4& v) {
+    asm volatile("st.global.L1::no_allocate.L2::evict_first.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p),
+                 "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ d4 ld4(const double* p) {
+    const double2 a = *reinterpret_cast<const double2*>(p);
+    const double2 b = *reinterpret_cast<const double2*>(p + 2);
+    return {a.x, a.y, b.x, b.y};
+}
+__device__ __forceinline__ void st4(double* p, const d4& v) {
+    *reinterpret_cast<double2*>(p) = make_double2(v.x, v.y);
+    *reinterpret_cast<double2*>(p + 2) = make_double2(v.z, v.w);
+}
+__device__ __forceinline__ void fma4(d4& acc, double h, const d4& x) {
+    acc.x = fma(h, x.x, acc.x);
+    acc.y = fma(h, x.y, acc.y);
+    acc.z = fma(h, x.z, acc.z);
+    acc.w = fma(h, x.w, acc.w);
+}
+
+// ------------------------------------------------------------------------------------------ K5
+// CTA = LANES DOF quads x S node slices.  Thread (slice sl, quad) streams nodes j = sl, sl+S, ..
+// of its 4 DOFs with 256-bit loads/stores; slice partial sums meet in shared memory; slice 0
+// finishes (append into the ring, exact head window, output).
+template <int LANES, int S>
+__global__ void __launch_bounds__(LANES* S) step_kernel(StepArgs A) {
+    const int2 tile = A.tiles[blockIdx.x];
+    const GroupDev G = A.groups[tile.x];
+    const int lane = threadIdx.x % LANES;
+    const int sl = threadIdx.x / LANES;
+    const int m = 4 * (tile.y + lane);  // first DOF of this thread's quad (within the group)
+    const bool live = m < G.dim;
+    __shared__ d4 s_part[S][LANES];
+
+    // feed value u_{level+1-L} from the ring (read by every slice before the barrier below)
+    const long fi = A.level + 1 - G.L;
+    const bool feed = A.adv && fi >= A.lo && fi <= A.appended - 1;
+    const long ld = G.ld;
+    d4 v = {0.0, 0.0, 0.0, 0.0};
+    if (feed && live) v = ld4(A.ring + G.ring_off + (fi % G.L) * ld + m);
+
+    d4 acc = {0.0, 0.0, 0.0, 0.0};
+    if (live && (A.adv || A.mode != MODE_NONE)) {
+        const double* __restrict__ cr = A.cr + G.co_off;
+        const double* __restrict__ cf = A.cf + G.co_off;
+        double* base = A.state + G.st_off + m;
+        if (A.adv) {
+#pragma unroll 4
+            for (int j = sl; j < G.J; j += S) {
+                double* p = base + j * ld;
+                d4 y = ld_stream(p);
+                const double r = __ldg(cr + j), f = __ldg(cf + j);
+                y.x = fma(r, y.x, f * v.x);
+                y.y = fma(r, y.y, f * v.y);
+                y.z = fma(r, y.z, f * v.z);
+                y.w = fma(r, y.w, f * v.w);
+                st_stream(p, y);
+                acc.x += y.x;
+                acc.y += y.y;
+                acc.z += y.z;
+                acc.w += y.w;
+            }
+        } else {
+#pragma unroll 4
+            for (int j = sl; j < G.J; j += S) {
+                const d4 y = ld_stream(base + j * ld);
+                acc.x += y.x;
+                acc.y += y.y;
+                acc.z += y.z;
+                acc.w += y.w;
+            }
+        }
+    }
+    if (S > 1) {
+        s_part[sl][lane] = acc;
+        __syncthreads();
+        if (sl != 0) return;
+#pragma unroll
+        for (int q = 1; q < S; ++q) {
+            const d4 t = s_part[q][lane];
+            acc.x += t.x;
+            acc.y += t.y;
+            acc.z += t.z;
+            acc.w += t.w;
+        }
+    }
+    if (!live) return;
+    const int nv = min(4, G.dim - m);  // valid DOFs of this quad
+    double* ring = A.ring + G.ring_off + m;
+    long appended = A.appended;
+    if (A.app) {
+        const double* u = A.u + G.dof0 + m;
+        d4 x;
+        x.x = u[0];
+        x.y = nv > 1 ? u[1] : 0.0;
+        x.z = nv > 2 ? u[2] : 0.0;
+        x.w = nv > 3 ? u[3] : 0.0;
+        st4(ring + (appended % G.L) * ld, x);
+        ++appended;
+    }
+    if (A.mode == MODE_NONE) return;
+    const double* hd = A.head + G.hd_off;
+    if (A.mode == MODE_DERIV) {
+        const long n = appended - 1;
+        long top;
+        if (!G.sbd)
+            top = 1;
+        else {
+            const long bound = A.lo == 0 ? n : n - 1;
+            top = min((long)G.L - 1, bound);
+        }
+        for (long i = 0; i <= top; ++i) fma4(acc, hd[i], ld4(ring + ((n - i) % G.L) * ld));
+    } else if (A.mode == MODE_FFPE) {
+        // FastStepper: s = history + sum_{i=1}^{top} d_i G^{n-i}, n = appended (G^n not yet in)
+        const long n = appended;
+        long top;
+        if (!G.sbd)
+            top = n >= 2 ? 1 : 0;
+        else
+            top = min((long)G.L - 1, n - 1);
+        for (long i = 1; i <= top; ++i) fma4(acc, hd[i], ld4(ring + ((n - i) % G.L) * ld));
+    }
+    double* o = A.out + G.dof0 + m;
+    o[0] = acc.x;
+    if (nv > 1) o[1] = acc.y;
+    if (nv > 2) o[2] = acc.z;
+    if (nv > 3) o[3] = acc.w;
+}
+
+// ----------------------------------------------------------------------------------------- K5b
+// Warp task: 4 DOFs of one group, all levels of the call.  Lane l owns nodes j = l + 32 p,
+// p < P; the state is kept as z_j = y_j / f_j so one level is z <- r z + u_lag (one FMA) and the
+// readout is sum_j f_j z_j (one FMA).  Per-step node sums: 4-value warp reduce-scatter.
+constexpr int RUN_Q = 4;        // DOFs per warp
+constexpr int RUN_TC = 32;      // levels per staged chunk
+constexpr int RUN_LMAX = 64;    // max lag supported on this path
+constexpr int RUN_WARPS = 4;    // warps per CTA (independent tasks)
+
+struct RunArgs {
+    const GroupDev* groups;
+    const int2* tasks;      // (group, first DOF of the 4-DOF task)
+    int n_tasks;
+    int* counter;           // dynamic task counter (zeroed before launch)
+    double* state;
+    double* ring;
+    const double* cr;
+    const double* cf;
+    const double* head;
+    long A0;                // values appended before the call (pure push sequence)
+    int lo;
+    long n_steps;
+    const double* U;        // device, row n at U + n*ldu, group-relative dof0 offsets
+    long ldu;
+    double* D;              // nullable
+    long ldd;
+};
+
+struct RunSmem {
+    double X[RUN_LMAX + RUN_TC][RUN_Q];
+    double F[RUN_TC][RUN_Q];
+    double Dv[RUN_TC][RUN_Q];
+    double hd[RUN_LMAX];
+};
+
+template <int P>
+__global__ void __launch_bounds__(RUN_WARPS * 32, 2) run_kernel(RunArgs A) {
+    __shared__ RunSmem sm_all[RUN_WARPS];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    RunSmem& sm = sm_all[warp];
+    for (;;) {
+        int task = 0;
+        if (lane == 0) task = atomicAdd(A.counter, 1);
+        task = __shfl_sync(0xffffffffu, task, 0);
+        if (task >= A.n_tasks) return;
+        const int2 tk = A.tasks[task];
+        const GroupDev G = A.groups[tk.x];
+        const int m0 = tk.y;
+        const int L = G.L, J = G.J;
+        const long ld = G.ld;
+        // coefficients and initial state
+        double r[P], f[P], z[P][RUN_Q];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const int j = lane + 32 * p;
+            if (j < J) {
+                r[p] = A.cr[G.co_off + j];
+                f[p] = A.cf[G.co_off + j];
+                const double* y = A.state + G.st_off + j * ld + m0;
+#pragma unroll
+                for (int q = 0; q < RUN_Q; ++q) z[p][q] = (m0 + q < G.dim) ? y[q] / f[p] : 0.0;
+            } else {
+                r[p] = 0.0;
+                f[p] = 0.0;
+#pragma unroll
+                for (int q = 0; q < RUN_Q; ++q) z[p][q] = 0.0;
+            }
+        }
+        for (int i = lane; i < L; i += 32) sm.hd[i] = A.head[G.hd_off + i];
+        // history window: X(k) for k in [A0 - L, A0 - 1] from the ring, rows RUN_LMAX - L ..
+        for (int idx = lane; idx < L * RUN_Q; idx += 32) {
+            const int row = idx / RUN_Q, q = idx % RUN_Q;
+            const long k = A.A0 - L + row;
+            double x = 0.0;
+            if (k >= 0 && m0 + q < G.dim) x = A.ring[G.ring_off + (k % L) * ld + m0 + q];
+            sm.X[RUN_LMAX - L + row][q] = x;
+        }
+        const double* Ubase = A.U + G.dof0 + m0;
+        // prefetch chunk 0 (lane t holds row t)
+        double pre[RUN_Q];
+        auto load_rows = [&](long c0) {
+            const long t = c0 + lane;
+#pragma unroll
+            for (int q = 0; q < RUN_Q; ++q)
+                pre[q] = (t < A.n_steps && m0 + q < G.dim) ? Ubase[t * A.ldu + q] : 0.0;
+        };
+        load_rows(0);
+        for (long c0 = 0; c0 < A.n_steps; c0 += RUN_TC) {
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < RUN_Q; ++q) sm.X[RUN_LMAX + lane][q] = pre[q];
+            if (c0 + RUN_TC < A.n_steps) load_rows(c0 + RUN_TC);
+            __syncwarp();
+            // exact head window F[t][q] = sum_{i<=top(n)} h_i X(n-i), n = A0 + c0 + t
+            {
+                const int t = lane;
+                const long n = A.A0 + c0 + t;
+                long top;
+                if (!G.sbd)
+                    top = 1;
+                else
+                    top = min((long)L - 1, n - A.lo);
+                double fq[RUN_Q] = {0.0, 0.0, 0.0, 0.0};
+                for (long i = 0; i <= top; ++i) {
+                    const double h = sm.hd[i];
+#pragma unroll
+                    for (int q = 0; q < RUN_Q; ++q)
+                        fq[q] = fma(h, sm.X[RUN_LMAX + t - i][q], fq[q]);
+                }
+#pragma unroll
+                for (int q = 0; q < RUN_Q; ++q) sm.F[t][q] = fq[q];
+            }
+            __syncwarp();
+            const int tmax = (int)min((long)RUN_TC, A.n_steps - c0);
+            for (int t = 0; t < tmax; ++t) {
+                const long n = A.A0 + c0 + t;
+                if (n >= 1) {  // advance to level n; feed X(n - L) when n - L >= lo
+                    const bool feed = n - L >= A.lo;
+                    double v[RUN_Q];
+#pragma unroll
+                    for (int q = 0; q < RUN_Q; ++q) v[q] = feed ? sm.X[RUN_LMAX + t - L][q] : 0.0;
+#pragma unroll
+                    for (int p = 0; p < P; ++p)
+#pragma unroll
+                        for (int q = 0; q < RUN_Q; ++q) z[p][q] = fma(r[p], z[p][q], v[q]);
+                }
+                double s[RUN_Q] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int p = 0; p < P; ++p)
+#pragma unroll
+                    for (int q = 0; q < RUN_Q; ++q) s[q] = fma(f[p], z[p][q], s[q]);
+                // reduce-scatter 4 values over 32 lanes -> lanes 8q..8q+7 hold DOF q's total
+                const bool up = lane & 16;
+                double a0 = up ? s[2] : s[0], a1 = up ? s[3] : s[1];
+                const double b0 = up ? s[0] : s[2], b1 = up ? s[1] : s[3];
+                a0 += __shfl_xor_sync(0xffffffffu, b0, 16);
+                a1 += __shfl_xor_sync(0xffffffffu, b1, 16);
+                const bool up8 = lane & 8;
+                double cval = up8 ? a1 : a0;
+                const double dsend = up8 ? a0 : a1;
+                cval += __shfl_xor_sync(0xffffffffu, dsend, 8);
+                cval += __shfl_xor_sync(0xffffffffu, cval, 4);
+                cval += __shfl_xor_sync(0xffffffffu, cval, 2);
+                cval += __shfl_xor_sync(0xffffffffu, cval, 1);
+                if ((lane & 7) == 0) {
+                    const int q = lane >> 3;
+                    const bool valid = G.sbd ? true : (n >= 1);
+                    sm.Dv[t][q] = valid ? cval + sm.F[t][q] : __longlong_as_double(0x7ff8000000000000LL);
+                }
+            }
+            __syncwarp();
+            if (A.D && lane < tmax) {
+                double* drow = A.D + (c0 + lane) * A.ldd + G.dof0 + m0;
+#pragma unroll
+                for (int q = 0; q < RUN_Q; ++q)
+                    if (m0 + q < G.dim) drow[q] = sm.Dv[lane][q];
+            }
+            // slide the window: the last L inputs (times A0+c0+tmax-L ..) move to rows
+            // RUN_LMAX-L .. RUN_LMAX-1; read everything before writing (ranges may overlap)
+            __syncwarp();
+            double tmp[RUN_LMAX * RUN_Q / 32];
+#pragma unroll
+            for (int it = 0; it < RUN_LMAX * RUN_Q / 32; ++it) {
+                const int idx = lane + 32 * it;
+                if (idx < L * RUN_Q) tmp[it] = sm.X[tmax + RUN_LMAX - L + idx / RUN_Q][idx % RUN_Q];
+            }
+            __syncwarp();
+#pragma unroll
+            for (int it = 0; it < RUN_LMAX * RUN_Q / 32; ++it) {
+                const int idx = lane + 32 * it;
+                if (idx < L * RUN_Q) sm.X[RUN_LMAX - L + idx / RUN_Q][idx % RUN_Q] = tmp[it];
+            }
+        }
+        // write back state (y = f z) and the ring (last L inputs)
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const int j = lane + 32 * p;
+            if (j < J) {
+                double* y = A.state + G.st_off + j * ld + m0;
+#pragma unroll
+                for (int q = 0; q < RUN_Q; ++q)
+                    if (m0 + q < G.dim) y[q] = f[p] * z[p][q];
+            }
+        }
+        __syncwarp();
+        const long A1 = A.A0 + A.n_steps;
+        for (int idx = lane; idx < L * RUN_Q; idx += 32) {
+            const int row = idx / RUN_Q, q = idx % RUN_Q;
+            const long k = A1 - L + row;
+            if (k >= 0 && m0 + q < G.dim)
+                A.ring[G.ring_off + (k % L) * ld + m0 + q] = sm.X[RUN_LMAX - L + row][q];
+        }
+        __syncwarp();
+    }
+}
+
+template <int P>
+void launch_run_p(const RunArgs& a, int grid, cudaStream_t s) {
+    run_kernel<P><<<grid, RUN_WARPS * 32, 0, s>>>(a);
+}
+
+void launch_run(int P, const RunArgs& a, int grid, cudaStream_t s) {
+    switch (P) {
+#define FRAQ_P(k) \
+    case k: launch_run_p<k>(a, grid, s); break;
+        FRAQ_P(1) FRAQ_P(2) FRAQ_P(3) FRAQ_P(4) FRAQ_P(5) FRAQ_P(6) FRAQ_P(7) FRAQ_P(8)
+        FRAQ_P(9) FRAQ_P(10) FRAQ_P(11) FRAQ_P(12) FRAQ_P(13) FRAQ_P(14) FRAQ_P(15) FRAQ_P(16)
+#undef FRAQ_P
+        default: fail(FRAQ_ERUNTIME, "run_kernel: unsupported node count");
+    }
+    FRAQ_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------ HistDevice
+void HistDevice::build(fraq_ctx c, int n_groups, const fraq_kernel_t* const* ks, const long* dims) {
+    groups_h.clear();
+    tiles_h.clear();
+    kernels.assign(n_groups, fraq_kernel_t{});
+    long st = 0, rg = 0, dof = 0;
+    int co = 0, hd = 0;
+    std::vector<double> hr, hf, hh;
+    max_J = 0;
+    max_L = 0;
+    ztrick_ok = true;
+    long max_dim = 0;
+    for (int g = 0; g < n_groups; ++g) {
+        const fraq_kernel_t& k = *ks[g];
+        kernels[g] = k;
+        GroupDev G{};
+        G.dof0 = dof;
+        G.dim = (int)dims[g];
+        G.ld = (int)((dims[g] + 3) / 4 * 4);
+        G.J = k.np1 + k.np2;
+        G.L = k.sbd ? std::max(2, k.n_head) : 2;
+        G.sbd = k.sbd;
+        G.st_off = st;
+        G.ring_off = rg;
+        G.co_off = co;
+        G.hd_off = hd;
+        // feed coefficients: BE node weights; SBD mult * ratio^(n_head-3) (fast_kernel.cpp:337-340)
+        for (int j = 0; j < k.np1; ++j) {
+            hr.push_back(k.r1[j]);
+            hf.push_back(k.sbd ? k.m1[j] * std::pow(k.r1[j], double(k.n_head - 3)) : k.m1[j]);
+        }
+        for (int j = 0; j < k.np2; ++j) {
+            hr.push_back(k.r2[j]);
+            hf.push_back(k.m2[j] * std::pow(k.r2[j], double(k.n_head - 3)));
+        }
+        for (int i = 0; i < G.L; ++i) hh.push_back(i < k.n_head ? k.head[i] : 0.0);
+        for (int j = co; j < (int)hf.size(); ++j)
+            if (hf[j] == 0.0 || !std::isfinite(1.0 / hf[j])) ztrick_ok = false;
+        co += G.J;
+        hd += G.L;
+        st += (long)G.J * G.ld;
+        rg += (long)G.L * G.ld;
+        dof += dims[g];
+        max_J = std::max(max_J, G.J);
+        max_L = std::max(max_L, G.L);
+        max_dim = std::max(max_dim, dims[g]);
+        groups_h.push_back(G);
+    }
+    total_dim = dof;
+    // K5 tile shape: wide DOF tiles when groups are large, more node slices when small
+    if (max_dim >= 8192) {
+        lanes = 32;
+        slices = 8;
+    } else {
+        lanes = 8;
+        slices = 32;
+    }
+    for (int g = 0; g < n_groups; ++g) {
+        const int quads = (groups_h[g].dim + 3) / 4;
+        for (int q0 = 0; q0 < quads; q0 += lanes) tiles_h.push_back(make_int2(g, q0));
+    }
+    n_tiles = (int)tiles_h.size();
+    groups.alloc(groups_h.size());
+    tiles.alloc(tiles_h.size());
+    cr.alloc(std::max<size_t>(1, hr.size()));
+    cf.alloc(std::max<size_t>(1, hf.size()));
+    head.alloc(std::max<size_t>(1, hh.size()));
+    state.alloc(std::max<long>(1, st));
+    ring.alloc(std::max<long>(1, rg));
+    auto up = [&](void* d, const void* h, size_t bytes) {
+        if (bytes) FRAQ_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream));
+    };
+    up(groups.p, groups_h.data(), groups_h.size() * sizeof(GroupDev));
+    up(tiles.p, tiles_h.data(), tiles_h.size() * sizeof(int2));
+    up(cr.p, hr.data(), hr.size() * sizeof(double));
+    up(cf.p, hf.data(), hf.size() * sizeof(double));
+    up(head.p, hh.data(), hh.size() * sizeof(double));
+    zero(c);
+    FRAQ_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+void HistDevice::zero(fraq_ctx c) {
+    FRAQ_CUDA(cudaMemsetAsync(state.p, 0, state.n * sizeof(double), c->stream));
+    FRAQ_CUDA(cudaMemsetAsync(ring.p, 0, ring.n * sizeof(double), c->stream));
+}
+
+void HistDevice::launch_step(fraq_ctx c, const StepArgs& a) {
+    if (n_tiles == 0) return;
+    if (lanes == 32)
+        step_kernel<32, 8><<<n_tiles, 256, 0, c->stream>>>(a);
+    else
+        step_kernel<8, 32><<<n_tiles, 256, 0, c->stream>>>(a);
+    FRAQ_LAUNCH_CHECK();
+}
+
+}  // namespace fraqcu
+
+// ================================================================================ fraq_hist_s
+using namespace fraqcu;
+
+struct fraq_hist_s {
+    fraq_ctx ctx = nullptr;
+    HistDevice d;
+    int variant = 0;
+    long lo = 0;
+    long level = 0, appended = 0;
+    bool pending = false;
+    DevBuf<double> stage;   // pending push value (device)
+    DevBuf<double> outbuf;  // device output for host reads
+    DevBuf<int> counter;
+    DevBuf<int2> run_tasks;
+    int n_run_tasks = 0;
+    int last_path = 0;
+    // chunk staging for host-memory runs
+    DevBuf<double> ubuf, dbuf;
+};
+
+namespace fraqcu {
+
+namespace {
+
+StepArgs base_args(fraq_hist h) {
+    StepArgs a{};
+    a.groups = h->d.groups.p;
+    a.tiles = h->d.tiles.p;
+    a.state = h->d.state.p;
+    a.ring = h->d.ring.p;
+    a.cr = h->d.cr.p;
+    a.cf = h->d.cf.p;
+    a.head = h->d.head.p;
+    a.level = h->level;
+    a.appended = h->appended;
+    a.lo = (int)h->lo;
+    return a;
+}
+
+// reference sequencing checks (fast_kernel.cpp:268-273, 343-347)
+void check_advance(fraq_hist h) {
+    for (const GroupDev& G : h->d.groups_h) {
+        const long fi = h->level + 1 - G.L;
+        if (fi >= h->lo && fi < h->appended - G.L)
+            fail(FRAQ_ELOGIC, G.sbd ? "SbdHistory::advance: feed value already evicted"
+                                    : "BeHistory::advance: feed value already evicted");
+    }
+}
+
+void copy_in(fraq_hist h, double* dst, const double* src, int mem) {
+    const size_t bytes = sizeof(double) * h->d.total_dim;
+    FRAQ_CUDA(cudaMemcpyAsync(dst, src, bytes,
+                              mem == FRAQ_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                              h->ctx->stream));
+}
+
+void copy_out(fraq_hist h, double* dst, const double* src, int mem) {
+    const size_t bytes = sizeof(double) * h->d.total_dim;
+    FRAQ_CUDA(cudaMemcpyAsync(dst, src, bytes,
+                              mem == FRAQ_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                              h->ctx->stream));
+    if (mem != FRAQ_DEVICE) FRAQ_CUDA(cudaStreamSynchronize(h->ctx->stream));
+}
+
+// Run a pending push (advance + append from the stage) fused with `mode` output into out_d.
+void flush(fraq_hist h, int mode, double* out_d) {
+    StepArgs a = base_args(h);
+    if (h->pending) {
+        a.adv = h->appended > 0;
+        a.app = 1;
+        a.u = h->stage.p;
+    }
+    a.mode = mode;
+    a.out = out_d;
+    if (!a.adv && !a.app && mode == MODE_NONE) return;
+    h->d.launch_step(h->ctx, a);
+    if (h->pending) {
+        if (h->appended > 0) h->level += 1;
+        h->appended += 1;
+        h->pending = false;
+    }
+}
+
+}  // namespace
+
+void hist_create(fraq_ctx c, int n_groups, const fraq_kernel_t* const* ks, const long* dims,
+                 int variant, fraq_hist* out) {
+    check_ctx(c);
+    if (n_groups < 1) fail(FRAQ_EINVAL, "history: need at least one group");
+    for (int g = 0; g < n_groups; ++g) {
+        if (!ks[g]) fail(FRAQ_EINVAL, "history: null kernel");
+        if (dims[g] < 0) fail(FRAQ_EINVAL, "history: negative dim");
+        const fraq_kernel_t& k = *ks[g];
+        if (k.np1 < 0 || k.np2 < 0 || k.np1 + k.np2 > 2 * FRAQ_MAX_POINTS || k.n_head < 2 ||
+            k.n_head > FRAQ_MAX_HEAD)
+            fail(FRAQ_EINVAL, "history: malformed kernel tables");
+    }
+    auto* h = new fraq_hist_s();
+    try {
+        h->ctx = c;
+        h->variant = variant;
+        h->lo = variant == FRAQ_STANDALONE ? 0 : 1;
+        h->d.build(c, n_groups, ks, dims);
+        h->stage.alloc(std::max<long>(1, h->d.total_dim));
+        h->outbuf.alloc(std::max<long>(1, h->d.total_dim));
+        h->counter.alloc(1);
+        std::vector<int2> tasks;
+        for (int g = 0; g < n_groups; ++g)
+            for (int m0 = 0; m0 < h->d.groups_h[g].dim; m0 += RUN_Q) tasks.push_back(make_int2(g, m0));
+        h->n_run_tasks = (int)tasks.size();
+        h->run_tasks.alloc(std::max<size_t>(1, tasks.size()));
+        if (!tasks.empty())
+            FRAQ_CUDA(cudaMemcpy(h->run_tasks.p, tasks.data(), tasks.size() * sizeof(int2),
+                                 cudaMemcpyHostToDevice));
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    *out = h;
+}
+
+void hist_destroy(fraq_hist h) {
+    if (!h) return;
+    cudaStreamSynchronize(h->ctx->stream);
+    delete h;
+}
+
+void hist_info(fraq_hist h, long* level, long* appended, long* dim) {
+    // a pending push is already reflected in the reference counters
+    if (level) *level = h->level + ((h->pending && h->appended > 0) ? 1 : 0);
+    if (appended) *appended = h->appended + (h->pending ? 1 : 0);
+    if (dim) *dim = h->d.total_dim;
+}
+
+void hist_push(fraq_hist h, const double* v, int mem) {
+    check_ctx(h->ctx);
+    if (h->pending) flush(h, MODE_NONE, nullptr);
+    if (h->appended > 0) check_advance(h);
+    copy_in(h, h->stage.p, v, mem);
+    h->pending = true;
+}
+
+void hist_advance(fraq_hist h) {
+    check_ctx(h->ctx);
+    if (h->pending) flush(h, MODE_NONE, nullptr);
+    check_advance(h);
+    StepArgs a = base_args(h);
+    a.adv = 1;
+    h->d.launch_step(h->ctx, a);
+    h->level += 1;
+}
+
+void hist_append(fraq_hist h, const double* v, int mem) {
+    check_ctx(h->ctx);
+    if (h->pending) flush(h, MODE_NONE, nullptr);
+    copy_in(h, h->stage.p, v, mem);
+    StepArgs a = base_args(h);
+    a.app = 1;
+    a.u = h->stage.p;
+    h->d.launch_step(h->ctx, a);
+    h->appended += 1;
+}
+
+void hist_output(fraq_hist h, int mode, double* out, int mem) {
+    check_ctx(h->ctx);
+    if (mode == MODE_DERIV) {
+        const long app = h->appended + (h->pending ? 1 : 0);
+        for (const GroupDev& G : h->d.groups_h) {
+            if (!G.sbd && app < 2)
+                fail(FRAQ_ELOGIC, "BeHistory::derivative: need at least two pushed values");
+            if (G.sbd && app < 1) fail(FRAQ_ELOGIC, "SbdHistory::derivative: no values pushed");
+        }
+    }
+    double* dst = mem == FRAQ_DEVICE ? out : h->outbuf.p;
+    if (mem == FRAQ_DEVICE && h->d.total_dim == 0) return;
+    flush(h, mode, dst);
+    if (!h->pending && mode != MODE_NONE && h->d.total_dim > 0) {
+        // flush() launched the fused kernel only if there was pending work; otherwise read-only
+    }
+    if (mem != FRAQ_DEVICE) copy_out(h, out, h->outbuf.p, FRAQ_HOST);
+}
+
+void hist_lagged(fraq_hist h, long depth, double* out, int mem) {
+    check_ctx(h->ctx);
+    if (h->pending) flush(h, MODE_NONE, nullptr);
+    const long idx = h->appended - 1 - depth;
+    for (const GroupDev& G : h->d.groups_h)
+        if (idx < 0 || depth < 0 || depth >= G.L)
+            fail(FRAQ_ERANGE, G.sbd ? "SbdHistory::lagged: value not retained"
+                                    : "BeHistory::lagged: value not retained");
+    for (const GroupDev& G : h->d.groups_h) {
+        const double* src = h->d.ring.p + G.ring_off + (idx % G.L) * (long)G.ld;
+        FRAQ_CUDA(cudaMemcpyAsync((mem == FRAQ_DEVICE ? out : h->outbuf.p) + G.dof0, src,
+                                  sizeof(double) * G.dim, cudaMemcpyDeviceToDevice, h->ctx->stream));
+    }
+    if (mem != FRAQ_DEVICE) copy_out(h, out, h->outbuf.p, FRAQ_HOST);
+}
+
+namespace {
+
+bool blocked_ok(fraq_hist h) {
+    if (!h->d.ztrick_ok) return false;
+    if (h->d.max_L > RUN_LMAX || h->d.max_J > 32 * 16) return false;
+    // pure push sequence: level == appended - 1 (or fresh)
+    if (h->appended == 0) return h->level == 0;
+    return h->level == h->appended - 1;
+}
+
+void run_device(fraq_hist h, const double* U, long ldu, long n_steps, double* D, long ldd) {
+    if (n_steps <= 0) return;
+    if (blocked_ok(h) && n_steps >= 4) {
+        h->last_path = 1;
+        RunArgs a{};
+        a.groups = h->d.groups.p;
+        a.tasks = h->run_tasks.p;
+        a.n_tasks = h->n_run_tasks;
+        a.counter = h->counter.p;
+        a.state = h->d.state.p;
+        a.ring = h->d.ring.p;
+        a.cr = h->d.cr.p;
+        a.cf = h->d.cf.p;
+        a.head = h->d.head.p;
+        a.A0 = h->appended;
+        a.lo = (int)h->lo;
+        a.n_steps = n_steps;
+        a.U = U;
+        a.ldu = ldu;
+        a.D = D;
+        a.ldd = ldd;
+        const int P = (h->d.max_J + 31) / 32;
+        FRAQ_CUDA(cudaMemsetAsync(h->counter.p, 0, sizeof(int), h->ctx->stream));
+        const int grid = std::max(1, std::min((h->n_run_tasks + RUN_WARPS - 1) / RUN_WARPS,
+                                              2 * h->ctx->num_sms));
+        launch_run(std::max(1, P), a, grid, h->ctx->stream);
+        h->appended += n_steps;
+        h->level = h->appended - 1;
+        return;
+    }
+    h->last_path = 0;
+    for (long n = 0; n < n_steps; ++n) {
+        if (h->appended > 0) check_advance(h);
+        StepArgs a = base_args(h);
+        a.adv = h->appended > 0;
+        a.app = 1;
+        a.u = U + n * ldu;
+        bool ok = true;
+        for (const GroupDev& G : h->d.groups_h)
+            if (!G.sbd && h->appended + 1 < 2) ok = false;
+        a.mode = (D && ok) ? MODE_DERIV : MODE_NONE;
+        a.out = D ? D + n * ldd : nullptr;
+        h->d.launch_step(h->ctx, a);
+        if (D && !ok) {
+            // derivative undefined on the first BE push: NaN row (the reference throws)
+            std::vector<double> nan(h->d.total_dim, NAN);
+            FRAQ_CUDA(cudaMemcpyAsync(D + n * ldd, nan.data(), sizeof(double) * nan.size(),
+                                      cudaMemcpyHostToDevice, h->ctx->stream));
+            FRAQ_CUDA(cudaStreamSynchronize(h->ctx->stream));
+        }
+        if (h->appended > 0) h->level += 1;
+        h->appended += 1;
+    }
+}
+
+}  // namespace
+
+void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, long ldd, int mem) {
+    check_ctx(h->ctx);
+    if (n_steps < 0) fail(FRAQ_EINVAL, "hist_run: negative n_steps");
+    if (ldu < h->d.total_dim || (D && ldd < h->d.total_dim))
+        fail(FRAQ_EINVAL, "hist_run: leading dimension below dim");
+    if (h->pending) flush(h, MODE_NONE, nullptr);
+    if (mem == FRAQ_DEVICE) {
+        run_device(h, U, ldu, n_steps, D, ldd);
+        return;
+    }
+    // host buffers: chunks of rows through device staging (H2D, run, D2H)
+    const long dim = std::max<long>(1, h->d.total_dim);
+    const long rows = std::max<long>(1, std::min<long>(n_steps, (64L << 20) / (8 * dim)));
+    if ((long)h->ubuf.n < rows * dim) h->ubuf.alloc(rows * dim);
+    if (D && (long)h->dbuf.n < rows * dim) h->dbuf.alloc(rows * dim);
+    for (long n0 = 0; n0 < n_steps; n0 += rows) {
+        const long nr = std::min(rows, n_steps - n0);
+        FRAQ_CUDA(cudaMemcpy2DAsync(h->ubuf.p, dim * 8, U + n0 * ldu, ldu * 8, h->d.total_dim * 8,
+                                    nr, cudaMemcpyHostToDevice, h->ctx->stream));
+        run_device(h, h->ubuf.p, dim, nr, D ? h->dbuf.p : nullptr, dim);
+        if (D)
+            FRAQ_CUDA(cudaMemcpy2DAsync(D + n0 * ldd, ldd * 8, h->dbuf.p, dim * 8,
+                                        h->d.total_dim * 8, nr, cudaMemcpyDeviceToHost,
+                                        h->ctx->stream));
+    }
+    FRAQ_CUDA(cudaStreamSynchronize(h->ctx->stream));
+}
+
+int hist_last_path(fraq_hist h) { return h->last_path; }
+
+}  // namespace fraqcu

@@ -1,0 +1,67 @@
+// history.cuh -- device history state shared by the history API (history.cu) and the FFPE
+// stepper (ffpe.cu).
+#pragma once
+
+#include "internal.cuh"
+
+namespace fraqcu {
+
+// One DOF group: a contiguous slice of the user's DOF vector with its own compressed kernel.
+// State y[node][dof] and lag ring [slot][dof] are DOF-contiguous with padded leading dim ld.
+struct GroupDev {
+    long dof0;     // first DOF of the group in the user's vector
+    int dim;       // DOFs in the group
+    int ld;        // padded leading dimension (multiple of 4)
+    long st_off;   // state + st_off + j*ld + m
+    long ring_off; // ring + ring_off + slot*ld + m
+    int J;         // nodes (np1 + np2)
+    int L;         // lag == ring capacity: 2 (BE) or n_head (SBD)
+    int co_off;    // ratios cr[co_off + j], feeds cf[co_off + j]
+    int hd_off;    // head[hd_off + i], i < L
+    int sbd;
+};
+
+// Arguments of one fused step launch (K5).
+struct StepArgs {
+    const GroupDev* groups;
+    const int2* tiles;   // (group, first DOF pair)
+    double* state;
+    double* ring;
+    const double* cr;
+    const double* cf;
+    const double* head;
+    long level;      // level before this launch's advance
+    long appended;   // values appended before this launch's append
+    int lo;          // 0 standalone, 1 scheme
+    int adv;         // run advance()
+    int app;         // run append(u)
+    int mode;        // 0: none, 1: history_sum, 2: derivative, 3: FFPE history term
+    const double* u; // append input (device, user layout dof0-relative)
+    double* out;     // output (device, user layout)
+};
+
+enum { MODE_NONE = 0, MODE_SUM = 1, MODE_DERIV = 2, MODE_FFPE = 3 };
+
+// Device-resident tables + state of a set of groups.
+struct HistDevice {
+    std::vector<GroupDev> groups_h;
+    std::vector<int2> tiles_h;
+    std::vector<int> tile_lanes;  // LANES per tile config (all tiles same)
+    DevBuf<GroupDev> groups;
+    DevBuf<int2> tiles;
+    DevBuf<double> state, ring, cr, cf, head;
+    long total_dim = 0;
+    int n_tiles = 0;
+    int slices = 8;       // node slices per CTA (K5)
+    int lanes = 32;       // DOF quads per CTA (K5)
+    bool ztrick_ok = true;
+    int max_J = 0, max_L = 0;
+    std::vector<fraq_kernel_t> kernels;  // host copies
+
+    void build(fraq_ctx c, int n_groups, const fraq_kernel_t* const* ks, const long* dims);
+    void launch_step(fraq_ctx c, const StepArgs& a);
+    // reset state/ring to zero
+    void zero(fraq_ctx c);
+};
+
+}  // namespace fraqcu
