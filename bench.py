@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 fast-CQ path on BASELINE.json's headline configuration (configs[1], C2).
+
+Workload C2: batched Riemann-Liouville derivative with the BDF2 (SBD) fast CQ, 65536 DOFs per GPU
+(CQ exponent 0.7 on the first half, 0.3 on the second), tau = 1/65536, reference auto-sized
+kernels (256 + 256 nodes, N_s = 17 / 15).  Signals u_k(t) = a_k t^b_k + c_k sin(w_k t), seeded
+(paper_1901_05128_b200/workloads.py), generated on the device before timing.
+
+One bench step = one pass of the hot path over the batch for LEVELS_PER_STEP (512) time levels:
+push + derivative for every DOF at every level, through SbdHistory.run on device buffers
+(temporally blocked kernel K5b).  K timed steps advance a fresh history from level 0; the default
+K = 128 covers the whole C2 horizon N = 65536.  Warm-up steps run on a separate history.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Prints one JSON line (rank 0).  --impl reference times the reference's own CPU implementation
+(oracle/_ref: the unmodified reference sources) on the host cores with the same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fast-CQ DOF-steps/s (fp64) and % of HBM roofline at 1/2/4/8 B200 vs CPU"
+UNIT = "DOF-steps/s"
+LEVELS_PER_STEP = 512
+DOFS = 65536
+N_LEVELS = 65536
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "fallback": True}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ----------------------------------------------------------------------------- clocks sampling
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 7 and f[0].isdigit():
+                rows.append(f)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[3:7]) if v == "Active"})
+        return {"sm_mhz": statistics.median(int(r[0]) for r in rows),
+                "sm_max_mhz": int(rows[0][1]), "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def reference_kernels(orc, tau):
+    """The reference's own auto-sized C2 kernels (fast_kernel.cpp:207-256), horizon N."""
+    return [orc.build_kernel_auto(True, 1.0 - 0.3, tau, N_LEVELS),
+            orc.build_kernel_auto(True, 1.0 - 0.7, tau, N_LEVELS)]
+
+
+def cpu_sample(orc, kernels, params, threads, target_s):
+    """Times the reference SbdHistory (push + derivative per level) on a DOF sample drawn from
+    both exponent halves, `threads` host threads.  Returns (DOF-steps/s, sample description)."""
+    per_group = max(64, 64 * threads // 2)
+    idx = np.concatenate([np.arange(per_group), DOFS // 2 + np.arange(per_group)])
+    # calibrate on 32 levels, then size the sample to ~target_s seconds
+    U = params.signal(0, 32, idx)
+    secs, _ = orc.bench_history(kernels, U, threads)
+    rate = 2 * per_group * 32 / max(secs, 1e-6)
+    levels = int(min(max(64, target_s * rate / (2 * per_group)), 16384))
+    U = params.signal(0, levels, idx)
+    secs, _ = orc.bench_history(kernels, U, threads)
+    dof_steps = 2 * per_group * levels
+    return dof_steps / secs, f"{2 * per_group} DOFs (both exponent halves) x {levels} levels", secs
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle.oracle import Oracle, ref_available
+    from paper_1901_05128_b200.workloads import c2_params
+    if not ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    orc = Oracle("reference")
+    params = c2_params()
+    kernels = reference_kernels(orc, params.tau)
+    threads = os.cpu_count() or 1
+    target = 1.0  # seconds of CPU work per step
+    for _ in range(args.warmup):
+        cpu_sample(orc, kernels, params, threads, target / 4)
+    vals, times = [], []
+    for _ in range(args.steps):
+        v, sample, secs = cpu_sample(orc, kernels, params, threads, target)
+        vals.append(v)
+        times.append(secs)
+    value = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2 (BDF2 fast CQ, 65536 DOFs, gamma 0.7 | 0.3, N = 65536)",
+                   "dofs_per_gpu": DOFS, "levels_per_step": LEVELS_PER_STEP},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": sample + " per step; reference SbdHistory push+derivative, "
+                                            "per-thread DOF slices (bench.cpp:194-223 pattern)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=N_LEVELS // LEVELS_PER_STEP)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    os.environ.setdefault("FRAQ_DEVICE", str(local))
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    import paper_1901_05128_b200 as fraq
+    from paper_1901_05128_b200.workloads import c2_params
+
+    params = c2_params(DOFS)
+    tau = params.tau
+    # device setup (K1-K4): auto-sized kernels for both exponents, as the reference picks them
+    t0 = time.time()
+    kernels = []
+    for g in (1.0 - 0.3, 1.0 - 0.7):
+        b = fraq.KernelBudget(horizon=N_LEVELS, eps_tol=1e-12)
+        kernels.append((fraq.build_sbd_kernel_auto(g, tau, b), b.achieved_eps))
+    setup_s = time.time() - t0
+    ks = [k for k, _ in kernels]
+    n_nodes = [len(k.ratio1) + len(k.ratio2) for k in ks]
+    n_head = [k.n_head for k in ks]
+
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.ExternalStream(fraq.context_stream())
+    # signals for the timed levels, generated on the device (rank-specific DOFs: weak scaling)
+    K, W = args.steps, args.warmup
+    levels = K * LEVELS_PER_STEP
+    gen = torch.Generator(device="cpu").manual_seed(1901051282 + rank)
+    if rank == 0:
+        a = torch.from_numpy(params.a); bb = torch.from_numpy(params.b)
+        c = torch.from_numpy(params.c); w = torch.from_numpy(params.w)
+    else:
+        a = torch.randn(DOFS, generator=gen, dtype=torch.float64)
+        c = torch.randn(DOFS, generator=gen, dtype=torch.float64)
+        bb = 0.1 + 1.9 * torch.rand(DOFS, generator=gen, dtype=torch.float64)
+        w = 1.0 + 19.0 * torch.rand(DOFS, generator=gen, dtype=torch.float64)
+    a, bb, c, w = (x.to(dev) for x in (a, bb, c, w))
+    U = torch.empty((levels, DOFS), dtype=torch.float64, device=dev)
+    for n0 in range(0, levels, 1024):
+        n1 = min(levels, n0 + 1024)
+        t = (torch.arange(n0, n1, device=dev, dtype=torch.float64) * tau)[:, None]
+        U[n0:n1] = a * torch.pow(t, bb) + c * torch.sin(w * t)
+    D = torch.empty_like(U)
+    Uw = U[:LEVELS_PER_STEP].clone()
+    Dw = torch.empty_like(Uw)
+    torch.cuda.synchronize()
+
+    # warm-up on a scratch history
+    hw = fraq.MultiHistory(ks, [DOFS // 2, DOFS - DOFS // 2])
+    for _ in range(W):
+        hw.run_device(Uw.data_ptr(), DOFS, LEVELS_PER_STEP, Dw.data_ptr(), DOFS)
+    fraq.synchronize()
+    del hw
+
+    h = fraq.MultiHistory(ks, [DOFS // 2, DOFS - DOFS // 2])
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        ev[0].record(stream)
+        for s in range(K):
+            off = s * LEVELS_PER_STEP * DOFS * 8
+            h.run_device(U.data_ptr() + off, DOFS, LEVELS_PER_STEP, D.data_ptr() + off, DOFS)
+            ev[s + 1].record(stream)
+        ev[K].synchronize()
+        torch.cuda.synchronize()
+    assert h.last_path == 1, "blocked kernel K5b did not run"
+    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(K)]
+    total_ms = ev[0].elapsed_time(ev[K])
+    t_local = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if pg:
+        pg.all_reduce(t_local, op=pg.ReduceOp.MAX)
+    total_ms = float(t_local.item())
+    dof_steps_local = DOFS * LEVELS_PER_STEP * K
+    value = world * dof_steps_local / (total_ms * 1e-3)
+
+    # sanity: outputs finite after the first level
+    assert torch.isfinite(D[1:LEVELS_PER_STEP * K]).all().item()
+
+    # roofline of the dominant kernel (K5b): fp64 FMA bound; algorithmic flops per DOF-step
+    # F = 4 N_nodes + 2 N_head, averaged over the two exponent halves
+    F = 0.5 * sum(4 * nn + 2 * hh for nn, hh in zip(n_nodes, n_head))
+    achieved_tf = F * dof_steps_local / (total_ms * 1e-3) / 1e12
+    fp64_peak = fraq.diag_fp64_peak()
+    # HBM figures: algorithmic bytes of one state pass per level, B = 8 (2 N_nodes + 2)
+    B = 0.5 * sum(8 * (2 * nn + 2) for nn in n_nodes)
+    pk = peaks()
+
+    # per-level fused kernel K5 (one HBM pass over the state per level) on the same workload
+    hs = fraq.MultiHistory(ks, [DOFS // 2, DOFS - DOFS // 2])
+    nstep = 24
+    hs.run_device(U.data_ptr(), DOFS, 3, D.data_ptr(), DOFS)  # level 0..2 via K5b (n_steps < 4)
+    torch.cuda.synchronize()
+    # force the per-level path: push/derivative on device pointers level by level
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for n in range(3, 3 + nstep):
+        hs.run_device(U.data_ptr() + n * DOFS * 8, DOFS, 1, D.data_ptr() + n * DOFS * 8, DOFS)
+    e1.record(stream)
+    e1.synchronize()
+    assert hs.last_path == 0
+    step_level_ms = e0.elapsed_time(e1) / nstep
+    hbm_step = B * DOFS / (step_level_ms * 1e-3) / 1e9
+    del hs
+
+    # e2e: the same metric through the C-ABI call with HOST buffers (pinned), copies inside
+    ke = max(1, min(args.e2e_steps, K))
+    Uh = U[:ke * LEVELS_PER_STEP].cpu().pin_memory()
+    Dh = torch.empty_like(Uh).pin_memory()
+    he = fraq.MultiHistory(ks, [DOFS // 2, DOFS - DOFS // 2])
+    torch.cuda.synchronize()
+    t_e = time.perf_counter()
+    for s in range(ke):
+        rows = slice(s * LEVELS_PER_STEP, (s + 1) * LEVELS_PER_STEP)
+        # host in, host out: H2D + K5b + D2H inside fraq_hist_run (pinned buffers)
+        he.run(Uh[rows].numpy(), True, Dh[rows].numpy())
+    e2e_s = time.perf_counter() - t_e
+    del he
+    e2e_val = world * DOFS * LEVELS_PER_STEP * ke / e2e_s
+    step_bytes = LEVELS_PER_STEP * DOFS * 8
+
+    # CPU baseline: the reference (oracle/_ref) on the host cores, rank 0 only, bounded sample
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            from oracle.oracle import Oracle, ref_available
+            kind = "reference" if ref_available() else "port"
+            orc = Oracle(kind)
+            rk = reference_kernels(orc, tau)
+            threads = os.cpu_count() or 1
+            v, sample, secs = cpu_sample(orc, rk, params, threads, 15.0)
+            cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
+                   "sample": sample + f" ({secs:.1f} s), reference SbdHistory push+derivative"}
+        except Exception as e:  # report, never fake
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": total_ms / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": "C2: BDF2 fast CQ, 65536 DOFs per GPU (gamma 0.7 | 0.3), tau = 1/65536,"
+                            " N = 65536 levels; one step = 512 levels x all DOFs (push+derivative)",
+                "dofs_per_gpu": DOFS, "levels_per_step": LEVELS_PER_STEP,
+                "nodes": n_nodes, "n_head": n_head,
+                "kernel_eps": [e for _, e in kernels],
+                "path": "SbdHistory.run on device buffers -> K5b (temporally blocked, fp64)",
+                "l2": "inputs larger than L2 (268 MB of signal per step)",
+                "parallelism": f"dof-sharded x{world}, no data-path collective",
+                "setup_s": setup_s},
+            "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": fp64_peak,
+                         "unit": "TFLOP/s", "frac": achieved_tf / fp64_peak, "traffic": None,
+                         "peak_source": "measured DFMA stream (fraq_diag_fp64_peak)",
+                         "flops_per_dof_step": F, "kernel": "run_kernel (K5b)",
+                         "hbm_equiv_gbs": B * dof_steps_local / (total_ms * 1e-3) / 1e9},
+            "roofline_step_kernel": {"bound": "hbm", "achieved": hbm_step,
+                                     "peak": pk.get("hbm_gbs"), "unit": "GB/s",
+                                     "frac": hbm_step / pk.get("hbm_gbs"),
+                                     "bytes_per_dof_step": B, "kernel": "step_kernel (K5)",
+                                     "ms_per_level": step_level_ms,
+                                     "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": step_bytes,
+                    "d2h_bytes_per_step": step_bytes, "steps": ke,
+                    "path": "MultiHistory.run(host numpy) -> fraq_hist_run(FRAQ_HOST)"},
+            "gpu_launches": K,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "step_ms_min_max": [min(step_ms), max(step_ms)],
+        }
+        print(json.dumps(line), flush=True)
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

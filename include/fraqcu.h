@@ -187,6 +187,11 @@ int fraq_run_observed(fraq_ctx ctx, const fraq_spec_t* spec, int scheme,
                       const fraq_kconf_t* kconf, fraq_observer_fn fn, void* user, double* g1,
                       double* g2, fraq_run_info_t* info);
 
+/* ---------------------------------------------------------------- diagnostics
+ * Measured fp64 FMA throughput of the context's GPU (TFLOP/s, 2 flops per DFMA): the roofline
+ * denominator of the fp64-bound temporally blocked history kernel. */
+int fraq_diag_fp64_peak(fraq_ctx ctx, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif

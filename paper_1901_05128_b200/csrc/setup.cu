@@ -111,12 +111,14 @@ __global__ void __launch_bounds__(kRuleThreads) rule_kernel(const RuleJob* jobs)
     const int i = threadIdx.x;
     if (i >= n) return;
     // Sturm count: number of eigenvalues < x (LDL^T pivots, guarded against zero pivots).
+    // (a zero pivot is replaced by -tiny and counted as negative, LAPACK dstebz style)
     auto count_below = [&](double x) {
         double q = s_al[0] - x;
+        if (q == 0.0) q = -1e-300;
         int cnt = q < 0.0;
         for (int k = 1; k < n; ++k) {
-            if (q == 0.0) q = -1e-300;
             q = (s_al[k] - x) - s_be[k] / q;
+            if (q == 0.0) q = -1e-300;
             cnt += q < 0.0;
         }
         return cnt;
