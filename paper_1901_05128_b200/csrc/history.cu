@@ -59,7 +59,7 @@ __device__ __forceinline__ void fma4(d4& acc, double h, const d4& x) {
 // of its 4 DOFs with 256-bit loads/stores; slice partial sums meet in shared memory; slice 0
 // finishes (append into the ring, exact head window, output).
 template <int LANES, int S>
-__global__ void __launch_bounds__(LANES* S) step_kernel(StepArgs A) {
+__global__ void __launch_bounds__(LANES* S, 6) step_kernel(StepArgs A) {
     const int2 tile = A.tiles[blockIdx.x];
     const GroupDev G = A.groups[tile.x];
     const int lane = threadIdx.x % LANES;
@@ -81,8 +81,29 @@ __global__ void __launch_bounds__(LANES* S) step_kernel(StepArgs A) {
         const double* __restrict__ cf = A.cf + G.co_off;
         double* base = A.state + G.st_off + m;
         if (A.adv) {
-#pragma unroll 4
-            for (int j = sl; j < G.J; j += S) {
+            // NB independent 256-bit loads in flight per thread before any store (the stores
+            // are volatile asm, so loads are batched explicitly rather than left to the scheduler)
+            constexpr int NB = 4;
+            int j = sl;
+            for (; j + (NB - 1) * S < G.J; j += NB * S) {
+                d4 y[NB];
+#pragma unroll
+                for (int b = 0; b < NB; ++b) y[b] = ld_stream(base + (j + b * S) * ld);
+#pragma unroll
+                for (int b = 0; b < NB; ++b) {
+                    const double r = __ldg(cr + j + b * S), f = __ldg(cf + j + b * S);
+                    y[b].x = fma(r, y[b].x, f * v.x);
+                    y[b].y = fma(r, y[b].y, f * v.y);
+                    y[b].z = fma(r, y[b].z, f * v.z);
+                    y[b].w = fma(r, y[b].w, f * v.w);
+                    st_stream(base + (j + b * S) * ld, y[b]);
+                    acc.x += y[b].x;
+                    acc.y += y[b].y;
+                    acc.z += y[b].z;
+                    acc.w += y[b].w;
+                }
+            }
+            for (; j < G.J; j += S) {
                 double* p = base + j * ld;
                 d4 y = ld_stream(p);
                 const double r = __ldg(cr + j), f = __ldg(cf + j);
@@ -277,27 +298,30 @@ __global__ void __launch_bounds__(RUN_WARPS * 32, 2) run_kernel(RunArgs A) {
             }
             __syncwarp();
             const int tmax = (int)min((long)RUN_TC, A.n_steps - c0);
-            for (int t = 0; t < tmax; ++t) {
-                const long n = A.A0 + c0 + t;
+            int t = 0;
+            // single level (odd tails and the very first push of a fresh history, which does not
+            // advance: fast_kernel.cpp:297-300)
+            auto one_level = [&](int tt) {
+                const long n = A.A0 + c0 + tt;
                 if (n >= 1) {  // advance to level n; feed X(n - L) when n - L >= lo
                     const bool feed = n - L >= A.lo;
                     double v[RUN_Q];
 #pragma unroll
-                    for (int q = 0; q < RUN_Q; ++q) v[q] = feed ? sm.X[RUN_LMAX + t - L][q] : 0.0;
+                    for (int q = 0; q < RUN_Q; ++q) v[q] = feed ? sm.X[RUN_LMAX + tt - L][q] : 0.0;
 #pragma unroll
                     for (int p = 0; p < P; ++p)
 #pragma unroll
                         for (int q = 0; q < RUN_Q; ++q) z[p][q] = fma(r[p], z[p][q], v[q]);
                 }
-                double s[RUN_Q] = {0.0, 0.0, 0.0, 0.0};
+                double sq[RUN_Q] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
                 for (int p = 0; p < P; ++p)
 #pragma unroll
-                    for (int q = 0; q < RUN_Q; ++q) s[q] = fma(f[p], z[p][q], s[q]);
+                    for (int q = 0; q < RUN_Q; ++q) sq[q] = fma(f[p], z[p][q], sq[q]);
                 // reduce-scatter 4 values over 32 lanes -> lanes 8q..8q+7 hold DOF q's total
                 const bool up = lane & 16;
-                double a0 = up ? s[2] : s[0], a1 = up ? s[3] : s[1];
-                const double b0 = up ? s[0] : s[2], b1 = up ? s[1] : s[3];
+                double a0 = up ? sq[2] : sq[0], a1 = up ? sq[3] : sq[1];
+                const double b0 = up ? sq[0] : sq[2], b1 = up ? sq[1] : sq[3];
                 a0 += __shfl_xor_sync(0xffffffffu, b0, 16);
                 a1 += __shfl_xor_sync(0xffffffffu, b1, 16);
                 const bool up8 = lane & 8;
@@ -310,9 +334,63 @@ __global__ void __launch_bounds__(RUN_WARPS * 32, 2) run_kernel(RunArgs A) {
                 if ((lane & 7) == 0) {
                     const int q = lane >> 3;
                     const bool valid = G.sbd ? true : (n >= 1);
-                    sm.Dv[t][q] = valid ? cval + sm.F[t][q] : __longlong_as_double(0x7ff8000000000000LL);
+                    sm.Dv[tt][q] = valid ? cval + sm.F[tt][q] : __longlong_as_double(0x7ff8000000000000LL);
+                }
+            };
+            if (A.A0 + c0 == 0) {  // level 0 of a fresh history: no advance
+                one_level(0);
+                t = 1;
+            }
+            // main loop: two levels per iteration (all advance).  Both node sums are reduced
+            // together (8-value reduce-scatter, 9 fp64 shuffles per pair) so the shuffle latency
+            // of one pair overlaps the FMAs of the next in the other warps and in this one.
+            for (; t + 1 < tmax; t += 2) {
+                const long n = A.A0 + c0 + t;
+                const bool feed0 = n - L >= A.lo, feed1 = n + 1 - L >= A.lo;
+                double v0[RUN_Q], v1[RUN_Q];
+#pragma unroll
+                for (int q = 0; q < RUN_Q; ++q) {
+                    v0[q] = feed0 ? sm.X[RUN_LMAX + t - L][q] : 0.0;
+                    v1[q] = feed1 ? sm.X[RUN_LMAX + t + 1 - L][q] : 0.0;
+                }
+                double s0[RUN_Q] = {0.0, 0.0, 0.0, 0.0}, s1[RUN_Q] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int p = 0; p < P; ++p)
+#pragma unroll
+                    for (int q = 0; q < RUN_Q; ++q) {
+                        const double z0 = fma(r[p], z[p][q], v0[q]);
+                        s0[q] = fma(f[p], z0, s0[q]);
+                        const double z1 = fma(r[p], z0, v1[q]);
+                        s1[q] = fma(f[p], z1, s1[q]);
+                        z[p][q] = z1;
+                    }
+                // value k = 4 t2 + q; after the cascade lane holds k = lane >> 2
+                const bool u16 = lane & 16;
+                double a[RUN_Q];
+#pragma unroll
+                for (int q = 0; q < RUN_Q; ++q) {
+                    const double keep = u16 ? s1[q] : s0[q];
+                    const double send = u16 ? s0[q] : s1[q];
+                    a[q] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+                }
+                const bool u8 = lane & 8;
+                double b[2];
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const double keep = u8 ? a[i + 2] : a[i];
+                    const double send = u8 ? a[i] : a[i + 2];
+                    b[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                }
+                const bool u4 = lane & 4;
+                double cval = (u4 ? b[1] : b[0]) + __shfl_xor_sync(0xffffffffu, u4 ? b[0] : b[1], 4);
+                cval += __shfl_xor_sync(0xffffffffu, cval, 2);
+                cval += __shfl_xor_sync(0xffffffffu, cval, 1);
+                if ((lane & 3) == 0) {
+                    const int k = lane >> 2, tt = t + (k >> 2), q = k & 3;
+                    sm.Dv[tt][q] = cval + sm.F[tt][q];
                 }
             }
+            if (t < tmax) one_level(t);
             __syncwarp();
             if (A.D && lane < tmax) {
                 double* drow = A.D + (c0 + lane) * A.ldd + G.dof0 + m0;
@@ -428,12 +506,13 @@ void HistDevice::build(fraq_ctx c, int n_groups, const fraq_kernel_t* const* ks,
     }
     total_dim = dof;
     // K5 tile shape: wide DOF tiles when groups are large, more node slices when small
+    // (large groups: 128-thread CTAs, 6 resident per SM -> the C2 grid (512 CTAs) is one wave)
     if (max_dim >= 8192) {
         lanes = 32;
-        slices = 8;
+        slices = 4;
     } else {
         lanes = 8;
-        slices = 32;
+        slices = 16;
     }
     for (int g = 0; g < n_groups; ++g) {
         const int quads = (groups_h[g].dim + 3) / 4;
@@ -467,9 +546,9 @@ void HistDevice::zero(fraq_ctx c) {
 void HistDevice::launch_step(fraq_ctx c, const StepArgs& a) {
     if (n_tiles == 0) return;
     if (lanes == 32)
-        step_kernel<32, 8><<<n_tiles, 256, 0, c->stream>>>(a);
+        step_kernel<32, 4><<<n_tiles, 128, 0, c->stream>>>(a);
     else
-        step_kernel<8, 32><<<n_tiles, 256, 0, c->stream>>>(a);
+        step_kernel<8, 16><<<n_tiles, 128, 0, c->stream>>>(a);
     FRAQ_LAUNCH_CHECK();
 }
 

@@ -52,7 +52,7 @@ struct HistDevice {
     DevBuf<double> state, ring, cr, cf, head;
     long total_dim = 0;
     int n_tiles = 0;
-    int slices = 8;       // node slices per CTA (K5)
+    int slices = 4;       // node slices per CTA (K5)
     int lanes = 32;       // DOF quads per CTA (K5)
     bool ztrick_ok = true;
     int max_J = 0, max_L = 0;
