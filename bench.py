@@ -239,7 +239,7 @@ def main():
             ev[s + 1].record(stream)
         ev[K].synchronize()
         torch.cuda.synchronize()
-    assert h.last_path == 1, "blocked kernel K5b did not run"
+    assert h.last_path >= 1, "temporally blocked kernel did not run"
     step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(K)]
     total_ms = ev[0].elapsed_time(ev[K])
     t_local = torch.tensor([total_ms], dtype=torch.float64, device=dev)

@@ -168,7 +168,8 @@ int fraq_hist_lagged(fraq_hist h, long depth, double* out, int mem);
  * temporally blocked kernel K5b (history kept on chip across the whole call). */
 int fraq_hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, long ldd,
                   int mem);
-/* Which kernel the last fraq_hist_run used: 1 = K5b temporally blocked, 0 = per-step K5. */
+/* Which kernel the last fraq_hist_run used: 0 = per-level K5, 1 = K5b (warp-per-4-DOF blocked,
+ * legacy, FRAQ_K5B=1), 2 = K5c (lane-per-DOF blocked, default). */
 int fraq_hist_last_path(fraq_hist h);
 
 /* ---------------------------------------------------------------- L4 FFPE
@@ -191,6 +192,8 @@ int fraq_run_observed(fraq_ctx ctx, const fraq_spec_t* spec, int scheme,
  * Measured fp64 FMA throughput of the context's GPU (TFLOP/s, 2 flops per DFMA): the roofline
  * denominator of the fp64-bound temporally blocked history kernel. */
 int fraq_diag_fp64_peak(fraq_ctx ctx, double* tflops);
+/* fp64 tensor-core (DMMA) throughput: tflops[0] alone, tflops[1] DMMA + DFMA interleaved. */
+int fraq_diag_dmma_peak(fraq_ctx ctx, double* tflops);
 
 #ifdef __cplusplus
 }

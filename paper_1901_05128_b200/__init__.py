@@ -58,6 +58,7 @@ EXTRA = [
     "build_be_kernel_auto",
     "build_sbd_kernel_auto",
     "context_stream",
+    "diag_dmma_peak",
     "diag_fp64_peak",
     "gamma_fn",
     "make_be_kernel",

@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -454,6 +455,221 @@ void launch_run(int P, const RunArgs& a, int grid, cudaStream_t s) {
     FRAQ_LAUNCH_CHECK();
 }
 
+// ----------------------------------------------------------------------------------------- K5c
+// Temporally blocked evaluation, B200 mapping: lane = DOF (32 consecutive DOFs per CTA), warp w
+// owns nodes j = 32 w + p (p < 32), levels processed in register blocks of 8.  Per node the 8
+// levels run back to back on one register (z <- r z + v_k; s_k += f z): 16 DFMA per pair of
+// broadcast shared-memory loads (r_j, f_j), no shuffles.  The node sum crosses warps once per
+// block through shared memory (double-buffered partials, one barrier per 8 levels).  State is kept
+// as z = y / f (two DFMA per node and level); inputs stream through a 32-level chunk window.
+constexpr int R2_TC = 32;      // levels per staged chunk
+constexpr int R2_TB = 8;       // levels per register block
+constexpr int R2_P = 32;       // nodes per warp
+constexpr int R2_LMAX = 64;    // max lag on this path
+constexpr int R2_MAXW = 16;    // max warps (512 nodes)
+
+__host__ __device__ inline size_t run2_smem_bytes(int nw) {
+    return sizeof(double) * ((size_t)(R2_LMAX + R2_TC) * 32 + R2_TC * 32 + 2 * 512 + R2_LMAX +
+                             (size_t)2 * nw * R2_TB * 32) + 16;
+}
+
+__global__ void __launch_bounds__(R2_MAXW * 32, 1) run2_kernel(RunArgs A) {
+    extern __shared__ double sm2[];
+    const int nw = blockDim.x >> 5;
+    double(*X)[32] = reinterpret_cast<double(*)[32]>(sm2);                  // [LMAX+TC][32]
+    double(*F)[32] = reinterpret_cast<double(*)[32]>(sm2 + (R2_LMAX + R2_TC) * 32);  // [TC][32]
+    double* cr = sm2 + (R2_LMAX + 2 * R2_TC) * 32;
+    double* cf = cr + 512;
+    double* hd = cf + 512;
+    double* part = hd + R2_LMAX;                                            // [2][nw][TB][32]
+    __shared__ int s_task;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) s_task = atomicAdd(A.counter, 1);
+        __syncthreads();
+        const int task = s_task;
+        if (task >= A.n_tasks) return;
+        const int2 tk = A.tasks[task];
+        const GroupDev G = A.groups[tk.x];
+        const int m = tk.y + lane;  // this lane's DOF within the group
+        const bool live = m < G.dim;
+        const int L = G.L, J = G.J;
+        const long ld = G.ld;
+        for (int j = tid; j < 512; j += blockDim.x) {
+            cr[j] = j < J ? A.cr[G.co_off + j] : 0.0;
+            cf[j] = j < J ? A.cf[G.co_off + j] : 0.0;
+        }
+        for (int i = tid; i < R2_LMAX; i += blockDim.x) hd[i] = i < L ? A.head[G.hd_off + i] : 0.0;
+        // initial state z = y / f for this warp's nodes
+        double z[R2_P];
+#pragma unroll
+        for (int p = 0; p < R2_P; ++p) {
+            const int j = warp * R2_P + p;
+            z[p] = 0.0;
+            if (j < J && live) {
+                const double f = A.cf[G.co_off + j];
+                z[p] = A.state[G.st_off + j * ld + m] / f;
+            }
+        }
+        // lag window: X(k), k in [A0 - L, A0 - 1], rows R2_LMAX - L .. R2_LMAX - 1
+        for (int idx = tid; idx < L * 32; idx += blockDim.x) {
+            const int row = idx >> 5, d = idx & 31;
+            const long k = A.A0 - L + row;
+            double x = 0.0;
+            if (k >= 0 && tk.y + d < G.dim) x = A.ring[G.ring_off + (k % L) * ld + tk.y + d];
+            X[R2_LMAX - L + row][d] = x;  // negative times read as zero
+        }
+        const double* Ub = A.U + G.dof0 + tk.y;
+        // chunk prefetch: thread handles rows (tid >> 5) + 16 i, DOF lane  (32 rows x 32 DOFs)
+        double pre[2];
+        auto load_chunk = [&](long c0) {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int row = warp + R2_MAXW * i;
+                const long t = c0 + row;
+                pre[i] = (row < R2_TC && t < A.n_steps && live) ? Ub[t * A.ldu + lane] : 0.0;
+            }
+        };
+        load_chunk(0);
+        int buf = 0, last_tmax = 0;
+        for (long c0 = 0; c0 < A.n_steps; c0 += R2_TC) {
+            const int tmax = (int)min((long)R2_TC, A.n_steps - c0);
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int row = warp + R2_MAXW * i;
+                if (row < R2_TC) X[R2_LMAX + row][lane] = pre[i];
+            }
+            if (nw < R2_MAXW) {  // fewer than 16 warps: remaining rows loaded directly
+                for (int row = warp + nw; row < R2_TC; row += nw)
+                    if (row >= R2_MAXW * 2 || (row % R2_MAXW) >= nw) {
+                        const long t = c0 + row;
+                        X[R2_LMAX + row][lane] =
+                            (t < A.n_steps && live) ? Ub[t * A.ldu + lane] : 0.0;
+                    }
+            }
+            if (c0 + R2_TC < A.n_steps) load_chunk(c0 + R2_TC);
+            __syncthreads();
+            for (int t0 = 0; t0 < tmax; t0 += R2_TB) {
+                const long n0 = A.A0 + c0 + t0;
+                const int kmax = min(R2_TB, tmax - t0);
+                double* pb = part + (size_t)buf * nw * R2_TB * 32;
+                // the scheme variant must not feed G(t_0) (level n = L, lo = 1): partial path
+                const bool special = A.lo == 1 && n0 <= L && L < n0 + R2_TB;
+                if (kmax == R2_TB && n0 >= 1 && !special) {
+                    // full block: every level advances; feeds X(n - L) (negative times are zero)
+                    double v[R2_TB], sacc[R2_TB];
+#pragma unroll
+                    for (int k = 0; k < R2_TB; ++k) {
+                        v[k] = X[R2_LMAX + t0 + k - L][lane];
+                        sacc[k] = 0.0;
+                    }
+                    const double* crw = cr + warp * R2_P;
+                    const double* cfw = cf + warp * R2_P;
+#pragma unroll
+                    for (int p0 = 0; p0 < R2_P; p0 += 4) {
+                        double rr[4], ff[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            rr[i] = crw[p0 + i];
+                            ff[i] = cfw[p0 + i];
+                        }
+#pragma unroll
+                        for (int k = 0; k < R2_TB; ++k)
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                z[p0 + i] = fma(rr[i], z[p0 + i], v[k]);
+                                sacc[k] = fma(ff[i], z[p0 + i], sacc[k]);
+                            }
+                    }
+#pragma unroll
+                    for (int k = 0; k < R2_TB; ++k) pb[(warp * R2_TB + k) * 32 + lane] = sacc[k];
+                } else {
+                    // partial block (chunk tail, or level 0 of a fresh history: no advance)
+                    for (int k = 0; k < kmax; ++k) {
+                        const long n = n0 + k;
+                        double sk = 0.0;
+                        if (n >= 1) {
+                            const double vk = (n - L >= A.lo) ? X[R2_LMAX + t0 + k - L][lane] : 0.0;
+#pragma unroll
+                            for (int p = 0; p < R2_P; ++p) {
+                                z[p] = fma(cr[warp * R2_P + p], z[p], vk);
+                                sk = fma(cf[warp * R2_P + p], z[p], sk);
+                            }
+                        } else {
+#pragma unroll
+                            for (int p = 0; p < R2_P; ++p) sk = fma(cf[warp * R2_P + p], z[p], sk);
+                        }
+                        pb[(warp * R2_TB + k) * 32 + lane] = sk;
+                    }
+                }
+                __syncthreads();
+                // cross-warp node sum + head window -> D rows (coalesced over the 32 DOFs)
+                // cross-warp node sum + exact head window sum_{i<=top(n)} h_i X(n-i) -> D
+                for (int idx = tid; A.D && idx < kmax * 32; idx += blockDim.x) {
+                    const int k = idx >> 5, d = idx & 31;
+                    const long n = n0 + k;
+                    const long top = G.sbd ? min((long)L - 1, n - A.lo) : 1;
+                    double fir = 0.0;
+                    for (long i = 0; i <= top; ++i)
+                        fir = fma(hd[i], X[R2_LMAX + t0 + k - i][d], fir);
+                    double sum = 0.0;
+                    for (int w = 0; w < nw; ++w) sum += pb[(w * R2_TB + k) * 32 + d];
+                    const bool valid = G.sbd ? true : (n >= 1);
+                    if (tk.y + d < G.dim)
+                        A.D[(c0 + t0 + k) * A.ldd + G.dof0 + tk.y + d] = valid ? sum + fir : qnan;
+                }
+                buf ^= 1;
+            }
+            last_tmax = tmax;
+            if (c0 + R2_TC < A.n_steps) {
+                // slide (full chunk, tmax = 32): rows R2_LMAX + 32 - L .. -> R2_LMAX - L .., in
+                // 32-row phases so sources are read before they are overwritten (L <= 64)
+                for (int base = 0; base < L; base += R2_TC) {
+                    __syncthreads();
+                    for (int idx = tid; idx < R2_TC * 32; idx += blockDim.x) {
+                        const int r = base + (idx >> 5);
+                        if (r < L) X[R2_LMAX - L + r][idx & 31] = X[R2_LMAX - L + r + R2_TC][idx & 31];
+                    }
+                }
+            }
+        }
+        // write back y = f z and the ring (last L inputs)
+#pragma unroll
+        for (int p = 0; p < R2_P; ++p) {
+            const int j = warp * R2_P + p;
+            if (j < J && live) A.state[G.st_off + j * ld + m] = cf[j] * z[p];
+        }
+        __syncthreads();
+        // ring <- last L inputs: time A1 - L + row sits in row R2_LMAX + last_tmax - L + row of
+        // the final (unslid) chunk window
+        const long A1 = A.A0 + A.n_steps;
+        for (int idx = tid; idx < L * 32; idx += blockDim.x) {
+            const int row = idx >> 5, d = idx & 31;
+            const long k = A1 - L + row;
+            if (k >= 0 && tk.y + d < G.dim)
+                A.ring[G.ring_off + (k % L) * ld + tk.y + d] = X[R2_LMAX + last_tmax - L + row][d];
+        }
+    }
+}
+
+void launch_run2(const RunArgs& a, int nw, int num_sms, cudaStream_t s) {
+    const size_t smem = run2_smem_bytes(nw);
+    static bool attr = false;
+    if (!attr) {
+        FRAQ_CUDA(cudaFuncSetAttribute(run2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)run2_smem_bytes(R2_MAXW)));
+        attr = true;
+    }
+    int per_sm = 1;
+    FRAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, run2_kernel, nw * 32, smem));
+    const int grid = std::max(1, std::min(a.n_tasks, std::max(1, per_sm) * num_sms));
+    run2_kernel<<<grid, nw * 32, smem, s>>>(a);
+    FRAQ_LAUNCH_CHECK();
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------------------ HistDevice
@@ -569,6 +785,8 @@ struct fraq_hist_s {
     DevBuf<int> counter;
     DevBuf<int2> run_tasks;
     int n_run_tasks = 0;
+    DevBuf<int2> run2_tasks;   // (group, first DOF of a 32-DOF tile) for K5c
+    int n_run2_tasks = 0;
     int last_path = 0;
     // chunk staging for host-memory runs
     DevBuf<double> ubuf, dbuf;
@@ -667,6 +885,14 @@ void hist_create(fraq_ctx c, int n_groups, const fraq_kernel_t* const* ks, const
         h->run_tasks.alloc(std::max<size_t>(1, tasks.size()));
         if (!tasks.empty())
             FRAQ_CUDA(cudaMemcpy(h->run_tasks.p, tasks.data(), tasks.size() * sizeof(int2),
+                                 cudaMemcpyHostToDevice));
+        std::vector<int2> t2;
+        for (int g = 0; g < n_groups; ++g)
+            for (int m0 = 0; m0 < h->d.groups_h[g].dim; m0 += 32) t2.push_back(make_int2(g, m0));
+        h->n_run2_tasks = (int)t2.size();
+        h->run2_tasks.alloc(std::max<size_t>(1, t2.size()));
+        if (!t2.empty())
+            FRAQ_CUDA(cudaMemcpy(h->run2_tasks.p, t2.data(), t2.size() * sizeof(int2),
                                  cudaMemcpyHostToDevice));
     } catch (...) {
         delete h;
@@ -785,9 +1011,17 @@ void run_device(fraq_hist h, const double* U, long ldu, long n_steps, double* D,
         a.ldd = ldd;
         const int P = (h->d.max_J + 31) / 32;
         FRAQ_CUDA(cudaMemsetAsync(h->counter.p, 0, sizeof(int), h->ctx->stream));
-        const int grid = std::max(1, std::min((h->n_run_tasks + RUN_WARPS - 1) / RUN_WARPS,
-                                              2 * h->ctx->num_sms));
-        launch_run(std::max(1, P), a, grid, h->ctx->stream);
+        static const bool legacy = std::getenv("FRAQ_K5B") != nullptr;
+        if (legacy) {
+            const int grid = std::max(1, std::min((h->n_run_tasks + RUN_WARPS - 1) / RUN_WARPS,
+                                                  2 * h->ctx->num_sms));
+            launch_run(std::max(1, P), a, grid, h->ctx->stream);
+        } else {
+            h->last_path = 2;
+            a.tasks = h->run2_tasks.p;
+            a.n_tasks = h->n_run2_tasks;
+            launch_run2(a, std::max(1, P), h->ctx->num_sms, h->ctx->stream);
+        }
         h->appended += n_steps;
         h->level = h->appended - 1;
         return;
