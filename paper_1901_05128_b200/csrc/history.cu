@@ -485,6 +485,7 @@ __global__ void __launch_bounds__(R2_MAXW * 32, 1) run2_kernel(RunArgs A) {
     __shared__ int s_task;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+    const bool fast_red = nw == R2_MAXW;  // 512 threads: one output pair per thread pair
     for (;;) {
         __syncthreads();
         if (tid == 0) s_task = atomicAdd(A.counter, 1);
@@ -508,10 +509,7 @@ __global__ void __launch_bounds__(R2_MAXW * 32, 1) run2_kernel(RunArgs A) {
         for (int p = 0; p < R2_P; ++p) {
             const int j = warp * R2_P + p;
             z[p] = 0.0;
-            if (j < J && live) {
-                const double f = A.cf[G.co_off + j];
-                z[p] = A.state[G.st_off + j * ld + m] / f;
-            }
+            if (j < J && live) z[p] = A.state[G.st_off + j * ld + m] / A.cf[G.co_off + j];
         }
         // lag window: X(k), k in [A0 - L, A0 - 1], rows R2_LMAX - L .. R2_LMAX - 1
         for (int idx = tid; idx < L * 32; idx += blockDim.x) {
@@ -522,7 +520,8 @@ __global__ void __launch_bounds__(R2_MAXW * 32, 1) run2_kernel(RunArgs A) {
             X[R2_LMAX - L + row][d] = x;  // negative times read as zero
         }
         const double* Ub = A.U + G.dof0 + tk.y;
-        // chunk prefetch: thread handles rows (tid >> 5) + 16 i, DOF lane  (32 rows x 32 DOFs)
+        double* Db = A.D ? A.D + G.dof0 + tk.y : nullptr;
+        // chunk prefetch: rows warp + 16 i (i < 2) of the next chunk, DOF lane
         double pre[2];
         auto load_chunk = [&](long c0) {
 #pragma unroll
@@ -552,6 +551,53 @@ __global__ void __launch_bounds__(R2_MAXW * 32, 1) run2_kernel(RunArgs A) {
             }
             if (c0 + R2_TC < A.n_steps) load_chunk(c0 + R2_TC);
             __syncthreads();
+            // exact head window for the chunk, all threads: F[t][d] = sum_{i<=top} h_i X(n-i)
+#ifndef FRAQ_EXP_NOFIR
+            for (int idx = tid; idx < R2_TC * 32; idx += blockDim.x) {
+                const int t = idx >> 5, d = idx & 31;
+                const long n = A.A0 + c0 + t;
+                const long top = G.sbd ? min((long)L - 1, n - A.lo) : 1;
+                double acc = 0.0;
+                for (long i = 0; i <= top; ++i) acc = fma(hd[i], X[R2_LMAX + t - i][d], acc);
+                F[t][d] = acc;
+            }
+            __syncthreads();
+#endif
+            // reduction of a finished block (partials in buffer pbuf): node sum over warps +
+            // head window -> D.  fast path (16 warps, full block): thread pair (2o, 2o+1) sums
+            // the two warp halves of output o = (k, d) and combines with one shuffle; straight-
+            // line code so it interleaves with the surrounding FMA block.
+            auto reduce_block = [&](int bt0, int bk, int pbuf) {
+                const double* pr = part + (size_t)pbuf * nw * R2_TB * 32;
+#ifdef FRAQ_EXP_NOREDUCE
+                return;
+#endif
+                if (fast_red && bk == R2_TB) {
+                    const int o = tid >> 1, h = tid & 1, k = o >> 5, d = o & 31;
+                    double sum = 0.0;
+#pragma unroll
+                    for (int w = 0; w < R2_MAXW / 2; ++w)
+                        sum += pr[((h * (R2_MAXW / 2) + w) * R2_TB + k) * 32 + d];
+                    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+                    const long n = A.A0 + c0 + bt0 + k;
+                    const bool valid = G.sbd ? true : (n >= 1);
+                    if (h == 0 && Db && tk.y + d < G.dim)
+                        Db[(c0 + bt0 + k) * A.ldd + d] = valid ? sum + F[bt0 + k][d] : qnan;
+                } else {
+                    for (int idx = tid; idx < bk * 32; idx += blockDim.x) {
+                        const int k = idx >> 5, d = idx & 31;
+                        double sum = 0.0;
+                        for (int w = 0; w < nw; ++w) sum += pr[(w * R2_TB + k) * 32 + d];
+                        const long n = A.A0 + c0 + bt0 + k;
+                        const bool valid = G.sbd ? true : (n >= 1);
+                        if (Db && tk.y + d < G.dim)
+                            Db[(c0 + bt0 + k) * A.ldd + d] = valid ? sum + F[bt0 + k][d] : qnan;
+                    }
+                }
+            };
+            int prev_t0 = -1, prev_k = 0, prev_buf = 0;
+            const double* crw = cr + warp * R2_P;
+            const double* cfw = cf + warp * R2_P;
             for (int t0 = 0; t0 < tmax; t0 += R2_TB) {
                 const long n0 = A.A0 + c0 + t0;
                 const int kmax = min(R2_TB, tmax - t0);
@@ -566,10 +612,25 @@ __global__ void __launch_bounds__(R2_MAXW * 32, 1) run2_kernel(RunArgs A) {
                         v[k] = X[R2_LMAX + t0 + k - L][lane];
                         sacc[k] = 0.0;
                     }
-                    const double* crw = cr + warp * R2_P;
-                    const double* cfw = cf + warp * R2_P;
 #pragma unroll
-                    for (int p0 = 0; p0 < R2_P; p0 += 4) {
+                    for (int p0 = 0; p0 < R2_P / 2; p0 += 4) {
+                        double rr[4], ff[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            rr[i] = crw[p0 + i];
+                            ff[i] = cfw[p0 + i];
+                        }
+#pragma unroll
+                        for (int k = 0; k < R2_TB; ++k)
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                z[p0 + i] = fma(rr[i], z[p0 + i], v[k]);
+                                sacc[k] = fma(ff[i], z[p0 + i], sacc[k]);
+                            }
+                    }
+                    if (prev_t0 >= 0) reduce_block(prev_t0, prev_k, prev_buf);
+#pragma unroll
+                    for (int p0 = R2_P / 2; p0 < R2_P; p0 += 4) {
                         double rr[4], ff[4];
 #pragma unroll
                         for (int i = 0; i < 4; ++i) {
@@ -587,42 +648,34 @@ __global__ void __launch_bounds__(R2_MAXW * 32, 1) run2_kernel(RunArgs A) {
 #pragma unroll
                     for (int k = 0; k < R2_TB; ++k) pb[(warp * R2_TB + k) * 32 + lane] = sacc[k];
                 } else {
-                    // partial block (chunk tail, or level 0 of a fresh history: no advance)
+                    if (prev_t0 >= 0) reduce_block(prev_t0, prev_k, prev_buf);
+                    // partial block (chunk tail, level 0 of a fresh history, scheme level L)
                     for (int k = 0; k < kmax; ++k) {
                         const long n = n0 + k;
-                        double sk = 0.0;
+                        double sk = 0.0;  // (partial path)
                         if (n >= 1) {
                             const double vk = (n - L >= A.lo) ? X[R2_LMAX + t0 + k - L][lane] : 0.0;
 #pragma unroll
                             for (int p = 0; p < R2_P; ++p) {
-                                z[p] = fma(cr[warp * R2_P + p], z[p], vk);
-                                sk = fma(cf[warp * R2_P + p], z[p], sk);
+                                z[p] = fma(crw[p], z[p], vk);
+                                sk = fma(cfw[p], z[p], sk);
                             }
                         } else {
 #pragma unroll
-                            for (int p = 0; p < R2_P; ++p) sk = fma(cf[warp * R2_P + p], z[p], sk);
+                            for (int p = 0; p < R2_P; ++p) sk = fma(cfw[p], z[p], sk);
                         }
                         pb[(warp * R2_TB + k) * 32 + lane] = sk;
                     }
                 }
+#ifndef FRAQ_EXP_NOSYNC
                 __syncthreads();
-                // cross-warp node sum + head window -> D rows (coalesced over the 32 DOFs)
-                // cross-warp node sum + exact head window sum_{i<=top(n)} h_i X(n-i) -> D
-                for (int idx = tid; A.D && idx < kmax * 32; idx += blockDim.x) {
-                    const int k = idx >> 5, d = idx & 31;
-                    const long n = n0 + k;
-                    const long top = G.sbd ? min((long)L - 1, n - A.lo) : 1;
-                    double fir = 0.0;
-                    for (long i = 0; i <= top; ++i)
-                        fir = fma(hd[i], X[R2_LMAX + t0 + k - i][d], fir);
-                    double sum = 0.0;
-                    for (int w = 0; w < nw; ++w) sum += pb[(w * R2_TB + k) * 32 + d];
-                    const bool valid = G.sbd ? true : (n >= 1);
-                    if (tk.y + d < G.dim)
-                        A.D[(c0 + t0 + k) * A.ldd + G.dof0 + tk.y + d] = valid ? sum + fir : qnan;
-                }
+#endif
+                prev_t0 = t0;
+                prev_k = kmax;
+                prev_buf = buf;
                 buf ^= 1;
             }
+            if (prev_t0 >= 0) reduce_block(prev_t0, prev_k, prev_buf);
             last_tmax = tmax;
             if (c0 + R2_TC < A.n_steps) {
                 // slide (full chunk, tmax = 32): rows R2_LMAX + 32 - L .. -> R2_LMAX - L .., in
@@ -636,7 +689,7 @@ __global__ void __launch_bounds__(R2_MAXW * 32, 1) run2_kernel(RunArgs A) {
                 }
             }
         }
-        // write back y = f z and the ring (last L inputs)
+        // write back y = f z
 #pragma unroll
         for (int p = 0; p < R2_P; ++p) {
             const int j = warp * R2_P + p;
