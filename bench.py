@@ -102,20 +102,23 @@ def reference_kernels(orc, tau):
             orc.build_kernel_auto(True, 1.0 - 0.7, tau, N_LEVELS)]
 
 
-def cpu_sample(orc, kernels, params, threads, target_s):
-    """Times the reference SbdHistory (push + derivative per level) on a DOF sample drawn from
-    both exponent halves, `threads` host threads.  Returns (DOF-steps/s, sample description)."""
-    per_group = max(64, 64 * threads // 2)
-    idx = np.concatenate([np.arange(per_group), DOFS // 2 + np.arange(per_group)])
-    # calibrate on 32 levels, then size the sample to ~target_s seconds
-    U = params.signal(0, 32, idx)
+def cpu_sample(orc, kernels, params, threads, target_s, dofs=DOFS):
+    """Times the reference SbdHistory (push + derivative per level) on the FULL C2 DOF set (both
+    exponent halves; each of `threads` host threads owns a contiguous DOF slice, so the per-thread
+    working set -- and hence the memory behaviour -- is that of a full run) for a bounded number
+    of levels sized to ~target_s seconds.  Per-level cost does not depend on the level index once
+    the lag window is full, so DOF-steps/s over the sample equals the full-run rate.
+    Returns (DOF-steps/s, sample description, seconds)."""
+    idx = np.arange(dofs)
+    warm = 32
+    U = params.signal(0, warm, idx)
     secs, _ = orc.bench_history(kernels, U, threads)
-    rate = 2 * per_group * 32 / max(secs, 1e-6)
-    levels = int(min(max(64, target_s * rate / (2 * per_group)), 16384))
+    rate = dofs * warm / max(secs, 1e-6)
+    levels = int(min(max(64, target_s * rate / dofs), 1024))
     U = params.signal(0, levels, idx)
     secs, _ = orc.bench_history(kernels, U, threads)
-    dof_steps = 2 * per_group * levels
-    return dof_steps / secs, f"{2 * per_group} DOFs (both exponent halves) x {levels} levels", secs
+    return (dofs * levels / secs, f"all {dofs} DOFs x {levels} levels (per-thread DOF slices "
+            f"as in a full run)", secs)
 
 
 def run_reference_arm(args):
@@ -131,7 +134,7 @@ def run_reference_arm(args):
     params = c2_params()
     kernels = reference_kernels(orc, params.tau)
     threads = os.cpu_count() or 1
-    target = 1.0  # seconds of CPU work per step
+    target = 1.5  # seconds of CPU work per step
     for _ in range(args.warmup):
         cpu_sample(orc, kernels, params, threads, target / 4)
     vals, times = [], []
