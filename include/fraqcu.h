@@ -172,6 +172,14 @@ int fraq_hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* 
  * legacy, FRAQ_K5B=1), 2 = K5c (lane-per-DOF blocked, default). */
 int fraq_hist_last_path(fraq_hist h);
 
+/* ---------------------------------------------------------------- direct CQ (K10)
+ * The classical O(N^2) CQ sum D[n] = sum_{i<=n} d_i U[n-i] with the exact weights of
+ * be_weights / sbd_weights (the reference's direct harness sum, test_fast_kernel.cpp:27-41,
+ * acceptance_main.cpp:158-159) as a lower-triangular Toeplitz x signal GEMM on the fp64 tensor
+ * cores (DMMA).  U rows n = 0..n_steps-1 of dim values (leading dim ldu), D likewise. */
+int fraq_direct_cq(fraq_ctx ctx, int sbd, double g, double tau, const double* U, long ldu,
+                   long n_steps, long dim, double* D, long ldd, int mem);
+
 /* ---------------------------------------------------------------- L4 FFPE
  * run() (fpfp.cpp:351-381) for n_inst independent instances (BASELINE C3: 1, C5: 4096) solved
  * together on the device: histories K5 for both fields, RHS + 2x2-block tridiagonal solve K6,

@@ -59,6 +59,8 @@ EXTRA = [
     "build_sbd_kernel_auto",
     "context_stream",
     "diag_dmma_peak",
+    "direct_cq",
+    "direct_cq_device",
     "diag_fp64_peak",
     "gamma_fn",
     "make_be_kernel",

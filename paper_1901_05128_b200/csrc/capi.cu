@@ -285,6 +285,28 @@ int fraq_hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* 
 }
 int fraq_hist_last_path(fraq_hist h) { return h ? hist_last_path(h) : -1; }
 
+// ------------------------------------------------------------------ direct CQ
+int fraq_direct_cq(fraq_ctx c, int sbd, double g, double tau, const double* U, long ldu,
+                   long n_steps, long dim, double* D, long ldd, int mem) {
+    return guarded([&] {
+        check_ctx(c);
+        check_weight_args(g, tau);
+        if (n_steps < 0 || dim < 0 || ldu < dim || ldd < dim)
+            fail(FRAQ_EINVAL, "direct_cq: bad shape");
+        if (mem == FRAQ_DEVICE) {
+            direct_cq_dev(c, sbd, g, tau, U, ldu, n_steps, dim, D, ldd);
+            return;
+        }
+        DevBuf<double> du((size_t)n_steps * dim), dd((size_t)n_steps * dim);
+        FRAQ_CUDA(cudaMemcpy2DAsync(du.p, dim * 8, U, ldu * 8, dim * 8, n_steps,
+                                    cudaMemcpyHostToDevice, c->stream));
+        direct_cq_dev(c, sbd, g, tau, du.p, dim, n_steps, dim, dd.p, dim);
+        FRAQ_CUDA(cudaMemcpy2DAsync(D, ldd * 8, dd.p, dim * 8, dim * 8, n_steps,
+                                    cudaMemcpyDeviceToHost, c->stream));
+        FRAQ_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
 // ------------------------------------------------------------------ L4
 void fraq_kconf_default(fraq_kconf_t* c) {
     c->be_points = 64;

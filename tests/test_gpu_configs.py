@@ -1,0 +1,223 @@
+"""GPU parity at the BASELINE.json configurations (SURVEY.md §8(c) per-config oracle plan).
+
+C1 full; C2 on sampled DOFs at the full horizon N = 65536 (lanes are independent: the reference's
+lane-independence test, test_fast_kernel.cpp:276-296); C3 full size; C5 on sampled instances.
+Oracle: the reference compiled from its sources (oracle/_ref) when present, else the pinned port.
+"""
+import numpy as np
+import pytest
+
+from paper_1901_05128_b200.workloads import c1_params, c2_params, c3_instance, c5_instances
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def orc():
+    from oracle.oracle import Oracle, ref_available
+    return Oracle("reference" if ref_available() else "port")
+
+
+@pytest.fixture(scope="module")
+def port():
+    from oracle.oracle import Oracle
+    return Oracle("port")
+
+
+def rel_linf(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    ok = ~np.isnan(b)
+    return np.max(np.abs(a[ok] - b[ok])) / np.max(np.abs(b[ok]))
+
+
+def test_c1_fast_and_direct(fraq, orc, port):
+    """C1: BE, gamma 0.5, 1024 DOFs, N = 4096: GPU fast == reference fast (<= 1e-10), GPU direct
+    (DMMA Toeplitz GEMM) == oracle direct, and the fast-vs-direct discrepancy reproduced."""
+    p = c1_params()
+    U = p.signal(0, p.n_steps + 1, None)              # levels 0..N (u(0) = 0)
+    b = fraq.KernelBudget(horizon=p.n_steps, eps_tol=1e-12)
+    k = fraq.build_be_kernel_auto(0.5, p.tau, b)
+    ko = orc.build_kernel_auto(False, 0.5, p.tau, p.n_steps)
+    assert len(k.ratios) == ko.np1 == 144
+    h = fraq.BeHistory(k, fraq.HistoryVariant.standalone, U.shape[1])
+    D = h.run(U)
+    assert h.last_path >= 1
+    D_ref = orc.hist_run(ko, U)
+    assert rel_linf(D, D_ref) <= 1e-10
+    Dd = fraq.direct_cq(False, 0.5, p.tau, U)
+    sample = np.arange(0, 1024, 64)
+    Dd_ref = port.direct_cq(False, 0.5, p.tau, U[:, sample])
+    assert rel_linf(Dd[:, sample], Dd_ref) <= 1e-10
+    gpu_gap = rel_linf(D[1:], Dd[1:])
+    ref_gap = rel_linf(D_ref[1:, sample], Dd_ref[1:])
+    assert gpu_gap == pytest.approx(rel_linf(D_ref[1:], Dd[1:]), rel=1e-2)
+    assert rel_linf(D[1:, sample], Dd[1:, sample]) == pytest.approx(ref_gap, rel=1e-2)
+    assert 1e-12 < gpu_gap < 1e-9  # survey probe: 3.38e-11 (its own seed)
+
+
+@pytest.mark.slow
+def test_c2_sampled_dofs_full_horizon(fraq, orc, port):
+    """C2: BDF2, 65536 DOFs (gamma 0.7 | 0.3), N = 65536: 16 + 16 sampled DOFs through the full
+    horizon with the production tables; GPU fast == reference fast; direct sums on 2 DOFs."""
+    p = c2_params()
+    half = 32768
+    idx = np.concatenate([np.arange(0, half, half // 16), half + np.arange(0, half, half // 16)])
+    U = p.signal(0, p.n_steps, idx)
+    ks, kos = [], []
+    for g in (0.7, 0.3):
+        b = fraq.KernelBudget(horizon=p.n_steps, eps_tol=1e-12)
+        ks.append(fraq.build_sbd_kernel_auto(g, p.tau, b))
+        kos.append(orc.build_kernel_auto(True, g, p.tau, p.n_steps))
+        assert (len(ks[-1].ratio1), ks[-1].n_head) == (kos[-1].np1, kos[-1].n_head)
+        assert b.achieved_eps == pytest.approx(kos[-1].achieved_eps, rel=1e-3)
+    h = fraq.MultiHistory(ks, [16, 16])
+    D = h.run(U)
+    for gi in range(2):
+        cols = slice(16 * gi, 16 * gi + 16)
+        D_ref = orc.hist_run(kos[gi], U[:, cols])
+        assert rel_linf(D[:, cols], D_ref) <= 1e-10
+        # direct O(N^2) sums on one DOF per exponent: GPU (DMMA) vs oracle, and the gap
+        c = 16 * gi
+        g = (0.7, 0.3)[gi]
+        Dd = fraq.direct_cq(True, g, p.tau, U[:, c:c + 1])
+        Dd_ref = port.direct_cq(True, g, p.tau, U[:, c:c + 1])
+        assert rel_linf(Dd, Dd_ref) <= 1e-10
+        gap_gpu = rel_linf(D[:, c:c + 1], Dd)
+        gap_ref = rel_linf(D_ref[:, :1], Dd_ref)
+        assert gap_gpu == pytest.approx(gap_ref, rel=1e-2)  # reference accuracy at its 256 cap
+
+
+def _modespace_be_truth(M, N, T, a, al1, al2, g1, g2):
+    """The reference's mode-space oracle (test_fpfp.cpp:21-180: DST projection, per-mode scalar
+    BE recursion with full direct sums, closed-form 2x2 solves) in extended precision."""
+    dt = np.longdouble
+    h = dt(1) / (M + 1)
+    tau = dt(T) / N
+    pi = np.arccos(dt(-1))
+    k = np.arange(1, M + 1, dtype=dt)
+    V = np.sin(np.outer(k, k) * pi * h)
+    lam = 4 / h ** 2 * np.sin(k * pi * h / 2) ** 2
+    c1 = 2 / dt(M + 1) * (V @ g1.astype(dt))
+    c2 = 2 / dt(M + 1) * (V @ g2.astype(dt))
+
+    def bew(g):
+        w = np.empty(N + 1, dtype=dt)
+        w[0] = 1
+        for i in range(1, N + 1):
+            w[i] = w[i - 1] * ((i - 1 - dt(g)) / i)
+        return w * tau ** (-dt(g))
+    d1, d2 = bew(1 - al1), bew(1 - al2)
+    U = np.zeros((N + 1, M), dtype=dt)
+    W = np.zeros((N + 1, M), dtype=dt)
+    U[0], W[0] = c1, c2
+    a = dt(a)
+    for n in range(1, N + 1):
+        s1 = np.tensordot(d1[1:n], U[n - 1:0:-1], axes=1) if n > 1 else np.zeros(M, dt)
+        s2 = np.tensordot(d2[1:n], W[n - 1:0:-1], axes=1) if n > 1 else np.zeros(M, dt)
+        r1 = U[n - 1] / tau - (a + lam) * s1 + a * s2
+        r2 = W[n - 1] / tau - (a + lam) * s2 + a * s1
+        a11, a12 = 1 / tau + d1[0] * (a + lam), -a * d2[0]
+        a21, a22 = -a * d1[0], 1 / tau + d2[0] * (a + lam)
+        det = a11 * a22 - a12 * a21
+        U[n] = (r1 * a22 - a12 * r2) / det
+        W[n] = (a11 * r2 - a21 * r1) / det
+    return (V.T @ U[N]).astype(np.float64), (V.T @ W[N]).astype(np.float64)
+
+
+@pytest.mark.parametrize("N", [64, 256])
+def test_c3_grid_against_extended_precision_truth(fraq, orc, N):
+    """C3 grid (M = 4095, tau = 1/16384, a = -5.5, discontinuous data): both the reference and the
+    B200 path carry O(kappa eps) rounding per implicit step (cond of the block system ~1.4e6), so
+    each is compared with the extended-precision mode-space truth; the B200 result must be at
+    least as accurate as the reference's (measured: 8.5e-10 vs 1.4e-9 at N = 64)."""
+    inst = c3_instance()
+    T = N / 16384
+    t1, t2 = _modespace_be_truth(4095, N, T, -5.5, 0.4, 0.8, inst.g1, inst.g2)
+    spec = fraq.ProblemSpec(alpha1=0.4, alpha2=0.8, coupling_a=-5.5, grid_m=4095, t_final=T,
+                            n_steps=N, initial="custom", custom_g1=list(inst.g1),
+                            custom_g2=list(inst.g2))
+    rr = fraq.run(spec, fraq.Scheme.BE)
+    g1, g2, _, _ = orc.run(0.4, 0.8, -5.5, 4095, T, N, "BE", "custom", inst.g1, inst.g2)
+    err_gpu = max(rel_linf(rr.final_state.g1, t1), rel_linf(rr.final_state.g2, t2))
+    err_ref = max(rel_linf(g1, t1), rel_linf(g2, t2))
+    assert err_gpu <= 1.5 * err_ref
+    assert err_gpu <= 1e-8
+
+
+def _modespace_fastbe(orc, inst, M, N, a, al1, al2):
+    """FastBE in mode space (DST-diagonalised, per-mode 2x2 solves, per-mode fast histories with
+    the reference's auto-sized node tables), fp64.  Same discrete scheme as the physical-space
+    FastStepper, without its ill-conditioned stencil + block solve: the accuracy anchor at M=4095."""
+    tau = 1.0 / 16384
+    ks = [orc.build_kernel_auto(False, 1 - al1, tau, N), orc.build_kernel_auto(False, 1 - al2, tau, N)]
+    h = 1.0 / (M + 1)
+    k = np.arange(1, M + 1)
+    V = np.sin(np.outer(k, k) * np.pi * h)
+    lam = 4 / h ** 2 * np.sin(k * np.pi * h / 2) ** 2
+    G = [[2 / (M + 1) * (V @ inst.g1)], [2 / (M + 1) * (V @ inst.g2)]]
+    y = [np.zeros((len(kk.r1), M)) for kk in ks]
+    d0 = [kk.head[0] for kk in ks]
+    d1 = [kk.head[1] for kk in ks]
+    for n in range(1, N + 1):
+        s = []
+        for f in range(2):
+            y[f] *= ks[f].r1[:, None]
+            if n - 2 >= 1:  # scheme variant: G^0 is never fed
+                y[f] += ks[f].m1[:, None] * G[f][n - 2][None, :]
+            sf = y[f].sum(axis=0)
+            s.append(sf + d1[f] * G[f][n - 1] if n >= 2 else sf)
+        r1 = G[0][n - 1] / tau - (a + lam) * s[0] + a * s[1]
+        r2 = G[1][n - 1] / tau - (a + lam) * s[1] + a * s[0]
+        a11, a12 = 1 / tau + d0[0] * (a + lam), -a * d0[1]
+        a21, a22 = -a * d0[0], 1 / tau + d0[1] * (a + lam)
+        det = a11 * a22 - a12 * a21
+        G[0].append((r1 * a22 - a12 * r2) / det)
+        G[1].append((a11 * r2 - a21 * r1) / det)
+        if n > 3:
+            G[0][n - 3] = G[1][n - 3] = None
+    return V.T @ G[0][N], V.T @ G[1][N]
+
+
+@pytest.mark.slow
+def test_c3_full(fraq, orc):
+    """C3 at full size: M = 4095, N = 16384, FastBE, alpha (0.4, 0.8), m = 0.45 (a = -5.5).
+    Same auto-sized kernels and certificates as the reference.  The physical-space scheme's
+    rounding drift on this grid is ~1e-7 absolute over 16384 implicit steps for ANY fp64
+    implementation (measured: reference vs the fp64 mode-space evaluation 6.8e-8, B200 4.3e-8);
+    the B200 state must be at least as close to the mode-space evaluation as the reference's."""
+    inst = c3_instance()
+    spec = fraq.ProblemSpec(alpha1=inst.alpha1, alpha2=inst.alpha2, coupling_a=inst.coupling_a,
+                            grid_m=4095, t_final=1.0, n_steps=16384, initial="custom",
+                            custom_g1=list(inst.g1), custom_g2=list(inst.g2))
+    rr = fraq.run(spec, fraq.Scheme.FastBE)
+    g1, g2, e1, e2 = orc.run(inst.alpha1, inst.alpha2, inst.coupling_a, 4095, 1.0, 16384,
+                             "FastBE", "custom", inst.g1, inst.g2)
+    assert rr.kernel_eps1 == pytest.approx(e1, rel=1e-3)
+    assert rr.kernel_eps2 == pytest.approx(e2, rel=1e-3)
+    t1, t2 = _modespace_fastbe(orc, inst, 4095, 16384, inst.coupling_a, inst.alpha1, inst.alpha2)
+    ad = lambda x, y: float(np.max(np.abs(np.asarray(x) - y)))
+    err_gpu = max(ad(rr.final_state.g1, t1), ad(rr.final_state.g2, t2))
+    err_ref = max(ad(g1, t1), ad(g2, t2))
+    assert err_gpu <= err_ref
+    assert max(ad(rr.final_state.g1, g1), ad(rr.final_state.g2, g2)) <= 3e-7
+
+
+@pytest.mark.parametrize("scheme", ["FastBE", "FastSBD"])
+def test_c5_sampled_instances(fraq, orc, scheme):
+    """C5-style instances (random alpha, m, step-function data) at M = 4095 batched on the GPU;
+    each equals the reference's single-instance run (shortened horizon N = 512)."""
+    insts = c5_instances(6)[1:6:2]
+    N = 512
+    specs = [fraq.ProblemSpec(alpha1=i.alpha1, alpha2=i.alpha2, coupling_a=i.coupling_a,
+                              grid_m=4095, t_final=N / 16384, n_steps=N, initial="custom",
+                              custom_g1=list(i.g1), custom_g2=list(i.g2)) for i in insts]
+    outs = fraq.run_batch(specs, getattr(fraq.Scheme, scheme))
+    for i, o in zip(insts, outs):
+        g1, g2, _, _ = orc.run(i.alpha1, i.alpha2, i.coupling_a, 4095, N / 16384, N, scheme,
+                               "custom", i.g1, i.g2)
+        # O(1) step-function data on the M = 4095 grid: agreement is limited by the scheme's
+        # rounding drift (~1e-8 absolute per 1000 implicit steps for any fp64 implementation,
+        # see test_c3_full / test_c3_grid_against_extended_precision_truth)
+        scale = max(np.max(np.abs(i.g1)), np.max(np.abs(i.g2)))
+        assert np.max(np.abs(np.array(o.final_state.g1) - g1)) <= 2e-8 * scale
+        assert np.max(np.abs(np.array(o.final_state.g2) - g2)) <= 2e-8 * scale
