@@ -169,7 +169,8 @@ int fraq_hist_lagged(fraq_hist h, long depth, double* out, int mem);
 int fraq_hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, long ldd,
                   int mem);
 /* Which kernel the last fraq_hist_run used: 0 = per-level K5, 1 = K5b (warp-per-4-DOF blocked,
- * legacy, FRAQ_K5B=1), 2 = K5c (lane-per-DOF blocked, default). */
+ * FRAQ_K5B=1), 2 = K5c (lane-per-DOF DFMA blocked, FRAQ_K5C=1), 3 = K5d (DMMA block GEMMs,
+ * default). */
 int fraq_hist_last_path(fraq_hist h);
 
 /* ---------------------------------------------------------------- direct CQ (K10)

@@ -19,6 +19,10 @@
 
 namespace fraqcu {
 
+// history_dmma.cu
+void build_frag_tables(fraq_ctx c, HistDevice& d);
+void launch_run3(const RunArgs& a, int nwg, int num_sms, cudaStream_t s);
+
 namespace {
 
 struct d4 {
@@ -193,25 +197,6 @@ constexpr int RUN_Q = 4;        // DOFs per warp
 constexpr int RUN_TC = 32;      // levels per staged chunk
 constexpr int RUN_LMAX = 64;    // max lag supported on this path
 constexpr int RUN_WARPS = 4;    // warps per CTA (independent tasks)
-
-struct RunArgs {
-    const GroupDev* groups;
-    const int2* tasks;      // (group, first DOF of the 4-DOF task)
-    int n_tasks;
-    int* counter;           // dynamic task counter (zeroed before launch)
-    double* state;
-    double* ring;
-    const double* cr;
-    const double* cf;
-    const double* head;
-    long A0;                // values appended before the call (pure push sequence)
-    int lo;
-    long n_steps;
-    const double* U;        // device, row n at U + n*ldu, group-relative dof0 offsets
-    long ldu;
-    double* D;              // nullable
-    long ldd;
-};
 
 struct RunSmem {
     double X[RUN_LMAX + RUN_TC][RUN_Q];
@@ -840,6 +825,8 @@ struct fraq_hist_s {
     int n_run_tasks = 0;
     DevBuf<int2> run2_tasks;   // (group, first DOF of a 32-DOF tile) for K5c
     int n_run2_tasks = 0;
+    DevBuf<int2> run3_tasks;   // (group, first DOF of a 16-DOF tile) for K5d
+    int n_run3_tasks = 0;
     int last_path = 0;
     // chunk staging for host-memory runs
     DevBuf<double> ubuf, dbuf;
@@ -942,6 +929,14 @@ void hist_create(fraq_ctx c, int n_groups, const fraq_kernel_t* const* ks, const
         std::vector<int2> t2;
         for (int g = 0; g < n_groups; ++g)
             for (int m0 = 0; m0 < h->d.groups_h[g].dim; m0 += 32) t2.push_back(make_int2(g, m0));
+        std::vector<int2> t3;
+        for (int g = 0; g < n_groups; ++g)
+            for (int m0 = 0; m0 < h->d.groups_h[g].dim; m0 += 16) t3.push_back(make_int2(g, m0));
+        h->n_run3_tasks = (int)t3.size();
+        h->run3_tasks.alloc(std::max<size_t>(1, t3.size()));
+        if (!t3.empty())
+            FRAQ_CUDA(cudaMemcpy(h->run3_tasks.p, t3.data(), t3.size() * sizeof(int2),
+                                 cudaMemcpyHostToDevice));
         h->n_run2_tasks = (int)t2.size();
         h->run2_tasks.alloc(std::max<size_t>(1, t2.size()));
         if (!t2.empty())
@@ -1065,7 +1060,16 @@ void run_device(fraq_hist h, const double* U, long ldu, long n_steps, double* D,
         const int P = (h->d.max_J + 31) / 32;
         FRAQ_CUDA(cudaMemsetAsync(h->counter.p, 0, sizeof(int), h->ctx->stream));
         static const bool legacy = std::getenv("FRAQ_K5B") != nullptr;
-        if (legacy) {
+        static const bool k5c = std::getenv("FRAQ_K5C") != nullptr;
+        if (!legacy && !k5c) {
+            // K5d (DMMA block formulation), default
+            h->last_path = 3;
+            build_frag_tables(h->ctx, h->d);
+            a.tasks = h->run3_tasks.p;
+            a.n_tasks = h->n_run3_tasks;
+            a.frag = h->d.frag.p;
+            launch_run3(a, std::max(1, (h->d.max_J + 63) / 64), h->ctx->num_sms, h->ctx->stream);
+        } else if (legacy) {
             const int grid = std::max(1, std::min((h->n_run_tasks + RUN_WARPS - 1) / RUN_WARPS,
                                                   2 * h->ctx->num_sms));
             launch_run(std::max(1, P), a, grid, h->ctx->stream);

@@ -42,6 +42,32 @@ struct StepArgs {
 
 enum { MODE_NONE = 0, MODE_SUM = 1, MODE_DERIV = 2, MODE_FFPE = 3 };
 
+// Arguments of the temporally blocked kernels (K5b/K5c/K5d).
+struct RunArgs {
+    const GroupDev* groups;
+    const int2* tasks;      // (group, first DOF of the 4-DOF task)
+    int n_tasks;
+    int* counter;           // dynamic task counter (zeroed before launch)
+    double* state;
+    double* ring;
+    const double* cr;
+    const double* cf;
+    const double* head;
+    long A0;                // values appended before the call (pure push sequence)
+    int lo;
+    long n_steps;
+    const double* U;        // device, row n at U + n*ldu, group-relative dof0 offsets
+    long ldu;
+    double* D;              // nullable
+    long ldd;
+    const double* frag;     // K5d fragment tables (per group kFragDoubles)
+};
+
+// K5d fragment tables per group (history_dmma.cu): C (64 node tiles x 2 x 32), R (64 x 2 x 32),
+// r^8 (64 x 4 x 2), raw r and f per node pair (64 x 4 x 2 x 2), local Toeplitz W (2 x 32).
+constexpr int kFragC = 0, kFragR = 4096, kFragR8 = 8192, kFragRF = 8704, kFragW = 9728;
+constexpr int kFragDoubles = 9792;
+
 // Device-resident tables + state of a set of groups.
 struct HistDevice {
     std::vector<GroupDev> groups_h;
@@ -57,6 +83,10 @@ struct HistDevice {
     bool ztrick_ok = true;
     int max_J = 0, max_L = 0;
     std::vector<fraq_kernel_t> kernels;  // host copies
+
+    // DMMA fragment tables for K5d (built on first use): per group kFragDoubles doubles
+    DevBuf<double> frag;
+    bool frag_built = false;
 
     void build(fraq_ctx c, int n_groups, const fraq_kernel_t* const* ks, const long* dims);
     void launch_step(fraq_ctx c, const StepArgs& a);

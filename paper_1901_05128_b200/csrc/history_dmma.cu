@@ -1,0 +1,410 @@
+// history_dmma.cu -- K5d: temporally blocked history evaluation on the fp64 tensor cores.
+//
+// The per-node recurrence y_j(n) = r_j y_j(n-1) + f_j v(n) (fast_kernel.cpp:268-289,343-365) and
+// the readout S(n) = sum_j y_j(n) (fast_kernel.cpp:302-308,378-388) are evaluated 8 levels at a
+// time in closed form, which turns both into small GEMMs (v_k = X(n0 + k - L), block start n0):
+//
+//   S(n0+k)   = sum_j r_j^(k+1) y_j(n0-1)  +  sum_{i<=k} w_(k-i) v_i,   w_m = sum_j f_j r_j^m
+//   y_j(n0+7) = r_j^8 y_j(n0-1)  +  sum_i f_j r_j^(7-i) v_i
+//
+// Both node contractions run as DMMA (mma.sync m8n8k4 f64).  Layout: a warp owns 16 DOFs x 64
+// nodes; the state Y^T (DOF rows x node columns) lives in DMMA accumulator fragments, which are
+// used directly as A operands of the readout GEMM by permuting the node order of its constant B
+// tables (thread (g,t) holds nodes 2t, 2t+1 of each 8-node tile).  Constant tables (r^(k+1),
+// f r^(7-i), r^8) sit in shared memory in fragment order: one contiguous 256-byte LDS per DMMA
+// B operand.  A CTA covers 32 DOFs x all nodes; node slices of one DOF group meet through
+// shared memory once per 8-level block.  Measured on B200: DMMA alone reaches 37 TF/s, whereas
+// DFMA with three distinct register operands is capped near 25 TF/s by register-file reads.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "history.cuh"
+
+namespace fraqcu {
+
+namespace {
+
+constexpr int D_TC = 32;      // levels per staged chunk
+constexpr int D_TB = 8;       // levels per block (one GEMM pair)
+constexpr int D_LMAX = 64;    // max lag
+constexpr int D_NT = 8;       // node tiles (8 nodes) per warp = 64 nodes
+constexpr int D_MAXWG = 8;    // max warps per DOF group (512 nodes)
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+// Fragment tables for one group (one CTA per group, 256 threads).
+__global__ void frag_tables_kernel(const GroupDev* groups, const double* cr, const double* cf,
+                                   double* frag) {
+    const GroupDev G = groups[blockIdx.x];
+    double* T = frag + (size_t)blockIdx.x * kFragDoubles;
+    auto node_r = [&](int j) { return j < G.J ? cr[G.co_off + j] : 0.0; };
+    auto node_f = [&](int j) { return j < G.J ? cf[G.co_off + j] : 0.0; };
+    for (int idx = threadIdx.x; idx < 64 * 2 * 32; idx += blockDim.x) {
+        const int nt = idx / 64, e = (idx / 32) % 2, lane = idx % 32, g = lane >> 2, t = lane & 3;
+        // readout B: row k = t <-> node 8 nt + 2t + e, column n = g <-> level g: r^(g+1)
+        const int j = 8 * nt + 2 * t + e;
+        const double r = node_r(j);
+        double p = r;
+        for (int q = 0; q < g; ++q) p *= r;
+        T[kFragC + idx] = j < G.J ? p : 0.0;
+        // state B: half h = e, row k = t <-> level 4h + t, column n = g <-> node 8 nt + g:
+        // f r^(7 - 4h - t)
+        const int jn = 8 * nt + g, lev = 4 * e + t;
+        const double rn = node_r(jn);
+        double pn = 1.0;
+        for (int q = 0; q < 7 - lev; ++q) pn *= rn;
+        T[kFragR + idx] = jn < G.J ? node_f(jn) * pn : 0.0;
+    }
+    for (int idx = threadIdx.x; idx < 64 * 4 * 2; idx += blockDim.x) {
+        const int nt = idx / 8, t = (idx / 2) % 4, e = idx % 2, j = 8 * nt + 2 * t + e;
+        const double r = node_r(j);
+        double p = 1.0;
+        for (int q = 0; q < 8; ++q) p *= r;
+        T[kFragR8 + idx] = j < G.J ? p : 0.0;
+        T[kFragRF + 2 * idx] = r;
+        T[kFragRF + 2 * idx + 1] = node_f(j);
+    }
+    // local Toeplitz: w_m = sum_j f_j r_j^m, m = 0..7; B[k = t + 4h][n = g] = w_(g - k) (g >= k)
+    __shared__ double wsum[8][256];
+    for (int m = 0; m < 8; ++m) {
+        double acc = 0.0;
+        for (int j = threadIdx.x; j < G.J; j += blockDim.x) {
+            double p = 1.0;
+            for (int q = 0; q < m; ++q) p *= cr[G.co_off + j];
+            acc += cf[G.co_off + j] * p;
+        }
+        wsum[m][threadIdx.x] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x < 8) {
+        double acc = 0.0;
+        for (int i = 0; i < (int)blockDim.x; ++i) acc += wsum[threadIdx.x][i];
+        wsum[threadIdx.x][0] = acc;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < 64; idx += blockDim.x) {
+        const int h = idx / 32, lane = idx % 32, g = lane >> 2, t = lane & 3, k = t + 4 * h;
+        T[kFragW + idx] = g >= k ? wsum[g - k][0] : 0.0;
+    }
+}
+
+struct DSmem {
+    double X[D_LMAX + D_TC][16];
+    double F[D_TC][16];      // exact head window of the chunk
+    double hd[D_LMAX];
+};
+
+// CTA = one 16-DOF group x all nodes: nwg warps (64 nodes each), 2 CTAs resident per SM so one
+// CTA's barrier / reduction phase overlaps the other's DMMA phase.  Within a CTA the cross-warp
+// reduction of block b-1 is issued after block b's readout DMMAs (software pipelining), so its
+// shared-memory latency hides under the asynchronous tensor pipe.
+__global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
+    extern __shared__ double dsm[];
+    DSmem& S = *reinterpret_cast<DSmem*>(dsm);
+    double* tab = dsm + sizeof(DSmem) / sizeof(double);         // kFragDoubles
+    double* part = tab + kFragR8 + 64;                            // [2][8 warps][2][8][8]
+    __shared__ int s_task, s_group;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int nwg = blockDim.x >> 5;  // warps = node slices of 64
+    const int sl = warp;
+    const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+    const bool fast_red = nwg == D_MAXWG;
+    if (tid == 0) s_group = -1;
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) s_task = atomicAdd(A.counter, 1);
+        __syncthreads();
+        const int task = s_task;
+        if (task >= A.n_tasks) return;
+        const int2 tk = A.tasks[task];
+        const GroupDev G = A.groups[tk.x];
+        const int L = G.L;
+        const long ld = G.ld;
+        if (s_group != tk.x) {  // (uniform) reload the group's constant tables (C, R, W)
+            const double* src = A.frag + (size_t)tk.x * kFragDoubles;
+            for (int i = tid; i < kFragR8; i += blockDim.x) tab[i] = src[i];
+            for (int i = tid; i < 64; i += blockDim.x) tab[kFragR8 + i] = src[kFragW + i];
+        }
+        const double* RFg = A.frag + (size_t)tk.x * kFragDoubles + kFragRF;  // partial blocks
+        for (int i = tid; i < D_LMAX; i += blockDim.x) S.hd[i] = i < L ? A.head[G.hd_off + i] : 0.0;
+        // state fragments Y[rb][ntl][e]: DOF tk.y + 8 rb + g, node 64 sl + 8 ntl + 2t + e
+        double Y[2][D_NT][2];
+#pragma unroll
+        for (int rb = 0; rb < 2; ++rb) {
+            const int m = tk.y + 8 * rb + g;
+#pragma unroll
+            for (int ntl = 0; ntl < D_NT; ++ntl)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int j = 64 * sl + 8 * ntl + 2 * t + e;
+                    Y[rb][ntl][e] =
+                        (j < G.J && m < G.dim) ? A.state[G.st_off + j * ld + m] : 0.0;
+                }
+        }
+        // lag window X(k), k in [A0 - L, A0 - 1] (negative times read as zero)
+        for (int idx = tid; idx < L * 16; idx += blockDim.x) {
+            const int row = idx >> 4, d = idx & 15;
+            const long k = A.A0 - L + row;
+            double x = 0.0;
+            if (k >= 0 && tk.y + d < G.dim) x = A.ring[G.ring_off + (k % L) * ld + tk.y + d];
+            S.X[D_LMAX - L + row][d] = x;
+        }
+        __syncthreads();
+        if (tid == 0) s_group = tk.x;
+        const double* Ub = A.U + G.dof0 + tk.y;
+        double* Db = A.D ? A.D + G.dof0 + tk.y : nullptr;
+        const double* Cfr = tab + kFragC;
+        const double* Rfr = tab + kFragR;
+        const double* Wfr = tab + kFragR8;  // (W is stored right after C and R in smem)
+        // per-warp table bases: immediate offsets in the unrolled loops
+        const double* cw = Cfr + (size_t)(8 * sl) * 64 + lane;
+        const double* rw = Rfr + (size_t)(8 * sl) * 64 + lane;
+        const double* r8w = Cfr + (size_t)(8 * sl) * 64 + 28 + t;  // r^8: readout row g = 7
+        // chunk prefetch: thread covers rows (tid >> 4) + 16 i of the next chunk, DOF tid & 15
+        const int prow = tid >> 4, pd = tid & 15;
+        const bool plive = tk.y + pd < G.dim;
+        double pre[2];
+        auto prefetch = [&](long c0) {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int row = prow + 16 * i;
+                const long tt = c0 + row;
+                pre[i] = (row < D_TC && row * 16 < D_TC * 16 && tt < A.n_steps && plive)
+                             ? Ub[tt * A.ldu + pd] : 0.0;
+            }
+        };
+        if (blockDim.x == 256) prefetch(0);
+        // deferred reduction of the previous block (node sum over warps + head window -> D)
+        long p_row = 0, p_n0 = 0;
+        int p_kmax = 0, p_buf = 0;
+        auto reduce_prev = [&]() {
+            const double* pb = part + (size_t)p_buf * 8 * 2 * 64;
+            if (fast_red && p_kmax == D_TB) {
+                // straight line: thread pair (2o, 2o+1), o = (k, d), 4 slices each
+                const int o = tid >> 1, hh = tid & 1, k = o >> 4, d = o & 15;
+                const int rb = d >> 3, gg = d & 7;
+                double sum = pb[(hh * 2 + rb) * 64 + gg * 8 + k];
+                sum += pb[((hh + 2) * 2 + rb) * 64 + gg * 8 + k];
+                sum += pb[((hh + 4) * 2 + rb) * 64 + gg * 8 + k];
+                sum += pb[((hh + 6) * 2 + rb) * 64 + gg * 8 + k];
+                sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+                const bool valid = G.sbd ? true : (p_n0 + k >= 1);
+                if (hh == 0 && Db && tk.y + d < G.dim)
+                    Db[(p_row + k) * A.ldd + d] = valid ? sum + S.F[(p_row + k) % D_TC][d] : qnan;
+            } else {
+                for (int o = tid >> 1; o < D_TB * 16; o += blockDim.x >> 1) {
+                    const int hh = tid & 1, k = o >> 4, d = o & 15;
+                    const int rb = d >> 3, gg = d & 7;
+                    double sum = 0.0;
+                    if (k < p_kmax)
+                        for (int w = hh; w < nwg; w += 2) sum += pb[(w * 2 + rb) * 64 + gg * 8 + k];
+                    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+                    const bool valid = G.sbd ? true : (p_n0 + k >= 1);
+                    if (hh == 0 && k < p_kmax && Db && tk.y + d < G.dim)
+                        Db[(p_row + k) * A.ldd + d] =
+                            valid ? sum + S.F[(p_row + k) % D_TC][d] : qnan;
+                }
+            }
+        };
+        int buf = 0, last_tmax = 0;
+        for (long c0 = 0; c0 < A.n_steps; c0 += D_TC) {
+            const int tmax = (int)min((long)D_TC, A.n_steps - c0);
+            __syncthreads();
+            if (blockDim.x == 256) {
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int row = prow + 16 * i;
+                    if (row < D_TC) S.X[D_LMAX + row][pd] = pre[i];
+                }
+                if (c0 + D_TC < A.n_steps) prefetch(c0 + D_TC);
+            } else {  // fewer than 8 warps: direct loads (no prefetch)
+                for (int idx = tid; idx < D_TC * 16; idx += blockDim.x) {
+                    const int row = idx >> 4, d = idx & 15;
+                    const long tt = c0 + row;
+                    S.X[D_LMAX + row][d] =
+                        (tt < A.n_steps && tk.y + d < G.dim) ? Ub[tt * A.ldu + d] : 0.0;
+                }
+            }
+            __syncthreads();
+#ifndef FRAQ_EXP_NOFIR
+            for (int idx = tid; idx < D_TC * 16; idx += blockDim.x) {
+                const int tt = idx >> 4, d = idx & 15;
+                const long n = A.A0 + c0 + tt;
+                const long top = G.sbd ? min((long)L - 1, n - A.lo) : 1;
+                double acc = 0.0;
+                for (long i = 0; i <= top; ++i) acc = fma(S.hd[i], S.X[D_LMAX + tt - i][d], acc);
+                S.F[tt][d] = acc;
+            }
+            __syncthreads();
+#endif
+            for (int t0 = 0; t0 < tmax; t0 += D_TB) {
+                const long n0 = A.A0 + c0 + t0;
+                const int kmax = min(D_TB, tmax - t0);
+                double* pw = part + ((size_t)(buf * 8 + warp) * 2) * 64;  // this warp's [2][8][8]
+                const bool special = A.lo == 1 && n0 <= L && L < n0 + D_TB;
+                if (kmax == D_TB && n0 >= 1 && !special) {
+                    // ---- readout GEMM from the block-start state + local Toeplitz
+                    double sacc[2][2][2];
+#pragma unroll
+                    for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+                        for (int p = 0; p < 2; ++p) sacc[rb][p][0] = sacc[rb][p][1] = 0.0;
+#pragma unroll
+                    for (int ntl = 0; ntl < D_NT; ++ntl)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const double b = cw[(ntl * 2 + e) * 32];
+#pragma unroll
+                            for (int rb = 0; rb < 2; ++rb) dmma(sacc[rb][ntl & 1], Y[rb][ntl][e], b);
+                        }
+                    double vf[2][2];
+#pragma unroll
+                    for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+                            vf[rb][h] = S.X[D_LMAX + t0 + 4 * h + t - L][8 * rb + g];
+                    if (sl == 0) {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const double b = Wfr[h * 32 + lane];
+#pragma unroll
+                            for (int rb = 0; rb < 2; ++rb) dmma(sacc[rb][1], vf[rb][h], b);
+                        }
+                    }
+                    // ---- state GEMM: Y <- r^8 (.) Y + V R
+#pragma unroll
+                    for (int ntl = 0; ntl < D_NT; ++ntl) {
+                        const double ra = r8w[(ntl * 2) * 32], rbv = r8w[(ntl * 2 + 1) * 32];
+                        const double b0 = rw[(ntl * 2) * 32], b1 = rw[(ntl * 2 + 1) * 32];
+#pragma unroll
+                        for (int rb = 0; rb < 2; ++rb) {
+                            Y[rb][ntl][0] *= ra;
+                            Y[rb][ntl][1] *= rbv;
+                            dmma(Y[rb][ntl], vf[rb][0], b0);
+                            dmma(Y[rb][ntl], vf[rb][1], b1);
+                        }
+                    }
+                    // partial readout (DOF g, levels 2t, 2t+1) -> shared memory
+#pragma unroll
+                    for (int rb = 0; rb < 2; ++rb) {
+                        pw[(rb * 8 + g) * 8 + 2 * t] = sacc[rb][0][0] + sacc[rb][1][0];
+                        pw[(rb * 8 + g) * 8 + 2 * t + 1] = sacc[rb][0][1] + sacc[rb][1][1];
+                    }
+                } else {
+                    // partial block: level by level, elementwise on the fragments
+                    for (int k = 0; k < kmax; ++k) {
+                        const long n = n0 + k;
+                        const bool adv = n >= 1;
+                        const bool feed = adv && (n - L >= A.lo);
+                        double ps[2] = {0.0, 0.0};
+#pragma unroll
+                        for (int rb = 0; rb < 2; ++rb) {
+                            const double v = feed ? S.X[D_LMAX + t0 + k - L][8 * rb + g] : 0.0;
+#pragma unroll
+                            for (int ntl = 0; ntl < D_NT; ++ntl)
+#pragma unroll
+                                for (int e = 0; e < 2; ++e) {
+                                    const int nt = 8 * sl + ntl;
+                                    if (adv) {
+                                        const double r = RFg[((nt * 4 + t) * 2 + e) * 2];
+                                        const double f = RFg[((nt * 4 + t) * 2 + e) * 2 + 1];
+                                        Y[rb][ntl][e] = fma(r, Y[rb][ntl][e], f * v);
+                                    }
+                                    ps[rb] += Y[rb][ntl][e];
+                                }
+                        }
+#pragma unroll
+                        for (int rb = 0; rb < 2; ++rb) {
+                            ps[rb] += __shfl_xor_sync(0xffffffffu, ps[rb], 1);
+                            ps[rb] += __shfl_xor_sync(0xffffffffu, ps[rb], 2);
+                            if (t == 0) pw[(rb * 8 + g) * 8 + k] = ps[rb];
+                        }
+                    }
+                }
+#ifndef FRAQ_EXP_NOSYNC
+                __syncthreads();
+#endif
+                p_row = c0 + t0;
+                p_n0 = n0;
+                p_kmax = kmax;
+                p_buf = buf;
+#ifndef FRAQ_EXP_NOREDUCE
+                reduce_prev();
+#endif
+                buf ^= 1;
+            }
+            last_tmax = tmax;
+            if (c0 + D_TC < A.n_steps) {
+                // slide (full chunk): rows R2_LMAX + 32 - L .. -> R2_LMAX - L .. (32-row phases;
+                // the pending reduction reads F and the partials, not X)
+                for (int base = 0; base < L; base += D_TC) {
+                    if (base) __syncthreads();
+                    for (int idx = tid; idx < D_TC * 16; idx += blockDim.x) {
+                        const int r = base + (idx >> 4);
+                        if (r < L) S.X[D_LMAX - L + r][idx & 15] = S.X[D_LMAX - L + r + D_TC][idx & 15];
+                    }
+                }
+            }
+        }
+        // write back the state and the ring
+#pragma unroll
+        for (int rb = 0; rb < 2; ++rb) {
+            const int m = tk.y + 8 * rb + g;
+#pragma unroll
+            for (int ntl = 0; ntl < D_NT; ++ntl)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int j = 64 * sl + 8 * ntl + 2 * t + e;
+                    if (j < G.J && m < G.dim) A.state[G.st_off + j * ld + m] = Y[rb][ntl][e];
+                }
+        }
+        __syncthreads();
+        const long A1 = A.A0 + A.n_steps;
+        for (int idx = tid; idx < L * 16; idx += blockDim.x) {
+            const int row = idx >> 4, d = idx & 15;
+            const long k = A1 - L + row;
+            if (k >= 0 && tk.y + d < G.dim)
+                A.ring[G.ring_off + (k % L) * ld + tk.y + d] = S.X[D_LMAX + last_tmax - L + row][d];
+        }
+    }
+}
+
+size_t run3_smem(int nwg) {
+    (void)nwg;
+    return sizeof(DSmem) + sizeof(double) * (kFragR8 + 64 + 2 * 8 * 2 * 64);
+}
+
+}  // namespace
+
+void build_frag_tables(fraq_ctx c, HistDevice& d) {
+    if (d.frag_built) return;
+    d.frag.alloc((size_t)d.groups_h.size() * kFragDoubles);
+    frag_tables_kernel<<<(unsigned)d.groups_h.size(), 256, 0, c->stream>>>(d.groups.p, d.cr.p,
+                                                                          d.cf.p, d.frag.p);
+    FRAQ_LAUNCH_CHECK();
+    d.frag_built = true;
+}
+
+void launch_run3(const RunArgs& a, int nwg, int num_sms, cudaStream_t s) {
+    const size_t smem = run3_smem(nwg);
+    static bool attr = false;
+    if (!attr) {
+        FRAQ_CUDA(cudaFuncSetAttribute(run3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)run3_smem(D_MAXWG)));
+        attr = true;
+    }
+    int per_sm = 1;
+    FRAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, run3_kernel, nwg * 32, smem));
+    const int grid = std::max(1, std::min(a.n_tasks, std::max(1, per_sm) * num_sms));
+    run3_kernel<<<grid, nwg * 32, smem, s>>>(a);
+    FRAQ_LAUNCH_CHECK();
+}
+
+}  // namespace fraqcu
