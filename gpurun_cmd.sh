@@ -1,3 +1,1 @@
-timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -3 gpurun_out/pytest_gpu.log
-python profiles/microbench/time_k5c.py .
-FRAQ_K5C=1 python profiles/microbench/time_k5c.py .
+for d in gpurun_variants/*; do python profiles/microbench/time_k5c.py $d 2>&1 | tail -1; done

@@ -12,9 +12,10 @@
 // used directly as A operands of the readout GEMM by permuting the node order of its constant B
 // tables (thread (g,t) holds nodes 2t, 2t+1 of each 8-node tile).  Constant tables (r^(k+1),
 // f r^(7-i), r^8) sit in shared memory in fragment order: one contiguous 256-byte LDS per DMMA
-// B operand.  A CTA covers 32 DOFs x all nodes; node slices of one DOF group meet through
-// shared memory once per 8-level block.  Measured on B200: DMMA alone reaches 37 TF/s, whereas
-// DFMA with three distinct register operands is capped near 25 TF/s by register-file reads.
+// B operand.  A CTA covers 16 DOFs x all nodes (8 warps of 64 nodes), two CTAs per SM; node
+// slices meet through shared memory once per 8-level block.  Measured on B200: DMMA alone
+// reaches 37 TF/s (latency 26 cycles), whereas DFMA with three distinct register operands is
+// capped near 25 TF/s by register-file reads (profiles/microbench/mb_operands.cu).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -270,13 +271,18 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
 #pragma unroll
                         for (int h = 0; h < 2; ++h)
                             vf[rb][h] = S.X[D_LMAX + t0 + 4 * h + t - L][8 * rb + g];
-                    if (sl == 0) {
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const double b = Wfr[h * 32 + lane];
-#pragma unroll
-                            for (int rb = 0; rb < 2; ++rb) dmma(sacc[rb][1], vf[rb][h], b);
-                        }
+                    // local Toeplitz: 4 DMMAs (rb, h) spread over warps 0..3 of the CTA
+                    for (int w4 = sl; w4 < 4; w4 += nwg) {  // (fewer than 4 warps: several each)
+                        const int hl = w4 & 1;
+                        const double b = Wfr[hl * 32 + lane];
+                        if (w4 == 0)
+                            dmma(sacc[0][1], vf[0][0], b);
+                        else if (w4 == 1)
+                            dmma(sacc[0][1], vf[0][1], b);
+                        else if (w4 == 2)
+                            dmma(sacc[1][1], vf[1][0], b);
+                        else
+                            dmma(sacc[1][1], vf[1][1], b);
                     }
                     // ---- state GEMM: Y <- r^8 (.) Y + V R
 #pragma unroll
