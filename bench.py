@@ -264,6 +264,11 @@ def main():
     # HBM figures: algorithmic bytes of one state pass per level, B = 8 (2 N_nodes + 2)
     B = 0.5 * sum(8 * (2 * nn + 2) for nn in n_nodes)
     pk = peaks()
+    try:  # DRAM traffic per K5d launch from the committed ncu --set full capture (profiles/)
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
+        traffic = tr["dram_bytes_per_launch"] / 1e9  # GB per launch (512 levels)
+    except Exception:
+        traffic = None
 
     # per-level fused kernel K5 (one HBM pass over the state per level) on the same workload
     hs = fraq.MultiHistory(ks, [DOFS // 2, DOFS - DOFS // 2])
@@ -330,7 +335,8 @@ def main():
                 "parallelism": f"dof-sharded x{world}, no data-path collective",
                 "setup_s": setup_s},
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": dmma_peak,
-                         "unit": "TFLOP/s", "frac": achieved_tf / dmma_peak, "traffic": None,
+                         "unit": "TFLOP/s", "frac": achieved_tf / dmma_peak,
+                         "traffic": traffic, "traffic_unit": "GB per launch (ncu, profiles/)",
                          "peak_source": "measured fp64 tensor-core (DMMA) stream on this GPU "
                                         "(fraq_diag_dmma_peak); DFMA stream %.1f TF/s" % fp64_peak,
                          "dtype": "f64",
