@@ -829,7 +829,19 @@ struct fraq_hist_s {
     int n_run3_tasks = 0;
     int last_path = 0;
     // chunk staging for host-memory runs
-    DevBuf<double> ubuf, dbuf;
+    DevBuf<double> ubuf[2], dbuf[2];
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_u[2] = {nullptr, nullptr}, ev_c[2] = {nullptr, nullptr},
+                ev_d[2] = {nullptr, nullptr};
+    ~fraq_hist_s() {
+        if (s_h2d) cudaStreamDestroy(s_h2d);
+        if (s_d2h) cudaStreamDestroy(s_d2h);
+        for (int i = 0; i < 2; ++i) {
+            if (ev_u[i]) cudaEventDestroy(ev_u[i]);
+            if (ev_c[i]) cudaEventDestroy(ev_c[i]);
+            if (ev_d[i]) cudaEventDestroy(ev_d[i]);
+        }
+    }
 };
 
 namespace fraqcu {
@@ -1120,22 +1132,55 @@ void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, l
         run_device(h, U, ldu, n_steps, D, ldd);
         return;
     }
-    // host buffers: chunks of rows through device staging (H2D, run, D2H)
+    // host buffers: chunks of rows through two device staging buffers.  Copies run on their
+    // own streams so the H2D of chunk i+1 and the D2H of chunk i-1 overlap the kernel on chunk
+    // i (the kernels themselves are sequential: each chunk continues the history state).
+    // Pinned host memory gives full overlap; pageable memory still works (staged copies).
     const long dim = std::max<long>(1, h->d.total_dim);
     const long rows = std::max<long>(1, std::min<long>(n_steps, (64L << 20) / (8 * dim)));
-    if ((long)h->ubuf.n < rows * dim) h->ubuf.alloc(rows * dim);
-    if (D && (long)h->dbuf.n < rows * dim) h->dbuf.alloc(rows * dim);
-    for (long n0 = 0; n0 < n_steps; n0 += rows) {
-        const long nr = std::min(rows, n_steps - n0);
-        FRAQ_CUDA(cudaMemcpy2DAsync(h->ubuf.p, dim * 8, U + n0 * ldu, ldu * 8, h->d.total_dim * 8,
-                                    nr, cudaMemcpyHostToDevice, h->ctx->stream));
-        run_device(h, h->ubuf.p, dim, nr, D ? h->dbuf.p : nullptr, dim);
-        if (D)
-            FRAQ_CUDA(cudaMemcpy2DAsync(D + n0 * ldd, ldd * 8, h->dbuf.p, dim * 8,
-                                        h->d.total_dim * 8, nr, cudaMemcpyDeviceToHost,
-                                        h->ctx->stream));
+    for (int i = 0; i < 2; ++i) {
+        if ((long)h->ubuf[i].n < rows * dim) h->ubuf[i].alloc(rows * dim);
+        if (D && (long)h->dbuf[i].n < rows * dim) h->dbuf[i].alloc(rows * dim);
+        if (!h->ev_u[i]) {
+            FRAQ_CUDA(cudaEventCreateWithFlags(&h->ev_u[i], cudaEventDisableTiming));
+            FRAQ_CUDA(cudaEventCreateWithFlags(&h->ev_c[i], cudaEventDisableTiming));
+            FRAQ_CUDA(cudaEventCreateWithFlags(&h->ev_d[i], cudaEventDisableTiming));
+        }
     }
-    FRAQ_CUDA(cudaStreamSynchronize(h->ctx->stream));
+    if (!h->s_h2d) {
+        FRAQ_CUDA(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
+        FRAQ_CUDA(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
+    }
+    cudaStream_t sc = h->ctx->stream;
+    // copies may only start after earlier work on the compute stream (state + buffers)
+    FRAQ_CUDA(cudaEventRecord(h->ev_c[0], sc));
+    FRAQ_CUDA(cudaEventRecord(h->ev_c[1], sc));
+    FRAQ_CUDA(cudaEventRecord(h->ev_d[0], sc));
+    FRAQ_CUDA(cudaEventRecord(h->ev_d[1], sc));
+    long i = 0;
+    for (long n0 = 0; n0 < n_steps; n0 += rows, ++i) {
+        const int b = (int)(i & 1);
+        const long nr = std::min(rows, n_steps - n0);
+        // H2D into ubuf[b] once the kernel that last read it (chunk i-2) finished
+        FRAQ_CUDA(cudaStreamWaitEvent(h->s_h2d, h->ev_c[b], 0));
+        FRAQ_CUDA(cudaMemcpy2DAsync(h->ubuf[b].p, dim * 8, U + n0 * ldu, ldu * 8,
+                                    h->d.total_dim * 8, nr, cudaMemcpyHostToDevice, h->s_h2d));
+        FRAQ_CUDA(cudaEventRecord(h->ev_u[b], h->s_h2d));
+        // kernel on chunk i: needs its inputs and dbuf[b] drained by the D2H of chunk i-2
+        FRAQ_CUDA(cudaStreamWaitEvent(sc, h->ev_u[b], 0));
+        if (D) FRAQ_CUDA(cudaStreamWaitEvent(sc, h->ev_d[b], 0));
+        run_device(h, h->ubuf[b].p, dim, nr, D ? h->dbuf[b].p : nullptr, dim);
+        FRAQ_CUDA(cudaEventRecord(h->ev_c[b], sc));
+        if (D) {
+            FRAQ_CUDA(cudaStreamWaitEvent(h->s_d2h, h->ev_c[b], 0));
+            FRAQ_CUDA(cudaMemcpy2DAsync(D + n0 * ldd, ldd * 8, h->dbuf[b].p, dim * 8,
+                                        h->d.total_dim * 8, nr, cudaMemcpyDeviceToHost, h->s_d2h));
+            FRAQ_CUDA(cudaEventRecord(h->ev_d[b], h->s_d2h));
+        }
+    }
+    FRAQ_CUDA(cudaStreamSynchronize(h->s_h2d));
+    FRAQ_CUDA(cudaStreamSynchronize(sc));
+    FRAQ_CUDA(cudaStreamSynchronize(h->s_d2h));
 }
 
 int hist_last_path(fraq_hist h) { return h->last_path; }
