@@ -87,11 +87,17 @@ typedef struct {
     const double* custom_g2;
 } fraq_spec_t;
 
-/* KernelConfig, fpfp.hpp:50-57. */
+/* KernelConfig, fpfp.hpp:50-57, plus the spatial solver of the fast schemes (addition):
+ * FRAQ_SOLVER_PHYSICAL (0, default) = the reference's physical-space stepper (stencil RHS +
+ * 2x2-block tridiagonal solve per level); FRAQ_SOLVER_MODAL (1) = the same scheme stepped in the
+ * DST eigenbasis (the reference's mode-space oracle, test_fpfp.cpp:21-180), every mode an
+ * independent 2x2 recursion -- exact in exact arithmetic, better conditioned in fp64. */
+enum { FRAQ_SOLVER_PHYSICAL = 0, FRAQ_SOLVER_MODAL = 1 };
 typedef struct {
     int be_points, sbd_points_1, sbd_points_2, sbd_head;
     double eps_tol;
     int auto_size;
+    int solver;
 } fraq_kconf_t;
 
 /* RunResult minus the state, fpfp.hpp:59-65, plus the chosen table sizes. */
@@ -193,6 +199,15 @@ int fraq_run(fraq_ctx ctx, const fraq_spec_t* specs, int n_inst, int scheme,
  * the level back to the host, so the loop time includes those copies. */
 typedef void (*fraq_observer_fn)(long n, const double* g1, const double* g2, int grid_m,
                                  void* user);
+/* Two-dimensional FFPE on the unit square (BASELINE C4; no reference capability -- the reference
+ * is 1D only): grid_m x grid_m interior points, five-point Laplacian, homogeneous Dirichlet, fast
+ * BE / BDF2 in time, stepped in the 2D DST eigenbasis (lambda_k + lambda_l).  g1_0 / g2_0 and the
+ * outputs g1 / g2 are grid_m * grid_m values, row-major (x fastest).  Scheme FRAQ_FASTBE or
+ * FRAQ_FASTSBD. */
+int fraq_run_2d(fraq_ctx ctx, double alpha1, double alpha2, double coupling_a, int grid_m,
+                double t_final, long n_steps, int scheme, const fraq_kconf_t* kconf,
+                const double* g1_0, const double* g2_0, double* g1, double* g2,
+                fraq_run_info_t* info);
 int fraq_run_observed(fraq_ctx ctx, const fraq_spec_t* spec, int scheme,
                       const fraq_kconf_t* kconf, fraq_observer_fn fn, void* user, double* g1,
                       double* g2, fraq_run_info_t* info);

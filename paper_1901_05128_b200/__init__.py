@@ -65,7 +65,10 @@ EXTRA = [
     "gamma_fn",
     "make_be_kernel",
     "make_sbd_kernel",
+    "run_2d",
     "run_batch",
+    "SOLVER_MODAL",
+    "SOLVER_PHYSICAL",
     "synchronize",
 ]
 

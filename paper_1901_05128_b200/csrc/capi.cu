@@ -25,6 +25,9 @@ void hist_output(fraq_hist h, int mode, double* out, int mem);
 void hist_lagged(fraq_hist h, long depth, double* out, int mem);
 void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, long ldd, int mem);
 int hist_last_path(fraq_hist h);
+void ffpe_run_2d(fraq_ctx c, double alpha1, double alpha2, double a, int m, double t_final,
+                 long N, int scheme, const fraq_kconf_t* kc, const double* g1_0,
+                 const double* g2_0, double* g1, double* g2, fraq_run_info_t* info);
 // ffpe.cu
 void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
               const fraq_kconf_t* kc, double* g1, double* g2, fraq_run_info_t* info,
@@ -315,6 +318,18 @@ void fraq_kconf_default(fraq_kconf_t* c) {
     c->sbd_head = 0;
     c->eps_tol = 1e-12;
     c->auto_size = 1;
+    c->solver = FRAQ_SOLVER_PHYSICAL;
+}
+
+int fraq_run_2d(fraq_ctx c, double alpha1, double alpha2, double coupling_a, int grid_m,
+                double t_final, long n_steps, int scheme, const fraq_kconf_t* kconf,
+                const double* g1_0, const double* g2_0, double* g1, double* g2,
+                fraq_run_info_t* info) {
+    return guarded([&] {
+        check_ctx(c);
+        ffpe_run_2d(c, alpha1, alpha2, coupling_a, grid_m, t_final, n_steps, scheme, kconf, g1_0,
+                    g2_0, g1, g2, info);
+    });
 }
 
 int fraq_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,

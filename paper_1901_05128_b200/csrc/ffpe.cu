@@ -310,6 +310,37 @@ void initial_field(const fraq_spec_t& s, double* g1, double* g2) {
 
 }  // namespace
 
+// Kernel tables for both fields of every instance (auto-sized like FastStepper, or fixed
+// sizes + certificate), batched over exponents on the device.  fpfp.cpp:185-227.
+void build_ffpe_kernels(fraq_ctx c, const std::vector<double>& gam, double tau, long N, bool sbd,
+                        const fraq_kconf_t& kc, std::vector<fraq_kernel_t>& ks,
+                        std::vector<double>& eps) {
+    const int n = (int)gam.size();
+    ks.resize(n);
+    eps.assign(n, 0.0);
+    if (kc.auto_size) {
+        std::vector<fraq_budget_t> bud(n);
+        for (auto& b : bud) b = fraq_budget_t{N, kc.eps_tol, 256, 256, 0.0};
+        build_kernel_auto_dev(c, sbd, n, gam.data(), tau, bud.data(), ks.data());
+        for (int t = 0; t < n; ++t) eps[t] = bud[t].achieved_eps;
+        return;
+    }
+    for (int t = 0; t < n; ++t) {
+        long am;
+        if (sbd) {
+            const int hh = kc.sbd_head > 0 ? kc.sbd_head : (gam[t] <= 0.5 ? 15 : 17);
+            build_sbd_kernel_dev(c, gam[t], tau, kc.sbd_points_1, kc.sbd_points_2, hh, &ks[t]);
+            kernel_error_report_dev(c, &ks[t], N > 8 ? N : 8, nullptr, &eps[t], &am);
+        } else {
+            build_be_kernel_dev(c, gam[t], tau, kc.be_points, &ks[t]);
+            kernel_error_report_dev(c, &ks[t], N > 2 ? N : 2, nullptr, &eps[t], &am);
+        }
+    }
+}
+
+void ffpe_run_modal(fraq_ctx c, const fraq_spec_t* specs, int n_inst, bool sbd,
+                    const fraq_kconf_t& kc, double* g1_out, double* g2_out, fraq_run_info_t* info);
+
 void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
               const fraq_kconf_t* kc_in, double* g1_out, double* g2_out, fraq_run_info_t* info,
               fraq_observer_fn obs, void* user) {
@@ -334,6 +365,12 @@ void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
     }
     const bool sbd = scheme == FRAQ_SBD || scheme == FRAQ_FASTSBD;
     const bool fast = scheme == FRAQ_FASTBE || scheme == FRAQ_FASTSBD;
+    if (kc.solver == FRAQ_SOLVER_MODAL) {
+        if (!fast) fail(FRAQ_EINVAL, "run: the modal solver needs a fast scheme");
+        if (obs) fail(FRAQ_EINVAL, "run: the modal solver does not stream intermediate states");
+        ffpe_run_modal(c, specs, n_inst, sbd, kc, g1_out, g2_out, info);
+        return;
+    }
     const double tau = s0.t_final / double(N);
     const double h = s0.length / double(m + 1);
     const double t_setup0 = now_s();
@@ -354,25 +391,7 @@ void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
     std::vector<double> d0(2 * n_inst);
     DevBuf<double> ctab;  // classical tables (2 n_inst x (N+1))
     if (fast) {
-        ks.resize(2 * n_inst);
-        if (kc.auto_size) {
-            std::vector<fraq_budget_t> bud(2 * n_inst);
-            for (auto& b : bud) b = fraq_budget_t{N, kc.eps_tol, 256, 256, 0.0};
-            build_kernel_auto_dev(c, sbd, 2 * n_inst, gam.data(), tau, bud.data(), ks.data());
-            for (int t = 0; t < 2 * n_inst; ++t) eps[t] = bud[t].achieved_eps;
-        } else {
-            for (int t = 0; t < 2 * n_inst; ++t) {
-                long am;
-                if (sbd) {
-                    const int hh = kc.sbd_head > 0 ? kc.sbd_head : (gam[t] <= 0.5 ? 15 : 17);
-                    build_sbd_kernel_dev(c, gam[t], tau, kc.sbd_points_1, kc.sbd_points_2, hh, &ks[t]);
-                    kernel_error_report_dev(c, &ks[t], N > 8 ? N : 8, nullptr, &eps[t], &am);
-                } else {
-                    build_be_kernel_dev(c, gam[t], tau, kc.be_points, &ks[t]);
-                    kernel_error_report_dev(c, &ks[t], N > 2 ? N : 2, nullptr, &eps[t], &am);
-                }
-            }
-        }
+        build_ffpe_kernels(c, gam, tau, N, sbd, kc, ks, eps);
         for (int t = 0; t < 2 * n_inst; ++t) d0[t] = ks[t].head[0];
     } else {
         ctab.alloc((size_t)2 * n_inst * (N + 1));

@@ -380,7 +380,7 @@ fraq_spec_t flat_spec(const ProblemSpec& s) {
 }
 fraq_kconf_t flat_kconf(const KernelConfig& k) {
     return fraq_kconf_t{k.be_points, k.sbd_points_1, k.sbd_points_2, k.sbd_head, k.eps_tol,
-                        k.auto_size ? 1 : 0};
+                        k.auto_size ? 1 : 0, k.solver};
 }
 int flat_scheme(Scheme s) {
     switch (s) {
@@ -423,6 +423,28 @@ RunResult run(const ProblemSpec& spec, Scheme scheme, const KernelConfig& kconf,
                        rr.final_state.g2.data(), &info));
     }
     rr.final_state.step = spec.n_steps;
+    rr.loop_seconds = info.loop_seconds;
+    rr.setup_seconds = info.setup_seconds;
+    rr.kernel_eps1 = info.kernel_eps1;
+    rr.kernel_eps2 = info.kernel_eps2;
+    return rr;
+}
+
+RunResult run_2d(double alpha1, double alpha2, double coupling_a, int grid_m, double t_final,
+                 long n_steps, Scheme scheme, const std::vector<double>& g1_0,
+                 const std::vector<double>& g2_0, const KernelConfig& kconf) {
+    const size_t mm = (size_t)grid_m * (size_t)grid_m;
+    if (g1_0.size() != mm || g2_0.size() != mm)
+        throw std::invalid_argument("run_2d: initial data must have grid_m^2 entries");
+    const fraq_kconf_t kc = flat_kconf(kconf);
+    RunResult rr;
+    rr.final_state.g1.resize(mm);
+    rr.final_state.g2.resize(mm);
+    fraq_run_info_t info{};
+    check(fraq_run_2d(default_context(), alpha1, alpha2, coupling_a, grid_m, t_final, n_steps,
+                      flat_scheme(scheme), &kc, g1_0.data(), g2_0.data(), rr.final_state.g1.data(),
+                      rr.final_state.g2.data(), &info));
+    rr.final_state.step = n_steps;
     rr.loop_seconds = info.loop_seconds;
     rr.setup_seconds = info.setup_seconds;
     rr.kernel_eps1 = info.kernel_eps1;

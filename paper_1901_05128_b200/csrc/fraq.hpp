@@ -198,6 +198,9 @@ struct KernelConfig {
     int sbd_head = 0;
     double eps_tol = 1e-12;
     bool auto_size = true;
+    // addition: spatial solver of the fast schemes, FRAQ_SOLVER_PHYSICAL (reference-shaped
+    // stencil + block solve) or FRAQ_SOLVER_MODAL (DST eigenbasis, independent modes)
+    int solver = FRAQ_SOLVER_PHYSICAL;
 };
 
 struct RunResult {
@@ -215,6 +218,12 @@ double l2_norm(std::span<const double> v, double h);
 /// device loop does not stream intermediate states back; pass n_steps-limited specs instead).
 RunResult run(const ProblemSpec& spec, Scheme scheme, const KernelConfig& kconf = {},
               const std::function<void(long, const StateField&)>& observer = nullptr);
+
+/// 2D FFPE on the unit square (grid_m^2 interior points, five-point Laplacian), fast schemes,
+/// stepped in the 2D DST eigenbasis.  Data row-major (x fastest).  No reference counterpart.
+RunResult run_2d(double alpha1, double alpha2, double coupling_a, int grid_m, double t_final,
+                 long n_steps, Scheme scheme, const std::vector<double>& g1_0,
+                 const std::vector<double>& g2_0, const KernelConfig& kconf = {});
 
 /// Many independent instances (same grid_m, n_steps, t_final) solved together.
 std::vector<RunResult> run_batch(const std::vector<ProblemSpec>& specs, Scheme scheme,

@@ -711,7 +711,8 @@ void launch_run2(const RunArgs& a, int nw, int num_sms, cudaStream_t s) {
 }  // namespace
 
 // ------------------------------------------------------------------------------ HistDevice
-void HistDevice::build(fraq_ctx c, int n_groups, const fraq_kernel_t* const* ks, const long* dims) {
+void HistDevice::build(fraq_ctx c, int n_groups, const fraq_kernel_t* const* ks, const long* dims,
+                       bool tables_only) {
     groups_h.clear();
     tiles_h.clear();
     kernels.assign(n_groups, fraq_kernel_t{});
@@ -778,8 +779,8 @@ void HistDevice::build(fraq_ctx c, int n_groups, const fraq_kernel_t* const* ks,
     cr.alloc(std::max<size_t>(1, hr.size()));
     cf.alloc(std::max<size_t>(1, hf.size()));
     head.alloc(std::max<size_t>(1, hh.size()));
-    state.alloc(std::max<long>(1, st));
-    ring.alloc(std::max<long>(1, rg));
+    state.alloc(tables_only ? 1 : std::max<long>(1, st));
+    ring.alloc(tables_only ? 1 : std::max<long>(1, rg));
     auto up = [&](void* d, const void* h, size_t bytes) {
         if (bytes) FRAQ_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream));
     };

@@ -88,7 +88,8 @@ struct HistDevice {
     DevBuf<double> frag;
     bool frag_built = false;
 
-    void build(fraq_ctx c, int n_groups, const fraq_kernel_t* const* ks, const long* dims);
+    void build(fraq_ctx c, int n_groups, const fraq_kernel_t* const* ks, const long* dims,
+               bool tables_only = false);
     void launch_step(fraq_ctx c, const StepArgs& a);
     // reset state/ring to zero
     void zero(fraq_ctx c);

@@ -1,0 +1,610 @@
+// modal.cu -- mode-space (DST-diagonalised) fast FFPE stepping, 1D and 2D.
+//
+// With homogeneous Dirichlet data the five-/three-point Laplacian is diagonalised by the type-I
+// discrete sine transform, and every operation of FastStepper (fpfp.cpp:259-349) is linear and
+// DOF-wise, so the scheme decouples exactly into independent modes: per mode k (eigenvalue
+// lambda_k, block_solver.cpp:21-24; 2D: lambda_k + lambda_l) a scalar 2x2 system per level with
+// its own fast history for both fields.  This is the reference's own mode-space oracle
+// (test_fpfp.cpp:21-180, acceptance crit 5) with the fast histories of fast_kernel.cpp in place of
+// the direct sums.  It removes the per-level grid-wide block solve: every mode runs all N levels
+// independently.
+//
+// K11 modal_kernel: one warp per mode; lane l holds node slice l of both fields (z = y / f in
+// registers).  Levels are processed in passes of P (P <= lag L: all feeds G^(n-L) of a pass are
+// known at its start): one node sweep updates the state for the P levels and accumulates
+// P x 2 partial readouts, plus the distributed old part of the exact head window; a warp
+// reduce-scatter produces the sums; then the P levels are solved in order (2x2 Cramer, the new part
+// of the head window, SBD correction), redundantly in every lane -- no barriers at all.
+// K12 dst_kernel: S = sin((k+1)(j+1) pi/(M+1)) applied as a DMMA GEMM (sine generated from an
+// integer-indexed table), forward (x 2/(M+1)) and inverse.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "history.cuh"
+
+namespace fraqcu {
+namespace {
+
+constexpr int MD_CAP = 64;  // max lag (ring of solved levels per mode)
+
+struct ModalField {          // per instance x field
+    const double* r;         // node ratios (J)
+    const double* f;         // feed coefficients (J)
+    const double* head;      // d_0 .. d_{L-1}
+    const double* corr;      // SBD correction sequence corr[e] (e = n-4), nullable
+    int J, L;
+};
+
+struct ModalInst {
+    double a, tau;
+    ModalField fld[2];
+};
+
+struct ModalArgs {
+    const ModalInst* inst;
+    const double* lam;       // eigenvalue per mode (per instance row: lam[m] shared)
+    int n_modes;             // modes per instance
+    int n_inst;
+    long N;
+    int sbd;
+    const double* c0;        // initial coefficients [inst][field][mode]
+    double* cN;              // final coefficients  [inst][field][mode]
+};
+
+// per-warp dynamic shared memory: ring [MD_CAP][2], and (CS) node coefficients [2][2][NPL*32]
+template <int NPL, int P, bool CS>
+__global__ void __launch_bounds__(128) modal_kernel(ModalArgs A) {
+    extern __shared__ double msm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long gw = (long)blockIdx.x * 4 + warp;
+    if (gw >= (long)A.n_modes * A.n_inst) return;
+    const int inst = (int)(gw / A.n_modes), mode = (int)(gw % A.n_modes);
+    const ModalInst I = A.inst[inst];
+    constexpr int per_warp = MD_CAP * 2 + (CS ? 4 * NPL * 32 : 0);
+    double* wsm = msm + (size_t)warp * per_warp;
+    double(*ring)[2] = reinterpret_cast<double(*)[2]>(wsm);
+    double* csm = wsm + MD_CAP * 2;  // [field][r|f][NPL*32]
+    const double lam = A.lam[mode];
+    const double a = I.a, tau = I.tau;
+    // coefficients and state: lane holds nodes j = lane + 32 p of each field
+    double rr[2][CS ? 1 : NPL], ff[2][CS ? 1 : NPL], z[2][NPL];
+#pragma unroll
+    for (int f = 0; f < 2; ++f)
+#pragma unroll
+        for (int p = 0; p < NPL; ++p) {
+            const int j = lane + 32 * p;
+            const bool ok = j < I.fld[f].J;
+            const double rv = ok ? I.fld[f].r[j] : 0.0, fv = ok ? I.fld[f].f[j] : 0.0;
+            if (CS) {
+                csm[(f * 2 + 0) * NPL * 32 + j] = rv;
+                csm[(f * 2 + 1) * NPL * 32 + j] = fv;
+            } else {
+                rr[f][CS ? 0 : p] = rv;
+                ff[f][CS ? 0 : p] = fv;
+            }
+            z[f][p] = 0.0;
+        }
+    __syncwarp();
+    const int L0 = I.fld[0].L, L1 = I.fld[1].L;
+    const int Lmin = min(L0, L1);
+    const double d10 = I.fld[0].head[0], d20 = I.fld[1].head[0];
+    const double g10 = A.c0[((long)inst * 2 + 0) * A.n_modes + mode];
+    const double g20 = A.c0[((long)inst * 2 + 1) * A.n_modes + mode];
+    // ring[n % CAP] = G^n (both fields); G^0 kept separately for the SBD correction
+    if (lane == 0) {
+        ring[0][0] = g10;
+        ring[0][1] = g20;
+    }
+    __syncwarp();
+    const double al = a + lam;
+    // main system (lead 1 for BE, 1.5 for SBD) -- Cramer like the reference's oracle
+    const double lead = A.sbd ? 1.5 : 1.0;
+    const double m11 = lead / tau + d10 * al, m12 = -a * d20, m21 = -a * d10,
+                 m22 = lead / tau + d20 * al;
+    const double det = m11 * m22 - m12 * m21;
+    double gprev1 = g10, gprev2 = g20, gpp1 = 0.0, gpp2 = 0.0;  // G^{n-1}, G^{n-2}
+    long n = 1;
+    if (A.sbd) {
+        // first step: 2/3 - 1/3 system (fpfp.cpp:293-308), no history contribution
+        const double f11 = 1.0 / tau + (2.0 / 3.0) * d10 * al, f12 = -(2.0 / 3.0) * a * d20;
+        const double f21 = -(2.0 / 3.0) * a * d10, f22 = 1.0 / tau + (2.0 / 3.0) * d20 * al;
+        const double r1 = g10 / tau - (d10 / 3.0) * al * g10 + (a * d20 / 3.0) * g20;
+        const double r2 = g20 / tau - (d20 / 3.0) * al * g20 + (a * d10 / 3.0) * g10;
+        const double dt = f11 * f22 - f12 * f21;
+        const double x1 = (r1 * f22 - f12 * r2) / dt, x2 = (f11 * r2 - f21 * r1) / dt;
+        if (lane == 0) {
+            ring[1][0] = x1;
+            ring[1][1] = x2;
+        }
+        __syncwarp();
+        gpp1 = gprev1;
+        gpp2 = gprev2;
+        gprev1 = x1;
+        gprev2 = x2;
+        // level 1 advanced the (zero) accumulators without a feed: nothing to do
+        n = 2;
+    }
+    while (n <= A.N) {
+        const int pcount = (int)min((long)P, A.N - n + 1);
+        // ---- node sweep for levels n .. n + pcount - 1 (feeds G^(n+k-L), lo = 1)
+        double part[P][2];
+#pragma unroll
+        for (int k = 0; k < P; ++k) part[k][0] = part[k][1] = 0.0;
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+            const int L = f ? L1 : L0;
+            double v[P];
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+                const long src = n + k - L;
+                v[k] = (k < pcount && src >= 1) ? ring[src % MD_CAP][f] : 0.0;
+            }
+#pragma unroll
+            for (int p = 0; p < NPL; ++p) {
+                const double rp = CS ? csm[(f * 2 + 0) * NPL * 32 + lane + 32 * p] : rr[f][CS ? 0 : p];
+                const double fp = CS ? csm[(f * 2 + 1) * NPL * 32 + lane + 32 * p] : ff[f][CS ? 0 : p];
+                double zz = z[f][p];
+#pragma unroll
+                for (int k = 0; k < P; ++k) {
+                    if (k < pcount) {
+                        zz = fma(rp, zz, v[k]);
+                        part[k][f] = fma(fp, zz, part[k][f]);
+                    }
+                }
+                z[f][p] = zz;
+            }
+            // old part of the exact head window: taps i > k (levels solved before this pass);
+            // lane handles taps i = lane + 1 (+32)
+            const double* hd = I.fld[f].head;
+            for (int i = lane + 1; i < L; i += 32) {
+                const double h = hd[i];
+#pragma unroll
+                for (int k = 0; k < P; ++k) {
+                    const long src = n + k - i;
+                    // BE: only d_1 G^{n-1} for n >= 2 (fpfp.cpp:270-275); SBD: i <= n - 1
+                    if (k < pcount && i > k && src >= (A.sbd ? 1 : 1) &&
+                        (A.sbd || i == 1))
+                        part[k][f] = fma(h, ring[src % MD_CAP][f], part[k][f]);
+                }
+            }
+        }
+        // ---- warp all-reduce of the 2P partials (butterfly)
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+#pragma unroll
+            for (int f = 0; f < 2; ++f) {
+                double s = part[k][f];
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                part[k][f] = s;
+            }
+        // ---- sequential solves of the pass
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            if (k < pcount) {
+                const long nn = n + k;
+                double s1 = part[k][0], s2 = part[k][1];
+                // new part of the head window: taps i = 1..k (levels solved in this pass)
+                for (int i = 1; i <= k; ++i) {
+                    const long src = nn - i;
+                    if (A.sbd) {
+                        if (i < L0 && src >= 1) s1 = fma(I.fld[0].head[i], ring[src % MD_CAP][0], s1);
+                        if (i < L1 && src >= 1) s2 = fma(I.fld[1].head[i], ring[src % MD_CAP][1], s2);
+                    } else if (i == 1 && src >= 1) {
+                        s1 = fma(I.fld[0].head[1], ring[src % MD_CAP][0], s1);
+                        s2 = fma(I.fld[1].head[1], ring[src % MD_CAP][1], s2);
+                    }
+                }
+                double r1, r2;
+                if (A.sbd) {
+                    // (1/2) d_{n-1} G^0 (exact head inside, reconstructed beyond: fpfp.cpp:327-334)
+                    const double c1 = (nn - 1 < L0) ? I.fld[0].head[nn - 1] : I.fld[0].corr[nn - 4];
+                    const double c2 = (nn - 1 < L1) ? I.fld[1].head[nn - 1] : I.fld[1].corr[nn - 4];
+                    s1 = fma(0.5 * c1, g10, s1);
+                    s2 = fma(0.5 * c2, g20, s2);
+                    r1 = (2.0 * gprev1 - 0.5 * gpp1) / tau - al * s1 + a * s2;
+                    r2 = (2.0 * gprev2 - 0.5 * gpp2) / tau - al * s2 + a * s1;
+                } else {
+                    r1 = gprev1 / tau - al * s1 + a * s2;
+                    r2 = gprev2 / tau - al * s2 + a * s1;
+                }
+                const double x1 = (r1 * m22 - m12 * r2) / det;
+                const double x2 = (m11 * r2 - m21 * r1) / det;
+                if (lane == 0) {
+                    ring[nn % MD_CAP][0] = x1;
+                    ring[nn % MD_CAP][1] = x2;
+                }
+                __syncwarp();
+                gpp1 = gprev1;
+                gpp2 = gprev2;
+                gprev1 = x1;
+                gprev2 = x2;
+            }
+        }
+        n += pcount;
+    }
+    (void)Lmin;
+    if (lane == 0) {
+        A.cN[((long)inst * 2 + 0) * A.n_modes + mode] = gprev1;
+        A.cN[((long)inst * 2 + 1) * A.n_modes + mode] = gprev2;
+    }
+}
+
+// ------------------------------------------------------------------------------ K12 DST on DMMA
+// Out[k][c] = scale * sum_j sin((k+1)(j+1) pi / (M+1)) In[j][c]  (In: M x C row-major, ldc = C)
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+constexpr int ST_M = 64, ST_N = 64, ST_K = 16;
+
+__global__ void __launch_bounds__(128) dst_kernel(const double* __restrict__ sintab, int M,
+                                                  const double* __restrict__ In, long ldi,
+                                                  long C, double* Out, long ldo, double scale) {
+    __shared__ double sA[ST_M][ST_K + 1];
+    __shared__ double sB[ST_K][ST_N + 1];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const long k0 = (long)blockIdx.y * ST_M, c0 = (long)blockIdx.x * ST_N;
+    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+    const int g = lane >> 2, t = lane & 3;
+    const long period = 2L * (M + 1);
+    double acc[4][4][2];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    for (long j0 = 0; j0 < M; j0 += ST_K) {
+        __syncthreads();
+        for (int idx = tid; idx < ST_M * ST_K; idx += 128) {
+            const int r = idx / ST_K, cc = idx % ST_K;
+            const long k = k0 + r, j = j0 + cc;
+            sA[r][cc] = (k < M && j < M) ? sintab[((k + 1) * (j + 1)) % period] : 0.0;
+        }
+        for (int idx = tid; idx < ST_K * ST_N; idx += 128) {
+            const int r = idx / ST_N, cc = idx % ST_N;
+            const long j = j0 + r, c = c0 + cc;
+            sB[r][cc] = (j < M && c < C) ? In[j * ldi + c] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < ST_K; kk += 4) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) af[x] = sA[wm + 8 * x + g][kk + t];
+#pragma unroll
+            for (int y = 0; y < 4; ++y) bf[y] = sB[kk + t][wn + 8 * y + g];
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+#pragma unroll
+                for (int y = 0; y < 4; ++y) dmma884(acc[x][y], af[x], bf[y]);
+        }
+    }
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const long k = k0 + wm + 8 * x + g, c = c0 + wn + 8 * y + 2 * t + e;
+                if (k < M && c < C) Out[k * ldo + c] = scale * acc[x][y][e];
+            }
+}
+
+__global__ void sintab_kernel(double* tab, int M) {
+    const long period = 2L * (M + 1);
+    const double pi = 3.14159265358979323846;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < period;
+         i += (long)gridDim.x * blockDim.x)
+        tab[i] = sin(pi * (double)i / (double)(M + 1));
+}
+
+__global__ void transpose_kernel(const double* in, long rows, long cols, double* out) {
+    __shared__ double tile[32][33];
+    const long bx = (long)blockIdx.x * 32, by = (long)blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const long r = by + i, c = bx + threadIdx.x;
+        if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * cols + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const long r = bx + i, c = by + threadIdx.x;
+        if (r < cols && c < rows) out[r * rows + c] = tile[threadIdx.x][i];
+    }
+}
+
+template <int NPL, int P, bool CS>
+void launch_modal_t(const ModalArgs& a, cudaStream_t s) {
+    const long warps = (long)a.n_modes * a.n_inst;
+    const size_t smem = sizeof(double) * 4 * (MD_CAP * 2 + (CS ? 4 * NPL * 32 : 0));
+    if (smem > 48 * 1024)
+        FRAQ_CUDA(cudaFuncSetAttribute(modal_kernel<NPL, P, CS>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    modal_kernel<NPL, P, CS><<<(unsigned)((warps + 3) / 4), 128, smem, s>>>(a);
+}
+
+void launch_modal(int npl, int P, const ModalArgs& a, cudaStream_t s) {
+    if (P == 8) {
+        if (npl <= 4) launch_modal_t<4, 8, false>(a, s);
+        else if (npl <= 8) launch_modal_t<8, 8, false>(a, s);
+        else launch_modal_t<16, 8, true>(a, s);
+    } else {
+        if (npl <= 4) launch_modal_t<4, 2, false>(a, s);
+        else if (npl <= 8) launch_modal_t<8, 2, false>(a, s);
+        else launch_modal_t<16, 2, true>(a, s);
+    }
+    FRAQ_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+// Apply the DST along the mode axis: Out (M x C) = scale * S In (M x C).
+void dst_apply(fraq_ctx c, int M, const double* sintab, const double* In, long C, double* Out,
+               double scale) {
+    dim3 grid((unsigned)((C + ST_N - 1) / ST_N), (unsigned)((M + ST_M - 1) / ST_M));
+    dst_kernel<<<grid, 128, 0, c->stream>>>(sintab, M, In, C, C, Out, C, scale);
+    FRAQ_LAUNCH_CHECK();
+}
+
+void transpose_dev(fraq_ctx c, const double* in, long rows, long cols, double* out) {
+    dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+    transpose_kernel<<<grid, dim3(32, 8), 0, c->stream>>>(in, rows, cols, out);
+    FRAQ_LAUNCH_CHECK();
+}
+
+void make_sintab(fraq_ctx c, int M, DevBuf<double>& tab) {
+    tab.alloc((size_t)2 * (M + 1));
+    sintab_kernel<<<64, 256, 0, c->stream>>>(tab.p, M);
+    FRAQ_LAUNCH_CHECK();
+}
+
+// Mode-space stepping of n_inst instances with per-instance kernels (device tables already in
+// HistDevice hd: group 2i = field 1, 2i+1 = field 2 of instance i).  c0 / cN: [inst][2][modes].
+void modal_run(fraq_ctx c, const HistDevice& hd, const std::vector<double>& a,
+               const std::vector<double>& tau, const double* corr, const std::vector<long>& corr_off,
+               const double* lam, int n_modes, int n_inst, long N, bool sbd, const double* c0,
+               double* cN) {
+    std::vector<ModalInst> mi(n_inst);
+    int maxJ = 0, minL = 1 << 30;
+    for (int i = 0; i < n_inst; ++i) {
+        mi[i].a = a[i];
+        mi[i].tau = tau[i];
+        for (int f = 0; f < 2; ++f) {
+            const GroupDev& G = hd.groups_h[2 * i + f];
+            ModalField& F = mi[i].fld[f];
+            F.r = hd.cr.p + G.co_off;
+            F.f = hd.cf.p + G.co_off;
+            F.head = hd.head.p + G.hd_off;
+            F.corr = (sbd && corr) ? corr + corr_off[2 * i + f] : nullptr;
+            F.J = G.J;
+            F.L = G.L;
+            maxJ = std::max(maxJ, G.J);
+            minL = std::min(minL, G.L);
+            if (G.L > MD_CAP - 8) fail(FRAQ_EINVAL, "modal run: head window longer than 56 levels");
+        }
+    }
+    DevBuf<ModalInst> dmi(n_inst);
+    FRAQ_CUDA(cudaMemcpyAsync(dmi.p, mi.data(), sizeof(ModalInst) * n_inst, cudaMemcpyHostToDevice,
+                              c->stream));
+    ModalArgs A{dmi.p, lam, n_modes, n_inst, N, sbd ? 1 : 0, c0, cN};
+    const int npl = (maxJ + 31) / 32;
+    if (npl > 16) fail(FRAQ_EINVAL, "modal run: more than 512 nodes per field");
+    launch_modal(npl, minL >= 8 ? 8 : 2, A, c->stream);
+    FRAQ_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+}  // namespace fraqcu
+
+// ============================================================================ host drivers
+namespace fraqcu {
+
+void build_ffpe_kernels(fraq_ctx c, const std::vector<double>& gam, double tau, long N, bool sbd,
+                        const fraq_kconf_t& kc, std::vector<fraq_kernel_t>& ks,
+                        std::vector<double>& eps);
+
+namespace {
+
+double now_s2() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// Shared tail of the 1D and 2D drivers: kernel tables, SBD correction sequences, stepping.
+// coef0 / coefN: [inst][2][modes] (device).
+struct ModalSetup {
+    std::vector<fraq_kernel_t> ks;
+    std::vector<double> eps;
+    HistDevice hd;
+    DevBuf<double> corr;
+    std::vector<long> corr_off;
+};
+
+void modal_prepare(fraq_ctx c, ModalSetup& S, const std::vector<double>& gam, double tau, long N,
+                   bool sbd, const fraq_kconf_t& kc) {
+    build_ffpe_kernels(c, gam, tau, N, sbd, kc, S.ks, S.eps);
+    const int ng = (int)gam.size();
+    std::vector<const fraq_kernel_t*> kp(ng);
+    std::vector<long> dims(ng, 1);
+    for (int t = 0; t < ng; ++t) kp[t] = &S.ks[t];
+    S.hd.build(c, ng, kp.data(), dims.data(), /*tables_only=*/true);
+    S.corr_off.assign(ng, 0);
+    if (sbd) {
+        S.corr.alloc((size_t)ng * (N + 1));
+        for (int t = 0; t < ng; ++t) {
+            corr_sequence_dev(c, &S.ks[t], N, S.corr.p + (size_t)t * (N + 1));
+            S.corr_off[t] = (long)t * (N + 1);
+        }
+    }
+}
+
+void fill_info(fraq_run_info_t* info, const ModalSetup& S, double loop_s, double setup_s) {
+    if (!info) return;
+    info->loop_seconds = loop_s;
+    info->setup_seconds = setup_s;
+    info->kernel_eps1 = S.eps[0];
+    info->kernel_eps2 = S.eps[1];
+    info->np[0] = S.ks[0].np1;
+    info->np[1] = S.ks[0].np2;
+    info->np[2] = S.ks[1].np1;
+    info->np[3] = S.ks[1].np2;
+    info->n_head[0] = S.ks[0].n_head;
+    info->n_head[1] = S.ks[1].n_head;
+}
+
+}  // namespace
+
+// 1D: n_inst instances sharing grid_m, n_steps, t_final.
+void ffpe_run_modal(fraq_ctx c, const fraq_spec_t* specs, int n_inst, bool sbd,
+                    const fraq_kconf_t& kc, double* g1_out, double* g2_out,
+                    fraq_run_info_t* info) {
+    const double t0 = now_s2();
+    const int M = specs[0].grid_m;
+    const long N = specs[0].n_steps;
+    const double tau = specs[0].t_final / double(N);
+    const double h = specs[0].length / double(M + 1);
+    const long C = 2L * n_inst;
+    // initial data, column c = 2 inst + field, row = grid point
+    std::vector<double> G0((size_t)M * C);
+    std::vector<double> gam(C), av(n_inst), tv(n_inst, tau);
+    for (int i = 0; i < n_inst; ++i) {
+        const fraq_spec_t& s = specs[i];
+        for (int j = 0; j < M; ++j) {
+            const double x = (j + 1) * h;
+            double v1, v2;
+            if (s.initial == FRAQ_POLY_SIN) {
+                v1 = x * (1.0 - x);
+                v2 = std::sin(x);
+            } else if (s.initial == FRAQ_INDICATOR) {
+                v1 = x > 0.5 ? 1.0 - x : 0.0;
+                v2 = x < 0.5 ? x : 0.0;
+            } else {
+                v1 = s.custom_g1[j];
+                v2 = s.custom_g2[j];
+            }
+            G0[(size_t)j * C + 2 * i] = v1;
+            G0[(size_t)j * C + 2 * i + 1] = v2;
+        }
+        gam[2 * i] = 1.0 - s.alpha1;
+        gam[2 * i + 1] = 1.0 - s.alpha2;
+        av[i] = s.coupling_a;
+    }
+    ModalSetup S;
+    modal_prepare(c, S, gam, tau, N, sbd, kc);
+    // eigenvalues lambda_k = (4/h^2) sin^2(k pi h / (2 L)) (block_solver.cpp:21-24)
+    std::vector<double> lam(M);
+    for (int k = 0; k < M; ++k) {
+        const double sk = std::sin((k + 1) * 3.14159265358979323846 * h / (2.0 * specs[0].length));
+        lam[k] = 4.0 / (h * h) * sk * sk;
+    }
+    DevBuf<double> dlam(M), dG((size_t)M * C), dW((size_t)M * C), dc0((size_t)M * C),
+        dcN((size_t)M * C), tab;
+    FRAQ_CUDA(cudaMemcpyAsync(dlam.p, lam.data(), sizeof(double) * M, cudaMemcpyHostToDevice, c->stream));
+    FRAQ_CUDA(cudaMemcpyAsync(dG.p, G0.data(), sizeof(double) * G0.size(), cudaMemcpyHostToDevice,
+                              c->stream));
+    make_sintab(c, M, tab);
+    const double t1 = now_s2();
+    cudaEvent_t e0, e1;
+    FRAQ_CUDA(cudaEventCreate(&e0));
+    FRAQ_CUDA(cudaEventCreate(&e1));
+    FRAQ_CUDA(cudaEventRecord(e0, c->stream));
+    // forward DST (projection, 2/(M+1) S G): rows = modes; then [C][M] for the stepper
+    dst_apply(c, M, tab.p, dG.p, C, dW.p, 2.0 / (M + 1));
+    transpose_dev(c, dW.p, M, C, dc0.p);
+    modal_run(c, S.hd, av, tv, sbd ? S.corr.p : nullptr, S.corr_off, dlam.p, M, n_inst, N, sbd,
+              dc0.p, dcN.p);
+    // inverse: g = S^T c (S symmetric)
+    transpose_dev(c, dcN.p, C, M, dW.p);
+    dst_apply(c, M, tab.p, dW.p, C, dG.p, 1.0);
+    FRAQ_CUDA(cudaEventRecord(e1, c->stream));
+    FRAQ_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    FRAQ_CUDA(cudaMemcpy(G0.data(), dG.p, sizeof(double) * G0.size(), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n_inst; ++i)
+        for (int j = 0; j < M; ++j) {
+            g1_out[(size_t)i * M + j] = G0[(size_t)j * C + 2 * i];
+            g2_out[(size_t)i * M + j] = G0[(size_t)j * C + 2 * i + 1];
+        }
+    fill_info(info, S, ms * 1e-3, t1 - t0);
+}
+
+// 2D: modes (k, l) with lambda_k + lambda_l; forward transform c = (2/(M+1))^2 S G S, inverse
+// g = S c S (S symmetric); data row-major (x fastest): G[y][x].
+void ffpe_run_2d(fraq_ctx c, double alpha1, double alpha2, double a, int M, double t_final,
+                 long N, int scheme, const fraq_kconf_t* kc_in, const double* g1_0,
+                 const double* g2_0, double* g1, double* g2, fraq_run_info_t* info) {
+    if (M < 1 || N < 1) fail(FRAQ_EINVAL, "run_2d: grid_m and n_steps must be >= 1");
+    if (scheme != FRAQ_FASTBE && scheme != FRAQ_FASTSBD)
+        fail(FRAQ_EINVAL, "run_2d: scheme must be FastBE or FastSBD");
+    fraq_kconf_t kc;
+    if (kc_in)
+        kc = *kc_in;
+    else
+        fraq_kconf_default(&kc);
+    const bool sbd = scheme == FRAQ_FASTSBD;
+    const double t0 = now_s2();
+    const double tau = t_final / double(N);
+    const double h = 1.0 / double(M + 1);
+    const long MM = (long)M * M;
+    ModalSetup S;
+    modal_prepare(c, S, {1.0 - alpha1, 1.0 - alpha2}, tau, N, sbd, kc);
+    std::vector<double> lam1(M), lam2(MM);
+    for (int k = 0; k < M; ++k) {
+        const double sk = std::sin((k + 1) * 3.14159265358979323846 * h / 2.0);
+        lam1[k] = 4.0 / (h * h) * sk * sk;
+    }
+    for (int ky = 0; ky < M; ++ky)
+        for (int kx = 0; kx < M; ++kx) lam2[(size_t)ky * M + kx] = lam1[ky] + lam1[kx];
+    DevBuf<double> dlam(MM), dA(2 * MM), dB(2 * MM), dc0(2 * MM), dcN(2 * MM), tab;
+    FRAQ_CUDA(cudaMemcpyAsync(dlam.p, lam2.data(), sizeof(double) * MM, cudaMemcpyHostToDevice,
+                              c->stream));
+    FRAQ_CUDA(cudaMemcpyAsync(dA.p, g1_0, sizeof(double) * MM, cudaMemcpyHostToDevice, c->stream));
+    FRAQ_CUDA(cudaMemcpyAsync(dA.p + MM, g2_0, sizeof(double) * MM, cudaMemcpyHostToDevice,
+                              c->stream));
+    make_sintab(c, M, tab);
+    const double t1 = now_s2();
+    cudaEvent_t e0, e1;
+    FRAQ_CUDA(cudaEventCreate(&e0));
+    FRAQ_CUDA(cudaEventCreate(&e1));
+    FRAQ_CUDA(cudaEventRecord(e0, c->stream));
+    const double sc = 2.0 / (M + 1);
+    // per field: Y = S G (along y), Z = S Y^T (along x), coefficients c[kx][ky] = Z -> stored
+    // as c[ky][kx] = Z^T after the second transpose
+    for (int f = 0; f < 2; ++f) {
+        double* G = dA.p + f * MM;
+        double* Y = dB.p + f * MM;
+        dst_apply(c, M, tab.p, G, M, Y, sc);      // Y[ky][x]
+        transpose_dev(c, Y, M, M, G);              // G <- Y^T [x][ky]
+        dst_apply(c, M, tab.p, G, M, Y, sc);      // Y[kx][ky]
+        transpose_dev(c, Y, M, M, dc0.p + f * MM); // c0[ky][kx]
+    }
+    modal_run(c, S.hd, {a}, {tau}, sbd ? S.corr.p : nullptr, S.corr_off, dlam.p, (int)MM, 1, N,
+              sbd, dc0.p, dcN.p);
+    for (int f = 0; f < 2; ++f) {
+        double* Cc = dcN.p + f * MM;   // [ky][kx]
+        double* Y = dB.p + f * MM;
+        double* G = dA.p + f * MM;
+        dst_apply(c, M, tab.p, Cc, M, Y, 1.0);    // Y[y][kx] = sum_ky S[y][ky] c[ky][kx]
+        transpose_dev(c, Y, M, M, G);              // [kx][y]
+        dst_apply(c, M, tab.p, G, M, Y, 1.0);     // [x][y]
+        transpose_dev(c, Y, M, M, G);              // [y][x]
+    }
+    FRAQ_CUDA(cudaEventRecord(e1, c->stream));
+    FRAQ_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    FRAQ_CUDA(cudaMemcpy(g1, dA.p, sizeof(double) * MM, cudaMemcpyDeviceToHost));
+    FRAQ_CUDA(cudaMemcpy(g2, dA.p + MM, sizeof(double) * MM, cudaMemcpyDeviceToHost));
+    fill_info(info, S, ms * 1e-3, t1 - t0);
+}
+
+}  // namespace fraqcu

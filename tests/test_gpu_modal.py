@@ -1,0 +1,97 @@
+"""GPU: mode-space (DST) FFPE stepping, 1D (solver=MODAL) and 2D (BASELINE C4).
+
+1D: equals the reference's physical-space FastStepper (oracle/_ref) on well-conditioned grids,
+and the fp64 mode-space evaluation at the C3 grid.  2D: equals the numpy restatement of the
+FastStepper algebra with the five-point Laplacian (tests/ffpe_refs.py) on small grids."""
+import numpy as np
+import pytest
+
+from ffpe_refs import fast_stepper_nd, modespace_fastbe
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def orc():
+    from oracle.oracle import Oracle, ref_available
+    return Oracle("reference" if ref_available() else "port")
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return np.max(np.abs(a - b)) / np.max(np.abs(b))
+
+
+def modal_kc(fraq, **kw):
+    kc = fraq.KernelConfig()
+    kc.solver = fraq.SOLVER_MODAL
+    for k, v in kw.items():
+        setattr(kc, k, v)
+    return kc
+
+
+@pytest.mark.parametrize("scheme", ["FastBE", "FastSBD"])
+@pytest.mark.parametrize("m,a,init", [(31, -1.0, "indicator"), (63, 2.0, "poly_sin"),
+                                      (50, 0.5, "poly_sin"), (127, -2.0, "indicator")])
+def test_modal_1d_matches_reference(fraq, orc, scheme, m, a, init):
+    spec = fraq.ProblemSpec(alpha1=0.3, alpha2=0.65, coupling_a=a, grid_m=m, t_final=0.5,
+                            n_steps=96, initial=init)
+    rr = fraq.run(spec, getattr(fraq.Scheme, scheme), modal_kc(fraq))
+    g1, g2, e1, e2 = orc.run(0.3, 0.65, a, m, 0.5, 96, scheme, init)
+    assert rel(rr.final_state.g1, g1) <= 1e-10
+    assert rel(rr.final_state.g2, g2) <= 1e-10
+    assert rr.kernel_eps1 == pytest.approx(e1, rel=1e-3)
+
+
+def test_modal_1d_fixed_kernels_and_batch(fraq, orc):
+    kc = modal_kc(fraq, auto_size=False, be_points=24, sbd_points_1=24, sbd_points_2=24, sbd_head=9)
+    kconf = dict(auto_size=False, be_points=24, sbd_points_1=24, sbd_points_2=24, sbd_head=9)
+    specs = [fraq.ProblemSpec(alpha1=0.2 + 0.15 * i, alpha2=0.7 - 0.1 * i, coupling_a=1.0 - i,
+                              grid_m=31, t_final=0.5, n_steps=64, initial="indicator")
+             for i in range(3)]
+    for scheme in ("FastBE", "FastSBD"):
+        outs = fraq.run_batch(specs, getattr(fraq.Scheme, scheme), kc)
+        for s, o in zip(specs, outs):
+            g1, g2, _, _ = orc.run(s.alpha1, s.alpha2, s.coupling_a, 31, 0.5, 64, scheme,
+                                   "indicator", kconf=kconf)
+            assert rel(o.final_state.g1, g1) <= 1e-10
+            assert rel(o.final_state.g2, g2) <= 1e-10
+
+
+def test_modal_rejects_classical_and_observer(fraq):
+    spec = fraq.ProblemSpec(alpha1=0.3, alpha2=0.6, grid_m=15, n_steps=8)
+    with pytest.raises(ValueError):
+        fraq.run(spec, fraq.Scheme.BE, modal_kc(fraq))
+
+
+@pytest.mark.slow
+def test_modal_c3_full_against_fp64_modespace(fraq, orc):
+    """C3 (M = 4095, N = 16384, FastBE): the modal GPU solver equals the fp64 mode-space
+    evaluation to ~1e-13 (the physical-space paths carry ~5e-8 rounding drift here)."""
+    from paper_1901_05128_b200.workloads import c3_instance
+    inst = c3_instance()
+    spec = fraq.ProblemSpec(alpha1=0.4, alpha2=0.8, coupling_a=-5.5, grid_m=4095, t_final=1.0,
+                            n_steps=16384, initial="custom", custom_g1=list(inst.g1),
+                            custom_g2=list(inst.g2))
+    rr = fraq.run(spec, fraq.Scheme.FastBE, modal_kc(fraq))
+    t1, t2 = modespace_fastbe(orc, inst.g1, inst.g2, 4095, 16384, -5.5, 0.4, 0.8)
+    ad = max(np.max(np.abs(np.array(rr.final_state.g1) - t1)),
+             np.max(np.abs(np.array(rr.final_state.g2) - t2)))
+    assert ad <= 1e-11
+
+
+@pytest.mark.parametrize("scheme", ["FastBE", "FastSBD"])
+@pytest.mark.parametrize("m,a", [(7, -3.0), (15, 2.0)])
+def test_2d_matches_physical_restatement(fraq, orc, scheme, m, a):
+    rng = np.random.default_rng(1901051284)
+    h = 1.0 / (m + 1)
+    x = (np.arange(m) + 1) * h
+    X, Y = np.meshgrid(x, x)                            # row-major, x fastest
+    g1 = ((X <= 0.5) & (Y <= 0.5)).astype(float).ravel()  # indicator of [0, 1/2]^2 (closed)
+    g2 = (1.0 + rng.uniform(-0.1, 0.1, m * m))
+    N, T = 48, 0.25
+    sbd = scheme == "FastSBD"
+    r1, r2 = fast_stepper_nd(orc, 0.3, 0.6, a, m, 2, T, N, sbd, g1, g2)
+    out = fraq.run_2d(0.3, 0.6, a, m, T, N, getattr(fraq.Scheme, scheme), g1, g2)
+    assert rel(out.final_state.g1, r1) <= 1e-10
+    assert rel(out.final_state.g2, r2) <= 1e-10
