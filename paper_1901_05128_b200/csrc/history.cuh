@@ -95,4 +95,17 @@ struct HistDevice {
     void zero(fraq_ctx c);
 };
 
+// K13 (modal_dmma.cu): mode-space FFPE stepping on DMMA; one entry per instance (device pointers).
+struct K13Inst {
+    double a, tau;
+    const double* r[2];
+    const double* f[2];
+    const double* head[2];
+    const double* corr[2];  // SBD correction sequence corr[n-4], nullable for BE
+    int J[2], L[2];
+};
+bool k13_supported(int maxJ, int minL, int maxL);
+void k13_run(fraq_ctx c, const std::vector<K13Inst>& in, const double* lam, int n_modes, long N,
+             bool sbd, const double* c0, double* cN);
+
 }  // namespace fraqcu

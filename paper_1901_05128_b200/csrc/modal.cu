@@ -28,6 +28,7 @@
 #include "history.cuh"
 
 namespace fraqcu {
+
 namespace {
 
 constexpr int MD_CAP = 64;  // max lag (ring of solved levels per mode)
@@ -371,7 +372,7 @@ void modal_run(fraq_ctx c, const HistDevice& hd, const std::vector<double>& a,
                const double* lam, int n_modes, int n_inst, long N, bool sbd, const double* c0,
                double* cN) {
     std::vector<ModalInst> mi(n_inst);
-    int maxJ = 0, minL = 1 << 30;
+    int maxJ = 0, minL = 1 << 30, maxL = 0;
     for (int i = 0; i < n_inst; ++i) {
         mi[i].a = a[i];
         mi[i].tau = tau[i];
@@ -386,8 +387,26 @@ void modal_run(fraq_ctx c, const HistDevice& hd, const std::vector<double>& a,
             F.L = G.L;
             maxJ = std::max(maxJ, G.J);
             minL = std::min(minL, G.L);
+            maxL = std::max(maxL, G.L);
             if (G.L > MD_CAP - 8) fail(FRAQ_EINVAL, "modal run: head window longer than 56 levels");
         }
+    }
+    if (k13_supported(maxJ, minL, maxL)) {
+        std::vector<K13Inst> ki(n_inst);
+        for (int i = 0; i < n_inst; ++i) {
+            ki[i].a = a[i];
+            ki[i].tau = tau[i];
+            for (int f = 0; f < 2; ++f) {
+                ki[i].r[f] = mi[i].fld[f].r;
+                ki[i].f[f] = mi[i].fld[f].f;
+                ki[i].head[f] = mi[i].fld[f].head;
+                ki[i].corr[f] = mi[i].fld[f].corr;
+                ki[i].J[f] = mi[i].fld[f].J;
+                ki[i].L[f] = mi[i].fld[f].L;
+            }
+        }
+        k13_run(c, ki, lam, n_modes, N, sbd, c0, cN);
+        return;
     }
     DevBuf<ModalInst> dmi(n_inst);
     FRAQ_CUDA(cudaMemcpyAsync(dmi.p, mi.data(), sizeof(ModalInst) * n_inst, cudaMemcpyHostToDevice,

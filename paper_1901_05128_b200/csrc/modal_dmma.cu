@@ -1,0 +1,470 @@
+// modal_dmma.cu -- K13: mode-space FFPE stepping on the fp64 tensor cores.
+//
+// Same scheme as K11 (modal.cu: per mode k a 2x2 system per level with a fast history per field,
+// the reference's FastStepper algebra fpfp.cpp:259-349 in the DST eigenbasis), re-blocked the way
+// K5d (history_dmma.cu) blocks the standalone history: 8 levels per block, node contractions as
+// DMMA GEMMs over a CTA tile of 16 modes x all nodes of both fields.
+//
+// Per field, with the history state y_j at level n0 - 1 - 8 delta (block start n0):
+//
+//   s(n0+k) = sum_j r_j^(k+1+8 delta) y_j  +  sum_{m=1}^{k+8 delta+L} c_m G^(n0+k-m)   (G^q, q >= 1)
+//
+// where c_m are the combined CQ weights of the scheme: the exact head d_m for m < L
+// (fpfp.cpp:270-275 BE, 313-324 SBD) and the compressed tail w_(m-L) = sum_j f_j r_j^(m-L) for
+// m >= L (the feed G^(n-L) enters y at level n, fast_kernel.cpp:268-289,343-365).  The first term
+// is the readout GEMM; the second is a short Toeplitz sum over solved levels.  The state moves
+// 8 levels per block: y <- r^8 (.) y + R V (R_ij = f_j r_j^(7-i), V = the block's 8 feeds).
+//
+// Warp specialisation: nwg GEMM warps (64 nodes of one field each; state in DMMA accumulator
+// fragments, as in K5d) and one solver warp.  The GEMM warps run one block ahead of the solver:
+// in iteration i they advance the state by block i-1-delta and issue the readout of block i,
+// while the solver reduces the partials of block i-1, adds the Toeplitz terms, and solves its 8
+// levels in order (one lane per mode, 2x2 Cramer, SBD correction 1/2 c_n G^0 of
+// fpfp.cpp:327-334).  delta = 0 when the lag L >= 8 (SBD: every feed of block i-1 is at least
+// 9 levels old), delta = 1 otherwise (BE, L = 2): the state then trails the readout by 8 more
+// levels, with readout table r^(k+9).  One __syncthreads per block separates the two roles.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <vector>
+
+#include "history.cuh"
+
+namespace fraqcu {
+
+namespace {
+
+constexpr int K13_CW = 64;  // combined weights c_m, m < 64
+
+struct K13Dev {
+    double a, itau;
+    const double* corr[2];
+    int L[2];
+};
+
+struct K13Args {
+    const K13Dev* inst;
+    const double* tabs;   // per (inst, field): TS doubles
+    int TS, Jp, nwf, nwg;
+    const double* lam;
+    int n_modes, nmb;
+    long n_tasks;
+    long N;
+    int sbd, delta, ring_mask;
+    const double* c0;     // [inst][2][modes]
+    double* cN;
+    int* counter;
+};
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+struct K13TabSrc {
+    const double* r;
+    const double* f;
+    const double* head;
+    int J, L;
+};
+
+// Tables of one (instance, field), CTA of 256 threads:
+//   C  [Jp/8][2][32]  readout B fragments: r_j^(g+1+8 delta), j = 8 nt + 2t + e
+//   R  [Jp/8][2][32]  state B fragments: f_j r_j^(7-4h-t), j = 8 nt + g
+//   R8 [Jp]           r_j^8 (natural node order == accumulator fragment order)
+//   CW [64]           combined weights c_m
+__global__ void k13_tables_kernel(const K13TabSrc* src, int Jp, int delta, double* tabs, int TS) {
+    const K13TabSrc S = src[blockIdx.x];
+    double* T = tabs + (size_t)blockIdx.x * TS;
+    auto node_r = [&](int j) { return j < S.J ? S.r[j] : 0.0; };
+    auto node_f = [&](int j) { return j < S.J ? S.f[j] : 0.0; };
+    for (int idx = threadIdx.x; idx < Jp * 8; idx += blockDim.x) {
+        const int nt = idx / 64, e = (idx / 32) % 2, lane = idx % 32, g = lane >> 2, t = lane & 3;
+        const int j = 8 * nt + 2 * t + e;
+        const double r = node_r(j);
+        double p = 1.0;
+        for (int q = 0; q < g + 1 + 8 * delta; ++q) p *= r;
+        T[idx] = j < S.J ? p : 0.0;
+        const int jn = 8 * nt + g, lev = 4 * e + t;
+        const double rn = node_r(jn);
+        double pn = 1.0;
+        for (int q = 0; q < 7 - lev; ++q) pn *= rn;
+        T[Jp * 8 + idx] = jn < S.J ? node_f(jn) * pn : 0.0;
+    }
+    for (int j = threadIdx.x; j < Jp; j += blockDim.x) {
+        const double r = node_r(j);
+        double p = 1.0;
+        for (int q = 0; q < 8; ++q) p *= r;
+        T[Jp * 16 + j] = j < S.J ? p : 0.0;
+    }
+    __shared__ double red[256];
+    const int mmax = 7 + 8 * delta + S.L;  // largest m the stepper uses
+    for (int m = 0; m < K13_CW; ++m) {
+        double v = 0.0;
+        if (m >= S.L && m <= mmax) {
+            double acc = 0.0;
+            for (int j = threadIdx.x; j < S.J; j += blockDim.x) {
+                double p = 1.0;
+                for (int q = 0; q < m - S.L; ++q) p *= S.r[j];
+                acc = fma(S.f[j], p, acc);
+            }
+            red[threadIdx.x] = acc;
+            __syncthreads();
+            for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+                if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+                __syncthreads();
+            }
+            v = red[0];
+            __syncthreads();
+        } else if (m < S.L) {
+            v = S.head[m];  // exact head; c_0 = d_0 is the diagonal of the level system
+        }
+        if (threadIdx.x == 0) T[Jp * 17 + m] = v;
+    }
+}
+
+// RB: 8-mode row blocks per CTA (modes = 8 RB); NT: 8-node tiles per GEMM warp.  At most 8 GEMM
+// warps + 1 solver warp per CTA, one CTA per SM (the register file is split per SM sub-partition:
+// 9 warps leave ~170 registers per thread for the state fragments and the table operands).
+template <int RB, int NT>
+__global__ void __launch_bounds__(288, 1) k13_kernel(K13Args A) {
+    constexpr int MODES = 8 * RB;
+    extern __shared__ double ksm[];
+    const int nwg = A.nwg, nwf = A.nwf, TS = A.TS, Jp = A.Jp;
+    const int RING = A.ring_mask + 1, mask = A.ring_mask;
+    double* tab = ksm;                                   // [2][TS]
+    double* part = tab + 2 * TS;                         // [2][nwg][8][MODES]
+    double* ring = part + 2 * nwg * 8 * MODES;           // [2][RING][MODES]
+    double* sA = ring + 2 * RING * MODES;                // [2][8][MODES]
+    double* g0s = sA + 2 * 8 * MODES;                    // [2][MODES]
+    __shared__ long s_task;
+    __shared__ int s_inst;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const bool solver = warp == nwg;
+    const long nb = (A.N + 7) / 8;
+    if (tid == 0) s_inst = -1;
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) s_task = atomicAdd(A.counter, 1);
+        __syncthreads();
+        const long task = s_task;
+        if (task >= A.n_tasks) return;
+        const int inst = (int)(task / A.nmb);
+        const int m0 = (int)(task % A.nmb) * MODES;
+        if (s_inst != inst) {
+            const double* src = A.tabs + (size_t)inst * 2 * TS;
+            for (int i = tid; i < 2 * TS; i += blockDim.x) tab[i] = src[i];
+        }
+        for (int i = tid; i < 2 * RING * MODES; i += blockDim.x) ring[i] = 0.0;
+        for (int i = tid; i < 2 * MODES; i += blockDim.x) {
+            const int f = i / MODES, d = i % MODES;
+            g0s[i] = (m0 + d < A.n_modes) ? A.c0[((long)inst * 2 + f) * A.n_modes + m0 + d] : 0.0;
+        }
+        __syncthreads();
+        if (tid == 0) s_inst = inst;
+        const double* cwt[2] = {tab + Jp * 17, tab + TS + Jp * 17};
+        if (!solver) {
+            // ------------------------------------------------------------ GEMM warps
+            const int f = warp / nwf, sl = warp % nwf;
+            const int Lf = f ? A.inst[inst].L[1] : A.inst[inst].L[0];
+            const double* Tf = tab + f * TS;
+            const double* cw = Tf + (size_t)(NT * sl) * 64 + lane;
+            const double* rw = Tf + Jp * 8 + (size_t)(NT * sl) * 64 + lane;
+            const double* r8p = Tf + Jp * 16 + 8 * NT * sl + 2 * t;
+            const double* rg = ring + f * RING * MODES;
+            double Y[RB][NT][2];
+#pragma unroll
+            for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+                for (int q = 0; q < NT; ++q) Y[rb][q][0] = Y[rb][q][1] = 0.0;
+            for (long i = 0; i <= nb; ++i) {
+                if (i < nb) {
+                    const long ib = i - 1 - A.delta;
+                    if (ib >= 0) {
+                        // ---- state: Y <- r^8 (.) Y + V R, feeds of block ib: G^(nb0 - L + 4h + t)
+                        const long nb0 = 1 + 8 * ib;
+                        double vf[RB][2];
+#pragma unroll
+                        for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const long lev = nb0 - Lf + 4 * h + t;
+                                vf[rb][h] = lev >= 1 ? rg[(lev & mask) * MODES + 8 * rb + g] : 0.0;
+                            }
+#pragma unroll
+                        for (int q = 0; q < NT; ++q) {
+                            const double ra = r8p[q * 8], rbv = r8p[q * 8 + 1];
+                            const double b0 = rw[(q * 2) * 32], b1 = rw[(q * 2 + 1) * 32];
+#pragma unroll
+                            for (int rb = 0; rb < RB; ++rb) {
+                                Y[rb][q][0] *= ra;
+                                Y[rb][q][1] *= rbv;
+                                dmma(Y[rb][q], vf[rb][0], b0);
+                                dmma(Y[rb][q], vf[rb][1], b1);
+                            }
+                        }
+                    }
+                    // ---- readout of block i: S[mode][k] = sum_j y_j C[j][k] (4 accumulators)
+                    constexpr int NACC = 4 / RB;
+                    double sacc[RB][NACC][2];
+#pragma unroll
+                    for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+                        for (int p = 0; p < NACC; ++p) sacc[rb][p][0] = sacc[rb][p][1] = 0.0;
+#pragma unroll
+                    for (int q = 0; q < NT; ++q)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const double b = cw[(q * 2 + e) * 32];
+#pragma unroll
+                            for (int rb = 0; rb < RB; ++rb) dmma(sacc[rb][q % NACC], Y[rb][q][e], b);
+                        }
+                    double* pw = part + ((size_t)(i & 1) * nwg + warp) * 8 * MODES;
+#pragma unroll
+                    for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            double v = sacc[rb][0][e];
+#pragma unroll
+                            for (int p = 1; p < NACC; ++p) v += sacc[rb][p][e];
+                            pw[(2 * t + e) * MODES + 8 * rb + g] = v;
+                        }
+                }
+                __syncthreads();
+            }
+        } else {
+            // ------------------------------------------------------------ solver warp
+            const int d = lane % MODES;
+            const bool live = lane < MODES && m0 + d < A.n_modes;
+            const K13Dev I = A.inst[inst];
+            const double lam = (m0 + d < A.n_modes) ? A.lam[m0 + d] : 0.0;
+            const double a = I.a, itau = I.itau, al = a + lam;
+            const double h10 = cwt[0][0], h20 = cwt[1][0];  // CW[0] = d_0
+            const double lead = A.sbd ? 1.5 : 1.0;
+            const double m11 = lead * itau + h10 * al, m12 = -a * h20, m21 = -a * h10,
+                         m22 = lead * itau + h20 * al;
+            const double idet = 1.0 / (m11 * m22 - m12 * m21);
+            const double g10 = g0s[d], g20 = g0s[MODES + d];
+            double gp1 = g10, gp2 = g20, gpp1 = 0.0, gpp2 = 0.0;
+            const int Lt[2] = {8 * A.delta + I.L[0], 8 * A.delta + I.L[1]};
+            double c1[8], c2[8];  // in-block weights c_1..c_7
+#pragma unroll
+            for (int m = 1; m < 8; ++m) {
+                c1[m] = cwt[0][m];
+                c2[m] = cwt[1][m];
+            }
+            // correction prefetch: fragment row k = g of each field (level n0 + g)
+            double cpre[2];
+            auto corr_load = [&](int b) {
+#pragma unroll
+                for (int f = 0; f < 2; ++f) {
+                    const int n = 1 + 8 * b + g;
+                    const int Lf = f ? I.L[1] : I.L[0];
+                    double v = 0.0;
+                    if (A.sbd && n >= 2 && n <= A.N && n - 1 >= Lf) v = (f ? I.corr[1] : I.corr[0])[n - 4];
+                    cpre[f] = v;
+                }
+            };
+            corr_load(0);
+            for (int i = 0; i <= (int)nb; ++i) {
+                if (i >= 1) {
+                    const int b = i - 1, n0 = 1 + 8 * b;
+                    const int kmax = (int)min(8L, A.N - n0 + 1);
+                    const int buf = b & 1;
+                    // ---- known part on DMMA: D[k][d] = partial readouts + sum_j c[k+Lt-j] G^(n0-Lt+j)
+                    //      (fragment: thread (g, t) holds rows k = g, columns d = 2t, 2t+1 of a tile)
+#pragma unroll
+                    for (int f = 0; f < 2; ++f) {
+                        const double* CWf = cwt[f];
+                        const int Ltf = Lt[f];
+                        const double* rg = ring + f * RING * MODES;
+                        const int n = n0 + g;
+                        double corr_c = 0.0;
+                        if (A.sbd && n >= 2) {
+                            const int Lf = f ? I.L[1] : I.L[0];
+                            corr_c = 0.5 * ((n - 1 < Lf) ? CWf[n - 1] : cpre[f]);
+                        }
+#pragma unroll
+                        for (int nt = 0; nt < RB; ++nt) {
+                            double D[2] = {0.0, 0.0};
+                            const double* pb = part + ((size_t)buf * nwg + f * nwf) * 8 * MODES + g * MODES + 8 * nt + 2 * t;
+                            for (int w = 0; w < nwf; ++w) {
+                                const double2 v = *reinterpret_cast<const double2*>(pb + w * 8 * MODES);
+                                D[0] += v.x;
+                                D[1] += v.y;
+                            }
+                            for (int j0 = 0; j0 < Ltf; j0 += 4) {
+                                const int j = j0 + t;
+                                const double av = j < Ltf ? CWf[g + Ltf - j] : 0.0;  // A[k=g][j=t]
+                                const int lev = n0 - Ltf + j;                         // B[j=t][d=g]
+                                const double bv = (j < Ltf && lev >= 1) ? rg[(lev & mask) * MODES + 8 * nt + g] : 0.0;
+                                // note: A row g / B column g are different roles of the same lane
+                                dmma(D, av, bv);
+                            }
+                            const double* g0f = g0s + f * MODES + 8 * nt + 2 * t;
+                            D[0] = fma(corr_c, g0f[0], D[0]);
+                            D[1] = fma(corr_c, g0f[1], D[1]);
+                            *reinterpret_cast<double2*>(sA + (f * 8 + g) * MODES + 8 * nt + 2 * t) = make_double2(D[0], D[1]);
+                        }
+                    }
+                    if (b + 1 < nb) corr_load(b + 1);  // latency hidden by the solve + barrier
+                    __syncwarp();
+                    if (lane < MODES) {
+                        double acc1[8], acc2[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            acc1[k] = sA[k * MODES + d];
+                            acc2[k] = sA[(8 + k) * MODES + d];
+                        }
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            if (k < kmax) {
+                                const long n = n0 + k;
+                                double x1, x2;
+                                if (A.sbd && n == 1) {
+                                    // first step: 2/3 - 1/3 system (fpfp.cpp:293-308)
+                                    const double f11 = itau + (2.0 / 3.0) * h10 * al,
+                                                 f12 = -(2.0 / 3.0) * a * h20;
+                                    const double f21 = -(2.0 / 3.0) * a * h10,
+                                                 f22 = itau + (2.0 / 3.0) * h20 * al;
+                                    const double r1 = g10 * itau - (h10 / 3.0) * al * g10 +
+                                                      (a * h20 / 3.0) * g20;
+                                    const double r2 = g20 * itau - (h20 / 3.0) * al * g20 +
+                                                      (a * h10 / 3.0) * g10;
+                                    const double dt = 1.0 / (f11 * f22 - f12 * f21);
+                                    x1 = (r1 * f22 - f12 * r2) * dt;
+                                    x2 = (f11 * r2 - f21 * r1) * dt;
+                                } else {
+                                    const double s1 = acc1[k], s2 = acc2[k];
+                                    double r1, r2;
+                                    if (A.sbd) {
+                                        r1 = (2.0 * gp1 - 0.5 * gpp1) * itau - al * s1 + a * s2;
+                                        r2 = (2.0 * gp2 - 0.5 * gpp2) * itau - al * s2 + a * s1;
+                                    } else {
+                                        r1 = gp1 * itau - al * s1 + a * s2;
+                                        r2 = gp2 * itau - al * s2 + a * s1;
+                                    }
+                                    x1 = (r1 * m22 - m12 * r2) * idet;
+                                    x2 = (m11 * r2 - m21 * r1) * idet;
+                                }
+                                ring[(n & mask) * MODES + d] = x1;
+                                ring[(RING + (n & mask)) * MODES + d] = x2;
+#pragma unroll
+                                for (int k2 = k + 1; k2 < 8; ++k2) {
+                                    acc1[k2] = fma(c1[k2 - k], x1, acc1[k2]);
+                                    acc2[k2] = fma(c2[k2 - k], x2, acc2[k2]);
+                                }
+                                gpp1 = gp1;
+                                gpp2 = gp2;
+                                gp1 = x1;
+                                gp2 = x2;
+                            }
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+            if (live) {
+                A.cN[((long)inst * 2 + 0) * A.n_modes + m0 + d] = gp1;
+                A.cN[((long)inst * 2 + 1) * A.n_modes + m0 + d] = gp2;
+            }
+        }
+    }
+}
+
+size_t k13_smem(int TS, int nwg, int ring, int modes) {
+    return sizeof(double) *
+           ((size_t)2 * TS + 2 * nwg * 8 * modes + 2 * ring * modes + 2 * 8 * modes + 2 * modes);
+}
+
+template <int RB, int NT>
+void k13_launch(const K13Args& a, size_t smem, int num_sms, cudaStream_t s) {
+    FRAQ_CUDA(cudaFuncSetAttribute(k13_kernel<RB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    int per_sm = 1;
+    const int threads = a.nwg * 32 + 32;
+    FRAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k13_kernel<RB, NT>, threads, smem));
+    const long grid = std::max(1L, std::min(a.n_tasks, (long)std::max(1, per_sm) * num_sms));
+    k13_kernel<RB, NT><<<(unsigned)grid, threads, smem, s>>>(a);
+    FRAQ_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+// Can K13 run these kernels?  (J <= 512 per field, lag windows fit the 64-slot ring)
+bool k13_supported(int maxJ, int minL, int maxL) {
+    if (std::getenv("FRAQ_MODAL_K11")) return false;
+    if (maxJ > 512 || maxJ < 1 || minL < 2) return false;
+    const int delta = minL >= 8 ? 0 : 1;
+    return 8 + 8 * delta + maxL + 8 <= 64 && 7 + 8 * delta + maxL < K13_CW;
+}
+
+void k13_run(fraq_ctx c, const std::vector<K13Inst>& in, const double* lam, int n_modes, long N,
+             bool sbd, const double* c0, double* cN) {
+    const int n_inst = (int)in.size();
+    int maxJ = 0, minL = 1 << 30, maxL = 0;
+    for (const K13Inst& I : in)
+        for (int f = 0; f < 2; ++f) {
+            maxJ = std::max(maxJ, I.J[f]);
+            minL = std::min(minL, I.L[f]);
+            maxL = std::max(maxL, I.L[f]);
+        }
+    const int delta = minL >= 8 ? 0 : 1;
+    // J <= 256: 16 modes x 64 nodes per GEMM warp; else 8 modes x 128 nodes per GEMM warp
+    const int RB = maxJ <= 256 ? 2 : 1, nodes_w = RB == 2 ? 64 : 128, modes = 8 * RB;
+    const int nwf = (maxJ + nodes_w - 1) / nodes_w, Jp = nodes_w * nwf, nwg = 2 * nwf;
+    const int TS = 17 * Jp + K13_CW;
+    const int span = 8 + 8 * delta + maxL + 8;
+    const int ring = span <= 32 ? 32 : 64;
+    // tables
+    std::vector<K13TabSrc> src(2 * n_inst);
+    std::vector<K13Dev> dv(n_inst);
+    for (int i = 0; i < n_inst; ++i) {
+        for (int f = 0; f < 2; ++f) src[2 * i + f] = {in[i].r[f], in[i].f[f], in[i].head[f], in[i].J[f], in[i].L[f]};
+        dv[i].a = in[i].a;
+        dv[i].itau = 1.0 / in[i].tau;
+        for (int f = 0; f < 2; ++f) {
+            dv[i].corr[f] = in[i].corr[f];
+            dv[i].L[f] = in[i].L[f];
+        }
+    }
+    DevBuf<K13TabSrc> dsrc(src.size());
+    DevBuf<K13Dev> ddv(dv.size());
+    DevBuf<double> tabs((size_t)2 * n_inst * TS);
+    DevBuf<int> counter(1);
+    FRAQ_CUDA(cudaMemcpyAsync(dsrc.p, src.data(), sizeof(K13TabSrc) * src.size(),
+                              cudaMemcpyHostToDevice, c->stream));
+    FRAQ_CUDA(cudaMemcpyAsync(ddv.p, dv.data(), sizeof(K13Dev) * dv.size(), cudaMemcpyHostToDevice,
+                              c->stream));
+    FRAQ_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), c->stream));
+    k13_tables_kernel<<<2 * n_inst, 256, 0, c->stream>>>(dsrc.p, Jp, delta, tabs.p, TS);
+    FRAQ_LAUNCH_CHECK();
+    K13Args A{};
+    A.inst = ddv.p;
+    A.tabs = tabs.p;
+    A.TS = TS;
+    A.Jp = Jp;
+    A.nwf = nwf;
+    A.nwg = nwg;
+    A.lam = lam;
+    A.n_modes = n_modes;
+    A.nmb = (n_modes + modes - 1) / modes;
+    A.n_tasks = (long)A.nmb * n_inst;
+    A.N = N;
+    A.sbd = sbd ? 1 : 0;
+    A.delta = delta;
+    A.ring_mask = ring - 1;
+    A.c0 = c0;
+    A.cN = cN;
+    A.counter = counter.p;
+    const size_t smem = k13_smem(TS, nwg, ring, modes);
+    if (RB == 2)
+        k13_launch<2, 8>(A, smem, c->num_sms, c->stream);
+    else
+        k13_launch<1, 16>(A, smem, c->num_sms, c->stream);
+    FRAQ_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+}  // namespace fraqcu

@@ -95,3 +95,35 @@ def test_2d_matches_physical_restatement(fraq, orc, scheme, m, a):
     out = fraq.run_2d(0.3, 0.6, a, m, T, N, getattr(fraq.Scheme, scheme), g1, g2)
     assert rel(out.final_state.g1, r1) <= 1e-10
     assert rel(out.final_state.g2, r2) <= 1e-10
+
+
+@pytest.mark.parametrize("scheme", ["FastBE", "FastSBD"])
+@pytest.mark.parametrize("m,N", [(37, 61), (255, 200), (1000, 123)])
+def test_k13_tensor_core_path_matches_k11(fraq, scheme, m, N, monkeypatch):
+    """K13 (DMMA block GEMMs + solver warp) against K11 (per-level warp sweep): same scheme,
+    different association; ragged mode counts (not multiples of 8/16) and level counts."""
+    spec = fraq.ProblemSpec(alpha1=0.35, alpha2=0.75, coupling_a=-2.5, grid_m=m, t_final=0.7,
+                            n_steps=N, initial="poly_sin")
+    k13 = fraq.run(spec, getattr(fraq.Scheme, scheme), modal_kc(fraq))
+    monkeypatch.setenv("FRAQ_MODAL_K11", "1")
+    k11 = fraq.run(spec, getattr(fraq.Scheme, scheme), modal_kc(fraq))
+    assert rel(k13.final_state.g1, k11.final_state.g1) <= 1e-12
+    assert rel(k13.final_state.g2, k11.final_state.g2) <= 1e-12
+
+
+def test_k13_batch_mixed_instances(fraq, orc):
+    """C5-like batch through K13 with per-instance kernels (different J and L per field)."""
+    from paper_1901_05128_b200.workloads import c5_instances
+    insts = c5_instances(6)
+    N = 80
+    for scheme in ("FastBE", "FastSBD"):
+        specs = [fraq.ProblemSpec(alpha1=i.alpha1, alpha2=i.alpha2, coupling_a=i.coupling_a,
+                                  grid_m=63, t_final=N / 16384, n_steps=N, initial="custom",
+                                  custom_g1=list(i.g1[::64][:63]), custom_g2=list(i.g2[::64][:63]))
+                 for i in insts]
+        outs = fraq.run_batch(specs, getattr(fraq.Scheme, scheme), modal_kc(fraq))
+        for s, o in zip(specs, outs):
+            g1, g2, _, _ = orc.run(s.alpha1, s.alpha2, s.coupling_a, 63, s.t_final, N, scheme,
+                                   "custom", custom_g1=s.custom_g1, custom_g2=s.custom_g2)
+            assert rel(o.final_state.g1, g1) <= 1e-10
+            assert rel(o.final_state.g2, g2) <= 1e-10
