@@ -246,9 +246,11 @@ __global__ void __launch_bounds__(288, 1) k13_kernel(K13Args A) {
             const double m11 = lead * itau + h10 * al, m12 = -a * h20, m21 = -a * h10,
                          m22 = lead * itau + h20 * al;
             const double idet = 1.0 / (m11 * m22 - m12 * m21);
+            const double M11 = m11 * idet, M12 = m12 * idet, M21 = m21 * idet, M22 = m22 * idet;
             const double g10 = g0s[d], g20 = g0s[MODES + d];
             double gp1 = g10, gp2 = g20, gpp1 = 0.0, gpp2 = 0.0;
             const int Lt[2] = {8 * A.delta + I.L[0], 8 * A.delta + I.L[1]};
+            const int Ltm = max(Lt[0], Lt[1]);
             double c1[8], c2[8];  // in-block weights c_1..c_7
 #pragma unroll
             for (int m = 1; m < 8; ++m) {
@@ -274,39 +276,55 @@ __global__ void __launch_bounds__(288, 1) k13_kernel(K13Args A) {
                     const int kmax = (int)min(8L, A.N - n0 + 1);
                     const int buf = b & 1;
                     // ---- known part on DMMA: D[k][d] = partial readouts + sum_j c[k+Lt-j] G^(n0-Lt+j)
-                    //      (fragment: thread (g, t) holds rows k = g, columns d = 2t, 2t+1 of a tile)
+                    //      (fragment: thread (g, t) holds rows k = g, columns d = 2t, 2t+1 of a tile;
+                    //      as A operand it holds A[k = g][j = t], as B operand B[j = t][d = g])
+                    double D[2][RB][2];
+#pragma unroll
+                    for (int f = 0; f < 2; ++f)
+#pragma unroll
+                        for (int nt = 0; nt < RB; ++nt) {
+                            const double* pb = part + ((size_t)buf * nwg + f * nwf) * 8 * MODES +
+                                               g * MODES + 8 * nt + 2 * t;
+                            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                            for (int w = 0; w < 4; ++w)
+                                if (w < nwf) {
+                                    const double2 v = *reinterpret_cast<const double2*>(pb + w * 8 * MODES);
+                                    s0 += v.x;
+                                    s1 += v.y;
+                                }
+                            D[f][nt][0] = s0;
+                            D[f][nt][1] = s1;
+                        }
+                    for (int j0 = 0; j0 < Ltm; j0 += 4) {
+                        const int j = j0 + t;
+#pragma unroll
+                        for (int f = 0; f < 2; ++f) {
+                            const int Ltf = Lt[f], lev = n0 - Ltf + j;
+                            const bool ok = j < Ltf;
+                            const double av = ok ? cwt[f][g + Ltf - j] : 0.0;
+                            const double* rg = ring + (f * RING + (lev & mask)) * MODES + g;
+#pragma unroll
+                            for (int nt = 0; nt < RB; ++nt) {
+                                const double bv = (ok && lev >= 1) ? rg[8 * nt] : 0.0;
+                                dmma(D[f][nt], av, bv);
+                            }
+                        }
+                    }
 #pragma unroll
                     for (int f = 0; f < 2; ++f) {
-                        const double* CWf = cwt[f];
-                        const int Ltf = Lt[f];
-                        const double* rg = ring + f * RING * MODES;
                         const int n = n0 + g;
                         double corr_c = 0.0;
                         if (A.sbd && n >= 2) {
                             const int Lf = f ? I.L[1] : I.L[0];
-                            corr_c = 0.5 * ((n - 1 < Lf) ? CWf[n - 1] : cpre[f]);
+                            corr_c = 0.5 * ((n - 1 < Lf) ? cwt[f][n - 1] : cpre[f]);
                         }
 #pragma unroll
                         for (int nt = 0; nt < RB; ++nt) {
-                            double D[2] = {0.0, 0.0};
-                            const double* pb = part + ((size_t)buf * nwg + f * nwf) * 8 * MODES + g * MODES + 8 * nt + 2 * t;
-                            for (int w = 0; w < nwf; ++w) {
-                                const double2 v = *reinterpret_cast<const double2*>(pb + w * 8 * MODES);
-                                D[0] += v.x;
-                                D[1] += v.y;
-                            }
-                            for (int j0 = 0; j0 < Ltf; j0 += 4) {
-                                const int j = j0 + t;
-                                const double av = j < Ltf ? CWf[g + Ltf - j] : 0.0;  // A[k=g][j=t]
-                                const int lev = n0 - Ltf + j;                         // B[j=t][d=g]
-                                const double bv = (j < Ltf && lev >= 1) ? rg[(lev & mask) * MODES + 8 * nt + g] : 0.0;
-                                // note: A row g / B column g are different roles of the same lane
-                                dmma(D, av, bv);
-                            }
                             const double* g0f = g0s + f * MODES + 8 * nt + 2 * t;
-                            D[0] = fma(corr_c, g0f[0], D[0]);
-                            D[1] = fma(corr_c, g0f[1], D[1]);
-                            *reinterpret_cast<double2*>(sA + (f * 8 + g) * MODES + 8 * nt + 2 * t) = make_double2(D[0], D[1]);
+                            *reinterpret_cast<double2*>(sA + (f * 8 + g) * MODES + 8 * nt + 2 * t) =
+                                make_double2(fma(corr_c, g0f[0], D[f][nt][0]),
+                                             fma(corr_c, g0f[1], D[f][nt][1]));
                         }
                     }
                     if (b + 1 < nb) corr_load(b + 1);  // latency hidden by the solve + barrier
@@ -318,6 +336,29 @@ __global__ void __launch_bounds__(288, 1) k13_kernel(K13Args A) {
                             acc1[k] = sA[k * MODES + d];
                             acc2[k] = sA[(8 + k) * MODES + d];
                         }
+                        if (kmax == 8 && !(A.sbd && n0 == 1)) {
+                            // full block: no predicates; x = M r with M = inverse level matrix
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) {
+                                const double l1 = A.sbd ? fma(2.0, gp1, -0.5 * gpp1) * itau : gp1 * itau;
+                                const double l2 = A.sbd ? fma(2.0, gp2, -0.5 * gpp2) * itau : gp2 * itau;
+                                const double r1 = fma(a, acc2[k], fma(-al, acc1[k], l1));
+                                const double r2 = fma(a, acc1[k], fma(-al, acc2[k], l2));
+                                const double x1 = fma(r1, M22, -(r2 * M12));
+                                const double x2 = fma(r2, M11, -(r1 * M21));
+                                ring[((n0 + k) & mask) * MODES + d] = x1;
+                                ring[(RING + ((n0 + k) & mask)) * MODES + d] = x2;
+#pragma unroll
+                                for (int k2 = k + 1; k2 < 8; ++k2) {
+                                    acc1[k2] = fma(c1[k2 - k], x1, acc1[k2]);
+                                    acc2[k2] = fma(c2[k2 - k], x2, acc2[k2]);
+                                }
+                                gpp1 = gp1;
+                                gpp2 = gp2;
+                                gp1 = x1;
+                                gp2 = x2;
+                            }
+                        } else {
 #pragma unroll
                         for (int k = 0; k < 8; ++k) {
                             if (k < kmax) {
@@ -361,6 +402,7 @@ __global__ void __launch_bounds__(288, 1) k13_kernel(K13Args A) {
                                 gp1 = x1;
                                 gp2 = x2;
                             }
+                        }
                         }
                     }
                 }
