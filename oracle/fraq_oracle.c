@@ -1042,3 +1042,110 @@ done:
     free(l2);
     return st;
 }
+
+/* ---- Mode-space fast FFPE stepping (TEST INFRASTRUCTURE) ----
+ * The reference's mode-space oracle (test_fpfp.cpp:79-134: mode_be / mode_sbd, solve2x2) with the
+ * O(n) history sums replaced by the fast histories of fast_kernel.cpp (scheme variant, one lane per
+ * mode), i.e. FastStepper (fpfp.cpp:259-349) with the discrete Laplacian replaced by its
+ * eigenvalues lam[k] (block_solver.cpp:21-24; in 2D lam_k + lam_l).  u0/v0 are the initial DST
+ * coefficients of both fields; uN/vN receive the coefficients after N levels. */
+static void solve2x2(double a11, double a12, double a21, double a22, double r1, double r2,
+                     double* x1, double* x2) {
+    const double det = a11 * a22 - a12 * a21;
+    *x1 = (r1 * a22 - a12 * r2) / det;
+    *x2 = (a11 * r2 - a21 * r1) / det;
+}
+
+int fo_modal_run(const fo_kernel* k1, const fo_kernel* k2, double a, double tau, long N,
+                 long nm, const double* lam, const double* u0, const double* v0, double* uN,
+                 double* vN) {
+    if (N < 1 || nm < 1 || k1->sbd != k2->sbd) return FO_EINVAL;
+    const int sbd = k1->sbd;
+    fo_hist hh1, hh2;
+    int st = fo_hist_init(&hh1, k1, 1, nm);
+    if (!st) st = fo_hist_init(&hh2, k2, 1, nm);
+    if (st) return st;
+    double *s1 = malloc(sizeof(double) * nm), *s2 = malloc(sizeof(double) * nm);
+    double *x1 = malloc(sizeof(double) * nm), *x2 = malloc(sizeof(double) * nm);
+    corr_pw* cp1 = calloc(1, sizeof(corr_pw));
+    corr_pw* cp2 = calloc(1, sizeof(corr_pw));
+    for (int j = 0; j < 512; ++j) cp1->p1[j] = cp1->p2[j] = cp2->p1[j] = cp2->p2[j] = 1.0;
+    const double d10 = k1->head[0], d20 = k2->head[0];
+    fo_hist_append(&hh1, u0);
+    fo_hist_append(&hh2, v0);
+    for (long n = 1; !st && n <= N; ++n) {
+        st = fo_hist_advance(&hh1);
+        if (!st) st = fo_hist_advance(&hh2);
+        if (st) break;
+        const double *u1, *v1;
+        fo_hist_lagged(&hh1, 0, &u1);
+        fo_hist_lagged(&hh2, 0, &v1);
+        if (sbd && n == 1) {
+            for (long k = 0; k < nm; ++k) {
+                const double al = a + lam[k];
+                const double r1 = u1[k] / tau - (d10 / 3.0) * al * u1[k] + (a * d20 / 3.0) * v1[k];
+                const double r2 = v1[k] / tau - (d20 / 3.0) * al * v1[k] + (a * d10 / 3.0) * u1[k];
+                solve2x2(1.0 / tau + (2.0 / 3.0) * d10 * al, -(2.0 / 3.0) * a * d20,
+                         -(2.0 / 3.0) * a * d10, 1.0 / tau + (2.0 / 3.0) * d20 * al, r1, r2,
+                         &x1[k], &x2[k]);
+            }
+        } else {
+            fo_hist_history_sum(&hh1, s1);
+            fo_hist_history_sum(&hh2, s2);
+            const double* u2 = NULL;
+            const double* v2 = NULL;
+            if (!sbd) {
+                if (n >= 2)
+                    for (long k = 0; k < nm; ++k) {
+                        s1[k] += k1->head[1] * u1[k];
+                        s2[k] += k2->head[1] * v1[k];
+                    }
+            } else {
+                for (int f = 0; f < 2; ++f) {
+                    const fo_kernel* kk = f ? k2 : k1;
+                    fo_hist* hh = f ? &hh2 : &hh1;
+                    double* ss = f ? s2 : s1;
+                    const long top = (kk->n_head - 1 < n - 1) ? kk->n_head - 1 : n - 1;
+                    for (long i = 1; i <= top; ++i) {
+                        const double* u;
+                        fo_hist_lagged(hh, i - 1, &u);
+                        for (long k = 0; k < nm; ++k) ss[k] += kk->head[i] * u[k];
+                    }
+                }
+                const double c1 = (n - 1 < k1->n_head) ? k1->head[n - 1] : corr_value(cp1, k1, n - 4);
+                const double c2 = (n - 1 < k2->n_head) ? k2->head[n - 1] : corr_value(cp2, k2, n - 4);
+                for (long k = 0; k < nm; ++k) {
+                    s1[k] += 0.5 * c1 * u0[k];
+                    s2[k] += 0.5 * c2 * v0[k];
+                }
+                fo_hist_lagged(&hh1, 1, &u2);
+                fo_hist_lagged(&hh2, 1, &v2);
+            }
+            const double lead = sbd ? 1.5 : 1.0;
+            for (long k = 0; k < nm; ++k) {
+                const double al = a + lam[k];
+                const double l1 = sbd ? (2.0 * u1[k] - 0.5 * u2[k]) / tau : u1[k] / tau;
+                const double l2 = sbd ? (2.0 * v1[k] - 0.5 * v2[k]) / tau : v1[k] / tau;
+                const double r1 = l1 - al * s1[k] + a * s2[k];
+                const double r2 = l2 - al * s2[k] + a * s1[k];
+                solve2x2(lead / tau + d10 * al, -a * d20, -a * d10, lead / tau + d20 * al, r1, r2,
+                         &x1[k], &x2[k]);
+            }
+        }
+        fo_hist_append(&hh1, x1);
+        fo_hist_append(&hh2, x2);
+    }
+    if (!st) {
+        memcpy(uN, x1, sizeof(double) * nm);
+        memcpy(vN, x2, sizeof(double) * nm);
+    }
+    free(s1);
+    free(s2);
+    free(x1);
+    free(x2);
+    free(cp1);
+    free(cp2);
+    fo_hist_free(&hh1);
+    fo_hist_free(&hh2);
+    return st;
+}

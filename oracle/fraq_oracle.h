@@ -129,6 +129,11 @@ int fo_run(const fo_spec* s, int scheme, const fo_kconf* kc, double* g1_out, dou
            double* eps1, double* eps2, int* np_out /* [4]: np1 field1, np2 field1, ... */,
            int* nhead_out /* [2] */);
 
+/* ---- mode-space fast FFPE stepping (test_fpfp.cpp:79-134 with fast histories) ---- */
+int fo_modal_run(const fo_kernel* k1, const fo_kernel* k2, double a, double tau, long N,
+                 long n_modes, const double* lam, const double* u0, const double* v0, double* uN,
+                 double* vN);
+
 #ifdef __cplusplus
 }
 #endif

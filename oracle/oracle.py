@@ -398,3 +398,36 @@ class Oracle:
             ptrs("head"), ptrs("m1"), ptrs("r1"), ptrs("m2"), ptrs("r2"), C.c_long(dofs),
             C.c_long(n_steps), _p(U), _p(D), C.c_int(threads), C.byref(secs)), "bench_history")
         return secs.value, D
+
+    def modal_run(self, k1: Kernel, k2: Kernel, a: float, tau: float, N: int, lam, u0, v0,
+                  threads: int = 1):
+        """Mode-space fast FFPE stepping (test_fpfp.cpp:79-134 with fast histories; lam = the
+        Laplacian eigenvalue of each mode, u0/v0 = initial DST coefficients).  Port: fo_modal_run
+        (single thread); reference: the reference's BeHistory/SbdHistory lanes, `threads`
+        workers over mode slices.  Returns (uN, vN, seconds)."""
+        lam, u0, v0 = _arr(lam), _arr(u0), _arr(v0)
+        nm = len(lam)
+        uN, vN = np.zeros(nm), np.zeros(nm)
+        if self.kind == "port":
+            f1, f2 = _to_fo(k1), _to_fo(k2)
+            import time as _t
+            t0 = _t.perf_counter()
+            _raise(self.lib.fo_modal_run(C.byref(f1), C.byref(f2), C.c_double(a), C.c_double(tau),
+                                         C.c_long(N), C.c_long(nm), _p(lam), _p(u0), _p(v0),
+                                         _p(uN), _p(vN)), "modal_run")
+            return uN, vN, _t.perf_counter() - t0
+        ks = [k1, k2]
+        keep = []
+
+        def ptrs(name):
+            arrs = [_arr(getattr(k, name)) if len(getattr(k, name)) else np.zeros(1) for k in ks]
+            keep.extend(arrs)
+            return (_dp * 2)(*[_p(x) for x in arrs])
+        secs = C.c_double()
+        _raise(self.lib.ref_modal_run(
+            C.c_int(int(k1.sbd)), (C.c_double * 2)(k1.gamma, k2.gamma), C.c_double(tau),
+            (C.c_int * 2)(k1.n_head, k2.n_head), (C.c_int * 2)(k1.np1, k2.np1),
+            (C.c_int * 2)(k1.np2, k2.np2), ptrs("head"), ptrs("m1"), ptrs("r1"), ptrs("m2"),
+            ptrs("r2"), C.c_double(a), C.c_long(N), C.c_long(nm), _p(lam), _p(u0), _p(v0),
+            _p(uN), _p(vN), C.c_int(threads), C.byref(secs)), "modal_run")
+        return uN, vN, secs.value

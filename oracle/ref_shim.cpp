@@ -355,4 +355,144 @@ int ref_bench_history(int sbd, int n_groups, const double* gammas, double tau, c
     });
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Mode-space FFPE restatement over the reference's own history lanes: the
+// reference's mode-space oracle algebra (test_fpfp.cpp:79-134, mode_be / mode_sbd, solve2x2)
+// with the O(n) sums replaced by fraq::BeHistory / SbdHistory (scheme variant, one lane per
+// mode), i.e. FastStepper (fpfp.cpp:259-349) with A -> diag(lam).  The SBD correction
+// c_n = sum m r^(n-4) uses running powers as CorrPowers does (fpfp.cpp:240-250; restated here,
+// it is internal to fpfp.cpp).  `threads` workers each own a contiguous slice of modes.
+// Kernel k (0, 1) of field k is given in flat form.  Returns the loop wall time (max over
+// workers) in *seconds.
+int ref_modal_run(int sbd, const double* gammas, double tau, const int* nh, const int* np1,
+                  const int* np2, const double* const* heads, const double* const* m1,
+                  const double* const* r1, const double* const* m2, const double* const* r2,
+                  double a, long N, long nm, const double* lam, const double* u0,
+                  const double* v0, double* uN, double* vN, int threads, double* seconds) {
+    return guard([&] {
+        FastKernelBE kb[2];
+        FastKernelSBD ks[2];
+        for (int f = 0; f < 2; ++f) {
+            const FlatKernel fk{sbd, nh[f], np1[f], np2[f], gammas[f], tau, heads[f],
+                                m1[f],  r1[f], m2 ? m2[f] : nullptr, r2 ? r2[f] : nullptr};
+            if (sbd)
+                ks[f] = to_sbd(fk);
+            else
+                kb[f] = to_be(fk);
+        }
+        const int T = (int)std::max(1L, std::min<long>(threads, nm));
+        std::vector<double> secs(T, 0.0);
+        auto corr_at = [&](const FastKernelSBD& k, std::vector<double>& p1, std::vector<double>& p2,
+                           long& e, long target) {
+            while (e < target) {
+                for (std::size_t j = 0; j < p1.size(); ++j) p1[j] *= k.ratio1[j];
+                for (std::size_t j = 0; j < p2.size(); ++j) p2[j] *= k.ratio2[j];
+                ++e;
+            }
+            double v = 0.0;
+            for (std::size_t j = 0; j < p1.size(); ++j) v += k.mult1[j] * p1[j];
+            for (std::size_t j = 0; j < p2.size(); ++j) v += k.mult2[j] * p2[j];
+            return v;
+        };
+        auto work = [&](int w) {
+            const long lo = nm * w / T, hi = nm * (w + 1) / T, d = hi - lo;
+            if (d <= 0) return;
+            std::vector<double> s1(d), s2(d), x1(u0 + lo, u0 + hi), x2(v0 + lo, v0 + hi);
+            const double d10 = sbd ? ks[0].head[0] : kb[0].head[0];
+            const double d20 = sbd ? ks[1].head[0] : kb[1].head[0];
+            auto drive = [&](auto& h1, auto& h2) {
+                std::vector<double> p11, p12, p21, p22;
+                long e1 = 0, e2 = 0;
+                if (sbd) {
+                    p11.assign(ks[0].ratio1.size(), 1.0);
+                    p12.assign(ks[0].ratio2.size(), 1.0);
+                    p21.assign(ks[1].ratio1.size(), 1.0);
+                    p22.assign(ks[1].ratio2.size(), 1.0);
+                }
+                const auto t0 = std::chrono::steady_clock::now();
+                h1.append(x1);
+                h2.append(x2);
+                for (long n = 1; n <= N; ++n) {
+                    h1.advance();
+                    h2.advance();
+                    const auto u1 = h1.lagged(0);
+                    const auto v1 = h2.lagged(0);
+                    if (sbd && n == 1) {
+                        for (long k = 0; k < d; ++k) {
+                            const double al = a + lam[lo + k];
+                            const double r1v = u1[k] / tau - (d10 / 3.0) * al * u1[k] + (a * d20 / 3.0) * v1[k];
+                            const double r2v = v1[k] / tau - (d20 / 3.0) * al * v1[k] + (a * d10 / 3.0) * u1[k];
+                            const double a11 = 1.0 / tau + (2.0 / 3.0) * d10 * al, a12 = -(2.0 / 3.0) * a * d20;
+                            const double a21 = -(2.0 / 3.0) * a * d10, a22 = 1.0 / tau + (2.0 / 3.0) * d20 * al;
+                            const double det = a11 * a22 - a12 * a21;
+                            x1[k] = (r1v * a22 - a12 * r2v) / det;
+                            x2[k] = (a11 * r2v - a21 * r1v) / det;
+                        }
+                    } else {
+                        h1.history_sum(s1);
+                        h2.history_sum(s2);
+                        std::span<const double> u2, v2;
+                        if (!sbd) {
+                            if (n >= 2)
+                                for (long k = 0; k < d; ++k) {
+                                    s1[k] += kb[0].head[1] * u1[k];
+                                    s2[k] += kb[1].head[1] * v1[k];
+                                }
+                        } else {
+                            for (int f = 0; f < 2; ++f) {
+                                const FastKernelSBD& kk = ks[f];
+                                auto& hh = f ? h2 : h1;
+                                std::vector<double>& ss = f ? s2 : s1;
+                                const long top = std::min<long>(kk.n_head - 1, n - 1);
+                                for (long i = 1; i <= top; ++i) {
+                                    const auto u = hh.lagged(i - 1);
+                                    for (long k = 0; k < d; ++k) ss[k] += kk.head[i] * u[k];
+                                }
+                            }
+                            const double c1 = (n - 1 < ks[0].n_head) ? ks[0].head[n - 1] : corr_at(ks[0], p11, p12, e1, n - 4);
+                            const double c2 = (n - 1 < ks[1].n_head) ? ks[1].head[n - 1] : corr_at(ks[1], p21, p22, e2, n - 4);
+                            for (long k = 0; k < d; ++k) {
+                                s1[k] += 0.5 * c1 * u0[lo + k];
+                                s2[k] += 0.5 * c2 * v0[lo + k];
+                            }
+                            u2 = h1.lagged(1);
+                            v2 = h2.lagged(1);
+                        }
+                        const double lead = sbd ? 1.5 : 1.0;
+                        for (long k = 0; k < d; ++k) {
+                            const double al = a + lam[lo + k];
+                            const double l1 = sbd ? (2.0 * u1[k] - 0.5 * u2[k]) / tau : u1[k] / tau;
+                            const double l2 = sbd ? (2.0 * v1[k] - 0.5 * v2[k]) / tau : v1[k] / tau;
+                            const double r1v = l1 - al * s1[k] + a * s2[k];
+                            const double r2v = l2 - al * s2[k] + a * s1[k];
+                            const double a11 = lead / tau + d10 * al, a12 = -a * d20;
+                            const double a21 = -a * d10, a22 = lead / tau + d20 * al;
+                            const double det = a11 * a22 - a12 * a21;
+                            x1[k] = (r1v * a22 - a12 * r2v) / det;
+                            x2[k] = (a11 * r2v - a21 * r1v) / det;
+                        }
+                    }
+                    h1.append(x1);
+                    h2.append(x2);
+                }
+                secs[w] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                std::memcpy(uN + lo, x1.data(), d * sizeof(double));
+                std::memcpy(vN + lo, x2.data(), d * sizeof(double));
+            };
+            if (sbd) {
+                SbdHistory h1(ks[0], HistoryVariant::scheme, d), h2(ks[1], HistoryVariant::scheme, d);
+                drive(h1, h2);
+            } else {
+                BeHistory h1(kb[0], HistoryVariant::scheme, d), h2(kb[1], HistoryVariant::scheme, d);
+                drive(h1, h2);
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int w = 0; w < T; ++w) pool.emplace_back(work, w);
+        for (auto& t : pool) t.join();
+        *seconds = *std::max_element(secs.begin(), secs.end());
+    });
+}
+
 }  // extern "C"

@@ -90,6 +90,19 @@ def c3_instance(grid_m: int = 4095) -> FfpeInstance:
     return FfpeInstance(0.4, 0.8, 0.45, coupling(0.45), g1, g2)
 
 
+def c4_instance(grid_m: int = 1023) -> FfpeInstance:
+    """C4 (2D, unit square, grid_m^2 interior points, row-major with x fastest): m = 0.4 (a = -3),
+    alpha = (0.3, 0.6); G0_1 = 1 on [0, 0.5]^2 (closed), G0_2 = 1 + U[-0.1, 0.1] at every
+    interior node (one draw per node in storage order)."""
+    rng = np.random.Generator(np.random.PCG64(SEEDS["C4"]))
+    h = 1.0 / (grid_m + 1)
+    x = (np.arange(grid_m) + 1) * h
+    X, Y = np.meshgrid(x, x)
+    g1 = ((X <= 0.5) & (Y <= 0.5)).astype(float).ravel()
+    g2 = 1.0 + rng.uniform(-0.1, 0.1, grid_m * grid_m)
+    return FfpeInstance(0.3, 0.6, 0.4, coupling(0.4), g1, g2)
+
+
 def c5_instances(n_inst: int = 4096, grid_m: int = 4095) -> list[FfpeInstance]:
     """C5: per instance alpha1, alpha2 ~ U[0.1, 0.9]; m from U on [0.1,0.45] u [0.55,0.9] (draw
     U[0, 0.7) then map); per field 8 sorted U(0,1) breakpoints and 9 levels ~ U[0,1], left-closed

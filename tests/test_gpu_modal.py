@@ -127,3 +127,100 @@ def test_k13_batch_mixed_instances(fraq, orc):
                                    "custom", custom_g1=s.custom_g1, custom_g2=s.custom_g2)
             assert rel(o.final_state.g1, g1) <= 1e-10
             assert rel(o.final_state.g2, g2) <= 1e-10
+
+
+# ------------------------------------------------------------------ full-size sampled-mode checks
+def _sines(idx, M):
+    """Rows sin((k+1)(j+1) pi/(M+1)) for k in idx, j = 0..M-1."""
+    return np.sin(np.outer(np.asarray(idx) + 1, np.arange(1, M + 1)) * np.pi / (M + 1))
+
+
+def _eig(M):
+    h = 1.0 / (M + 1)
+    return 4.0 / h ** 2 * np.sin(np.arange(1, M + 1) * np.pi * h / 2) ** 2
+
+
+def _sample_modes(M, n, seed):
+    rng = np.random.default_rng(seed)
+    return np.unique(np.concatenate([[0, 1, M // 2, M - 2, M - 1], rng.integers(0, M, n)]))
+
+
+@pytest.mark.slow
+def test_c4_full_size_sampled_modes(fraq, orc):
+    """C4 at full size (1023^2, N = 8192, FastSBD): DST coefficients of the GPU result on sampled
+    (ky, kx) modes -- extremes of lambda included -- equal the mode-space restatement over the
+    reference's SbdHistory lanes run on the same modes."""
+    from paper_1901_05128_b200.workloads import c4_instance
+    M, N = 1023, 8192
+    inst = c4_instance(M)
+    out = fraq.run_2d(inst.alpha1, inst.alpha2, inst.coupling_a, M, 1.0, N, fraq.Scheme.FastSBD,
+                      inst.g1, inst.g2)
+    ky = _sample_modes(M, 12, 7)
+    kx = _sample_modes(M, 12, 8)
+    Sy, Sx = _sines(ky, M), _sines(kx, M)
+    sc = (2.0 / (M + 1)) ** 2
+
+    def coef(g):
+        return (sc * Sy @ np.asarray(g).reshape(M, M) @ Sx.T).ravel()  # [ky][kx]
+    lam1 = _eig(M)
+    lam = (lam1[ky][:, None] + lam1[kx][None, :]).ravel()
+    tau = 1.0 / N
+    k1 = orc.build_kernel_auto(True, 1 - inst.alpha1, tau, N)
+    k2 = orc.build_kernel_auto(True, 1 - inst.alpha2, tau, N)
+    c1, c2 = coef(inst.g1), coef(inst.g2)
+    uN, vN, _ = orc.modal_run(k1, k2, inst.coupling_a, tau, N, lam, c1, c2, threads=8)
+    s = max(np.abs(c1).max(), np.abs(c2).max())
+    assert np.abs(coef(out.final_state.g1) - uN).max() <= 1e-10 * s
+    assert np.abs(coef(out.final_state.g2) - vN).max() <= 1e-10 * s
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("scheme", ["FastBE", "FastSBD"])
+def test_c3_full_size_sampled_modes(fraq, orc, scheme):
+    """C3 (M = 4095, N = 16384) through the modal solver vs the mode-space restatement on sampled
+    modes (both schemes)."""
+    from paper_1901_05128_b200.workloads import c3_instance
+    M, N = 4095, 16384
+    inst = c3_instance(M)
+    spec = fraq.ProblemSpec(alpha1=inst.alpha1, alpha2=inst.alpha2, coupling_a=inst.coupling_a,
+                            grid_m=M, t_final=1.0, n_steps=N, initial="custom",
+                            custom_g1=list(inst.g1), custom_g2=list(inst.g2))
+    rr = fraq.run(spec, getattr(fraq.Scheme, scheme), modal_kc(fraq))
+    k = _sample_modes(M, 40, 3)
+    S = _sines(k, M) * (2.0 / (M + 1))
+    sbd = scheme == "FastSBD"
+    tau = 1.0 / N
+    k1 = orc.build_kernel_auto(sbd, 1 - inst.alpha1, tau, N)
+    k2 = orc.build_kernel_auto(sbd, 1 - inst.alpha2, tau, N)
+    c1, c2 = S @ inst.g1, S @ inst.g2
+    uN, vN, _ = orc.modal_run(k1, k2, inst.coupling_a, tau, N, _eig(M)[k], c1, c2, threads=8)
+    s = max(np.abs(c1).max(), np.abs(c2).max())
+    assert np.abs(S @ np.array(rr.final_state.g1) - uN).max() <= 1e-10 * s
+    assert np.abs(S @ np.array(rr.final_state.g2) - vN).max() <= 1e-10 * s
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("scheme", ["FastBE", "FastSBD"])
+def test_c5_batch_full_horizon_sampled(fraq, orc, scheme):
+    """C5: a batch of 16 instances (full M = 4095, N = 16384) in one modal launch; two instances
+    checked on sampled modes against the mode-space restatement."""
+    from paper_1901_05128_b200.workloads import c5_instances
+    M, N = 4095, 16384
+    insts = c5_instances(16)
+    specs = [fraq.ProblemSpec(alpha1=i.alpha1, alpha2=i.alpha2, coupling_a=i.coupling_a, grid_m=M,
+                              t_final=1.0, n_steps=N, initial="custom", custom_g1=list(i.g1),
+                              custom_g2=list(i.g2)) for i in insts]
+    outs = fraq.run_batch(specs, getattr(fraq.Scheme, scheme), modal_kc(fraq))
+    sbd = scheme == "FastSBD"
+    tau = 1.0 / N
+    k = _sample_modes(M, 24, 11)
+    S = _sines(k, M) * (2.0 / (M + 1))
+    for ii in (0, 13):
+        inst, o = insts[ii], outs[ii]
+        k1 = orc.build_kernel_auto(sbd, 1 - inst.alpha1, tau, N)
+        k2 = orc.build_kernel_auto(sbd, 1 - inst.alpha2, tau, N)
+        c1, c2 = S @ inst.g1, S @ inst.g2
+        uN, vN, _ = orc.modal_run(k1, k2, inst.coupling_a, tau, N, _eig(M)[k], c1, c2, threads=8)
+        s = max(np.abs(c1).max(), np.abs(c2).max())
+        assert np.abs(S @ np.array(o.final_state.g1) - uN).max() <= 1e-10 * s
+        assert np.abs(S @ np.array(o.final_state.g2) - vN).max() <= 1e-10 * s
