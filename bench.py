@@ -167,7 +167,17 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="C2", choices=["C2", "C3", "C4", "C5", "C5-SBD"],
+                    help="C2 (default, BASELINE configs[1]) or an FFPE config (bench_ffpe.py)")
     args = ap.parse_args()
+    if args.workload != "C2":
+        import bench_ffpe
+        if args.steps == N_LEVELS // LEVELS_PER_STEP:
+            args.steps = {"C3": 20, "C4": 3, "C5": 4, "C5-SBD": 4}[args.workload]
+        if args.impl == "reference":
+            rank, world, _ = dist_env()
+            bench_ffpe.run_reference(args, rank, world, METRIC)
+            return
     if args.impl == "reference":
         run_reference_arm(args)
         return
@@ -183,6 +193,13 @@ def main():
         pg = dist
     import paper_1901_05128_b200 as fraq
     from paper_1901_05128_b200.workloads import c2_params
+    if args.workload != "C2":
+        import bench_ffpe
+        bench_ffpe.run_gpu(args, rank, world, local, pg, METRIC, Clocks, fraq, torch)
+        if pg:
+            pg.barrier()
+            pg.destroy_process_group()
+        return
 
     params = c2_params(DOFS)
     tau = params.tau

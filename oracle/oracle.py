@@ -347,6 +347,7 @@ class Oracle:
                                     C.c_int(INITIAL[initial]), _p(cg1), _p(cg2),
                                     C.c_int(SCHEMES[scheme]), ki, C.c_double(eps_tol), _p(g1),
                                     _p(g2), C.byref(e1), C.byref(e2), C.byref(loop)), "run")
+            self.last_loop_seconds = loop.value  # fraq::run's own loop timer (fpfp.cpp:361-366)
         return g1, g2, e1.value, e2.value
 
     def block_solve(self, d01, d02, a, tau, m, lead, rhs1, rhs2):

@@ -454,8 +454,19 @@ void k13_run(fraq_ctx c, const std::vector<K13Inst>& in, const double* lam, int 
             maxL = std::max(maxL, I.L[f]);
         }
     const int delta = minL >= 8 ? 0 : 1;
-    // J <= 256: 16 modes x 64 nodes per GEMM warp; else 8 modes x 128 nodes per GEMM warp
-    const int RB = maxJ <= 256 ? 2 : 1, nodes_w = RB == 2 ? 64 : 128, modes = 8 * RB;
+    // J <= 256: 16 modes x 64 nodes per GEMM warp; else 8 modes x 8 NT nodes per GEMM warp with
+    // the narrowest NT in {12, 13, 14, 16} that covers J in 4 warps (C4: 408 nodes -> NT = 13)
+    const int RB = maxJ <= 256 ? 2 : 1, modes = 8 * RB;
+    int NT = 8;
+    if (RB == 1) {
+        NT = 16;
+        for (int cand : {12, 13, 14})
+            if (4 * 8 * cand >= maxJ) {
+                NT = cand;
+                break;
+            }
+    }
+    const int nodes_w = 8 * NT;
     const int nwf = (maxJ + nodes_w - 1) / nodes_w, Jp = nodes_w * nwf, nwg = 2 * nwf;
     const int TS = 17 * Jp + K13_CW;
     const int span = 8 + 8 * delta + maxL + 8;
@@ -504,6 +515,12 @@ void k13_run(fraq_ctx c, const std::vector<K13Inst>& in, const double* lam, int 
     const size_t smem = k13_smem(TS, nwg, ring, modes);
     if (RB == 2)
         k13_launch<2, 8>(A, smem, c->num_sms, c->stream);
+    else if (NT == 12)
+        k13_launch<1, 12>(A, smem, c->num_sms, c->stream);
+    else if (NT == 13)
+        k13_launch<1, 13>(A, smem, c->num_sms, c->stream);
+    else if (NT == 14)
+        k13_launch<1, 14>(A, smem, c->num_sms, c->stream);
     else
         k13_launch<1, 16>(A, smem, c->num_sms, c->stream);
     FRAQ_CUDA(cudaStreamSynchronize(c->stream));
