@@ -88,11 +88,13 @@ typedef struct {
 } fraq_spec_t;
 
 /* KernelConfig, fpfp.hpp:50-57, plus the spatial solver of the fast schemes (addition):
- * FRAQ_SOLVER_PHYSICAL (0, default) = the reference's physical-space stepper (stencil RHS +
- * 2x2-block tridiagonal solve per level); FRAQ_SOLVER_MODAL (1) = the same scheme stepped in the
- * DST eigenbasis (the reference's mode-space oracle, test_fpfp.cpp:21-180), every mode an
- * independent 2x2 recursion -- exact in exact arithmetic, better conditioned in fp64. */
-enum { FRAQ_SOLVER_PHYSICAL = 0, FRAQ_SOLVER_MODAL = 1 };
+ * FRAQ_SOLVER_PHYSICAL (0) = the reference's physical-space stepper (stencil RHS + 2x2-block
+ * tridiagonal solve per level); FRAQ_SOLVER_MODAL (1) = the same scheme stepped in the DST
+ * eigenbasis (the reference's mode-space oracle, test_fpfp.cpp:21-180), every mode an independent
+ * 2x2 recursion -- exact in exact arithmetic, better conditioned in fp64; FRAQ_SOLVER_AUTO (2,
+ * default) = MODAL for the fast schemes without an observer (PHYSICAL if the modal path rejects
+ * the kernels, e.g. a head window over 56 levels), PHYSICAL otherwise. */
+enum { FRAQ_SOLVER_PHYSICAL = 0, FRAQ_SOLVER_MODAL = 1, FRAQ_SOLVER_AUTO = 2 };
 typedef struct {
     int be_points, sbd_points_1, sbd_points_2, sbd_head;
     double eps_tol;

@@ -67,6 +67,7 @@ EXTRA = [
     "make_sbd_kernel",
     "run_2d",
     "run_batch",
+    "SOLVER_AUTO",
     "SOLVER_MODAL",
     "SOLVER_PHYSICAL",
     "synchronize",

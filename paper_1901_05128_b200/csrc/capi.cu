@@ -318,7 +318,7 @@ void fraq_kconf_default(fraq_kconf_t* c) {
     c->sbd_head = 0;
     c->eps_tol = 1e-12;
     c->auto_size = 1;
-    c->solver = FRAQ_SOLVER_PHYSICAL;
+    c->solver = FRAQ_SOLVER_AUTO;
 }
 
 int fraq_run_2d(fraq_ctx c, double alpha1, double alpha2, double coupling_a, int grid_m,

@@ -371,6 +371,17 @@ void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
         ffpe_run_modal(c, specs, n_inst, sbd, kc, g1_out, g2_out, info);
         return;
     }
+    if (kc.solver == FRAQ_SOLVER_AUTO && fast && !obs) {
+        bool done = false;
+        try {
+            ffpe_run_modal(c, specs, n_inst, sbd, kc, g1_out, g2_out, info);
+            done = true;
+        } catch (const Error& e) {
+            if (e.code != FRAQ_EINVAL || std::string(e.what()).find("modal run:") != 0) throw;
+        }
+        if (done) return;
+    }
+    if (kc.solver < 0 || kc.solver > FRAQ_SOLVER_AUTO) fail(FRAQ_EINVAL, "run: unknown solver");
     const double tau = s0.t_final / double(N);
     const double h = s0.length / double(m + 1);
     const double t_setup0 = now_s();

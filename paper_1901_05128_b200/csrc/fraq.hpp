@@ -199,8 +199,9 @@ struct KernelConfig {
     double eps_tol = 1e-12;
     bool auto_size = true;
     // addition: spatial solver of the fast schemes, FRAQ_SOLVER_PHYSICAL (reference-shaped
-    // stencil + block solve) or FRAQ_SOLVER_MODAL (DST eigenbasis, independent modes)
-    int solver = FRAQ_SOLVER_PHYSICAL;
+    // stencil + block solve), FRAQ_SOLVER_MODAL (DST eigenbasis, independent modes) or
+    // FRAQ_SOLVER_AUTO (modal where it applies)
+    int solver = FRAQ_SOLVER_AUTO;
 };
 
 struct RunResult {

@@ -179,7 +179,8 @@ def _modespace_fastbe(orc, inst, M, N, a, al1, al2):
 
 
 @pytest.mark.slow
-def test_c3_full(fraq, orc):
+@pytest.mark.parametrize("solver", ["SOLVER_PHYSICAL", "SOLVER_AUTO"])
+def test_c3_full(fraq, orc, solver):
     """C3 at full size: M = 4095, N = 16384, FastBE, alpha (0.4, 0.8), m = 0.45 (a = -5.5).
     Same auto-sized kernels and certificates as the reference.  The physical-space scheme's
     rounding drift on this grid is ~1e-7 absolute over 16384 implicit steps for ANY fp64
@@ -189,7 +190,9 @@ def test_c3_full(fraq, orc):
     spec = fraq.ProblemSpec(alpha1=inst.alpha1, alpha2=inst.alpha2, coupling_a=inst.coupling_a,
                             grid_m=4095, t_final=1.0, n_steps=16384, initial="custom",
                             custom_g1=list(inst.g1), custom_g2=list(inst.g2))
-    rr = fraq.run(spec, fraq.Scheme.FastBE)
+    kc = fraq.KernelConfig()
+    kc.solver = getattr(fraq, solver)
+    rr = fraq.run(spec, fraq.Scheme.FastBE, kc)
     g1, g2, e1, e2 = orc.run(inst.alpha1, inst.alpha2, inst.coupling_a, 4095, 1.0, 16384,
                              "FastBE", "custom", inst.g1, inst.g2)
     assert rr.kernel_eps1 == pytest.approx(e1, rel=1e-3)
@@ -202,8 +205,9 @@ def test_c3_full(fraq, orc):
     assert max(ad(rr.final_state.g1, g1), ad(rr.final_state.g2, g2)) <= 3e-7
 
 
+@pytest.mark.parametrize("solver", ["SOLVER_PHYSICAL", "SOLVER_AUTO"])
 @pytest.mark.parametrize("scheme", ["FastBE", "FastSBD"])
-def test_c5_sampled_instances(fraq, orc, scheme):
+def test_c5_sampled_instances(fraq, orc, scheme, solver):
     """C5-style instances (random alpha, m, step-function data) at M = 4095 batched on the GPU;
     each equals the reference's single-instance run (shortened horizon N = 512)."""
     insts = c5_instances(6)[1:6:2]
@@ -211,7 +215,9 @@ def test_c5_sampled_instances(fraq, orc, scheme):
     specs = [fraq.ProblemSpec(alpha1=i.alpha1, alpha2=i.alpha2, coupling_a=i.coupling_a,
                               grid_m=4095, t_final=N / 16384, n_steps=N, initial="custom",
                               custom_g1=list(i.g1), custom_g2=list(i.g2)) for i in insts]
-    outs = fraq.run_batch(specs, getattr(fraq.Scheme, scheme))
+    kc = fraq.KernelConfig()
+    kc.solver = getattr(fraq, solver)
+    outs = fraq.run_batch(specs, getattr(fraq.Scheme, scheme), kc)
     for i, o in zip(insts, outs):
         g1, g2, _, _ = orc.run(i.alpha1, i.alpha2, i.coupling_a, 4095, N / 16384, N, scheme,
                                "custom", i.g1, i.g2)

@@ -285,9 +285,10 @@ def test_multi_group_history(fraq, orc):
 
 
 # ------------------------------------------------------------------ L4 FFPE
+@pytest.mark.parametrize("solver", ["SOLVER_PHYSICAL", "SOLVER_AUTO"])
 @pytest.mark.parametrize("scheme", ["BE", "FastBE", "SBD", "FastSBD"])
 @pytest.mark.parametrize("grid_m,a", [(31, -1.0), (31, 2.0), (50, 0.5), (63, -5.5)])
-def test_ffpe_matches_oracle(fraq, orc, scheme, grid_m, a):
+def test_ffpe_matches_oracle(fraq, orc, scheme, grid_m, a, solver):
     kconf = dict(auto_size=False, be_points=24, sbd_points_1=24, sbd_points_2=24, sbd_head=9)
     g1, g2, e1, e2 = orc.run(0.3, 0.65, a, grid_m, 0.5, 64, scheme, "indicator", kconf=kconf)
     spec = fraq.ProblemSpec(alpha1=0.3, alpha2=0.65, coupling_a=a, grid_m=grid_m, t_final=0.5,
@@ -297,17 +298,21 @@ def test_ffpe_matches_oracle(fraq, orc, scheme, grid_m, a):
     kc.be_points = 24
     kc.sbd_points_1 = kc.sbd_points_2 = 24
     kc.sbd_head = 9
+    kc.solver = getattr(fraq, solver)
     rr = fraq.run(spec, getattr(fraq.Scheme, scheme), kc)
     assert rel_linf(rr.final_state.g1, g1) <= 1e-10
     assert rel_linf(rr.final_state.g2, g2) <= 1e-10
 
 
+@pytest.mark.parametrize("solver", ["SOLVER_PHYSICAL", "SOLVER_AUTO"])
 @pytest.mark.parametrize("scheme", ["FastBE", "FastSBD"])
-def test_ffpe_auto_kernels_match_oracle(fraq, orc, scheme):
+def test_ffpe_auto_kernels_match_oracle(fraq, orc, scheme, solver):
     g1, g2, e1, e2 = orc.run(0.3, 0.6, 2.0, 63, 1.0, 200, scheme, "poly_sin")
     spec = fraq.ProblemSpec(alpha1=0.3, alpha2=0.6, coupling_a=2.0, grid_m=63, t_final=1.0,
                             n_steps=200)
-    rr = fraq.run(spec, getattr(fraq.Scheme, scheme))
+    kc = fraq.KernelConfig()
+    kc.solver = getattr(fraq, solver)
+    rr = fraq.run(spec, getattr(fraq.Scheme, scheme), kc)
     assert rel_linf(rr.final_state.g1, g1) <= 1e-10
     assert rel_linf(rr.final_state.g2, g2) <= 1e-10
     assert rr.kernel_eps1 == pytest.approx(e1, rel=1e-3)
@@ -322,10 +327,13 @@ def test_ffpe_observer_and_batch(fraq):
     assert seen[-1][1] == rr.final_state.g1[3]
     specs = [fraq.ProblemSpec(alpha1=0.2 + 0.1 * i, alpha2=0.5, coupling_a=1.0, grid_m=15,
                               t_final=0.1, n_steps=12) for i in range(3)]
-    outs = fraq.run_batch(specs, fraq.Scheme.FastSBD)
-    for s, o in zip(specs, outs):
-        single = fraq.run(s, fraq.Scheme.FastSBD)
-        assert rel_linf(o.final_state.g1, single.final_state.g1) <= 1e-14
+    for solver in (fraq.SOLVER_PHYSICAL, fraq.SOLVER_AUTO):
+        kc = fraq.KernelConfig()
+        kc.solver = solver
+        outs = fraq.run_batch(specs, fraq.Scheme.FastSBD, kc)
+        for s, o in zip(specs, outs):
+            single = fraq.run(s, fraq.Scheme.FastSBD, kc)
+            assert rel_linf(o.final_state.g1, single.final_state.g1) <= 1e-14
 
 
 def test_ffpe_zero_stays_zero(fraq):
@@ -333,5 +341,8 @@ def test_ffpe_zero_stays_zero(fraq):
                             n_steps=12, initial="custom", custom_g1=[0.0] * 15,
                             custom_g2=[0.0] * 15)
     for s in ("BE", "FastBE", "SBD", "FastSBD"):
-        rr = fraq.run(spec, getattr(fraq.Scheme, s))
-        assert all(v == 0.0 for v in rr.final_state.g1 + rr.final_state.g2)
+        for solver in (fraq.SOLVER_PHYSICAL, fraq.SOLVER_AUTO):
+            kc = fraq.KernelConfig()
+            kc.solver = solver
+            rr = fraq.run(spec, getattr(fraq.Scheme, s), kc)
+            assert all(v == 0.0 for v in rr.final_state.g1 + rr.final_state.g2)
