@@ -191,8 +191,11 @@ int fraq_direct_cq(fraq_ctx ctx, int sbd, double g, double tau, const double* U,
 
 /* ---------------------------------------------------------------- L4 FFPE
  * run() (fpfp.cpp:351-381) for n_inst independent instances (BASELINE C3: 1, C5: 4096) solved
- * together on the device: histories K5 for both fields, RHS + 2x2-block tridiagonal solve K6,
- * SBD correction sequence K7.  g1/g2: host, n_inst * grid_m values (row per instance). */
+ * together on the device.  kconf->solver selects the spatial solver of the fast schemes:
+ * PHYSICAL = histories K5 for both fields, RHS + 2x2-block tridiagonal solve K6, SBD correction
+ * sequence K7 (the reference's FastStepper shape); MODAL / AUTO (default) = DST (K12, DMMA),
+ * per-mode stepping on DMMA (K13), inverse DST.  Classical schemes always run physically.
+ * g1/g2: host, n_inst * grid_m values (row per instance). */
 void fraq_kconf_default(fraq_kconf_t* c);
 int fraq_run(fraq_ctx ctx, const fraq_spec_t* specs, int n_inst, int scheme,
              const fraq_kconf_t* kconf, double* g1, double* g2, fraq_run_info_t* info);
