@@ -213,6 +213,19 @@ int fraq_run_2d(fraq_ctx ctx, double alpha1, double alpha2, double coupling_a, i
                 double t_final, long n_steps, int scheme, const fraq_kconf_t* kconf,
                 const double* g1_0, const double* g2_0, double* g1, double* g2,
                 fraq_run_info_t* info);
+/* Building blocks of the mode-sharded 2D solve, no reference counterpart:
+ * fraq_dst2d: n_fields grid_m x grid_m arrays; forward (inverse = 0) c[ky][kx] =
+ * (2/(M+1))^2 sum_y,x S[ky][y] S[kx][x] G[y][x], inverse (1) G = S c S, S[k][j] =
+ * sin((k+1)(j+1) pi/(M+1)) -- the mode basis of the reference's mode-space oracle
+ * (test_fpfp.cpp:39-54) in 2D.  fraq_modal_run: one instance stepped over n_modes modes with
+ * eigenvalues lam[] (fast BE/BDF2, the FastStepper algebra fpfp.cpp:259-349 per mode);
+ * c0 / cN: [2][n_modes] field-major.  mem: FRAQ_HOST or FRAQ_DEVICE for all arrays. */
+int fraq_dst2d(fraq_ctx ctx, int grid_m, int n_fields, const double* in, double* out, int inverse,
+               int mem);
+int fraq_modal_run(fraq_ctx ctx, double alpha1, double alpha2, double coupling_a, double t_final,
+                   long n_steps, int scheme, const fraq_kconf_t* kconf, long n_modes,
+                   const double* lam, const double* c0, double* cN, int mem,
+                   fraq_run_info_t* info);
 int fraq_run_observed(fraq_ctx ctx, const fraq_spec_t* spec, int scheme,
                       const fraq_kconf_t* kconf, fraq_observer_fn fn, void* user, double* g1,
                       double* g2, fraq_run_info_t* info);

@@ -61,6 +61,10 @@ EXTRA = [
     "diag_dmma_peak",
     "direct_cq",
     "direct_cq_device",
+    "dst2d",
+    "dst2d_device",
+    "modal_run",
+    "modal_run_device",
     "diag_fp64_peak",
     "gamma_fn",
     "make_be_kernel",

@@ -25,6 +25,10 @@ void hist_output(fraq_hist h, int mode, double* out, int mem);
 void hist_lagged(fraq_hist h, long depth, double* out, int mem);
 void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, long ldd, int mem);
 int hist_last_path(fraq_hist h);
+void dst2d(fraq_ctx c, int M, int n_fields, const double* in, double* out, bool inverse, int mem);
+void modal_run_modes(fraq_ctx c, double alpha1, double alpha2, double a, double t_final, long N,
+                     int scheme, const fraq_kconf_t* kc, long n_modes, const double* lam,
+                     const double* c0, double* cN, int mem, fraq_run_info_t* info);
 void ffpe_run_2d(fraq_ctx c, double alpha1, double alpha2, double a, int m, double t_final,
                  long N, int scheme, const fraq_kconf_t* kc, const double* g1_0,
                  const double* g2_0, double* g1, double* g2, fraq_run_info_t* info);
@@ -329,6 +333,25 @@ int fraq_run_2d(fraq_ctx c, double alpha1, double alpha2, double coupling_a, int
         check_ctx(c);
         ffpe_run_2d(c, alpha1, alpha2, coupling_a, grid_m, t_final, n_steps, scheme, kconf, g1_0,
                     g2_0, g1, g2, info);
+    });
+}
+
+int fraq_dst2d(fraq_ctx c, int grid_m, int n_fields, const double* in, double* out, int inverse,
+               int mem) {
+    return guarded([&] {
+        check_ctx(c);
+        dst2d(c, grid_m, n_fields, in, out, inverse != 0, mem);
+    });
+}
+
+int fraq_modal_run(fraq_ctx c, double alpha1, double alpha2, double coupling_a, double t_final,
+                   long n_steps, int scheme, const fraq_kconf_t* kconf, long n_modes,
+                   const double* lam, const double* c0, double* cN, int mem,
+                   fraq_run_info_t* info) {
+    return guarded([&] {
+        check_ctx(c);
+        modal_run_modes(c, alpha1, alpha2, coupling_a, t_final, n_steps, scheme, kconf, n_modes,
+                        lam, c0, cN, mem, info);
     });
 }
 

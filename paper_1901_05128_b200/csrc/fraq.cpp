@@ -452,6 +452,26 @@ RunResult run_2d(double alpha1, double alpha2, double coupling_a, int grid_m, do
     return rr;
 }
 
+void dst2d(int grid_m, int n_fields, const double* in, double* out, bool inverse, int mem) {
+    check(fraq_dst2d(default_context(), grid_m, n_fields, in, out, inverse ? 1 : 0, mem));
+}
+
+RunResult modal_run(double alpha1, double alpha2, double coupling_a, double t_final,
+                    long n_steps, Scheme scheme, long n_modes, const double* lam,
+                    const double* c0, double* cN, int mem, const KernelConfig& kconf) {
+    const fraq_kconf_t kc = flat_kconf(kconf);
+    fraq_run_info_t info{};
+    check(fraq_modal_run(default_context(), alpha1, alpha2, coupling_a, t_final, n_steps,
+                         flat_scheme(scheme), &kc, n_modes, lam, c0, cN, mem, &info));
+    RunResult rr;
+    rr.final_state.step = n_steps;
+    rr.loop_seconds = info.loop_seconds;
+    rr.setup_seconds = info.setup_seconds;
+    rr.kernel_eps1 = info.kernel_eps1;
+    rr.kernel_eps2 = info.kernel_eps2;
+    return rr;
+}
+
 std::vector<RunResult> run_batch(const std::vector<ProblemSpec>& specs, Scheme scheme,
                                  const KernelConfig& kconf) {
     std::vector<fraq_spec_t> fs;

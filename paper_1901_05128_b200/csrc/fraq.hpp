@@ -226,6 +226,18 @@ RunResult run_2d(double alpha1, double alpha2, double coupling_a, int grid_m, do
                  long n_steps, Scheme scheme, const std::vector<double>& g1_0,
                  const std::vector<double>& g2_0, const KernelConfig& kconf = {});
 
+/// 2D DST of n_fields grid_m^2 arrays: forward coefficients c[ky][kx] = (2/(M+1))^2 S G S, or the
+/// inverse synthesis G = S c S.  mem: FRAQ_HOST or FRAQ_DEVICE for in / out.
+void dst2d(int grid_m, int n_fields, const double* in, double* out, bool inverse,
+           int mem = FRAQ_HOST);
+
+/// One instance (fast BE / BDF2) stepped over n_modes modes with eigenvalues lam; c0 / cN are
+/// [2][n_modes] (field-major).  The per-rank work of the mode-sharded 2D solve.
+RunResult modal_run(double alpha1, double alpha2, double coupling_a, double t_final,
+                    long n_steps, Scheme scheme, long n_modes, const double* lam,
+                    const double* c0, double* cN, int mem = FRAQ_HOST,
+                    const KernelConfig& kconf = {});
+
 /// Many independent instances (same grid_m, n_steps, t_final) solved together.
 std::vector<RunResult> run_batch(const std::vector<ProblemSpec>& specs, Scheme scheme,
                                  const KernelConfig& kconf = {});

@@ -105,7 +105,17 @@ struct K13Inst {
     int J[2], L[2];
 };
 bool k13_supported(int maxJ, int minL, int maxL);
-void k13_run(fraq_ctx c, const std::vector<K13Inst>& in, const double* lam, int n_modes, long N,
-             bool sbd, const double* c0, double* cN);
+// Setup (node fragment tables, combined weights) and launch are split so that the loop timers
+// see only the stepping.
+struct K13Plan {
+    DevBuf<double> tabs;
+    DevBuf<unsigned char> inst;  // per-instance device records
+    DevBuf<int> counter;
+    int n_inst = 0, RB = 2, NT = 8, nwf = 1, Jp = 64, nwg = 2, TS = 0, ring = 32, delta = 0;
+    bool sbd = false;
+};
+void k13_prepare(fraq_ctx c, const std::vector<K13Inst>& in, bool sbd, K13Plan& plan);
+void k13_exec(fraq_ctx c, K13Plan& plan, const double* lam, int n_modes, long N, const double* c0,
+              double* cN);
 
 }  // namespace fraqcu

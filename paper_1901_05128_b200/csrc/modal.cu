@@ -345,6 +345,21 @@ void launch_modal(int npl, int P, const ModalArgs& a, cudaStream_t s) {
 
 }  // namespace
 
+struct ModalPlan {
+    bool use_k13 = false;
+    K13Plan k13;
+    DevBuf<ModalInst> dmi;  // K11 instance records
+    int n_inst = 0, npl = 0, P = 2;
+    bool sbd = false;
+};
+
+struct Dst2D {
+    int M = 0;
+    DevBuf<double> tab, A, B;
+    void init(fraq_ctx c, int m);
+    void apply(fraq_ctx c, int n_fields, const double* in, double* out, bool inverse);
+};
+
 // Apply the DST along the mode axis: Out (M x C) = scale * S In (M x C).
 void dst_apply(fraq_ctx c, int M, const double* sintab, const double* In, long C, double* Out,
                double scale) {
@@ -367,10 +382,11 @@ void make_sintab(fraq_ctx c, int M, DevBuf<double>& tab) {
 
 // Mode-space stepping of n_inst instances with per-instance kernels (device tables already in
 // HistDevice hd: group 2i = field 1, 2i+1 = field 2 of instance i).  c0 / cN: [inst][2][modes].
-void modal_run(fraq_ctx c, const HistDevice& hd, const std::vector<double>& a,
-               const std::vector<double>& tau, const double* corr, const std::vector<long>& corr_off,
-               const double* lam, int n_modes, int n_inst, long N, bool sbd, const double* c0,
-               double* cN) {
+// modal_plan does the setup (K13 fragment tables, or the K11 instance records); modal_exec
+// launches the stepping only.
+void modal_plan(fraq_ctx c, const HistDevice& hd, const std::vector<double>& a,
+                const std::vector<double>& tau, const double* corr,
+                const std::vector<long>& corr_off, int n_inst, bool sbd, ModalPlan& P) {
     std::vector<ModalInst> mi(n_inst);
     int maxJ = 0, minL = 1 << 30, maxL = 0;
     for (int i = 0; i < n_inst; ++i) {
@@ -391,7 +407,10 @@ void modal_run(fraq_ctx c, const HistDevice& hd, const std::vector<double>& a,
             if (G.L > MD_CAP - 8) fail(FRAQ_EINVAL, "modal run: head window longer than 56 levels");
         }
     }
-    if (k13_supported(maxJ, minL, maxL)) {
+    P.n_inst = n_inst;
+    P.sbd = sbd;
+    P.use_k13 = k13_supported(maxJ, minL, maxL);
+    if (P.use_k13) {
         std::vector<K13Inst> ki(n_inst);
         for (int i = 0; i < n_inst; ++i) {
             ki[i].a = a[i];
@@ -405,17 +424,46 @@ void modal_run(fraq_ctx c, const HistDevice& hd, const std::vector<double>& a,
                 ki[i].L[f] = mi[i].fld[f].L;
             }
         }
-        k13_run(c, ki, lam, n_modes, N, sbd, c0, cN);
+        k13_prepare(c, ki, sbd, P.k13);
         return;
     }
-    DevBuf<ModalInst> dmi(n_inst);
-    FRAQ_CUDA(cudaMemcpyAsync(dmi.p, mi.data(), sizeof(ModalInst) * n_inst, cudaMemcpyHostToDevice,
-                              c->stream));
-    ModalArgs A{dmi.p, lam, n_modes, n_inst, N, sbd ? 1 : 0, c0, cN};
-    const int npl = (maxJ + 31) / 32;
-    if (npl > 16) fail(FRAQ_EINVAL, "modal run: more than 512 nodes per field");
-    launch_modal(npl, minL >= 8 ? 8 : 2, A, c->stream);
-    FRAQ_CUDA(cudaStreamSynchronize(c->stream));
+    P.npl = (maxJ + 31) / 32;
+    if (P.npl > 16) fail(FRAQ_EINVAL, "modal run: more than 512 nodes per field");
+    P.P = minL >= 8 ? 8 : 2;
+    P.dmi.alloc(n_inst);
+    FRAQ_CUDA(cudaMemcpyAsync(P.dmi.p, mi.data(), sizeof(ModalInst) * n_inst,
+                              cudaMemcpyHostToDevice, c->stream));
+}
+
+void modal_exec(fraq_ctx c, ModalPlan& P, const double* lam, int n_modes, long N,
+                const double* c0, double* cN) {
+    if (P.use_k13) {
+        k13_exec(c, P.k13, lam, n_modes, N, c0, cN);
+        return;
+    }
+    ModalArgs A{P.dmi.p, lam, n_modes, P.n_inst, N, P.sbd ? 1 : 0, c0, cN};
+    launch_modal(P.npl, P.P, A, c->stream);
+}
+
+// 2D DST workspace: forward out[f][ky][kx] = (2/(M+1))^2 sum S[ky][y] S[kx][x] in[f][y][x],
+// inverse out[f][y][x] = sum S[y][ky] S[x][kx] in[f][ky][kx] (S symmetric); each as two DMMA GEMMs
+// along y and x with transposes in between.
+void Dst2D::init(fraq_ctx c, int m) {
+    M = m;
+    make_sintab(c, M, tab);
+    A.alloc((size_t)M * M);
+    B.alloc((size_t)M * M);
+}
+
+void Dst2D::apply(fraq_ctx c, int n_fields, const double* in, double* out, bool inverse) {
+    const long MM = (long)M * M;
+    const double sc = inverse ? 1.0 : 2.0 / (M + 1);
+    for (int f = 0; f < n_fields; ++f) {
+        dst_apply(c, M, tab.p, in + f * MM, M, A.p, sc);   // A[k][x]
+        transpose_dev(c, A.p, M, M, B.p);                  // B[x][k]
+        dst_apply(c, M, tab.p, B.p, M, A.p, sc);           // A[l][k]
+        transpose_dev(c, A.p, M, M, out + f * MM);         // out[k][l]
+    }
 }
 
 }  // namespace fraqcu
@@ -441,10 +489,13 @@ struct ModalSetup {
     HistDevice hd;
     DevBuf<double> corr;
     std::vector<long> corr_off;
+    ModalPlan plan;
 };
 
-void modal_prepare(fraq_ctx c, ModalSetup& S, const std::vector<double>& gam, double tau, long N,
-                   bool sbd, const fraq_kconf_t& kc) {
+// gam: 2 exponents per instance (field 1, field 2); a: coupling per instance.
+void modal_prepare(fraq_ctx c, ModalSetup& S, const std::vector<double>& gam,
+                   const std::vector<double>& a, double tau, long N, bool sbd,
+                   const fraq_kconf_t& kc) {
     build_ffpe_kernels(c, gam, tau, N, sbd, kc, S.ks, S.eps);
     const int ng = (int)gam.size();
     std::vector<const fraq_kernel_t*> kp(ng);
@@ -459,7 +510,31 @@ void modal_prepare(fraq_ctx c, ModalSetup& S, const std::vector<double>& gam, do
             S.corr_off[t] = (long)t * (N + 1);
         }
     }
+    const int n_inst = ng / 2;
+    modal_plan(c, S.hd, a, std::vector<double>(n_inst, tau), sbd ? S.corr.p : nullptr, S.corr_off,
+               n_inst, sbd, S.plan);
 }
+
+struct EventTimer {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaStream_t s;
+    explicit EventTimer(cudaStream_t st) : s(st) {
+        FRAQ_CUDA(cudaEventCreate(&e0));
+        FRAQ_CUDA(cudaEventCreate(&e1));
+        FRAQ_CUDA(cudaEventRecord(e0, s));
+    }
+    double stop() {
+        FRAQ_CUDA(cudaEventRecord(e1, s));
+        FRAQ_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        FRAQ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        return ms * 1e-3;
+    }
+    ~EventTimer() {
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
+};
 
 void fill_info(fraq_run_info_t* info, const ModalSetup& S, double loop_s, double setup_s) {
     if (!info) return;
@@ -513,7 +588,7 @@ void ffpe_run_modal(fraq_ctx c, const fraq_spec_t* specs, int n_inst, bool sbd,
         av[i] = s.coupling_a;
     }
     ModalSetup S;
-    modal_prepare(c, S, gam, tau, N, sbd, kc);
+    modal_prepare(c, S, gam, av, tau, N, sbd, kc);
     // eigenvalues lambda_k = (4/h^2) sin^2(k pi h / (2 L)) (block_solver.cpp:21-24)
     std::vector<double> lam(M);
     for (int k = 0; k < M; ++k) {
@@ -527,103 +602,136 @@ void ffpe_run_modal(fraq_ctx c, const fraq_spec_t* specs, int n_inst, bool sbd,
                               c->stream));
     make_sintab(c, M, tab);
     const double t1 = now_s2();
-    cudaEvent_t e0, e1;
-    FRAQ_CUDA(cudaEventCreate(&e0));
-    FRAQ_CUDA(cudaEventCreate(&e1));
-    FRAQ_CUDA(cudaEventRecord(e0, c->stream));
+    EventTimer timer(c->stream);
     // forward DST (projection, 2/(M+1) S G): rows = modes; then [C][M] for the stepper
     dst_apply(c, M, tab.p, dG.p, C, dW.p, 2.0 / (M + 1));
     transpose_dev(c, dW.p, M, C, dc0.p);
-    modal_run(c, S.hd, av, tv, sbd ? S.corr.p : nullptr, S.corr_off, dlam.p, M, n_inst, N, sbd,
-              dc0.p, dcN.p);
+    modal_exec(c, S.plan, dlam.p, M, N, dc0.p, dcN.p);
     // inverse: g = S^T c (S symmetric)
     transpose_dev(c, dcN.p, C, M, dW.p);
     dst_apply(c, M, tab.p, dW.p, C, dG.p, 1.0);
-    FRAQ_CUDA(cudaEventRecord(e1, c->stream));
-    FRAQ_CUDA(cudaEventSynchronize(e1));
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    const double loop_s = timer.stop();
     FRAQ_CUDA(cudaMemcpy(G0.data(), dG.p, sizeof(double) * G0.size(), cudaMemcpyDeviceToHost));
     for (int i = 0; i < n_inst; ++i)
         for (int j = 0; j < M; ++j) {
             g1_out[(size_t)i * M + j] = G0[(size_t)j * C + 2 * i];
             g2_out[(size_t)i * M + j] = G0[(size_t)j * C + 2 * i + 1];
         }
-    fill_info(info, S, ms * 1e-3, t1 - t0);
+    fill_info(info, S, loop_s, t1 - t0);
 }
 
-// 2D: modes (k, l) with lambda_k + lambda_l; forward transform c = (2/(M+1))^2 S G S, inverse
-// g = S c S (S symmetric); data row-major (x fastest): G[y][x].
-void ffpe_run_2d(fraq_ctx c, double alpha1, double alpha2, double a, int M, double t_final,
-                 long N, int scheme, const fraq_kconf_t* kc_in, const double* g1_0,
-                 const double* g2_0, double* g1, double* g2, fraq_run_info_t* info) {
-    if (M < 1 || N < 1) fail(FRAQ_EINVAL, "run_2d: grid_m and n_steps must be >= 1");
-    if (scheme != FRAQ_FASTBE && scheme != FRAQ_FASTSBD)
-        fail(FRAQ_EINVAL, "run_2d: scheme must be FastBE or FastSBD");
-    fraq_kconf_t kc;
-    if (kc_in)
-        kc = *kc_in;
-    else
-        fraq_kconf_default(&kc);
-    const bool sbd = scheme == FRAQ_FASTSBD;
-    const double t0 = now_s2();
-    const double tau = t_final / double(N);
+std::vector<double> eig2d(int M) {
     const double h = 1.0 / double(M + 1);
-    const long MM = (long)M * M;
-    ModalSetup S;
-    modal_prepare(c, S, {1.0 - alpha1, 1.0 - alpha2}, tau, N, sbd, kc);
-    std::vector<double> lam1(M), lam2(MM);
+    std::vector<double> lam1(M), lam2((size_t)M * M);
     for (int k = 0; k < M; ++k) {
         const double sk = std::sin((k + 1) * 3.14159265358979323846 * h / 2.0);
         lam1[k] = 4.0 / (h * h) * sk * sk;
     }
     for (int ky = 0; ky < M; ++ky)
         for (int kx = 0; kx < M; ++kx) lam2[(size_t)ky * M + kx] = lam1[ky] + lam1[kx];
-    DevBuf<double> dlam(MM), dA(2 * MM), dB(2 * MM), dc0(2 * MM), dcN(2 * MM), tab;
+    return lam2;
+}
+
+fraq_kconf_t kconf_or_default(const fraq_kconf_t* kc_in) {
+    fraq_kconf_t kc;
+    if (kc_in)
+        kc = *kc_in;
+    else
+        fraq_kconf_default(&kc);
+    return kc;
+}
+
+// 2D: modes (k, l) with lambda_k + lambda_l; forward transform c = (2/(M+1))^2 S G S, inverse
+// g = S c S (S symmetric); data row-major (x fastest): G[y][x], coefficients c[ky][kx].
+void ffpe_run_2d(fraq_ctx c, double alpha1, double alpha2, double a, int M, double t_final,
+                 long N, int scheme, const fraq_kconf_t* kc_in, const double* g1_0,
+                 const double* g2_0, double* g1, double* g2, fraq_run_info_t* info) {
+    if (M < 1 || N < 1) fail(FRAQ_EINVAL, "run_2d: grid_m and n_steps must be >= 1");
+    if (scheme != FRAQ_FASTBE && scheme != FRAQ_FASTSBD)
+        fail(FRAQ_EINVAL, "run_2d: scheme must be FastBE or FastSBD");
+    const fraq_kconf_t kc = kconf_or_default(kc_in);
+    const bool sbd = scheme == FRAQ_FASTSBD;
+    const double t0 = now_s2();
+    const double tau = t_final / double(N);
+    const long MM = (long)M * M;
+    ModalSetup S;
+    modal_prepare(c, S, {1.0 - alpha1, 1.0 - alpha2}, {a}, tau, N, sbd, kc);
+    const std::vector<double> lam2 = eig2d(M);
+    DevBuf<double> dlam(MM), dA(2 * MM), dc0(2 * MM), dcN(2 * MM);
     FRAQ_CUDA(cudaMemcpyAsync(dlam.p, lam2.data(), sizeof(double) * MM, cudaMemcpyHostToDevice,
                               c->stream));
     FRAQ_CUDA(cudaMemcpyAsync(dA.p, g1_0, sizeof(double) * MM, cudaMemcpyHostToDevice, c->stream));
     FRAQ_CUDA(cudaMemcpyAsync(dA.p + MM, g2_0, sizeof(double) * MM, cudaMemcpyHostToDevice,
                               c->stream));
-    make_sintab(c, M, tab);
+    Dst2D dst;
+    dst.init(c, M);
     const double t1 = now_s2();
-    cudaEvent_t e0, e1;
-    FRAQ_CUDA(cudaEventCreate(&e0));
-    FRAQ_CUDA(cudaEventCreate(&e1));
-    FRAQ_CUDA(cudaEventRecord(e0, c->stream));
-    const double sc = 2.0 / (M + 1);
-    // per field: Y = S G (along y), Z = S Y^T (along x), coefficients c[kx][ky] = Z -> stored
-    // as c[ky][kx] = Z^T after the second transpose
-    for (int f = 0; f < 2; ++f) {
-        double* G = dA.p + f * MM;
-        double* Y = dB.p + f * MM;
-        dst_apply(c, M, tab.p, G, M, Y, sc);      // Y[ky][x]
-        transpose_dev(c, Y, M, M, G);              // G <- Y^T [x][ky]
-        dst_apply(c, M, tab.p, G, M, Y, sc);      // Y[kx][ky]
-        transpose_dev(c, Y, M, M, dc0.p + f * MM); // c0[ky][kx]
-    }
-    modal_run(c, S.hd, {a}, {tau}, sbd ? S.corr.p : nullptr, S.corr_off, dlam.p, (int)MM, 1, N,
-              sbd, dc0.p, dcN.p);
-    for (int f = 0; f < 2; ++f) {
-        double* Cc = dcN.p + f * MM;   // [ky][kx]
-        double* Y = dB.p + f * MM;
-        double* G = dA.p + f * MM;
-        dst_apply(c, M, tab.p, Cc, M, Y, 1.0);    // Y[y][kx] = sum_ky S[y][ky] c[ky][kx]
-        transpose_dev(c, Y, M, M, G);              // [kx][y]
-        dst_apply(c, M, tab.p, G, M, Y, 1.0);     // [x][y]
-        transpose_dev(c, Y, M, M, G);              // [y][x]
-    }
-    FRAQ_CUDA(cudaEventRecord(e1, c->stream));
-    FRAQ_CUDA(cudaEventSynchronize(e1));
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    EventTimer timer(c->stream);
+    dst.apply(c, 2, dA.p, dc0.p, false);
+    modal_exec(c, S.plan, dlam.p, (int)MM, N, dc0.p, dcN.p);
+    dst.apply(c, 2, dcN.p, dA.p, true);
+    const double loop_s = timer.stop();
     FRAQ_CUDA(cudaMemcpy(g1, dA.p, sizeof(double) * MM, cudaMemcpyDeviceToHost));
     FRAQ_CUDA(cudaMemcpy(g2, dA.p + MM, sizeof(double) * MM, cudaMemcpyDeviceToHost));
-    fill_info(info, S, ms * 1e-3, t1 - t0);
+    fill_info(info, S, loop_s, t1 - t0);
+}
+
+// 2D DST of n_fields grid_m x grid_m arrays (forward: coefficients [ky][kx] from G[y][x] with the
+// (2/(M+1))^2 projection scale; inverse: synthesis).  mem: FRAQ_HOST or FRAQ_DEVICE for in / out.
+void dst2d(fraq_ctx c, int M, int n_fields, const double* in, double* out, bool inverse, int mem) {
+    if (M < 1 || n_fields < 1) fail(FRAQ_EINVAL, "dst2d: grid_m and n_fields must be >= 1");
+    const long n = (long)n_fields * M * M;
+    Dst2D dst;
+    dst.init(c, M);
+    if (mem == FRAQ_DEVICE) {
+        dst.apply(c, n_fields, in, out, inverse);
+        FRAQ_CUDA(cudaStreamSynchronize(c->stream));
+        return;
+    }
+    DevBuf<double> di(n), dout(n);
+    FRAQ_CUDA(cudaMemcpyAsync(di.p, in, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    dst.apply(c, n_fields, di.p, dout.p, inverse);
+    FRAQ_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    FRAQ_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+// One instance stepped over a caller-chosen set of modes (eigenvalues lam[n_modes]); c0 / cN are
+// [2][n_modes] (field-major).  The building block of the mode-sharded 2D driver: every rank
+// steps its slab of modes.  mem: FRAQ_HOST or FRAQ_DEVICE for lam / c0 / cN.
+void modal_run_modes(fraq_ctx c, double alpha1, double alpha2, double a, double t_final, long N,
+                     int scheme, const fraq_kconf_t* kc_in, long n_modes, const double* lam,
+                     const double* c0, double* cN, int mem, fraq_run_info_t* info) {
+    if (N < 1 || n_modes < 1 || n_modes > (1L << 30))
+        fail(FRAQ_EINVAL, "modal_run: n_steps and n_modes must be >= 1");
+    if (scheme != FRAQ_FASTBE && scheme != FRAQ_FASTSBD)
+        fail(FRAQ_EINVAL, "modal_run: scheme must be FastBE or FastSBD");
+    const fraq_kconf_t kc = kconf_or_default(kc_in);
+    const bool sbd = scheme == FRAQ_FASTSBD;
+    const double t0 = now_s2();
+    const double tau = t_final / double(N);
+    ModalSetup S;
+    modal_prepare(c, S, {1.0 - alpha1, 1.0 - alpha2}, {a}, tau, N, sbd, kc);
+    DevBuf<double> dl, d0, dN;
+    const double *pl = lam, *p0 = c0;
+    double* pN = cN;
+    if (mem != FRAQ_DEVICE) {
+        dl.alloc(n_modes);
+        d0.alloc(2 * n_modes);
+        dN.alloc(2 * n_modes);
+        FRAQ_CUDA(cudaMemcpyAsync(dl.p, lam, sizeof(double) * n_modes, cudaMemcpyHostToDevice, c->stream));
+        FRAQ_CUDA(cudaMemcpyAsync(d0.p, c0, sizeof(double) * 2 * n_modes, cudaMemcpyHostToDevice, c->stream));
+        pl = dl.p;
+        p0 = d0.p;
+        pN = dN.p;
+    }
+    const double t1 = now_s2();
+    EventTimer timer(c->stream);
+    modal_exec(c, S.plan, pl, (int)n_modes, N, p0, pN);
+    const double loop_s = timer.stop();
+    if (mem != FRAQ_DEVICE) {
+        FRAQ_CUDA(cudaMemcpy(cN, dN.p, sizeof(double) * 2 * n_modes, cudaMemcpyDeviceToHost));
+    }
+    fill_info(info, S, loop_s, t1 - t0);
 }
 
 }  // namespace fraqcu

@@ -443,8 +443,7 @@ bool k13_supported(int maxJ, int minL, int maxL) {
     return 8 + 8 * delta + maxL + 8 <= 64 && 7 + 8 * delta + maxL < K13_CW;
 }
 
-void k13_run(fraq_ctx c, const std::vector<K13Inst>& in, const double* lam, int n_modes, long N,
-             bool sbd, const double* c0, double* cN) {
+void k13_prepare(fraq_ctx c, const std::vector<K13Inst>& in, bool sbd, K13Plan& P) {
     const int n_inst = (int)in.size();
     int maxJ = 0, minL = 1 << 30, maxL = 0;
     for (const K13Inst& I : in)
@@ -453,29 +452,33 @@ void k13_run(fraq_ctx c, const std::vector<K13Inst>& in, const double* lam, int 
             minL = std::min(minL, I.L[f]);
             maxL = std::max(maxL, I.L[f]);
         }
-    const int delta = minL >= 8 ? 0 : 1;
+    P.n_inst = n_inst;
+    P.sbd = sbd;
+    P.delta = minL >= 8 ? 0 : 1;
     // J <= 256: 16 modes x 64 nodes per GEMM warp; else 8 modes x 8 NT nodes per GEMM warp with
     // the narrowest NT in {12, 13, 14, 16} that covers J in 4 warps (C4: 408 nodes -> NT = 13)
-    const int RB = maxJ <= 256 ? 2 : 1, modes = 8 * RB;
-    int NT = 8;
-    if (RB == 1) {
-        NT = 16;
+    P.RB = maxJ <= 256 ? 2 : 1;
+    P.NT = 8;
+    if (P.RB == 1) {
+        P.NT = 16;
         for (int cand : {12, 13, 14})
             if (4 * 8 * cand >= maxJ) {
-                NT = cand;
+                P.NT = cand;
                 break;
             }
     }
-    const int nodes_w = 8 * NT;
-    const int nwf = (maxJ + nodes_w - 1) / nodes_w, Jp = nodes_w * nwf, nwg = 2 * nwf;
-    const int TS = 17 * Jp + K13_CW;
-    const int span = 8 + 8 * delta + maxL + 8;
-    const int ring = span <= 32 ? 32 : 64;
-    // tables
+    const int nodes_w = 8 * P.NT;
+    P.nwf = (maxJ + nodes_w - 1) / nodes_w;
+    P.Jp = nodes_w * P.nwf;
+    P.nwg = 2 * P.nwf;
+    P.TS = 17 * P.Jp + K13_CW;
+    const int span = 8 + 8 * P.delta + maxL + 8;
+    P.ring = span <= 32 ? 32 : 64;
     std::vector<K13TabSrc> src(2 * n_inst);
     std::vector<K13Dev> dv(n_inst);
     for (int i = 0; i < n_inst; ++i) {
-        for (int f = 0; f < 2; ++f) src[2 * i + f] = {in[i].r[f], in[i].f[f], in[i].head[f], in[i].J[f], in[i].L[f]};
+        for (int f = 0; f < 2; ++f)
+            src[2 * i + f] = {in[i].r[f], in[i].f[f], in[i].head[f], in[i].J[f], in[i].L[f]};
         dv[i].a = in[i].a;
         dv[i].itau = 1.0 / in[i].tau;
         for (int f = 0; f < 2; ++f) {
@@ -484,46 +487,51 @@ void k13_run(fraq_ctx c, const std::vector<K13Inst>& in, const double* lam, int 
         }
     }
     DevBuf<K13TabSrc> dsrc(src.size());
-    DevBuf<K13Dev> ddv(dv.size());
-    DevBuf<double> tabs((size_t)2 * n_inst * TS);
-    DevBuf<int> counter(1);
+    P.inst.alloc(sizeof(K13Dev) * dv.size());
+    P.tabs.alloc((size_t)2 * n_inst * P.TS);
+    P.counter.alloc(1);
     FRAQ_CUDA(cudaMemcpyAsync(dsrc.p, src.data(), sizeof(K13TabSrc) * src.size(),
                               cudaMemcpyHostToDevice, c->stream));
-    FRAQ_CUDA(cudaMemcpyAsync(ddv.p, dv.data(), sizeof(K13Dev) * dv.size(), cudaMemcpyHostToDevice,
-                              c->stream));
-    FRAQ_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), c->stream));
-    k13_tables_kernel<<<2 * n_inst, 256, 0, c->stream>>>(dsrc.p, Jp, delta, tabs.p, TS);
+    FRAQ_CUDA(cudaMemcpyAsync(P.inst.p, dv.data(), sizeof(K13Dev) * dv.size(),
+                              cudaMemcpyHostToDevice, c->stream));
+    k13_tables_kernel<<<2 * n_inst, 256, 0, c->stream>>>(dsrc.p, P.Jp, P.delta, P.tabs.p, P.TS);
     FRAQ_LAUNCH_CHECK();
+    FRAQ_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+void k13_exec(fraq_ctx c, K13Plan& P, const double* lam, int n_modes, long N, const double* c0,
+              double* cN) {
+    const int modes = 8 * P.RB;
     K13Args A{};
-    A.inst = ddv.p;
-    A.tabs = tabs.p;
-    A.TS = TS;
-    A.Jp = Jp;
-    A.nwf = nwf;
-    A.nwg = nwg;
+    A.inst = reinterpret_cast<const K13Dev*>(P.inst.p);
+    A.tabs = P.tabs.p;
+    A.TS = P.TS;
+    A.Jp = P.Jp;
+    A.nwf = P.nwf;
+    A.nwg = P.nwg;
     A.lam = lam;
     A.n_modes = n_modes;
     A.nmb = (n_modes + modes - 1) / modes;
-    A.n_tasks = (long)A.nmb * n_inst;
+    A.n_tasks = (long)A.nmb * P.n_inst;
     A.N = N;
-    A.sbd = sbd ? 1 : 0;
-    A.delta = delta;
-    A.ring_mask = ring - 1;
+    A.sbd = P.sbd ? 1 : 0;
+    A.delta = P.delta;
+    A.ring_mask = P.ring - 1;
     A.c0 = c0;
     A.cN = cN;
-    A.counter = counter.p;
-    const size_t smem = k13_smem(TS, nwg, ring, modes);
-    if (RB == 2)
+    A.counter = P.counter.p;
+    FRAQ_CUDA(cudaMemsetAsync(P.counter.p, 0, sizeof(int), c->stream));
+    const size_t smem = k13_smem(P.TS, P.nwg, P.ring, modes);
+    if (P.RB == 2)
         k13_launch<2, 8>(A, smem, c->num_sms, c->stream);
-    else if (NT == 12)
+    else if (P.NT == 12)
         k13_launch<1, 12>(A, smem, c->num_sms, c->stream);
-    else if (NT == 13)
+    else if (P.NT == 13)
         k13_launch<1, 13>(A, smem, c->num_sms, c->stream);
-    else if (NT == 14)
+    else if (P.NT == 14)
         k13_launch<1, 14>(A, smem, c->num_sms, c->stream);
     else
         k13_launch<1, 16>(A, smem, c->num_sms, c->stream);
-    FRAQ_CUDA(cudaStreamSynchronize(c->stream));
 }
 
 }  // namespace fraqcu

@@ -46,3 +46,156 @@ def gather_scalars(value: float, device=None) -> list[float]:
     out = [torch.zeros_like(t) for _ in range(dist.get_world_size())]
     dist.all_gather(out, t)
     return [float(x.item()) for x in out]
+
+
+# ----------------------------------------------------------------------------- C4: mode shards
+def eig_2d(M: int):
+    """lambda_k + lambda_l of the five-point Dirichlet Laplacian on the unit square, [ky][kx]
+    flattened (block_solver.cpp:21-24 per axis)."""
+    import numpy as np
+    h = 1.0 / (M + 1)
+    lam1 = 4.0 / h ** 2 * np.sin(np.arange(1, M + 1) * np.pi * h / 2) ** 2
+    return (lam1[:, None] + lam1[None, :]).ravel()
+
+
+def slab_rows(M: int, rank: int, world: int) -> tuple[int, int, int]:
+    """ky rows [lo, hi) owned by `rank` and the padded slab height (equal on every rank, so the
+    coefficient gather is a plain all-gather of equal buffers)."""
+    per = -(-M // world)
+    lo = min(M, rank * per)
+    return lo, min(M, lo + per), per
+
+
+class FraqOps:
+    """Device building blocks (fraq_dst2d, fraq_modal_run) on the library's CUDA stream; tensors
+    on the current GPU.  The all-gather runs on the same stream (NCCL over NVLink)."""
+
+    def __init__(self, fraq, torch):
+        self.fraq, self.torch = fraq, torch
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        self.stream = torch.cuda.ExternalStream(fraq.context_stream())
+
+    def tensor(self, x):
+        return self.torch.as_tensor(x, dtype=self.torch.float64).to(self.dev).contiguous()
+
+    def empty(self, *shape):
+        return self.torch.empty(*shape, dtype=self.torch.float64, device=self.dev)
+
+    def mark(self):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record(self.stream)
+        return e
+
+    @staticmethod
+    def seconds(a, b):
+        b.synchronize()
+        return a.elapsed_time(b) * 1e-3
+
+    def dst2d(self, M, x, inverse):
+        out = self.empty(*x.shape)
+        self.fraq.dst2d_device(M, x.numel() // (M * M), x.data_ptr(), out.data_ptr(), inverse)
+        return out
+
+    def step(self, alpha1, alpha2, a, t_final, N, scheme, lam, c0, kconf):
+        cN = self.empty(*c0.shape)
+        rr = self.fraq.modal_run_device(alpha1, alpha2, a, t_final, N, scheme, lam.numel(),
+                                        lam.data_ptr(), c0.data_ptr(), cN.data_ptr(),
+                                        kconf if kconf is not None else self.fraq.KernelConfig())
+        return cN, rr.loop_seconds
+
+
+class OracleOps:
+    """CPU stand-in with the same interface (numpy DST + the mode-space oracle), for the gloo
+    tests of the sharding logic.  TEST INFRASTRUCTURE: uses oracle/."""
+
+    def __init__(self, orc, torch):
+        self.orc, self.torch = orc, torch
+        self.stream = None
+
+    def tensor(self, x):
+        return self.torch.as_tensor(x, dtype=self.torch.float64).contiguous()
+
+    def empty(self, *shape):
+        return self.torch.empty(*shape, dtype=self.torch.float64)
+
+    def mark(self):
+        import time
+        return time.perf_counter()
+
+    @staticmethod
+    def seconds(a, b):
+        return b - a
+
+    def dst2d(self, M, x, inverse):
+        import numpy as np
+        S = np.sin(np.outer(np.arange(1, M + 1), np.arange(1, M + 1)) * np.pi / (M + 1))
+        sc = 1.0 if inverse else (2.0 / (M + 1)) ** 2
+        g = x.numpy().reshape(-1, M, M)
+        return self.tensor(np.stack([sc * S @ gi @ S for gi in g]).reshape(x.shape))
+
+    def step(self, alpha1, alpha2, a, t_final, N, scheme, lam, c0, kconf):
+        sbd = scheme == "FastSBD"
+        tau = t_final / N
+        k1 = self.orc.build_kernel_auto(sbd, 1 - alpha1, tau, N)
+        k2 = self.orc.build_kernel_auto(sbd, 1 - alpha2, tau, N)
+        u, v, secs = self.orc.modal_run(k1, k2, a, tau, N, lam.numpy(), c0[0].numpy(),
+                                        c0[1].numpy())
+        import numpy as np
+        return self.tensor(np.stack([u, v])), secs
+
+
+def run_2d_sharded(ops, alpha1, alpha2, a, M, t_final, N, scheme, g1_0, g2_0, kconf=None,
+                   scheme_arg=None, timings=None):
+    """C4 across the ranks of the default process group.  Every rank projects
+    the initial data (the forward 2D DST is ~1e-3 of the stepping), steps its slab of ky rows of
+    modes -- independent 2x2 recursions, no exchange -- and one all-gather of the coefficient
+    slabs (2 x M^2 doubles in total) precedes the inverse DST.  g1_0 / g2_0: numpy arrays or
+    tensors already on the ops' device.  Returns (g1, g2) as tensors on the ops' device.
+    `scheme_arg` is what ops.step receives (the fraq.Scheme value on the GPU, the scheme name for
+    the oracle ops).  If `timings` is a dict it receives the device seconds of the phases
+    (forward, step -- the library's own loop timer, setup excluded --, gather, inverse)."""
+    import contextlib
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    lo, hi, per = slab_rows(M, rank, world)
+    ctx = torch.cuda.stream(ops.stream) if ops.stream is not None else contextlib.nullcontext()
+    T = timings if timings is not None else {}
+    with ctx:
+        if isinstance(g1_0, torch.Tensor):
+            g = torch.cat([g1_0.reshape(-1), g2_0.reshape(-1)]).to(torch.float64).contiguous()
+        else:
+            g = ops.tensor(np.concatenate([np.asarray(g1_0), np.asarray(g2_0)]))
+        lam = ops.tensor(eig_2d(M)[lo * M:hi * M])
+        send = ops.empty(2, per * M)
+        send.zero_()
+        m0 = ops.mark()
+        c = ops.dst2d(M, g, inverse=False).view(2, M * M)
+        m1 = ops.mark()
+        T["forward"] = ops.seconds(m0, m1)
+        T["step"] = 0.0
+        if hi > lo:
+            cN, T["step"] = ops.step(alpha1, alpha2, a, t_final, N,
+                                     scheme if scheme_arg is None else scheme_arg, lam,
+                                     c[:, lo * M:hi * M].contiguous(), kconf)
+            send[:, :(hi - lo) * M] = cN
+        m2 = ops.mark()
+        if world > 1:
+            recv = ops.empty(world * 2, per * M)  # concatenated along dim 0 (NCCL and gloo)
+            dist.all_gather_into_tensor(recv, send)
+            recv = recv.view(world, 2, per * M)
+        else:
+            recv = send.view(1, 2, per * M)
+        full = ops.empty(2, M * M)
+        for r in range(world):
+            rlo, rhi, _ = slab_rows(M, r, world)
+            if rhi > rlo:
+                full[:, rlo * M:rhi * M] = recv[r, :, :(rhi - rlo) * M]
+        m3 = ops.mark()
+        out = ops.dst2d(M, full.contiguous().view(-1), inverse=True).view(2, M * M)
+        m4 = ops.mark()
+        T["gather"] = ops.seconds(m2, m3)
+        T["inverse"] = ops.seconds(m3, m4)
+    return out[0], out[1]

@@ -73,3 +73,61 @@ def test_two_rank_shards_match_single_process():
     assert np.array_equal(stitched, full)  # lanes are independent: bitwise
     assert all(r[4] == 2.0 for r in res)   # max over ranks
     assert res[0][5] == res[1][5] and len(res[0][5]) == 2
+
+
+def _worker_2d(rank, world, port, q, scheme):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.oracle import Oracle
+    from paper_1901_05128_b200.parallel import OracleOps, run_2d_sharded
+    g1, g2 = _c4_like(9)
+    ops = OracleOps(Oracle("port"), torch)
+    try:
+        r1, r2 = run_2d_sharded(ops, 0.3, 0.6, -3.0, 9, 0.25, 40, scheme, g1, g2)
+        q.put((rank, r1.numpy(), r2.numpy()))
+    except Exception as e:  # report instead of hanging the parent
+        q.put((rank, repr(e), None))
+    dist.destroy_process_group()
+
+
+def _c4_like(M):
+    h = 1.0 / (M + 1)
+    x = (np.arange(M) + 1) * h
+    X, Y = np.meshgrid(x, x)
+    g1 = ((X <= 0.5) & (Y <= 0.5)).astype(float).ravel()
+    g2 = 1.0 + np.random.default_rng(1901051284).uniform(-0.1, 0.1, M * M)
+    return g1, g2
+
+
+@pytest.mark.parametrize("scheme", ["FastBE", "FastSBD"])
+def test_c4_mode_shards_two_ranks(scheme):
+    """C4's mode-sharded driver (parallel.run_2d_sharded) on 2 gloo ranks: odd row split (9 rows ->
+    5 + 4, padded slabs), one all-gather of the coefficient slabs; every rank's result equals the
+    single-process run of the same driver and the physical-space 2D restatement to 1e-10."""
+    import torch
+    from oracle.oracle import Oracle
+    from paper_1901_05128_b200.parallel import OracleOps, run_2d_sharded
+    from ffpe_refs import fast_stepper_nd
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_2d, args=(r, 2, port, q, scheme)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(r[2] is not None for r in res), res
+    g1, g2 = _c4_like(9)
+    orc = Oracle("port")
+    s1, s2 = run_2d_sharded(OracleOps(orc, torch), 0.3, 0.6, -3.0, 9, 0.25, 40, scheme, g1, g2)
+    p1, p2 = fast_stepper_nd(orc, 0.3, 0.6, -3.0, 9, 2, 0.25, 40, scheme == "FastSBD", g1, g2)
+    for _, r1, r2 in res:
+        assert np.abs(r1 - s1.numpy()).max() <= 1e-14 * np.abs(s1.numpy()).max()
+        assert np.abs(r2 - s2.numpy()).max() <= 1e-14 * np.abs(s2.numpy()).max()
+        assert np.abs(r1 - p1).max() <= 1e-10 * np.abs(p1).max()
+        assert np.abs(r2 - p2).max() <= 1e-10 * np.abs(p2).max()

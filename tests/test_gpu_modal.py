@@ -224,3 +224,45 @@ def test_c5_batch_full_horizon_sampled(fraq, orc, scheme):
         s = max(np.abs(c1).max(), np.abs(c2).max())
         assert np.abs(S @ np.array(o.final_state.g1) - uN).max() <= 1e-10 * s
         assert np.abs(S @ np.array(o.final_state.g2) - vN).max() <= 1e-10 * s
+
+
+def test_dst2d_roundtrip_and_modal_run_blocks(fraq):
+    """fraq_dst2d forward/inverse against the dense sine transform, and fraq_modal_run on the
+    full mode set equals run_2d (the building blocks of the mode-sharded C4 driver)."""
+    M = 37
+    rng = np.random.default_rng(2)
+    g = rng.standard_normal(2 * M * M)
+    S = np.sin(np.outer(np.arange(1, M + 1), np.arange(1, M + 1)) * np.pi / (M + 1))
+    c = fraq.dst2d(M, g)
+    ref = np.concatenate([((2 / (M + 1)) ** 2 * S @ gi.reshape(M, M) @ S).ravel()
+                          for gi in g.reshape(2, -1)])
+    assert np.abs(c - ref).max() <= 1e-13 * np.abs(ref).max()
+    back = fraq.dst2d(M, c, inverse=True)
+    assert np.abs(back - g).max() <= 1e-12 * np.abs(g).max()
+    from paper_1901_05128_b200.parallel import eig_2d
+    for scheme in ("FastBE", "FastSBD"):
+        sch = getattr(fraq.Scheme, scheme)
+        full = fraq.run_2d(0.3, 0.6, -3.0, M, 0.5, 64, sch, g[:M * M], g[M * M:])
+        cN, rr = fraq.modal_run(0.3, 0.6, -3.0, 0.5, 64, sch, eig_2d(M), c)
+        out = fraq.dst2d(M, cN, inverse=True)
+        assert np.abs(out[:M * M] - np.array(full.final_state.g1)).max() <= 1e-12 * np.abs(g).max()
+        assert np.abs(out[M * M:] - np.array(full.final_state.g2)).max() <= 1e-12 * np.abs(g).max()
+        assert rr.loop_seconds > 0
+
+
+def test_sharded_driver_single_rank_equals_run_2d(fraq):
+    """parallel.run_2d_sharded with the device ops (world = 1: one slab, no gather) equals
+    run_2d; the multi-rank slab/gather logic is covered on CPU (tests/test_dist.py)."""
+    import torch
+    from paper_1901_05128_b200.parallel import FraqOps, run_2d_sharded
+    M = 63
+    rng = np.random.default_rng(3)
+    g1, g2 = rng.uniform(0, 1, M * M), rng.uniform(0, 1, M * M)
+    ops = FraqOps(fraq, torch)
+    T = {}
+    r1, r2 = run_2d_sharded(ops, 0.3, 0.6, -3.0, M, 1.0, 200, "FastSBD", g1, g2,
+                            scheme_arg=fraq.Scheme.FastSBD, timings=T)
+    full = fraq.run_2d(0.3, 0.6, -3.0, M, 1.0, 200, fraq.Scheme.FastSBD, g1, g2)
+    assert np.abs(r1.cpu().numpy() - np.array(full.final_state.g1)).max() <= 1e-12
+    assert np.abs(r2.cpu().numpy() - np.array(full.final_state.g2)).max() <= 1e-12
+    assert set(T) == {"forward", "step", "gather", "inverse"} and T["step"] > 0
