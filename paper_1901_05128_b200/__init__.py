@@ -61,6 +61,16 @@ EXTRA = [
     "diag_dmma_peak",
     "direct_cq",
     "direct_cq_device",
+    "BenchRow",
+    "ConvergenceReport",
+    "ConvergenceRow",
+    "ExperimentConfig",
+    "format_double",
+    "parse_config_text",
+    "parse_fraction_list",
+    "resolve_config",
+    "run_convergence",
+    "timing_sweep",
     "dst2d",
     "dst2d_device",
     "modal_run",
@@ -79,34 +89,6 @@ EXTRA = [
 
 globals().update({name: getattr(_impl, name) for name in __all__ + EXTRA
                   if hasattr(_impl, name)})
-
-
-def parse_fraction(text: str) -> float:
-    """"1/3200" exactly (numerator/denominator) or a plain decimal (bench.cpp:42-57)."""
-    t = text.strip()
-    if "/" in t:
-        num, den = t.split("/", 1)
-        try:
-            n, d = int(num), int(den)
-        except ValueError as e:
-            raise ValueError("bad fraction: " + text) from e
-        if d == 0:
-            raise ValueError("bad fraction: " + text)
-        return float(n) / float(d)
-    try:
-        return float(t)
-    except ValueError as e:
-        raise ValueError("bad number: " + text) from e
-
-
-def compute_rates(tau_and_error):
-    """rate_k = ln(E_k / E_{k+1}) / ln 2 for halving taus; NaN for zero errors (bench.cpp:140-153)."""
-    rates = []
-    for (tc, ec), (tf, ef) in zip(tau_and_error, tau_and_error[1:]):
-        if abs(tc / tf - 2.0) > 1e-9:
-            raise ValueError("compute_rates: taus must halve")
-        rates.append(float("nan") if ec == 0.0 or ef == 0.0 else _math.log(ec / ef) / _math.log(2.0))
-    return rates
 
 
 __all__ = __all__ + EXTRA

@@ -21,6 +21,7 @@ INC = os.path.join(ROOT, "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CUDA_HOME = os.path.dirname(os.path.dirname(NVCC))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CLI = os.path.join(os.path.dirname(os.path.abspath(__file__)), "fraq")
 CU_SOURCES = ["setup.cu", "history.cu", "history_dmma.cu", "ffpe.cu", "modal.cu", "modal_dmma.cu", "direct.cu",
               "capi.cu", "diag.cu"]
 
@@ -60,10 +61,15 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> None:
     if force or _stale(CUDA_LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-o", CUDA_LIB, *objs, "-lcudart"])
     cxx = os.environ.get("CXX", "g++")
-    fraq_cpp = os.path.join(CSRC, "fraq.cpp")
-    if force or _stale(CXX_LIB, [fraq_cpp, CUDA_LIB] + headers):
-        _run([cxx, "-O2", "-std=c++20", "-fPIC", "-shared", f"-I{INC}", f"-I{CSRC}", fraq_cpp,
+    cxx_srcs = [os.path.join(CSRC, f) for f in ("fraq.cpp", "fraq_bench.cpp")]
+    if force or _stale(CXX_LIB, cxx_srcs + [CUDA_LIB] + headers):
+        _run([cxx, "-O2", "-std=c++20", "-fPIC", "-shared", f"-I{INC}", f"-I{CSRC}", *cxx_srcs,
               "-o", CXX_LIB, f"-L{HERE}", "-lfraqcu", "-Wl,-rpath,$ORIGIN"])
+    # the `fraq` command line (reference: tools/fraq_main.cpp)
+    cli_cpp = os.path.join(CSRC, "fraq_cli.cpp")
+    if force or _stale(CLI, [cli_cpp, CXX_LIB] + headers):
+        _run([cxx, "-O2", "-std=c++20", f"-I{INC}", f"-I{CSRC}", cli_cpp, "-o", CLI,
+              f"-L{HERE}", "-lfraq", "-lfraqcu", "-Wl,-rpath,$ORIGIN"])
     py_cpp = os.path.join(CSRC, "fraq_py.cpp")
     if force or _stale(EXT, [py_cpp, CXX_LIB] + headers):
         import pybind11
