@@ -22,6 +22,7 @@ namespace fraqcu {
 // history_dmma.cu
 void build_frag_tables(fraq_ctx c, HistDevice& d);
 void launch_run3(const RunArgs& a, int nwg, int num_sms, cudaStream_t s);
+int run3_max_lag();
 
 namespace {
 
@@ -1074,7 +1075,7 @@ void run_device(fraq_hist h, const double* U, long ldu, long n_steps, double* D,
         FRAQ_CUDA(cudaMemsetAsync(h->counter.p, 0, sizeof(int), h->ctx->stream));
         static const bool legacy = std::getenv("FRAQ_K5B") != nullptr;
         static const bool k5c = std::getenv("FRAQ_K5C") != nullptr;
-        if (!legacy && !k5c) {
+        if (!legacy && !k5c && h->d.max_L <= run3_max_lag()) {
             // K5d (DMMA block formulation), default
             h->last_path = 3;
             build_frag_tables(h->ctx, h->d);

@@ -30,7 +30,7 @@ namespace {
 
 constexpr int D_TC = 32;      // levels per staged chunk
 constexpr int D_TB = 8;       // levels per block (one GEMM pair)
-constexpr int D_LMAX = 64;    // max lag
+constexpr int D_LMAX = 32;    // max lag (longer head windows take K5c)
 constexpr int D_NT = 8;       // node tiles (8 nodes) per warp = 64 nodes
 constexpr int D_MAXWG = 8;    // max warps per DOF group (512 nodes)
 
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
     extern __shared__ double dsm[];
     DSmem& S = *reinterpret_cast<DSmem*>(dsm);
     double* tab = dsm + sizeof(DSmem) / sizeof(double);         // kFragDoubles
-    double* part = tab + kFragR8 + 64;                            // [2][8 warps][2][8][8]
+    double* part = tab + kFragR8 + 64;  // [2 buffers][2 slots][8 warps][2][8][8]
     __shared__ int s_task, s_group;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
     const int nwg = blockDim.x >> 5;  // warps = node slices of 64
@@ -182,36 +182,27 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
             }
         };
         if (blockDim.x == 256) prefetch(0);
-        // deferred reduction of the previous block (node sum over warps + head window -> D)
-        long p_row = 0, p_n0 = 0;
-        int p_kmax = 0, p_buf = 0;
-        auto reduce_prev = [&]() {
-            const double* pb = part + (size_t)p_buf * 8 * 2 * 64;
-            if (fast_red && p_kmax == D_TB) {
-                // straight line: thread pair (2o, 2o+1), o = (k, d), 4 slices each
-                const int o = tid >> 1, hh = tid & 1, k = o >> 4, d = o & 15;
-                const int rb = d >> 3, gg = d & 7;
-                double sum = pb[(hh * 2 + rb) * 64 + gg * 8 + k];
-                sum += pb[((hh + 2) * 2 + rb) * 64 + gg * 8 + k];
-                sum += pb[((hh + 4) * 2 + rb) * 64 + gg * 8 + k];
-                sum += pb[((hh + 6) * 2 + rb) * 64 + gg * 8 + k];
-                sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-                const bool valid = G.sbd ? true : (p_n0 + k >= 1);
-                if (hh == 0 && Db && tk.y + d < G.dim)
-                    Db[(p_row + k) * A.ldd + d] = valid ? sum + S.F[(p_row + k) % D_TC][d] : qnan;
-            } else {
-                for (int o = tid >> 1; o < D_TB * 16; o += blockDim.x >> 1) {
-                    const int hh = tid & 1, k = o >> 4, d = o & 15;
-                    const int rb = d >> 3, gg = d & 7;
-                    double sum = 0.0;
-                    if (k < p_kmax)
-                        for (int w = hh; w < nwg; w += 2) sum += pb[(w * 2 + rb) * 64 + gg * 8 + k];
-                    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-                    const bool valid = G.sbd ? true : (p_n0 + k >= 1);
-                    if (hh == 0 && k < p_kmax && Db && tk.y + d < G.dim)
-                        Db[(p_row + k) * A.ldd + d] =
-                            valid ? sum + S.F[(p_row + k) % D_TC][d] : qnan;
+        // reduction of a pair of blocks (node sum over warps + head window -> D): one output
+        // (slot, level k, DOF d) per thread, two independent add chains over the warp partials
+        long p_row0 = 0, p_row1 = 0, p_n00 = 0, p_n01 = 0;
+        int p_kmax0 = 0, p_kmax1 = 0, p_buf = 0;
+        auto reduce_pair = [&]() {
+            for (int o = tid; o < 2 * D_TB * 16; o += blockDim.x) {
+                const int slot = o >> 7, k = (o >> 4) & 7, d = o & 15;
+                const long prow = slot ? p_row1 : p_row0, pn0 = slot ? p_n01 : p_n00;
+                if (k >= (slot ? p_kmax1 : p_kmax0)) continue;
+                const double* pb = part + ((size_t)(p_buf * 2 + slot) * D_MAXWG) * 128 +
+                                   ((d >> 3) * 8 + (d & 7)) * 8 + k;
+                double s0 = 0.0, s1 = 0.0;
+                for (int w = 0; w + 1 < nwg; w += 2) {
+                    s0 += pb[w * 128];
+                    s1 += pb[(w + 1) * 128];
                 }
+                if (nwg & 1) s0 += pb[(nwg - 1) * 128];
+                const double sum = s0 + s1;
+                const bool valid = G.sbd ? true : (pn0 + k >= 1);
+                if (Db && tk.y + d < G.dim)
+                    Db[(prow + k) * A.ldd + d] = valid ? sum + S.F[(prow + k) % D_TC][d] : qnan;
             }
         };
         int buf = 0, last_tmax = 0;
@@ -245,10 +236,10 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
             }
             __syncthreads();
 #endif
-            for (int t0 = 0; t0 < tmax; t0 += D_TB) {
+            auto do_block = [&](int t0, int slot) {
                 const long n0 = A.A0 + c0 + t0;
                 const int kmax = min(D_TB, tmax - t0);
-                double* pw = part + ((size_t)(buf * 8 + warp) * 2) * 64;  // this warp's [2][8][8]
+                double* pw = part + ((size_t)(buf * 2 + slot) * D_MAXWG + warp) * 128;
                 const bool special = A.lo == 1 && n0 <= L && L < n0 + D_TB;
                 if (kmax == D_TB && n0 >= 1 && !special) {
                     // ---- readout GEMM from the block-start state + local Toeplitz
@@ -334,16 +325,24 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
                         }
                     }
                 }
-#ifndef FRAQ_EXP_NOSYNC
+            };
+            for (int t0 = 0; t0 < tmax; t0 += 2 * D_TB) {
+                // two blocks per barrier: their partials go to slots 0 / 1 of buffer `buf`
+                const int nblk = t0 + D_TB < tmax ? 2 : 1;
+                do_block(t0, 0);
+                p_row0 = c0 + t0;
+                p_n00 = A.A0 + c0 + t0;
+                p_kmax0 = min(D_TB, tmax - t0);
+                p_kmax1 = 0;
+                if (nblk == 2) {
+                    do_block(t0 + D_TB, 1);
+                    p_row1 = c0 + t0 + D_TB;
+                    p_n01 = A.A0 + c0 + t0 + D_TB;
+                    p_kmax1 = min(D_TB, tmax - t0 - D_TB);
+                }
                 __syncthreads();
-#endif
-                p_row = c0 + t0;
-                p_n0 = n0;
-                p_kmax = kmax;
                 p_buf = buf;
-#ifndef FRAQ_EXP_NOREDUCE
-                reduce_prev();
-#endif
+                reduce_pair();
                 buf ^= 1;
             }
             last_tmax = tmax;
@@ -384,7 +383,7 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
 
 size_t run3_smem(int nwg) {
     (void)nwg;
-    return sizeof(DSmem) + sizeof(double) * (kFragR8 + 64 + 2 * 8 * 2 * 64);
+    return sizeof(DSmem) + sizeof(double) * (kFragR8 + 64 + 2 * 2 * D_MAXWG * 128);
 }
 
 }  // namespace
@@ -397,6 +396,8 @@ void build_frag_tables(fraq_ctx c, HistDevice& d) {
     FRAQ_LAUNCH_CHECK();
     d.frag_built = true;
 }
+
+int run3_max_lag() { return D_LMAX; }
 
 void launch_run3(const RunArgs& a, int nwg, int num_sms, cudaStream_t s) {
     const size_t smem = run3_smem(nwg);
