@@ -57,6 +57,7 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> None:
                    f"-I{INC}", "-c", s, "-o", o]
             if verbose_ptxas:
                 cmd += ["-Xptxas", "-v"]
+            cmd += os.environ.get("FRAQ_NVCC_FLAGS", "").split()  # experiment switches only
             _run(cmd)
     if force or _stale(CUDA_LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-o", CUDA_LIB, *objs, "-lcudart"])

@@ -106,7 +106,11 @@ struct DSmem {
 // CTA's barrier / reduction phase overlaps the other's DMMA phase.  Within a CTA the cross-warp
 // reduction of block b-1 is issued after block b's readout DMMAs (software pipelining), so its
 // shared-memory latency hides under the asynchronous tensor pipe.
+#ifdef FRAQ_EXP_ONECTA
+__global__ void __launch_bounds__(256, 1) run3_kernel(RunArgs A) {
+#else
 __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
+#endif
     extern __shared__ double dsm[];
     DSmem& S = *reinterpret_cast<DSmem*>(dsm);
     double* tab = dsm + sizeof(DSmem) / sizeof(double);         // kFragDoubles
@@ -187,12 +191,14 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
         long p_row0 = 0, p_row1 = 0, p_n00 = 0, p_n01 = 0;
         int p_kmax0 = 0, p_kmax1 = 0, p_buf = 0;
         auto reduce_pair = [&]() {
+#ifdef FRAQ_EXP_NOREDUCE
+            return;
+#endif
             for (int o = tid; o < 2 * D_TB * 16; o += blockDim.x) {
                 const int slot = o >> 7, k = (o >> 4) & 7, d = o & 15;
                 const long prow = slot ? p_row1 : p_row0, pn0 = slot ? p_n01 : p_n00;
                 if (k >= (slot ? p_kmax1 : p_kmax0)) continue;
-                const double* pb = part + ((size_t)(p_buf * 2 + slot) * D_MAXWG) * 128 +
-                                   ((d >> 3) * 8 + (d & 7)) * 8 + k;
+                const double* pb = part + ((size_t)(p_buf * 2 + slot) * D_MAXWG) * 128 + k * 16 + d;
                 double s0 = 0.0, s1 = 0.0;
                 for (int w = 0; w + 1 < nwg; w += 2) {
                     s0 += pb[w * 128];
@@ -206,6 +212,7 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
             }
         };
         int buf = 0, last_tmax = 0;
+        bool pending = false;
         for (long c0 = 0; c0 < A.n_steps; c0 += D_TC) {
             const int tmax = (int)min((long)D_TC, A.n_steps - c0);
             __syncthreads();
@@ -236,7 +243,7 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
             }
             __syncthreads();
 #endif
-            auto do_block = [&](int t0, int slot) {
+            auto do_block = [&](int t0, int slot, bool mid_reduce) {
                 const long n0 = A.A0 + c0 + t0;
                 const int kmax = min(D_TB, tmax - t0);
                 double* pw = part + ((size_t)(buf * 2 + slot) * D_MAXWG + warp) * 128;
@@ -275,6 +282,9 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
                         else
                             dmma(sacc[1][1], vf[1][1], b);
                     }
+                    // deferred reduction of the previous pair: its LDS / DADD / STG latency
+                    // overlaps the readout DMMAs just issued (asynchronous tensor pipe)
+                    if (mid_reduce) reduce_pair();
                     // ---- state GEMM: Y <- r^8 (.) Y + V R
 #pragma unroll
                     for (int ntl = 0; ntl < D_NT; ++ntl) {
@@ -291,10 +301,12 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
                     // partial readout (DOF g, levels 2t, 2t+1) -> shared memory
 #pragma unroll
                     for (int rb = 0; rb < 2; ++rb) {
-                        pw[(rb * 8 + g) * 8 + 2 * t] = sacc[rb][0][0] + sacc[rb][1][0];
-                        pw[(rb * 8 + g) * 8 + 2 * t + 1] = sacc[rb][0][1] + sacc[rb][1][1];
+                        // [level][DOF] layout: the reduction reads consecutive DOFs (no conflicts)
+                        pw[(2 * t) * 16 + 8 * rb + g] = sacc[rb][0][0] + sacc[rb][1][0];
+                        pw[(2 * t + 1) * 16 + 8 * rb + g] = sacc[rb][0][1] + sacc[rb][1][1];
                     }
                 } else {
+                    if (mid_reduce) reduce_pair();
                     // partial block: level by level, elementwise on the fragments
                     for (int k = 0; k < kmax; ++k) {
                         const long n = n0 + k;
@@ -321,7 +333,7 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
                         for (int rb = 0; rb < 2; ++rb) {
                             ps[rb] += __shfl_xor_sync(0xffffffffu, ps[rb], 1);
                             ps[rb] += __shfl_xor_sync(0xffffffffu, ps[rb], 2);
-                            if (t == 0) pw[(rb * 8 + g) * 8 + k] = ps[rb];
+                            if (t == 0) pw[k * 16 + 8 * rb + g] = ps[rb];
                         }
                     }
                 }
@@ -329,21 +341,27 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
             for (int t0 = 0; t0 < tmax; t0 += 2 * D_TB) {
                 // two blocks per barrier: their partials go to slots 0 / 1 of buffer `buf`
                 const int nblk = t0 + D_TB < tmax ? 2 : 1;
-                do_block(t0, 0);
+                do_block(t0, 0, pending);  // reduces the previous pair (p_* still describe it)
+                if (nblk == 2) do_block(t0 + D_TB, 1, false);
                 p_row0 = c0 + t0;
                 p_n00 = A.A0 + c0 + t0;
                 p_kmax0 = min(D_TB, tmax - t0);
                 p_kmax1 = 0;
                 if (nblk == 2) {
-                    do_block(t0 + D_TB, 1);
                     p_row1 = c0 + t0 + D_TB;
                     p_n01 = A.A0 + c0 + t0 + D_TB;
                     p_kmax1 = min(D_TB, tmax - t0 - D_TB);
                 }
+#ifndef FRAQ_EXP_NOSYNC
                 __syncthreads();
+#endif
                 p_buf = buf;
-                reduce_pair();
+                pending = true;
                 buf ^= 1;
+            }
+            if (pending) {  // the chunk's last pair (S.F / S.X are rewritten next chunk)
+                reduce_pair();
+                pending = false;
             }
             last_tmax = tmax;
             if (c0 + D_TC < A.n_steps) {
@@ -409,6 +427,9 @@ void launch_run3(const RunArgs& a, int nwg, int num_sms, cudaStream_t s) {
     }
     int per_sm = 1;
     FRAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, run3_kernel, nwg * 32, smem));
+#ifdef FRAQ_EXP_ONECTA
+    per_sm = 1;
+#endif
     const int grid = std::max(1, std::min(a.n_tasks, std::max(1, per_sm) * num_sms));
     run3_kernel<<<grid, nwg * 32, smem, s>>>(a);
     FRAQ_LAUNCH_CHECK();
