@@ -129,7 +129,7 @@ __global__ void k13_tables_kernel(const K13TabSrc* src, int Jp, int delta, doubl
 // warps + 1 solver warp per CTA, one CTA per SM (the register file is split per SM sub-partition:
 // 9 warps leave ~170 registers per thread for the state fragments and the table operands).
 template <int RB, int NT>
-__global__ void __launch_bounds__(288, 1) k13_kernel(K13Args A) {
+__global__ void __launch_bounds__(320, 1) k13_kernel(K13Args A) {
     constexpr int MODES = 8 * RB;
     extern __shared__ double ksm[];
     const int nwg = A.nwg, nwf = A.nwf, TS = A.TS, Jp = A.Jp;
@@ -142,7 +142,10 @@ __global__ void __launch_bounds__(288, 1) k13_kernel(K13Args A) {
     __shared__ long s_task;
     __shared__ int s_inst;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-    const bool solver = warp == nwg;
+    // warps nwg, nwg + 1: solver warps (field 0 / field 1 of the known part); warp nwg also runs
+    // the coupled sequential solve
+    const bool solver = warp >= nwg;
+    const int sf = solver ? warp - nwg : 0;
     const long nb = (A.N + 7) / 8;
     if (tid == 0) s_inst = -1;
     for (;;) {
@@ -249,25 +252,21 @@ __global__ void __launch_bounds__(288, 1) k13_kernel(K13Args A) {
             const double M11 = m11 * idet, M12 = m12 * idet, M21 = m21 * idet, M22 = m22 * idet;
             const double g10 = g0s[d], g20 = g0s[MODES + d];
             double gp1 = g10, gp2 = g20, gpp1 = 0.0, gpp2 = 0.0;
-            const int Lt[2] = {8 * A.delta + I.L[0], 8 * A.delta + I.L[1]};
-            const int Ltm = max(Lt[0], Lt[1]);
             double c1[8], c2[8];  // in-block weights c_1..c_7
 #pragma unroll
             for (int m = 1; m < 8; ++m) {
                 c1[m] = cwt[0][m];
                 c2[m] = cwt[1][m];
             }
-            // correction prefetch: fragment row k = g of each field (level n0 + g)
-            double cpre[2];
+            // correction prefetch (this warp's field): fragment row k = g (level n0 + g)
+            const int Lsf = sf ? I.L[1] : I.L[0];
+            const double* corr_f = sf ? I.corr[1] : I.corr[0];
+            const double* CWs = sf ? cwt[1] : cwt[0];
+            const int Lts = 8 * A.delta + Lsf;
+            double cpre = 0.0;
             auto corr_load = [&](int b) {
-#pragma unroll
-                for (int f = 0; f < 2; ++f) {
-                    const int n = 1 + 8 * b + g;
-                    const int Lf = f ? I.L[1] : I.L[0];
-                    double v = 0.0;
-                    if (A.sbd && n >= 2 && n <= A.N && n - 1 >= Lf) v = (f ? I.corr[1] : I.corr[0])[n - 4];
-                    cpre[f] = v;
-                }
+                const int n = 1 + 8 * b + g;
+                cpre = (A.sbd && n >= 2 && n <= A.N && n - 1 >= Lsf) ? corr_f[n - 4] : 0.0;
             };
             corr_load(0);
             for (int i = 0; i <= (int)nb; ++i) {
@@ -278,58 +277,48 @@ __global__ void __launch_bounds__(288, 1) k13_kernel(K13Args A) {
                     // ---- known part on DMMA: D[k][d] = partial readouts + sum_j c[k+Lt-j] G^(n0-Lt+j)
                     //      (fragment: thread (g, t) holds rows k = g, columns d = 2t, 2t+1 of a tile;
                     //      as A operand it holds A[k = g][j = t], as B operand B[j = t][d = g])
-                    double D[2][RB][2];
+                    double D[RB][2];
 #pragma unroll
-                    for (int f = 0; f < 2; ++f)
+                    for (int nt = 0; nt < RB; ++nt) {
+                        const double* pb = part + ((size_t)buf * nwg + sf * nwf) * 8 * MODES +
+                                           g * MODES + 8 * nt + 2 * t;
+                        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                        for (int w = 0; w < 4; ++w)
+                            if (w < nwf) {
+                                const double2 v = *reinterpret_cast<const double2*>(pb + w * 8 * MODES);
+                                s0 += v.x;
+                                s1 += v.y;
+                            }
+                        D[nt][0] = s0;
+                        D[nt][1] = s1;
+                    }
+                    for (int j0 = 0; j0 < Lts; j0 += 4) {
+                        const int j = j0 + t, lev = n0 - Lts + j;
+                        const bool ok = j < Lts;
+                        const double av = ok ? CWs[g + Lts - j] : 0.0;
+                        const double* rg = ring + (sf * RING + (lev & mask)) * MODES + g;
 #pragma unroll
                         for (int nt = 0; nt < RB; ++nt) {
-                            const double* pb = part + ((size_t)buf * nwg + f * nwf) * 8 * MODES +
-                                               g * MODES + 8 * nt + 2 * t;
-                            double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-                            for (int w = 0; w < 4; ++w)
-                                if (w < nwf) {
-                                    const double2 v = *reinterpret_cast<const double2*>(pb + w * 8 * MODES);
-                                    s0 += v.x;
-                                    s1 += v.y;
-                                }
-                            D[f][nt][0] = s0;
-                            D[f][nt][1] = s1;
-                        }
-                    for (int j0 = 0; j0 < Ltm; j0 += 4) {
-                        const int j = j0 + t;
-#pragma unroll
-                        for (int f = 0; f < 2; ++f) {
-                            const int Ltf = Lt[f], lev = n0 - Ltf + j;
-                            const bool ok = j < Ltf;
-                            const double av = ok ? cwt[f][g + Ltf - j] : 0.0;
-                            const double* rg = ring + (f * RING + (lev & mask)) * MODES + g;
-#pragma unroll
-                            for (int nt = 0; nt < RB; ++nt) {
-                                const double bv = (ok && lev >= 1) ? rg[8 * nt] : 0.0;
-                                dmma(D[f][nt], av, bv);
-                            }
+                            const double bv = (ok && lev >= 1) ? rg[8 * nt] : 0.0;
+                            dmma(D[nt], av, bv);
                         }
                     }
-#pragma unroll
-                    for (int f = 0; f < 2; ++f) {
+                    {
                         const int n = n0 + g;
-                        double corr_c = 0.0;
-                        if (A.sbd && n >= 2) {
-                            const int Lf = f ? I.L[1] : I.L[0];
-                            corr_c = 0.5 * ((n - 1 < Lf) ? cwt[f][n - 1] : cpre[f]);
-                        }
+                        const double corr_c =
+                            (A.sbd && n >= 2) ? 0.5 * ((n - 1 < Lsf) ? CWs[n - 1] : cpre) : 0.0;
 #pragma unroll
                         for (int nt = 0; nt < RB; ++nt) {
-                            const double* g0f = g0s + f * MODES + 8 * nt + 2 * t;
-                            *reinterpret_cast<double2*>(sA + (f * 8 + g) * MODES + 8 * nt + 2 * t) =
-                                make_double2(fma(corr_c, g0f[0], D[f][nt][0]),
-                                             fma(corr_c, g0f[1], D[f][nt][1]));
+                            const double* g0f = g0s + sf * MODES + 8 * nt + 2 * t;
+                            *reinterpret_cast<double2*>(sA + (sf * 8 + g) * MODES + 8 * nt + 2 * t) =
+                                make_double2(fma(corr_c, g0f[0], D[nt][0]),
+                                             fma(corr_c, g0f[1], D[nt][1]));
                         }
                     }
                     if (b + 1 < nb) corr_load(b + 1);  // latency hidden by the solve + barrier
-                    __syncwarp();
-                    if (lane < MODES) {
+                    asm volatile("bar.sync 1, 64;" ::: "memory");  // both fields' known parts ready
+                    if (sf == 0 && lane < MODES) {
                         double acc1[8], acc2[8];
 #pragma unroll
                         for (int k = 0; k < 8; ++k) {
@@ -408,7 +397,7 @@ __global__ void __launch_bounds__(288, 1) k13_kernel(K13Args A) {
                 }
                 __syncthreads();
             }
-            if (live) {
+            if (live && sf == 0) {
                 A.cN[((long)inst * 2 + 0) * A.n_modes + m0 + d] = gp1;
                 A.cN[((long)inst * 2 + 1) * A.n_modes + m0 + d] = gp2;
             }
@@ -426,7 +415,7 @@ void k13_launch(const K13Args& a, size_t smem, int num_sms, cudaStream_t s) {
     FRAQ_CUDA(cudaFuncSetAttribute(k13_kernel<RB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
     int per_sm = 1;
-    const int threads = a.nwg * 32 + 32;
+    const int threads = a.nwg * 32 + 64;
     FRAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k13_kernel<RB, NT>, threads, smem));
     const long grid = std::max(1L, std::min(a.n_tasks, (long)std::max(1, per_sm) * num_sms));
     k13_kernel<RB, NT><<<(unsigned)grid, threads, smem, s>>>(a);

@@ -1,8 +1,8 @@
 # Builds K5d timing variants (experiment switches) into gpurun_variants/<name> (run here, CPU).
 set -e
 cd "$(dirname "$0")/../.."
-for v in "base:" "noreduce:-DFRAQ_EXP_NOREDUCE" "gemm_only:-DFRAQ_EXP_NOREDUCE -DFRAQ_EXP_NOSYNC -DFRAQ_EXP_NOFIR" \
-         "onecta:-DFRAQ_EXP_ONECTA" "onecta_gemm_only:-DFRAQ_EXP_ONECTA -DFRAQ_EXP_NOREDUCE -DFRAQ_EXP_NOSYNC -DFRAQ_EXP_NOFIR"; do
+for v in "base:" "noreduce:-DFRAQ_EXP_NOREDUCE" "nofir:-DFRAQ_EXP_NOFIR" "nosync:-DFRAQ_EXP_NOSYNC" "gemm_only:-DFRAQ_EXP_NOREDUCE -DFRAQ_EXP_NOSYNC -DFRAQ_EXP_NOFIR" \
+         ; do
   name=${v%%:*}; flags=${v#*:}
   rm -rf gpurun_variants/$name; mkdir -p gpurun_variants/$name
   cp -r paper_1901_05128_b200 include gpurun_variants/$name/
