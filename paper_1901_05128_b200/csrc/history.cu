@@ -1139,7 +1139,15 @@ void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, l
     // i (the kernels themselves are sequential: each chunk continues the history state).
     // Pinned host memory gives full overlap; pageable memory still works (staged copies).
     const long dim = std::max<long>(1, h->d.total_dim);
-    const long rows = std::max<long>(1, std::min<long>(n_steps, (64L << 20) / (8 * dim)));
+    // chunk height: ~1/16 of the call in multiples of the kernel's 32-level staging chunk, so the
+    // pipeline fill (first H2D) and drain (last D2H) stay short; at most 64 MB per buffer.
+    // (C2, 512 levels x 65536 DOFs per call: 32-level chunks reach 87% of the measured
+    // concurrent PCIe bound; 128-level chunks 72%.)
+    const long cap = std::max<long>(1, (64L << 20) / (8 * dim));
+    long rows = std::min<long>(cap, std::max<long>(32, ((n_steps / 16 + 31) / 32) * 32));
+    if (const char* e = std::getenv("FRAQ_HOST_CHUNK"))  // experiment override (levels per chunk)
+        rows = std::max<long>(1, std::atol(e));
+    rows = std::max<long>(1, std::min<long>(rows, std::max<long>(1, n_steps)));
     for (int i = 0; i < 2; ++i) {
         if ((long)h->ubuf[i].n < rows * dim) h->ubuf[i].alloc(rows * dim);
         if (D && (long)h->dbuf[i].n < rows * dim) h->dbuf[i].alloc(rows * dim);
