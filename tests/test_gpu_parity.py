@@ -346,3 +346,62 @@ def test_ffpe_zero_stays_zero(fraq):
             kc.solver = solver
             rr = fraq.run(spec, getattr(fraq.Scheme, s), kc)
             assert all(v == 0.0 for v in rr.final_state.g1 + rr.final_state.g2)
+
+
+@pytest.mark.parametrize("nh", [31, 32, 33, 40, 60])
+@pytest.mark.parametrize("variant", ["standalone", "scheme"])
+def test_run_blocked_long_heads(fraq, orc, nh, variant):
+    """Head windows around the K5d lag limit (32): L <= 32 takes K5d (path 3), longer heads the
+    K5c kernel (path 2); both equal the reference history."""
+    rng = np.random.default_rng(nh)
+    o = orc.build_sbd_kernel(0.55, 2e-3, 60, 70, nh)
+    k = kernel_from_oracle(fraq, o)
+    dim, n = 19, 260
+    U = rng.uniform(-1, 1, (n, dim))
+    D_ref = orc.hist_run(o, U, variant == "scheme")
+    h = fraq.SbdHistory(k, getattr(fraq.HistoryVariant, variant), dim)
+    D = np.array(h.run(U), dtype=float)
+    assert h.last_path == (3 if nh <= 32 else 2)
+    ok = ~np.isnan(D_ref)
+    assert np.array_equal(np.isnan(D), np.isnan(D_ref))
+    scale = np.maximum(np.abs(D_ref[ok]), 2e-3 ** -0.55)
+    assert np.max(np.abs(D[ok] - D_ref[ok]) / scale) <= 1e-12
+
+
+def test_run_zero_steps_and_continuation(fraq, orc):
+    o = orc.build_be_kernel(0.5, 1e-3, 40)
+    k = kernel_from_oracle(fraq, o)
+    h = fraq.BeHistory(k, fraq.HistoryVariant.standalone, 5)
+    U = np.random.default_rng(0).uniform(-1, 1, (50, 5))
+    assert len(h.run(U[:0])) == 0 and h.appended == 0
+    D1 = np.array(h.run(U[:20]), dtype=float)
+    assert len(h.run(U[20:20])) == 0 and h.appended == 20
+    D2 = np.array(h.run(U[20:]), dtype=float)
+    D_ref = orc.hist_run(o, U)
+    D = np.concatenate([D1, D2])
+    ok = ~np.isnan(D_ref)
+    assert np.max(np.abs(D[ok] - D_ref[ok])) <= 1e-12 * np.max(np.abs(D_ref[ok]))
+
+
+@pytest.mark.parametrize("nh", [5, 9, 45, 60])
+def test_ffpe_sbd_head_lengths_all_solver_paths(fraq, orc, nh):
+    """SBD head windows that select every modal path: K13 with state lag delta = 1 (L < 8) and
+    0 (L >= 8), K11 (40 < L <= 56), and beyond 56 the AUTO solver's physical fallback (the
+    explicit MODAL solver must refuse)."""
+    kconf = dict(auto_size=False, sbd_points_1=24, sbd_points_2=24, sbd_head=nh)
+    g1, g2, _, _ = orc.run(0.3, 0.65, -1.5, 31, 0.5, 120, "FastSBD", "indicator", kconf=kconf)
+    spec = fraq.ProblemSpec(alpha1=0.3, alpha2=0.65, coupling_a=-1.5, grid_m=31, t_final=0.5,
+                            n_steps=120, initial="indicator")
+    for solver in ("SOLVER_AUTO", "SOLVER_MODAL", "SOLVER_PHYSICAL"):
+        kc = fraq.KernelConfig()
+        kc.auto_size = False
+        kc.sbd_points_1 = kc.sbd_points_2 = 24
+        kc.sbd_head = nh
+        kc.solver = getattr(fraq, solver)
+        if solver == "SOLVER_MODAL" and nh > 56:
+            with pytest.raises(ValueError):
+                fraq.run(spec, fraq.Scheme.FastSBD, kc)
+            continue
+        rr = fraq.run(spec, fraq.Scheme.FastSBD, kc)
+        assert rel_linf(rr.final_state.g1, g1) <= 1e-10
+        assert rel_linf(rr.final_state.g2, g2) <= 1e-10
