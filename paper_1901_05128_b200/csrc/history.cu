@@ -1148,9 +1148,11 @@ void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, l
     if (const char* e = std::getenv("FRAQ_HOST_CHUNK"))  // experiment override (levels per chunk)
         rows = std::max<long>(1, std::atol(e));
     rows = std::max<long>(1, std::min<long>(rows, std::max<long>(1, n_steps)));
+    // a remainder under 32 rows joins the last chunk (keeps it on the blocked kernels)
+    const long cap_rows = rows + 31;
     for (int i = 0; i < 2; ++i) {
-        if ((long)h->ubuf[i].n < rows * dim) h->ubuf[i].alloc(rows * dim);
-        if (D && (long)h->dbuf[i].n < rows * dim) h->dbuf[i].alloc(rows * dim);
+        if ((long)h->ubuf[i].n < cap_rows * dim) h->ubuf[i].alloc(cap_rows * dim);
+        if (D && (long)h->dbuf[i].n < cap_rows * dim) h->dbuf[i].alloc(cap_rows * dim);
         if (!h->ev_u[i]) {
             FRAQ_CUDA(cudaEventCreateWithFlags(&h->ev_u[i], cudaEventDisableTiming));
             FRAQ_CUDA(cudaEventCreateWithFlags(&h->ev_c[i], cudaEventDisableTiming));
@@ -1168,9 +1170,9 @@ void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, l
     FRAQ_CUDA(cudaEventRecord(h->ev_d[0], sc));
     FRAQ_CUDA(cudaEventRecord(h->ev_d[1], sc));
     long i = 0;
-    for (long n0 = 0; n0 < n_steps; n0 += rows, ++i) {
+    for (long n0 = 0, nr = 0; n0 < n_steps; n0 += nr, ++i) {
         const int b = (int)(i & 1);
-        const long nr = std::min(rows, n_steps - n0);
+        nr = (n_steps - n0 - rows < 32) ? n_steps - n0 : rows;
         // H2D into ubuf[b] once the kernel that last read it (chunk i-2) finished
         FRAQ_CUDA(cudaStreamWaitEvent(h->s_h2d, h->ev_c[b], 0));
         FRAQ_CUDA(cudaMemcpy2DAsync(h->ubuf[b].p, dim * 8, U + n0 * ldu, ldu * 8,
