@@ -292,8 +292,10 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
                         const double b0 = rw[(ntl * 2) * 32], b1 = rw[(ntl * 2 + 1) * 32];
 #pragma unroll
                         for (int rb = 0; rb < 2; ++rb) {
+#ifndef FRAQ_EXP_NODMUL
                             Y[rb][ntl][0] *= ra;
                             Y[rb][ntl][1] *= rbv;
+#endif
                             dmma(Y[rb][ntl], vf[rb][0], b0);
                             dmma(Y[rb][ntl], vf[rb][1], b1);
                         }
