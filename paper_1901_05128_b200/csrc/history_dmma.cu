@@ -100,6 +100,7 @@ struct DSmem {
     double X[D_LMAX + D_TC][16];
     double F[D_TC][16];      // exact head window of the chunk
     double hd[D_LMAX];
+    double hf[16][32];       // head-window Toeplitz as DMMA B fragments (DMMA FIR)
 };
 
 // CTA = one 16-DOF group x all nodes: nwg warps (64 nodes each), 2 CTAs resident per SM so one
@@ -139,6 +140,17 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
         }
         const double* RFg = A.frag + (size_t)tk.x * kFragDoubles + kFragRF;  // partial blocks
         for (int i = tid; i < D_LMAX; i += blockDim.x) S.hd[i] = i < L ? A.head[G.hd_off + i] : 0.0;
+        // Exact head window as one more K-segment of the readout GEMM: for a block at n0,
+        // FIR^T[d][k] = sum_jj X[js + jj][d] H[jj][k], js = n0 + 8 - KW, H[jj][k] = d_(k+KW-8-jj)
+        // (zero outside the taps) -- shift invariant: B fragments per group.
+        const int taps = G.sbd ? L : 2;
+        const int KW = ((taps + 7) + 3) & ~3;
+        for (int i = tid; i < (KW / 4) * 32; i += blockDim.x) {
+            const int kk = i >> 5, ln = i & 31, gg = ln >> 2, tt = ln & 3;
+            const int ii = gg + KW - 8 - (4 * kk + tt);
+            S.hf[kk][ln] = (ii >= 0 && ii < taps) ? A.head[G.hd_off + ii] : 0.0;
+        }
+        const int nkk = KW / 4;
         // state fragments Y[rb][ntl][e]: DOF tk.y + 8 rb + g, node 64 sl + 8 ntl + 2t + e
         double Y[2][D_NT][2];
 #pragma unroll
@@ -190,6 +202,7 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
         // (slot, level k, DOF d) per thread, two independent add chains over the warp partials
         long p_row0 = 0, p_row1 = 0, p_n00 = 0, p_n01 = 0;
         int p_kmax0 = 0, p_kmax1 = 0, p_buf = 0;
+        bool p_dfir0 = false, p_dfir1 = false;
         auto reduce_pair = [&]() {
 #ifdef FRAQ_EXP_NOREDUCE
             return;
@@ -207,9 +220,17 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
                 if (nwg & 1) s0 += pb[(nwg - 1) * 128];
                 const double sum = s0 + s1;
                 const bool valid = G.sbd ? true : (pn0 + k >= 1);
+                const bool dfir = slot ? p_dfir1 : p_dfir0;
                 if (Db && tk.y + d < G.dim)
-                    Db[(prow + k) * A.ldd + d] = valid ? sum + S.F[(prow + k) % D_TC][d] : qnan;
+                    Db[(prow + k) * A.ldd + d] =
+                        valid ? sum + (dfir ? 0.0 : S.F[(prow + k) % D_TC][d]) : qnan;
             }
+        };
+        // full blocks whose whole head window is valid take the FIR through DMMA
+        auto dfir_block = [&](long n0, int kmax) {
+            const bool special = A.lo == 1 && n0 <= L && L < n0 + D_TB;
+            const bool ok = G.sbd ? (n0 - (L - 1) >= A.lo) : (n0 >= 1);
+            return kmax == D_TB && n0 >= 1 && !special && ok;
         };
         int buf = 0, last_tmax = 0;
         bool pending = false;
@@ -233,6 +254,8 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
             }
             __syncthreads();
 #ifndef FRAQ_EXP_NOFIR
+            const bool chunk_dfir = tmax == D_TC && dfir_block(A.A0 + c0, D_TB);
+            if (!chunk_dfir) {
             for (int idx = tid; idx < D_TC * 16; idx += blockDim.x) {
                 const int tt = idx >> 4, d = idx & 15;
                 const long n = A.A0 + c0 + tt;
@@ -242,6 +265,7 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
                 S.F[tt][d] = acc;
             }
             __syncthreads();
+            }
 #endif
             auto do_block = [&](int t0, int slot, bool mid_reduce) {
                 const long n0 = A.A0 + c0 + t0;
@@ -282,6 +306,14 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
                         else
                             dmma(sacc[1][1], vf[1][1], b);
                     }
+                    // head-window FIR: warp w < nkk adds k-step w for both row blocks
+                    if (dfir_block(n0, kmax))
+                        for (int kk = sl; kk < nkk; kk += nwg) {  // (fewer warps: several each)
+                            const double b = S.hf[kk][lane];
+                            const int xr = D_LMAX + t0 + 8 - KW + 4 * kk + t;
+                            dmma(sacc[0][1], S.X[xr][g], b);
+                            dmma(sacc[1][1], S.X[xr][8 + g], b);
+                        }
                     // deferred reduction of the previous pair: its LDS / DADD / STG latency
                     // overlaps the readout DMMAs just issued (asynchronous tensor pipe)
                     if (mid_reduce) reduce_pair();
@@ -348,11 +380,13 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
                 p_row0 = c0 + t0;
                 p_n00 = A.A0 + c0 + t0;
                 p_kmax0 = min(D_TB, tmax - t0);
+                p_dfir0 = dfir_block(p_n00, p_kmax0);
                 p_kmax1 = 0;
                 if (nblk == 2) {
                     p_row1 = c0 + t0 + D_TB;
                     p_n01 = A.A0 + c0 + t0 + D_TB;
                     p_kmax1 = min(D_TB, tmax - t0 - D_TB);
+                    p_dfir1 = dfir_block(p_n01, p_kmax1);
                 }
 #ifndef FRAQ_EXP_NOSYNC
                 __syncthreads();
