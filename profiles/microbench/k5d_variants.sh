@@ -1,7 +1,7 @@
 # Builds K5d timing variants (experiment switches) into gpurun_variants/<name> (run here, CPU).
 set -e
 cd "$(dirname "$0")/../.."
-for v in "base:" "nodmul:-DFRAQ_EXP_NODMUL" "gemm_only:-DFRAQ_EXP_NOREDUCE -DFRAQ_EXP_NOSYNC -DFRAQ_EXP_NOFIR" "gemm_nodmul:-DFRAQ_EXP_NOREDUCE -DFRAQ_EXP_NOSYNC -DFRAQ_EXP_NOFIR -DFRAQ_EXP_NODMUL" \
+for v in "base:" "noreduce:-DFRAQ_EXP_NOREDUCE" "nosync:-DFRAQ_EXP_NOSYNC" "nodmul:-DFRAQ_EXP_NODMUL" "gemm_only:-DFRAQ_EXP_NOREDUCE -DFRAQ_EXP_NOSYNC -DFRAQ_EXP_NOFIR" \
          ; do
   name=${v%%:*}; flags=${v#*:}
   rm -rf gpurun_variants/$name; mkdir -p gpurun_variants/$name
