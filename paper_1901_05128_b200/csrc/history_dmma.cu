@@ -121,7 +121,6 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
     const int nwg = blockDim.x >> 5;  // warps = node slices of 64
     const int sl = warp;
     const double qnan = __longlong_as_double(0x7ff8000000000000LL);
-    const bool fast_red = nwg == D_MAXWG;
     if (tid == 0) s_group = -1;
     for (;;) {
         __syncthreads();
