@@ -8,7 +8,7 @@ kernels (256 + 256 nodes, N_s = 17 / 15).  Signals u_k(t) = a_k t^b_k + c_k sin(
 
 One bench step = one pass of the hot path over the batch for LEVELS_PER_STEP (512) time levels:
 push + derivative for every DOF at every level, through SbdHistory.run on device buffers
-(temporally blocked kernel K5b).  K timed steps advance a fresh history from level 0; the default
+(temporally blocked kernel K5d, fp64 tensor cores).  K timed steps advance a fresh history from level 0; the default
 K = 128 covers the whole C2 horizon N = 65536.  Warm-up steps run on a separate history.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
@@ -272,7 +272,7 @@ def main():
     # sanity: outputs finite after the first level
     assert torch.isfinite(D[1:LEVELS_PER_STEP * K]).all().item()
 
-    # roofline of the dominant kernel (K5b): fp64 FMA bound; algorithmic flops per DOF-step
+    # roofline of the dominant kernel (K5d): fp64 tensor-pipe bound; algorithmic flops per DOF-step
     # F = 4 N_nodes + 2 N_head, averaged over the two exponent halves
     F = 0.5 * sum(4 * nn + 2 * hh for nn, hh in zip(n_nodes, n_head))
     achieved_tf = F * dof_steps_local / (total_ms * 1e-3) / 1e12
@@ -290,7 +290,7 @@ def main():
     # per-level fused kernel K5 (one HBM pass over the state per level) on the same workload
     hs = fraq.MultiHistory(ks, [DOFS // 2, DOFS - DOFS // 2])
     nstep = 24
-    hs.run_device(U.data_ptr(), DOFS, 3, D.data_ptr(), DOFS)  # level 0..2 via K5b (n_steps < 4)
+    hs.run_device(U.data_ptr(), DOFS, 3, D.data_ptr(), DOFS)  # levels 0..2 (n_steps < 4: per-level K5)
     torch.cuda.synchronize()
     # force the per-level path: push/derivative on device pointers level by level
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
@@ -313,7 +313,7 @@ def main():
     t_e = time.perf_counter()
     for s in range(ke):
         rows = slice(s * LEVELS_PER_STEP, (s + 1) * LEVELS_PER_STEP)
-        # host in, host out: H2D + K5b + D2H inside fraq_hist_run (pinned buffers)
+        # host in, host out: H2D + K5d + D2H inside fraq_hist_run (pinned buffers)
         he.run(Uh[rows].numpy(), True, Dh[rows].numpy())
     e2e_s = time.perf_counter() - t_e
     del he

@@ -173,12 +173,14 @@ int fraq_hist_lagged(fraq_hist h, long depth, double* out, int mem);
 /* Batched standalone evaluation: pushes U[n * ldu + 0 .. dim) for n = 0..n_steps-1 and writes the
  * derivative after each push to D[n * ldd + ...] (NaN where the reference would throw
  * "too early"); D may be NULL.  Equivalent to n_steps x (push; derivative).  Uses the
- * temporally blocked kernel K5b (history kept on chip across the whole call). */
+ * temporally blocked kernel K5d (8-level block GEMMs on the fp64 tensor cores, the history kept
+ * on chip across the whole call); mem = FRAQ_HOST streams U / D through pinned staging buffers
+ * with the copies overlapping the kernels. */
 int fraq_hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, long ldd,
                   int mem);
-/* Which kernel the last fraq_hist_run used: 0 = per-level K5, 1 = K5b (warp-per-4-DOF blocked,
- * FRAQ_K5B=1), 2 = K5c (lane-per-DOF DFMA blocked, FRAQ_K5C=1), 3 = K5d (DMMA block GEMMs,
- * default). */
+/* Which kernel the last fraq_hist_run used: 0 = per-level K5 (calls under 4 levels, or more than
+ * 512 nodes), 1 = K5b (warp-per-4-DOF blocked, FRAQ_K5B=1), 2 = K5c (lane-per-DOF DFMA blocked:
+ * FRAQ_K5C=1, or head windows over 32 levels), 3 = K5d (DMMA block GEMMs, default). */
 int fraq_hist_last_path(fraq_hist h);
 
 /* ---------------------------------------------------------------- direct CQ (K10)
