@@ -12,6 +12,7 @@ push + derivative for every DOF at every level, through SbdHistory.run on device
 K = 128 covers the whole C2 horizon N = 65536.  Warm-up steps run on a separate history.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--workload C2 | C3 | C4 | C5 | C5-SBD]     (FFPE configs: bench_ffpe.py)
 
 Prints one JSON line (rank 0).  --impl reference times the reference's own CPU implementation
 (oracle/_ref: the unmodified reference sources) on the host cores with the same metric.
