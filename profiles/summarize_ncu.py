@@ -33,7 +33,28 @@ def launches(path):
     print(f"== launch list {path}: {sum(v[0] for v in agg.values())} launches, {tot/1e6:.3f} ms "
           "(cold-cache, serialised: compare shares)")
     for k, v in sorted(agg.items(), key=lambda x: -x[1][1])[:20]:
-        print(f"{v[0]:6d} x {v[1]/1e6/v[0]:9.4f} ms = {v[1]/1e6:9.3f} ms {100*v[1]/tot:5.1f}%  {k}")
+        print(f"{v[0]:6d} x {v[1]/1e6/v[0]:9.4f} ms = {v[1]/1e6:9.3f} ms {100*v[1]/tot:5.1f}%  "
+              f"[{role(k)}] {k}")
+    # the bench's timed step is the history kernel alone; everything else is setup, the live
+    # peak diagnostics behind roofline.peak, or the side measurements (K5 roofline, e2e)
+    roles = collections.defaultdict(float)
+    for k, v in agg.items():
+        roles[role(k)] += v[1]
+    print("   by role: " + ", ".join(f"{r} {100 * t / tot:.1f}%" for r, t in
+                                      sorted(roles.items(), key=lambda x: -x[1])))
+
+
+def role(name):
+    if "run3_kernel" in name or "k13_kernel" in name:
+        return "timed step"
+    if "dmma_kernel" in name or "dfma_kernel" in name:
+        return "peak diagnostic"
+    if any(x in name for x in ("scan_kernel", "chain_kernel", "cauchy_kernel", "rule_kernel",
+                               "frag_tables", "reconstruct", "k13_tables")):
+        return "setup"
+    if "step_kernel" in name:
+        return "K5 roofline side run"
+    return "other (torch input generation / checks)"
 
 
 def full(path):
