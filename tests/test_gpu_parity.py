@@ -405,3 +405,24 @@ def test_ffpe_sbd_head_lengths_all_solver_paths(fraq, orc, nh):
         rr = fraq.run(spec, fraq.Scheme.FastSBD, kc)
         assert rel_linf(rr.final_state.g1, g1) <= 1e-10
         assert rel_linf(rr.final_state.g2, g2) <= 1e-10
+
+
+@pytest.mark.parametrize("sbd", [False, True])
+@pytest.mark.parametrize("np_", [7, 64, 256])
+def test_run_blocked_scheme_variant(fraq, orc, sbd, np_):
+    """Blocked runs in the scheme variant (lo = 1: G^0 never fed, SBD head taps i <= n-1), split
+    over calls so the DMMA head window meets block starts near the lag boundary."""
+    rng = np.random.default_rng(np_ + 7 * sbd)
+    g, tau = 0.45, 1e-3
+    o = orc.build_sbd_kernel(g, tau, np_ // 2 + 1, np_ - np_ // 2, 13) if sbd else orc.build_be_kernel(g, tau, np_)
+    k = kernel_from_oracle(fraq, o)
+    dim, n = 21, 301
+    U = rng.uniform(-1, 1, (n, dim))
+    D_ref = orc.hist_run(o, U, True)
+    h = (fraq.SbdHistory if sbd else fraq.BeHistory)(k, fraq.HistoryVariant.scheme, dim)
+    parts = [h.run(U[a:b]) for a, b in ((0, 9), (9, 40), (40, 173), (173, n))]
+    D = np.concatenate([np.array(p, dtype=float).reshape(-1, dim) for p in parts])
+    assert np.array_equal(np.isnan(D), np.isnan(D_ref))
+    ok = ~np.isnan(D_ref)
+    scale = np.maximum(np.abs(D_ref[ok]), tau ** (-g))
+    assert np.max(np.abs(D[ok] - D_ref[ok]) / scale) <= 1e-12
