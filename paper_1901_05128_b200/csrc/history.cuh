@@ -61,6 +61,7 @@ struct RunArgs {
     double* D;              // nullable
     long ldd;
     const double* frag;     // K5d fragment tables (per group kFragDoubles)
+    int use_tma;            // K5d: stage input chunks with TMA (tensor map over U)
 };
 
 // K5d fragment tables per group (history_dmma.cu): C (64 node tiles x 2 x 32), R (64 x 2 x 32),

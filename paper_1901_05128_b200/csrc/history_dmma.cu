@@ -16,10 +16,14 @@
 // slices meet through shared memory once per 8-level block.  Measured on B200: DMMA alone
 // reaches 37 TF/s (latency 26 cycles), whereas DFMA with three distinct register operands is
 // capped near 25 TF/s by register-file reads (profiles/microbench/mb_operands.cu).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "history.cuh"
@@ -38,6 +42,37 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                  : "+d"(d[0]), "+d"(d[1])
                  : "d"(a), "d"(b));
+}
+
+// ---- TMA / mbarrier (input chunk staging)
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* m) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(m)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// one elected thread: arm the barrier with the byte count, then the 2D tile load that completes it
+__device__ __forceinline__ void tma_tile(const CUtensorMap* map, void* dst, unsigned long long* m,
+                                         int col, int row, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(col), "r"(row), "r"(smem_u32(m))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned parity) {
+    unsigned done = 0;
+    while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, "
+            "0, p; }"
+            : "=r"(done)
+            : "r"(smem_u32(m)), "r"(parity)
+            : "memory");
 }
 
 // Fragment tables for one group (one CTA per group, 256 threads).
@@ -97,10 +132,11 @@ __global__ void frag_tables_kernel(const GroupDev* groups, const double* cr, con
 }
 
 struct DSmem {
-    double X[D_LMAX + D_TC][16];
-    double F[D_TC][16];      // exact head window of the chunk
+    double X[D_LMAX + D_TC][16];  // lag rows + the current chunk (row n at D_LMAX + n - c0)
+    double Xn[D_TC][16];          // TMA landing tile of the next chunk (128-byte aligned)
     double hd[D_LMAX];
-    double hf[16][32];       // head-window Toeplitz as DMMA B fragments (DMMA FIR)
+    double hf[16][32];            // head-window Toeplitz as DMMA B fragments (DMMA FIR)
+    unsigned long long mbar;      // completion barrier of the Xn tile
 };
 
 // CTA = one 16-DOF group x all nodes: nwg warps (64 nodes each), 2 CTAs resident per SM so one
@@ -108,11 +144,13 @@ struct DSmem {
 // reduction of block b-1 is issued after block b's readout DMMAs (software pipelining), so its
 // shared-memory latency hides under the asynchronous tensor pipe.
 #ifdef FRAQ_EXP_ONECTA
-__global__ void __launch_bounds__(256, 1) run3_kernel(RunArgs A) {
+__global__ void __launch_bounds__(256, 1)
+    run3_kernel(RunArgs A, const __grid_constant__ CUtensorMap umap) {
 #else
-__global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
+__global__ void __launch_bounds__(256, 2)
+    run3_kernel(RunArgs A, const __grid_constant__ CUtensorMap umap) {
 #endif
-    extern __shared__ double dsm[];
+    extern __shared__ __align__(128) double dsm[];
     DSmem& S = *reinterpret_cast<DSmem*>(dsm);
     double* tab = dsm + sizeof(DSmem) / sizeof(double);         // kFragDoubles
     double* part = tab + kFragR8 + 64;  // [2 buffers][2 slots][8 warps][2][8][8]
@@ -196,7 +234,16 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
                              ? Ub[tt * A.ldu + pd] : 0.0;
             }
         };
-        if (blockDim.x == 256) prefetch(0);
+        const bool tma = A.use_tma && blockDim.x == 256;
+        unsigned tphase = 0;
+        if (tma) {
+            if (tid == 0) {
+                mbar_init(&S.mbar);
+                tma_tile(&umap, &S.Xn[0][0], &S.mbar, (int)(G.dof0 + tk.y), 0, D_TC * 16 * 8);
+            }
+        } else if (blockDim.x == 256) {
+            prefetch(0);
+        }
         // reduction of a pair of blocks (node sum over warps + head window -> D): one output
         // (slot, level k, DOF d) per thread, two independent add chains over the warp partials
         long p_row0 = 0, p_row1 = 0, p_n00 = 0, p_n01 = 0;
@@ -218,11 +265,18 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
                 }
                 if (nwg & 1) s0 += pb[(nwg - 1) * 128];
                 const double sum = s0 + s1;
+                double fir = 0.0;
+                if (!(slot ? p_dfir1 : p_dfir0)) {
+                    // blocks outside the DMMA head window (early levels, chunk tails): exact
+                    // head sum from the staged rows, reference tap rule and order
+                    const long n = pn0 + k;
+                    const long top = G.sbd ? min((long)L - 1, n - A.lo) : 1;
+                    const int tt = (int)((prow + k) % D_TC);
+                    for (long i = 0; i <= top; ++i) fir = fma(S.hd[i], S.X[D_LMAX + tt - i][d], fir);
+                }
                 const bool valid = G.sbd ? true : (pn0 + k >= 1);
-                const bool dfir = slot ? p_dfir1 : p_dfir0;
                 if (Db && tk.y + d < G.dim)
-                    Db[(prow + k) * A.ldd + d] =
-                        valid ? sum + (dfir ? 0.0 : S.F[(prow + k) % D_TC][d]) : qnan;
+                    Db[(prow + k) * A.ldd + d] = valid ? sum + fir : qnan;
             }
         };
         // full blocks whose whole head window is valid take the FIR through DMMA
@@ -236,7 +290,16 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
         for (long c0 = 0; c0 < A.n_steps; c0 += D_TC) {
             const int tmax = (int)min((long)D_TC, A.n_steps - c0);
             __syncthreads();
-            if (blockDim.x == 256) {
+            if (tma) {
+                // the chunk's tile landed (TMA, zero-filled past the ends): move it into the window
+                mbar_wait(&S.mbar, tphase);
+                tphase ^= 1;
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int row = prow + 16 * i;
+                    S.X[D_LMAX + row][pd] = plive ? S.Xn[row][pd] : 0.0;
+                }
+            } else if (blockDim.x == 256) {
 #pragma unroll
                 for (int i = 0; i < 2; ++i) {
                     const int row = prow + 16 * i;
@@ -252,20 +315,10 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
                 }
             }
             __syncthreads();
-#ifndef FRAQ_EXP_NOFIR
-            const bool chunk_dfir = tmax == D_TC && dfir_block(A.A0 + c0, D_TB);
-            if (!chunk_dfir) {
-            for (int idx = tid; idx < D_TC * 16; idx += blockDim.x) {
-                const int tt = idx >> 4, d = idx & 15;
-                const long n = A.A0 + c0 + tt;
-                const long top = G.sbd ? min((long)L - 1, n - A.lo) : 1;
-                double acc = 0.0;
-                for (long i = 0; i <= top; ++i) acc = fma(S.hd[i], S.X[D_LMAX + tt - i][d], acc);
-                S.F[tt][d] = acc;
-            }
-            __syncthreads();
-            }
-#endif
+            if (tma && tid == 0 && c0 + D_TC < A.n_steps)  // Xn is free again: next chunk's tile
+                tma_tile(&umap, &S.Xn[0][0], &S.mbar, (int)(G.dof0 + tk.y), (int)(c0 + D_TC),
+                         D_TC * 16 * 8);
+            // (head window: DMMA segment of the readout, or per output in reduce_pair)
             auto do_block = [&](int t0, int slot, bool mid_reduce) {
                 const long n0 = A.A0 + c0 + t0;
                 const int kmax = min(D_TB, tmax - t0);
@@ -394,7 +447,7 @@ __global__ void __launch_bounds__(256, 2) run3_kernel(RunArgs A) {
                 pending = true;
                 buf ^= 1;
             }
-            if (pending) {  // the chunk's last pair (S.F / S.X are rewritten next chunk)
+            if (pending) {  // the chunk's last pair (S.X is rewritten next chunk)
                 reduce_pair();
                 pending = false;
             }
@@ -466,7 +519,34 @@ void launch_run3(const RunArgs& a, int nwg, int num_sms, cudaStream_t s) {
     per_sm = 1;
 #endif
     const int grid = std::max(1, std::min(a.n_tasks, std::max(1, per_sm) * num_sms));
-    run3_kernel<<<grid, nwg * 32, smem, s>>>(a);
+    // tensor map over the caller's input rows U[n_steps][ldu] (doubles): 16-DOF x 32-level boxes,
+    // zero fill outside -- used when the layout meets the TMA alignment rules
+    CUtensorMap umap;
+    std::memset(&umap, 0, sizeof(umap));
+    RunArgs b = a;
+    b.use_tma = 0;
+    static auto encode = []() -> decltype(&cuTensorMapEncodeTiled) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+                cudaSuccess || q != cudaDriverEntryPointSuccess)
+            return nullptr;
+        return reinterpret_cast<decltype(&cuTensorMapEncodeTiled)>(fn);
+    }();
+    const bool aligned = (reinterpret_cast<uintptr_t>(a.U) % 16 == 0) && (a.ldu % 2 == 0) &&
+                         a.ldu >= 16 && a.n_steps >= 1 && a.n_steps < (1L << 31) &&
+                         a.ldu < (1L << 31) && !std::getenv("FRAQ_NO_TMA");
+    if (encode && aligned && nwg == D_MAXWG) {
+        const cuuint64_t dims[2] = {(cuuint64_t)a.ldu, (cuuint64_t)a.n_steps};
+        const cuuint64_t strides[1] = {(cuuint64_t)a.ldu * 8};
+        const cuuint32_t box[2] = {16, (cuuint32_t)D_TC}, estr[2] = {1, 1};
+        if (encode(&umap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(a.U), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+            b.use_tma = 1;
+    }
+    run3_kernel<<<grid, nwg * 32, smem, s>>>(b, umap);
     FRAQ_LAUNCH_CHECK();
 }
 
