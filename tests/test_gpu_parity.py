@@ -426,3 +426,26 @@ def test_run_blocked_scheme_variant(fraq, orc, sbd, np_):
     ok = ~np.isnan(D_ref)
     scale = np.maximum(np.abs(D_ref[ok]), tau ** (-g))
     assert np.max(np.abs(D[ok] - D_ref[ok]) / scale) <= 1e-12
+
+
+def test_multi_history_many_ragged_groups(fraq, orc):
+    """Many DOF groups of ragged sizes (1, 3, 16, 17, 33, ...) with different kernels (BE sizes
+    differ per group) in one device state: K5d tasks straddle no group boundary, leading
+    dimensions are padded, and every group equals its own reference history."""
+    rng = np.random.default_rng(77)
+    dims = [1, 3, 16, 17, 33, 5, 64, 2]
+    os_ = [orc.build_be_kernel(0.2 + 0.08 * i, 1e-3, 20 + 13 * i) for i in range(len(dims))]
+    ks = [kernel_from_oracle(fraq, o) for o in os_]
+    h = fraq.MultiHistory(ks, dims)
+    n = 150
+    U = rng.uniform(-1, 1, (n, sum(dims)))
+    D = np.array(h.run(U), dtype=float)
+    assert h.last_path == 3
+    c = 0
+    for o, dm in zip(os_, dims):
+        D_ref = orc.hist_run(o, U[:, c:c + dm])
+        Dg = D[:, c:c + dm]
+        ok = ~np.isnan(D_ref)
+        assert np.array_equal(np.isnan(Dg), ~ok)
+        assert np.max(np.abs(Dg[ok] - D_ref[ok])) <= 1e-12 * max(1.0, np.max(np.abs(D_ref[ok])))
+        c += dm
