@@ -601,13 +601,16 @@ void build_kernel_auto_dev(fraq_ctx c, bool sbd, int n, const double* gammas, do
         if (sbd && h < 8) h = 8;
         H = std::max(H, h);
     }
-    const long L = H + 1;
-    // classical tables for every exponent up to its own horizon (shared stride L)
+    // classical tables for every exponent (shared stride L).  They also supply the exact head
+    // d_0 .. d_(n_head-1), and the initial SBD head (15 / 17) may exceed a short horizon: the
+    // tables reach at least index 17 (heads only grow while below the horizon).
+    const long HT = std::max<long>(H, 17);
+    const long L = HT + 1;
     DevBuf<double> tables((size_t)n * L);
     {
         std::vector<double> gs(gammas, gammas + n);
         // all horizons padded to the max: the chains are exact prefixes
-        weights_batch(c, sbd, gs, tau, H, tables.p);
+        weights_batch(c, sbd, gs, tau, HT, tables.p);
     }
     std::vector<int> np(n, sbd ? 41 : 64), done(n, 0), head(n, 0);
     std::vector<double> tol(n);

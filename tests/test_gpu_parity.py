@@ -449,3 +449,28 @@ def test_multi_history_many_ragged_groups(fraq, orc):
         assert np.array_equal(np.isnan(Dg), ~ok)
         assert np.max(np.abs(Dg[ok] - D_ref[ok])) <= 1e-12 * max(1.0, np.max(np.abs(D_ref[ok])))
         c += dm
+
+
+@pytest.mark.parametrize("H", [8, 12, 16])
+def test_auto_sbd_head_longer_than_horizon(fraq, orc, H):
+    """Short horizons: the initial SBD head (15 / 17) exceeds horizon + 1, and every head entry
+    must still be the exact weight d_i (the reference builds the head from sbd_weights up to
+    n_head - 1, fast_kernel.cpp:78-124, whatever the horizon).  Regression: the batched device
+    sizer used to take the head from the horizon-long sizing tables."""
+    tau = 1.0 / 4096
+    for g in (0.3, 0.5, 0.7):
+        b = fraq.KernelBudget(horizon=H, eps_tol=1e-12)
+        k = fraq.build_sbd_kernel_auto(g, tau, b)
+        o = orc.build_kernel_auto(True, g, tau, H)
+        assert k.n_head == o.n_head
+        assert np.allclose(np.array(k.head), np.array(o.head), rtol=1e-15, atol=0)
+    # the batched path (several exponents in one sizing pass), as the FFPE steppers use it
+    specs = [fraq.ProblemSpec(alpha1=0.2 + 0.1 * i, alpha2=0.5, coupling_a=1.0, grid_m=15,
+                              t_final=0.1, n_steps=H) for i in range(3)]
+    kc = fraq.KernelConfig()
+    kc.solver = fraq.SOLVER_MODAL
+    outs = fraq.run_batch(specs, fraq.Scheme.FastSBD, kc)
+    for s, o in zip(specs, outs):
+        g1, g2, _, _ = orc.run(s.alpha1, s.alpha2, 1.0, 15, 0.1, H, "FastSBD", "poly_sin")
+        assert rel_linf(o.final_state.g1, g1) <= 1e-10
+        assert rel_linf(o.final_state.g2, g2) <= 1e-10
