@@ -792,7 +792,6 @@ void HistDevice::build(fraq_ctx c, int n_groups, const fraq_kernel_t* const* ks,
     up(head.p, hh.data(), hh.size() * sizeof(double));
     zero(c);
     FRAQ_CUDA(cudaStreamSynchronize(c->stream));
-    if (!tables_only) k5t_prepare(*this);  // TMA-streamed per-level step when the layout allows
 }
 
 void HistDevice::zero(fraq_ctx c) {
@@ -802,10 +801,6 @@ void HistDevice::zero(fraq_ctx c) {
 
 void HistDevice::launch_step(fraq_ctx c, const StepArgs& a) {
     if (n_tiles == 0) return;
-    if (k5t_ok) {  // TMA-streamed step (history_tma.cu)
-        k5t_launch(c, *this, a);
-        return;
-    }
     if (lanes == 32)
         step_kernel<32, 4><<<n_tiles, 128, 0, c->stream>>>(a);
     else

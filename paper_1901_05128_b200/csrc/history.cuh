@@ -90,11 +90,6 @@ struct HistDevice {
     // DMMA fragment tables for K5d (built on first use): per group kFragDoubles doubles
     DevBuf<double> frag;
     bool frag_built = false;
-    // K5t (history_tma.cu): per-group tensor maps over the state and 32-DOF warp tiles
-    std::vector<CUtensorMap> k5t_maps;  // 64-byte aligned (cuTensorMapEncodeTiled requires it)
-    DevBuf<int2> k5t_tiles;
-    int n_k5t_tiles = 0;
-    bool k5t_ok = false;
 
     void build(fraq_ctx c, int n_groups, const fraq_kernel_t* const* ks, const long* dims,
                bool tables_only = false);
@@ -112,8 +107,6 @@ struct K13Inst {
     const double* corr[2];  // SBD correction sequence corr[n-4], nullable for BE
     int J[2], L[2];
 };
-bool k5t_prepare(HistDevice& d);
-void k5t_launch(fraq_ctx c, const HistDevice& d, const StepArgs& a);
 bool k13_supported(int maxJ, int minL, int maxL);
 // Setup (node fragment tables, combined weights) and launch are split so that the loop timers
 // see only the stepping.
