@@ -129,7 +129,9 @@ __global__ void k13_tables_kernel(const K13TabSrc* src, int Jp, int delta, doubl
 // warps + 1 solver warp per CTA, one CTA per SM (the register file is split per SM sub-partition:
 // 9 warps leave ~170 registers per thread for the state fragments and the table operands).
 template <int RB, int NT>
-__global__ void __launch_bounds__(320, 1) k13_kernel(K13Args A) {
+// RB = 2 (J <= 256; ~90 KB of shared memory): two CTAs per SM, so one CTA's solver phase
+// overlaps the other's GEMMs and each SM sub-partition runs 4 GEMM warps.
+__global__ void __launch_bounds__(320, RB == 2 ? 2 : 1) k13_kernel(K13Args A) {
     constexpr int MODES = 8 * RB;
     extern __shared__ double ksm[];
     const int nwg = A.nwg, nwf = A.nwf, TS = A.TS, Jp = A.Jp;
@@ -252,12 +254,8 @@ __global__ void __launch_bounds__(320, 1) k13_kernel(K13Args A) {
             const double M11 = m11 * idet, M12 = m12 * idet, M21 = m21 * idet, M22 = m22 * idet;
             const double g10 = g0s[d], g20 = g0s[MODES + d];
             double gp1 = g10, gp2 = g20, gpp1 = 0.0, gpp2 = 0.0;
-            double c1[8], c2[8];  // in-block weights c_1..c_7
-#pragma unroll
-            for (int m = 1; m < 8; ++m) {
-                c1[m] = cwt[0][m];
-                c2[m] = cwt[1][m];
-            }
+            const double* c1 = cwt[0];  // in-block weights c_1..c_7 (shared memory, broadcast)
+            const double* c2 = cwt[1];
             // correction prefetch (this warp's field): fragment row k = g (level n0 + g)
             const int Lsf = sf ? I.L[1] : I.L[0];
             const double* corr_f = sf ? I.corr[1] : I.corr[0];
