@@ -179,8 +179,8 @@ int fraq_hist_lagged(fraq_hist h, long depth, double* out, int mem);
 int fraq_hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, long ldd,
                   int mem);
 /* Which kernel the last fraq_hist_run used: 0 = per-level K5 (calls under 4 levels, or more than
- * 512 nodes), 1 = K5b (warp-per-4-DOF blocked, FRAQ_K5B=1), 2 = K5c (lane-per-DOF DFMA blocked:
- * FRAQ_K5C=1, or head windows over 32 levels), 3 = K5d (DMMA block GEMMs, default). */
+ * 512 nodes), 2 = K5c (lane-per-DOF DFMA blocked: FRAQ_K5C=1, or head windows over 32 levels),
+ * 3 = K5d (DMMA block GEMMs, default).  (1 was the retired warp-per-4-DOF kernel K5b.) */
 int fraq_hist_last_path(fraq_hist h);
 
 /* ---------------------------------------------------------------- direct CQ (K10)

@@ -4,9 +4,9 @@
 //                      append into the lag ring and the readout (node sum + exact head window).
 //                      One HBM pass over the state per level.  BeHistory/SbdHistory
 //                      advance/append/history_sum/derivative, fast_kernel.cpp:268-409.
-// K5b (run_kernel)     temporally blocked standalone evaluation over many levels: each warp owns
-//                      4 DOFs x all nodes in registers for the whole call, so the state never
-//                      leaves the SM; inputs stream in, derivatives stream out.  fp64-FMA bound.
+// K5c (run2_kernel)    temporally blocked evaluation, lane per DOF, DFMA (head windows over 32
+//                      levels); the default blocked path K5d (DMMA block GEMMs) is in
+//                      history_dmma.cu.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -188,257 +188,6 @@ __global__ void __launch_bounds__(LANES* S, 6) step_kernel(StepArgs A) {
     if (nv > 1) o[1] = acc.y;
     if (nv > 2) o[2] = acc.z;
     if (nv > 3) o[3] = acc.w;
-}
-
-// ----------------------------------------------------------------------------------------- K5b
-// Warp task: 4 DOFs of one group, all levels of the call.  Lane l owns nodes j = l + 32 p,
-// p < P; the state is kept as z_j = y_j / f_j so one level is z <- r z + u_lag (one FMA) and the
-// readout is sum_j f_j z_j (one FMA).  Per-step node sums: 4-value warp reduce-scatter.
-constexpr int RUN_Q = 4;        // DOFs per warp
-constexpr int RUN_TC = 32;      // levels per staged chunk
-constexpr int RUN_LMAX = 64;    // max lag supported on this path
-constexpr int RUN_WARPS = 4;    // warps per CTA (independent tasks)
-
-struct RunSmem {
-    double X[RUN_LMAX + RUN_TC][RUN_Q];
-    double F[RUN_TC][RUN_Q];
-    double Dv[RUN_TC][RUN_Q];
-    double hd[RUN_LMAX];
-};
-
-template <int P>
-__global__ void __launch_bounds__(RUN_WARPS * 32, 2) run_kernel(RunArgs A) {
-    __shared__ RunSmem sm_all[RUN_WARPS];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    RunSmem& sm = sm_all[warp];
-    for (;;) {
-        int task = 0;
-        if (lane == 0) task = atomicAdd(A.counter, 1);
-        task = __shfl_sync(0xffffffffu, task, 0);
-        if (task >= A.n_tasks) return;
-        const int2 tk = A.tasks[task];
-        const GroupDev G = A.groups[tk.x];
-        const int m0 = tk.y;
-        const int L = G.L, J = G.J;
-        const long ld = G.ld;
-        // coefficients and initial state
-        double r[P], f[P], z[P][RUN_Q];
-#pragma unroll
-        for (int p = 0; p < P; ++p) {
-            const int j = lane + 32 * p;
-            if (j < J) {
-                r[p] = A.cr[G.co_off + j];
-                f[p] = A.cf[G.co_off + j];
-                const double* y = A.state + G.st_off + j * ld + m0;
-#pragma unroll
-                for (int q = 0; q < RUN_Q; ++q) z[p][q] = (m0 + q < G.dim) ? y[q] / f[p] : 0.0;
-            } else {
-                r[p] = 0.0;
-                f[p] = 0.0;
-#pragma unroll
-                for (int q = 0; q < RUN_Q; ++q) z[p][q] = 0.0;
-            }
-        }
-        for (int i = lane; i < L; i += 32) sm.hd[i] = A.head[G.hd_off + i];
-        // history window: X(k) for k in [A0 - L, A0 - 1] from the ring, rows RUN_LMAX - L ..
-        for (int idx = lane; idx < L * RUN_Q; idx += 32) {
-            const int row = idx / RUN_Q, q = idx % RUN_Q;
-            const long k = A.A0 - L + row;
-            double x = 0.0;
-            if (k >= 0 && m0 + q < G.dim) x = A.ring[G.ring_off + (k % L) * ld + m0 + q];
-            sm.X[RUN_LMAX - L + row][q] = x;
-        }
-        const double* Ubase = A.U + G.dof0 + m0;
-        // prefetch chunk 0 (lane t holds row t)
-        double pre[RUN_Q];
-        auto load_rows = [&](long c0) {
-            const long t = c0 + lane;
-#pragma unroll
-            for (int q = 0; q < RUN_Q; ++q)
-                pre[q] = (t < A.n_steps && m0 + q < G.dim) ? Ubase[t * A.ldu + q] : 0.0;
-        };
-        load_rows(0);
-        for (long c0 = 0; c0 < A.n_steps; c0 += RUN_TC) {
-            __syncwarp();
-#pragma unroll
-            for (int q = 0; q < RUN_Q; ++q) sm.X[RUN_LMAX + lane][q] = pre[q];
-            if (c0 + RUN_TC < A.n_steps) load_rows(c0 + RUN_TC);
-            __syncwarp();
-            // exact head window F[t][q] = sum_{i<=top(n)} h_i X(n-i), n = A0 + c0 + t
-            {
-                const int t = lane;
-                const long n = A.A0 + c0 + t;
-                long top;
-                if (!G.sbd)
-                    top = 1;
-                else
-                    top = min((long)L - 1, n - A.lo);
-                double fq[RUN_Q] = {0.0, 0.0, 0.0, 0.0};
-                for (long i = 0; i <= top; ++i) {
-                    const double h = sm.hd[i];
-#pragma unroll
-                    for (int q = 0; q < RUN_Q; ++q)
-                        fq[q] = fma(h, sm.X[RUN_LMAX + t - i][q], fq[q]);
-                }
-#pragma unroll
-                for (int q = 0; q < RUN_Q; ++q) sm.F[t][q] = fq[q];
-            }
-            __syncwarp();
-            const int tmax = (int)min((long)RUN_TC, A.n_steps - c0);
-            int t = 0;
-            // single level (odd tails and the very first push of a fresh history, which does not
-            // advance: fast_kernel.cpp:297-300)
-            auto one_level = [&](int tt) {
-                const long n = A.A0 + c0 + tt;
-                if (n >= 1) {  // advance to level n; feed X(n - L) when n - L >= lo
-                    const bool feed = n - L >= A.lo;
-                    double v[RUN_Q];
-#pragma unroll
-                    for (int q = 0; q < RUN_Q; ++q) v[q] = feed ? sm.X[RUN_LMAX + tt - L][q] : 0.0;
-#pragma unroll
-                    for (int p = 0; p < P; ++p)
-#pragma unroll
-                        for (int q = 0; q < RUN_Q; ++q) z[p][q] = fma(r[p], z[p][q], v[q]);
-                }
-                double sq[RUN_Q] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-                for (int p = 0; p < P; ++p)
-#pragma unroll
-                    for (int q = 0; q < RUN_Q; ++q) sq[q] = fma(f[p], z[p][q], sq[q]);
-                // reduce-scatter 4 values over 32 lanes -> lanes 8q..8q+7 hold DOF q's total
-                const bool up = lane & 16;
-                double a0 = up ? sq[2] : sq[0], a1 = up ? sq[3] : sq[1];
-                const double b0 = up ? sq[0] : sq[2], b1 = up ? sq[1] : sq[3];
-                a0 += __shfl_xor_sync(0xffffffffu, b0, 16);
-                a1 += __shfl_xor_sync(0xffffffffu, b1, 16);
-                const bool up8 = lane & 8;
-                double cval = up8 ? a1 : a0;
-                const double dsend = up8 ? a0 : a1;
-                cval += __shfl_xor_sync(0xffffffffu, dsend, 8);
-                cval += __shfl_xor_sync(0xffffffffu, cval, 4);
-                cval += __shfl_xor_sync(0xffffffffu, cval, 2);
-                cval += __shfl_xor_sync(0xffffffffu, cval, 1);
-                if ((lane & 7) == 0) {
-                    const int q = lane >> 3;
-                    const bool valid = G.sbd ? true : (n >= 1);
-                    sm.Dv[tt][q] = valid ? cval + sm.F[tt][q] : __longlong_as_double(0x7ff8000000000000LL);
-                }
-            };
-            if (A.A0 + c0 == 0) {  // level 0 of a fresh history: no advance
-                one_level(0);
-                t = 1;
-            }
-            // main loop: two levels per iteration (all advance).  Both node sums are reduced
-            // together (8-value reduce-scatter, 9 fp64 shuffles per pair) so the shuffle latency
-            // of one pair overlaps the FMAs of the next in the other warps and in this one.
-            for (; t + 1 < tmax; t += 2) {
-                const long n = A.A0 + c0 + t;
-                const bool feed0 = n - L >= A.lo, feed1 = n + 1 - L >= A.lo;
-                double v0[RUN_Q], v1[RUN_Q];
-#pragma unroll
-                for (int q = 0; q < RUN_Q; ++q) {
-                    v0[q] = feed0 ? sm.X[RUN_LMAX + t - L][q] : 0.0;
-                    v1[q] = feed1 ? sm.X[RUN_LMAX + t + 1 - L][q] : 0.0;
-                }
-                double s0[RUN_Q] = {0.0, 0.0, 0.0, 0.0}, s1[RUN_Q] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-                for (int p = 0; p < P; ++p)
-#pragma unroll
-                    for (int q = 0; q < RUN_Q; ++q) {
-                        const double z0 = fma(r[p], z[p][q], v0[q]);
-                        s0[q] = fma(f[p], z0, s0[q]);
-                        const double z1 = fma(r[p], z0, v1[q]);
-                        s1[q] = fma(f[p], z1, s1[q]);
-                        z[p][q] = z1;
-                    }
-                // value k = 4 t2 + q; after the cascade lane holds k = lane >> 2
-                const bool u16 = lane & 16;
-                double a[RUN_Q];
-#pragma unroll
-                for (int q = 0; q < RUN_Q; ++q) {
-                    const double keep = u16 ? s1[q] : s0[q];
-                    const double send = u16 ? s0[q] : s1[q];
-                    a[q] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-                }
-                const bool u8 = lane & 8;
-                double b[2];
-#pragma unroll
-                for (int i = 0; i < 2; ++i) {
-                    const double keep = u8 ? a[i + 2] : a[i];
-                    const double send = u8 ? a[i] : a[i + 2];
-                    b[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-                }
-                const bool u4 = lane & 4;
-                double cval = (u4 ? b[1] : b[0]) + __shfl_xor_sync(0xffffffffu, u4 ? b[0] : b[1], 4);
-                cval += __shfl_xor_sync(0xffffffffu, cval, 2);
-                cval += __shfl_xor_sync(0xffffffffu, cval, 1);
-                if ((lane & 3) == 0) {
-                    const int k = lane >> 2, tt = t + (k >> 2), q = k & 3;
-                    sm.Dv[tt][q] = cval + sm.F[tt][q];
-                }
-            }
-            if (t < tmax) one_level(t);
-            __syncwarp();
-            if (A.D && lane < tmax) {
-                double* drow = A.D + (c0 + lane) * A.ldd + G.dof0 + m0;
-#pragma unroll
-                for (int q = 0; q < RUN_Q; ++q)
-                    if (m0 + q < G.dim) drow[q] = sm.Dv[lane][q];
-            }
-            // slide the window: the last L inputs (times A0+c0+tmax-L ..) move to rows
-            // RUN_LMAX-L .. RUN_LMAX-1; read everything before writing (ranges may overlap)
-            __syncwarp();
-            double tmp[RUN_LMAX * RUN_Q / 32];
-#pragma unroll
-            for (int it = 0; it < RUN_LMAX * RUN_Q / 32; ++it) {
-                const int idx = lane + 32 * it;
-                if (idx < L * RUN_Q) tmp[it] = sm.X[tmax + RUN_LMAX - L + idx / RUN_Q][idx % RUN_Q];
-            }
-            __syncwarp();
-#pragma unroll
-            for (int it = 0; it < RUN_LMAX * RUN_Q / 32; ++it) {
-                const int idx = lane + 32 * it;
-                if (idx < L * RUN_Q) sm.X[RUN_LMAX - L + idx / RUN_Q][idx % RUN_Q] = tmp[it];
-            }
-        }
-        // write back state (y = f z) and the ring (last L inputs)
-#pragma unroll
-        for (int p = 0; p < P; ++p) {
-            const int j = lane + 32 * p;
-            if (j < J) {
-                double* y = A.state + G.st_off + j * ld + m0;
-#pragma unroll
-                for (int q = 0; q < RUN_Q; ++q)
-                    if (m0 + q < G.dim) y[q] = f[p] * z[p][q];
-            }
-        }
-        __syncwarp();
-        const long A1 = A.A0 + A.n_steps;
-        for (int idx = lane; idx < L * RUN_Q; idx += 32) {
-            const int row = idx / RUN_Q, q = idx % RUN_Q;
-            const long k = A1 - L + row;
-            if (k >= 0 && m0 + q < G.dim)
-                A.ring[G.ring_off + (k % L) * ld + m0 + q] = sm.X[RUN_LMAX - L + row][q];
-        }
-        __syncwarp();
-    }
-}
-
-template <int P>
-void launch_run_p(const RunArgs& a, int grid, cudaStream_t s) {
-    run_kernel<P><<<grid, RUN_WARPS * 32, 0, s>>>(a);
-}
-
-void launch_run(int P, const RunArgs& a, int grid, cudaStream_t s) {
-    switch (P) {
-#define FRAQ_P(k) \
-    case k: launch_run_p<k>(a, grid, s); break;
-        FRAQ_P(1) FRAQ_P(2) FRAQ_P(3) FRAQ_P(4) FRAQ_P(5) FRAQ_P(6) FRAQ_P(7) FRAQ_P(8)
-        FRAQ_P(9) FRAQ_P(10) FRAQ_P(11) FRAQ_P(12) FRAQ_P(13) FRAQ_P(14) FRAQ_P(15) FRAQ_P(16)
-#undef FRAQ_P
-        default: fail(FRAQ_ERUNTIME, "run_kernel: unsupported node count");
-    }
-    FRAQ_LAUNCH_CHECK();
 }
 
 // ----------------------------------------------------------------------------------------- K5c
@@ -823,8 +572,6 @@ struct fraq_hist_s {
     DevBuf<double> stage;   // pending push value (device)
     DevBuf<double> outbuf;  // device output for host reads
     DevBuf<int> counter;
-    DevBuf<int2> run_tasks;
-    int n_run_tasks = 0;
     DevBuf<int2> run2_tasks;   // (group, first DOF of a 32-DOF tile) for K5c
     int n_run2_tasks = 0;
     DevBuf<int2> run3_tasks;   // (group, first DOF of a 16-DOF tile) for K5d
@@ -932,14 +679,6 @@ void hist_create(fraq_ctx c, int n_groups, const fraq_kernel_t* const* ks, const
         h->stage.alloc(std::max<long>(1, h->d.total_dim));
         h->outbuf.alloc(std::max<long>(1, h->d.total_dim));
         h->counter.alloc(1);
-        std::vector<int2> tasks;
-        for (int g = 0; g < n_groups; ++g)
-            for (int m0 = 0; m0 < h->d.groups_h[g].dim; m0 += RUN_Q) tasks.push_back(make_int2(g, m0));
-        h->n_run_tasks = (int)tasks.size();
-        h->run_tasks.alloc(std::max<size_t>(1, tasks.size()));
-        if (!tasks.empty())
-            FRAQ_CUDA(cudaMemcpy(h->run_tasks.p, tasks.data(), tasks.size() * sizeof(int2),
-                                 cudaMemcpyHostToDevice));
         std::vector<int2> t2;
         for (int g = 0; g < n_groups; ++g)
             for (int m0 = 0; m0 < h->d.groups_h[g].dim; m0 += 32) t2.push_back(make_int2(g, m0));
@@ -1044,7 +783,7 @@ namespace {
 
 bool blocked_ok(fraq_hist h) {
     if (!h->d.ztrick_ok) return false;
-    if (h->d.max_L > RUN_LMAX || h->d.max_J > 32 * 16) return false;
+    if (h->d.max_L > R2_LMAX || h->d.max_J > 32 * 16) return false;
     // pure push sequence: level == appended - 1 (or fresh)
     if (h->appended == 0) return h->level == 0;
     return h->level == h->appended - 1;
@@ -1053,11 +792,8 @@ bool blocked_ok(fraq_hist h) {
 void run_device(fraq_hist h, const double* U, long ldu, long n_steps, double* D, long ldd) {
     if (n_steps <= 0) return;
     if (blocked_ok(h) && n_steps >= 4) {
-        h->last_path = 1;
         RunArgs a{};
         a.groups = h->d.groups.p;
-        a.tasks = h->run_tasks.p;
-        a.n_tasks = h->n_run_tasks;
         a.counter = h->counter.p;
         a.state = h->d.state.p;
         a.ring = h->d.ring.p;
@@ -1073,9 +809,8 @@ void run_device(fraq_hist h, const double* U, long ldu, long n_steps, double* D,
         a.ldd = ldd;
         const int P = (h->d.max_J + 31) / 32;
         FRAQ_CUDA(cudaMemsetAsync(h->counter.p, 0, sizeof(int), h->ctx->stream));
-        static const bool legacy = std::getenv("FRAQ_K5B") != nullptr;
         static const bool k5c = std::getenv("FRAQ_K5C") != nullptr;
-        if (!legacy && !k5c && h->d.max_L <= run3_max_lag()) {
+        if (!k5c && h->d.max_L <= run3_max_lag()) {
             // K5d (DMMA block formulation), default
             h->last_path = 3;
             build_frag_tables(h->ctx, h->d);
@@ -1083,10 +818,6 @@ void run_device(fraq_hist h, const double* U, long ldu, long n_steps, double* D,
             a.n_tasks = h->n_run3_tasks;
             a.frag = h->d.frag.p;
             launch_run3(a, std::max(1, (h->d.max_J + 63) / 64), h->ctx->num_sms, h->ctx->stream);
-        } else if (legacy) {
-            const int grid = std::max(1, std::min((h->n_run_tasks + RUN_WARPS - 1) / RUN_WARPS,
-                                                  2 * h->ctx->num_sms));
-            launch_run(std::max(1, P), a, grid, h->ctx->stream);
         } else {
             h->last_path = 2;
             a.tasks = h->run2_tasks.p;
