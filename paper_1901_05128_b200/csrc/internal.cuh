@@ -5,6 +5,7 @@
 
 #include <cstdio>
 #include <stdexcept>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -34,8 +35,18 @@ void set_last_error(const std::string& m);
 
 #define FRAQ_LAUNCH_CHECK() FRAQ_CUDA(cudaGetLastError())
 
+// The library is thread-safe by serialisation: calls share a context's stream and setup scratch
+// buffers, so concurrent callers (the reference's run() is reentrant and releases the GIL; its
+// harness runs solves in worker threads) take turns.  One mutex per library (inline function,
+// not per template instance); recursive, since an observer callback may call back into the API.
+inline std::recursive_mutex& api_mutex() {
+    static std::recursive_mutex m;
+    return m;
+}
+
 template <class F>
 int guarded(F&& f) {
+    std::lock_guard<std::recursive_mutex> lock(api_mutex());
     try {
         f();
         return FRAQ_OK;

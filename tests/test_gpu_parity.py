@@ -474,3 +474,24 @@ def test_auto_sbd_head_longer_than_horizon(fraq, orc, H):
         g1, g2, _, _ = orc.run(s.alpha1, s.alpha2, 1.0, 15, 0.1, H, "FastSBD", "poly_sin")
         assert rel_linf(o.final_state.g1, g1) <= 1e-10
         assert rel_linf(o.final_state.g2, g2) <= 1e-10
+
+
+def test_concurrent_runs_from_threads(fraq):
+    """fraq.run releases the GIL (as the reference's binding does); solves issued from several
+    Python threads at once are serialised by the library and equal the sequential results."""
+    import threading
+    specs = [fraq.ProblemSpec(alpha1=0.2 + 0.15 * i, alpha2=0.6, coupling_a=1.0 - i,
+                              grid_m=63, t_final=0.5, n_steps=96) for i in range(4)]
+    seq = [fraq.run(s, fraq.Scheme.FastSBD) for s in specs]
+    out = [None] * 4
+
+    def work(i):
+        for _ in range(3):
+            out[i] = fraq.run(specs[i], fraq.Scheme.FastSBD)
+    th = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for a, b in zip(out, seq):
+        assert list(a.final_state.g1) == list(b.final_state.g1)
