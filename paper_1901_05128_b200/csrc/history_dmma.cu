@@ -35,6 +35,7 @@ namespace {
 constexpr int D_TC = 32;      // levels per staged chunk
 constexpr int D_TB = 8;       // levels per block (one GEMM pair)
 constexpr int D_LMAX = 32;    // max lag (longer head windows take K5c)
+constexpr int D_RING = D_LMAX + 2 * D_TC;  // input ring: lag chunk, current chunk, next chunk
 constexpr int D_NT = 8;       // node tiles (8 nodes) per warp = 64 nodes
 constexpr int D_MAXWG = 8;    // max warps per DOF group (512 nodes)
 
@@ -131,13 +132,21 @@ __global__ void frag_tables_kernel(const GroupDev* groups, const double* cr, con
     }
 }
 
+// Input rows live in a ring of three 32-level segments (call-relative level n at row n mod 96):
+// the lag chunk, the current chunk and the chunk TMA is landing, so no rows are ever moved.
 struct DSmem {
-    double X[D_LMAX + D_TC][16];  // lag rows + the current chunk (row n at D_LMAX + n - c0)
-    double Xn[D_TC][16];          // TMA landing tile of the next chunk (128-byte aligned)
+    double X[D_RING][16];         // 128-byte aligned: TMA lands a 16-DOF x 32-level box per segment
     double hd[D_LMAX];
     double hf[16][32];            // head-window Toeplitz as DMMA B fragments (DMMA FIR)
-    unsigned long long mbar;      // completion barrier of the Xn tile
+    unsigned long long mbar[2];   // completion barriers, chunk k on mbar[k & 1]
 };
+__device__ __forceinline__ int xrow(long n) {  // ring row of call-relative level n >= -D_RING
+    return (int)((n + D_RING) % D_RING);
+}
+__device__ __forceinline__ int xwrap(int r) {  // r in [-D_RING, 2 D_RING) -> ring row (32-bit)
+    r = r < 0 ? r + D_RING : r;
+    return r >= D_RING ? r - D_RING : r;
+}
 
 // CTA = one 16-DOF group x all nodes: nwg warps (64 nodes each), 2 CTAs resident per SM so one
 // CTA's barrier / reduction phase overlaps the other's DMMA phase.  Within a CTA the cross-warp
@@ -208,8 +217,10 @@ __global__ void __launch_bounds__(256, 2)
             const long k = A.A0 - L + row;
             double x = 0.0;
             if (k >= 0 && tk.y + d < G.dim) x = A.ring[G.ring_off + (k % L) * ld + tk.y + d];
-            S.X[D_LMAX - L + row][d] = x;
+            S.X[D_RING - L + row][d] = x;
         }
+        // (segment 2 is written through the generic proxy here and by TMA two chunks later)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
         if (tid == 0) s_group = tk.x;
         const double* Ub = A.U + G.dof0 + tk.y;
@@ -235,11 +246,11 @@ __global__ void __launch_bounds__(256, 2)
             }
         };
         const bool tma = A.use_tma && blockDim.x == 256;
-        unsigned tphase = 0;
         if (tma) {
             if (tid == 0) {
-                mbar_init(&S.mbar);
-                tma_tile(&umap, &S.Xn[0][0], &S.mbar, (int)(G.dof0 + tk.y), 0, D_TC * 16 * 8);
+                mbar_init(&S.mbar[0]);
+                mbar_init(&S.mbar[1]);
+                tma_tile(&umap, &S.X[0][0], &S.mbar[0], (int)(G.dof0 + tk.y), 0, D_TC * 16 * 8);
             }
         } else if (blockDim.x == 256) {
             prefetch(0);
@@ -271,8 +282,11 @@ __global__ void __launch_bounds__(256, 2)
                     // head sum from the staged rows, reference tap rule and order
                     const long n = pn0 + k;
                     const long top = G.sbd ? min((long)L - 1, n - A.lo) : 1;
-                    const int tt = (int)((prow + k) % D_TC);
-                    for (long i = 0; i <= top; ++i) fir = fma(S.hd[i], S.X[D_LMAX + tt - i][d], fir);
+                    int xr = xrow(prow + k);
+                    for (long i = 0; i <= top; ++i) {
+                        fir = fma(S.hd[i], S.X[xr][d], fir);
+                        xr = xr ? xr - 1 : D_RING - 1;
+                    }
                 }
                 const bool valid = G.sbd ? true : (pn0 + k >= 1);
                 if (Db && tk.y + d < G.dim)
@@ -285,39 +299,40 @@ __global__ void __launch_bounds__(256, 2)
             const bool ok = G.sbd ? (n0 - (L - 1) >= A.lo) : (n0 >= 1);
             return kmax == D_TB && n0 >= 1 && !special && ok;
         };
-        int buf = 0, last_tmax = 0;
+        int buf = 0;
         bool pending = false;
-        for (long c0 = 0; c0 < A.n_steps; c0 += D_TC) {
+        unsigned ck = 0;  // chunk counter (mbarrier slot and phase)
+        int seg = 0;      // this chunk's ring segment (first row)
+        for (long c0 = 0; c0 < A.n_steps; c0 += D_TC, ++ck, seg = xwrap(seg + D_TC)) {
             const int tmax = (int)min((long)D_TC, A.n_steps - c0);
+            // (everyone is done with the previous chunk, whose reduction may read the lag segment)
             __syncthreads();
             if (tma) {
-                // the chunk's tile landed (TMA, zero-filled past the ends): move it into the window
-                mbar_wait(&S.mbar, tphase);
-                tphase ^= 1;
+                // next chunk's tile into the segment two chunks back (free after the barrier)
+                if (tid == 0 && c0 + D_TC < A.n_steps)
+                    tma_tile(&umap, &S.X[xwrap(seg + D_TC)][0], &S.mbar[(ck + 1) & 1],
+                             (int)(G.dof0 + tk.y), (int)(c0 + D_TC), D_TC * 16 * 8);
+                // this chunk's tile landed (TMA, zero-filled past the ends of U); the mbarrier
+                // completion makes it visible to every waiting thread
+                mbar_wait(&S.mbar[ck & 1], (ck >> 1) & 1);
+            } else {
+                if (blockDim.x == 256) {
 #pragma unroll
-                for (int i = 0; i < 2; ++i) {
-                    const int row = prow + 16 * i;
-                    S.X[D_LMAX + row][pd] = plive ? S.Xn[row][pd] : 0.0;
+                    for (int i = 0; i < 2; ++i) {
+                        const int row = prow + 16 * i;
+                        if (row < D_TC) S.X[seg + row][pd] = pre[i];
+                    }
+                    if (c0 + D_TC < A.n_steps) prefetch(c0 + D_TC);
+                } else {  // fewer than 8 warps: direct loads (no prefetch)
+                    for (int idx = tid; idx < D_TC * 16; idx += blockDim.x) {
+                        const int row = idx >> 4, d = idx & 15;
+                        const long tt = c0 + row;
+                        S.X[seg + row][d] =
+                            (tt < A.n_steps && tk.y + d < G.dim) ? Ub[tt * A.ldu + d] : 0.0;
+                    }
                 }
-            } else if (blockDim.x == 256) {
-#pragma unroll
-                for (int i = 0; i < 2; ++i) {
-                    const int row = prow + 16 * i;
-                    if (row < D_TC) S.X[D_LMAX + row][pd] = pre[i];
-                }
-                if (c0 + D_TC < A.n_steps) prefetch(c0 + D_TC);
-            } else {  // fewer than 8 warps: direct loads (no prefetch)
-                for (int idx = tid; idx < D_TC * 16; idx += blockDim.x) {
-                    const int row = idx >> 4, d = idx & 15;
-                    const long tt = c0 + row;
-                    S.X[D_LMAX + row][d] =
-                        (tt < A.n_steps && tk.y + d < G.dim) ? Ub[tt * A.ldu + d] : 0.0;
-                }
+                __syncthreads();
             }
-            __syncthreads();
-            if (tma && tid == 0 && c0 + D_TC < A.n_steps)  // Xn is free again: next chunk's tile
-                tma_tile(&umap, &S.Xn[0][0], &S.mbar, (int)(G.dof0 + tk.y), (int)(c0 + D_TC),
-                         D_TC * 16 * 8);
             // (head window: DMMA segment of the readout, or per output in reduce_pair)
             auto do_block = [&](int t0, int slot, bool mid_reduce) {
                 const long n0 = A.A0 + c0 + t0;
@@ -326,45 +341,45 @@ __global__ void __launch_bounds__(256, 2)
                 const bool special = A.lo == 1 && n0 <= L && L < n0 + D_TB;
                 if (kmax == D_TB && n0 >= 1 && !special) {
                     // ---- readout GEMM from the block-start state + local Toeplitz
-                    double sacc[2][2][2];
+                    // one accumulator chain per row block: 16+ dependent DMMAs at 26 cycles each
+                    // stay well inside a warp's share of the pipe (4+ warps per SMSP)
+                    double sacc[2][2];
 #pragma unroll
-                    for (int rb = 0; rb < 2; ++rb)
-#pragma unroll
-                        for (int p = 0; p < 2; ++p) sacc[rb][p][0] = sacc[rb][p][1] = 0.0;
+                    for (int rb = 0; rb < 2; ++rb) sacc[rb][0] = sacc[rb][1] = 0.0;
 #pragma unroll
                     for (int ntl = 0; ntl < D_NT; ++ntl)
 #pragma unroll
                         for (int e = 0; e < 2; ++e) {
                             const double b = cw[(ntl * 2 + e) * 32];
 #pragma unroll
-                            for (int rb = 0; rb < 2; ++rb) dmma(sacc[rb][ntl & 1], Y[rb][ntl][e], b);
+                            for (int rb = 0; rb < 2; ++rb) dmma(sacc[rb], Y[rb][ntl][e], b);
                         }
                     double vf[2][2];
 #pragma unroll
                     for (int rb = 0; rb < 2; ++rb)
 #pragma unroll
                         for (int h = 0; h < 2; ++h)
-                            vf[rb][h] = S.X[D_LMAX + t0 + 4 * h + t - L][8 * rb + g];
+                            vf[rb][h] = S.X[xwrap(seg + t0 + 4 * h + t - L)][8 * rb + g];
                     // local Toeplitz: 4 DMMAs (rb, h) spread over warps 0..3 of the CTA
                     for (int w4 = sl; w4 < 4; w4 += nwg) {  // (fewer than 4 warps: several each)
                         const int hl = w4 & 1;
                         const double b = Wfr[hl * 32 + lane];
                         if (w4 == 0)
-                            dmma(sacc[0][1], vf[0][0], b);
+                            dmma(sacc[0], vf[0][0], b);
                         else if (w4 == 1)
-                            dmma(sacc[0][1], vf[0][1], b);
+                            dmma(sacc[0], vf[0][1], b);
                         else if (w4 == 2)
-                            dmma(sacc[1][1], vf[1][0], b);
+                            dmma(sacc[1], vf[1][0], b);
                         else
-                            dmma(sacc[1][1], vf[1][1], b);
+                            dmma(sacc[1], vf[1][1], b);
                     }
                     // head-window FIR: warp w < nkk adds k-step w for both row blocks
                     if (dfir_block(n0, kmax))
                         for (int kk = sl; kk < nkk; kk += nwg) {  // (fewer warps: several each)
                             const double b = S.hf[kk][lane];
-                            const int xr = D_LMAX + t0 + 8 - KW + 4 * kk + t;
-                            dmma(sacc[0][1], S.X[xr][g], b);
-                            dmma(sacc[1][1], S.X[xr][8 + g], b);
+                            const int xr = xwrap(seg + t0 + 8 - KW + 4 * kk + t);
+                            dmma(sacc[0], S.X[xr][g], b);
+                            dmma(sacc[1], S.X[xr][8 + g], b);
                         }
                     // deferred reduction of the previous pair: its LDS / DADD / STG latency
                     // overlaps the readout DMMAs just issued (asynchronous tensor pipe)
@@ -388,8 +403,8 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
                     for (int rb = 0; rb < 2; ++rb) {
                         // [level][DOF] layout: the reduction reads consecutive DOFs (no conflicts)
-                        pw[(2 * t) * 16 + 8 * rb + g] = sacc[rb][0][0] + sacc[rb][1][0];
-                        pw[(2 * t + 1) * 16 + 8 * rb + g] = sacc[rb][0][1] + sacc[rb][1][1];
+                        pw[(2 * t) * 16 + 8 * rb + g] = sacc[rb][0];
+                        pw[(2 * t + 1) * 16 + 8 * rb + g] = sacc[rb][1];
                     }
                 } else {
                     if (mid_reduce) reduce_pair();
@@ -401,7 +416,7 @@ __global__ void __launch_bounds__(256, 2)
                         double ps[2] = {0.0, 0.0};
 #pragma unroll
                         for (int rb = 0; rb < 2; ++rb) {
-                            const double v = feed ? S.X[D_LMAX + t0 + k - L][8 * rb + g] : 0.0;
+                            const double v = feed ? S.X[xwrap(seg + t0 + k - L)][8 * rb + g] : 0.0;
 #pragma unroll
                             for (int ntl = 0; ntl < D_NT; ++ntl)
 #pragma unroll
@@ -447,23 +462,14 @@ __global__ void __launch_bounds__(256, 2)
                 pending = true;
                 buf ^= 1;
             }
-            if (pending) {  // the chunk's last pair (S.X is rewritten next chunk)
+            // the chunk's last pair: its reduction reads S.X only for blocks outside the DMMA
+            // head window; otherwise it is deferred behind the next chunk's first readout DMMAs
+            if (pending && !(p_dfir0 && (p_kmax1 == 0 || p_dfir1) && c0 + D_TC < A.n_steps)) {
                 reduce_pair();
                 pending = false;
             }
-            last_tmax = tmax;
-            if (c0 + D_TC < A.n_steps) {
-                // slide (full chunk): rows R2_LMAX + 32 - L .. -> R2_LMAX - L .. (32-row phases;
-                // the pending reduction reads F and the partials, not X)
-                for (int base = 0; base < L; base += D_TC) {
-                    if (base) __syncthreads();
-                    for (int idx = tid; idx < D_TC * 16; idx += blockDim.x) {
-                        const int r = base + (idx >> 4);
-                        if (r < L) S.X[D_LMAX - L + r][idx & 15] = S.X[D_LMAX - L + r + D_TC][idx & 15];
-                    }
-                }
-            }
         }
+        if (pending) reduce_pair();  // (deferred past the last chunk)
         // write back the state and the ring
 #pragma unroll
         for (int rb = 0; rb < 2; ++rb) {
@@ -482,7 +488,7 @@ __global__ void __launch_bounds__(256, 2)
             const int row = idx >> 4, d = idx & 15;
             const long k = A1 - L + row;
             if (k >= 0 && tk.y + d < G.dim)
-                A.ring[G.ring_off + (k % L) * ld + tk.y + d] = S.X[D_LMAX + last_tmax - L + row][d];
+                A.ring[G.ring_off + (k % L) * ld + tk.y + d] = S.X[xrow(A.n_steps - L + row)][d];
         }
     }
 }

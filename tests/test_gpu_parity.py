@@ -284,6 +284,40 @@ def test_multi_group_history(fraq, orc):
     assert rel_linf(D, np.concatenate([D1, D2], axis=1)) <= 1e-12
 
 
+@pytest.mark.parametrize("sbd", [False, True])
+def test_blocked_input_staging_tma_and_registers(fraq, orc, sbd, monkeypatch):
+    """K5d input staging: TMA tiles into the three-segment ring (even leading dimension, 512-node
+    groups) and the register-staged fallback (FRAQ_NO_TMA) give identical results, equal to the
+    reference history.  Two groups of 20 and 28 DOFs: 16-DOF tiles straddle the group boundary
+    (neighbour columns are loaded but never reach live outputs) and the end of U (zero fill).
+    Calls of 300, 37 and 95 levels cover partial chunks and the ring wrap."""
+    rng = np.random.default_rng(41 + sbd)
+    if sbd:
+        o1 = orc.build_sbd_kernel(0.7, 1e-3, 256, 256, 17)
+        o2 = orc.build_sbd_kernel(0.3, 1e-3, 250, 256, 15)
+    else:
+        o1 = orc.build_be_kernel(0.7, 1e-3, 512)
+        o2 = orc.build_be_kernel(0.3, 1e-3, 480)
+    k1, k2 = kernel_from_oracle(fraq, o1), kernel_from_oracle(fraq, o2)
+    U = rng.uniform(-1, 1, (432, 48))
+    ref = np.concatenate([orc.hist_run(o1, U[:, :20]), orc.hist_run(o2, U[:, 20:])], axis=1)
+    outs = []
+    for no_tma in (False, True):
+        if no_tma:
+            monkeypatch.setenv("FRAQ_NO_TMA", "1")
+        else:
+            monkeypatch.delenv("FRAQ_NO_TMA", raising=False)
+        h = fraq.MultiHistory([k1, k2], [20, 28])
+        D = np.concatenate([h.run(U[:300]), h.run(U[300:337]), h.run(U[337:])])
+        assert h.last_path == 3
+        outs.append(D)
+    assert np.array_equal(outs[0], outs[1], equal_nan=True)
+    assert np.array_equal(np.isnan(outs[0]), np.isnan(ref))
+    ok = ~np.isnan(ref)
+    scale = np.maximum(np.abs(ref[ok]), 1e-3 ** -0.7)
+    assert np.max(np.abs(outs[0][ok] - ref[ok]) / scale) <= 1e-12
+
+
 # ------------------------------------------------------------------ L4 FFPE
 @pytest.mark.parametrize("solver", ["SOLVER_PHYSICAL", "SOLVER_AUTO"])
 @pytest.mark.parametrize("scheme", ["BE", "FastBE", "SBD", "FastSBD"])
