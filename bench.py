@@ -6,10 +6,12 @@ Workload C2: batched Riemann-Liouville derivative with the BDF2 (SBD) fast CQ, 6
 kernels (256 + 256 nodes, N_s = 17 / 15).  Signals u_k(t) = a_k t^b_k + c_k sin(w_k t), seeded
 (paper_1901_05128_b200/workloads.py), generated on the device before timing.
 
-One bench step = one pass of the hot path over the batch for LEVELS_PER_STEP (512) time levels:
-push + derivative for every DOF at every level, through SbdHistory.run on device buffers
-(temporally blocked kernel K5d, fp64 tensor cores).  K timed steps advance a fresh history from level 0; the default
-K = 128 covers the whole C2 horizon N = 65536.  Warm-up steps run on a separate history.
+One bench step = one pass of the hot path over the batch for LEVELS_PER_STEP (1024) time levels:
+push + derivative for every DOF at every level, through MultiHistory.run_device on device buffers
+(temporally blocked kernel K5d, fp64 tensor cores).  K timed steps advance a fresh history from
+level 0; the default K = 64 covers the whole C2 horizon N = 65536.  Warm-up steps run on a
+separate history.  Each K5d launch reads and writes the 268 MB history state once (a fixed
+~0.15 ms per launch: 3% of a 1024-level step, 6% of a 512-level one).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
                     [--workload C2 | C3 | C4 | C5 | C5-SBD]     (FFPE configs: bench_ffpe.py)
@@ -34,7 +36,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "fast-CQ DOF-steps/s (fp64) and % of HBM roofline at 1/2/4/8 B200 vs CPU"
 UNIT = "DOF-steps/s"
-LEVELS_PER_STEP = 512
+LEVELS_PER_STEP = 1024
 DOFS = 65536
 N_LEVELS = 65536
 
@@ -166,7 +168,7 @@ def main():
     ap.add_argument("--steps", type=int, default=N_LEVELS // LEVELS_PER_STEP)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default="C2", choices=["C2", "C3", "C4", "C5", "C5-SBD"],
                     help="C2 (default, BASELINE configs[1]) or an FFPE config (bench_ffpe.py)")
@@ -219,7 +221,10 @@ def main():
     stream = torch.cuda.ExternalStream(fraq.context_stream())
     # signals for the timed levels, generated on the device (rank-specific DOFs: weak scaling)
     K, W = args.steps, args.warmup
-    levels = K * LEVELS_PER_STEP
+    # input / output buffers for at most one horizon of steps (reused cyclically beyond that;
+    # every step's 537 MB of signal is larger than L2 either way)
+    nbuf = max(1, min(K, N_LEVELS // LEVELS_PER_STEP))
+    levels = nbuf * LEVELS_PER_STEP
     gen = torch.Generator(device="cpu").manual_seed(1901051282 + rank)
     if rank == 0:
         a = torch.from_numpy(params.a); bb = torch.from_numpy(params.b)
@@ -255,7 +260,7 @@ def main():
     with Clocks(local) as clk:
         ev[0].record(stream)
         for s in range(K):
-            off = s * LEVELS_PER_STEP * DOFS * 8
+            off = (s % nbuf) * LEVELS_PER_STEP * DOFS * 8
             h.run_device(U.data_ptr() + off, DOFS, LEVELS_PER_STEP, D.data_ptr() + off, DOFS)
             ev[s + 1].record(stream)
         ev[K].synchronize()
@@ -271,7 +276,7 @@ def main():
     value = world * dof_steps_local / (total_ms * 1e-3)
 
     # sanity: outputs finite after the first level
-    assert torch.isfinite(D[1:LEVELS_PER_STEP * K]).all().item()
+    assert torch.isfinite(D[1:]).all().item()
 
     # roofline of the dominant kernel (K5d): fp64 tensor-pipe bound; algorithmic flops per DOF-step
     # F = 4 N_nodes + 2 N_head, averaged over the two exponent halves
@@ -283,8 +288,9 @@ def main():
     B = 0.5 * sum(8 * (2 * nn + 2) for nn in n_nodes)
     pk = peaks()
     try:  # DRAM traffic per K5d launch from the committed ncu --set full capture (profiles/)
-        tr = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
-        traffic = tr["dram_bytes_per_launch"] / 1e9  # GB per launch (512 levels)
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r01b_traffic.json")))
+        assert tr["levels_per_launch"] == LEVELS_PER_STEP
+        traffic = tr["dram_bytes_per_launch"] / 1e9  # GB per launch (one step)
     except Exception:
         traffic = None
 
@@ -306,10 +312,14 @@ def main():
     del hs
 
     # e2e: the same metric through the C-ABI call with HOST buffers (pinned), copies inside
-    ke = max(1, min(args.e2e_steps, K))
+    ke = max(1, min(args.e2e_steps, K, nbuf))
     Uh = U[:ke * LEVELS_PER_STEP].cpu().pin_memory()
     Dh = torch.empty_like(Uh).pin_memory()
     he = fraq.MultiHistory(ks, [DOFS // 2, DOFS - DOFS // 2])
+    # untimed warm-up calls (first-call device state, staging buffers, streams, fragment tables)
+    for s in range(min(args.warmup, ke)):
+        rows = slice(s * LEVELS_PER_STEP, (s + 1) * LEVELS_PER_STEP)
+        he.run(Uh[rows].numpy(), True, Dh[rows].numpy())
     torch.cuda.synchronize()
     t_e = time.perf_counter()
     for s in range(ke):
@@ -344,12 +354,12 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {
                 "workload": "C2: BDF2 fast CQ, 65536 DOFs per GPU (gamma 0.7 | 0.3), tau = 1/65536,"
-                            " N = 65536 levels; one step = 512 levels x all DOFs (push+derivative)",
+                            " N = 65536 levels; one step = 1024 levels x all DOFs (push+derivative)",
                 "dofs_per_gpu": DOFS, "levels_per_step": LEVELS_PER_STEP,
                 "nodes": n_nodes, "n_head": n_head,
                 "kernel_eps": [e for _, e in kernels],
                 "path": "MultiHistory.run_device -> K5d (temporally blocked, fp64 tensor cores)",
-                "l2": "inputs larger than L2 (268 MB of signal per step)",
+                "l2": "inputs larger than L2 (537 MB of signal per step)",
                 "parallelism": f"dof-sharded x{world}, no data-path collective",
                 "setup_s": setup_s},
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": dmma_peak,

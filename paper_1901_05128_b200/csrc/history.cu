@@ -871,13 +871,13 @@ void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, l
     // Pinned host memory gives full overlap; pageable memory still works (staged copies).
     const long dim = std::max<long>(1, h->d.total_dim);
     // chunk height: ~1/16 of the call in multiples of the kernel's 32-level staging chunk, so the
-    // pipeline fill (first H2D) and drain (last D2H) stay short; at most 64 MB per buffer.
-    // (C2, 512 levels x 65536 DOFs per call: 32-level chunks reach 87% of the measured
-    // concurrent PCIe bound; 128-level chunks 72%.)
-    const long cap = std::max<long>(1, (64L << 20) / (8 * dim));
+    // pipeline fill (first H2D) and drain (last D2H) stay short, and at most ~16 MB per chunk
+    // (but 32 levels at least).  (C2, 65536 DOFs: 32-level chunks reach 87% of the measured
+    // concurrent PCIe bound; 64-level chunks 79%, 128-level chunks 72%.)
+    const long cap = std::max<long>(32, ((16L << 20) / (8 * dim)) / 32 * 32);
     long rows = std::min<long>(cap, std::max<long>(32, ((n_steps / 16 + 31) / 32) * 32));
-    if (const char* e = std::getenv("FRAQ_HOST_CHUNK"))  // experiment override (levels per chunk)
-        rows = std::max<long>(1, std::atol(e));
+    const char* ce = std::getenv("FRAQ_HOST_CHUNK");  // experiment override (levels per chunk)
+    if (ce && *ce) rows = std::max<long>(1, std::atol(ce));
     rows = std::max<long>(1, std::min<long>(rows, std::max<long>(1, n_steps)));
     // a remainder under 32 rows joins the last chunk (keeps it on the blocked kernels)
     const long cap_rows = rows + 31;
