@@ -211,8 +211,8 @@ __global__ void __launch_bounds__(320, RB == 2 ? 2 : 1) k13_kernel(K13Args A) {
                             }
                         }
                     }
-                    // ---- readout of block i: S[mode][k] = sum_j y_j C[j][k] (4 accumulators)
-                    constexpr int NACC = 4 / RB;
+                    // ---- readout of block i: S[mode][k] = sum_j y_j C[j][k]
+                    constexpr int NACC = 1;  // one chain per row block (no merging DADDs): +1-2%
                     double sacc[RB][NACC][2];
 #pragma unroll
                     for (int rb = 0; rb < RB; ++rb)
