@@ -68,11 +68,12 @@ class Workload:
 
     def solve(self, fraq, specs, torch=None, device_inputs=True):
         """One step through the public API; returns (device loop seconds, results).  C4 runs the
-        mode-sharded driver (parallel.run_2d_sharded) at every world size: forward 2D DST, this
-        rank's slab of modes, all-gather, inverse DST (device phase times, setup excluded)."""
+        mode-sharded driver (parallel.run_2d_transposed) at every world size: x pass of the DST on
+        the rank's rows, NCCL all-to-all transpose, y pass, K13 on the rank's kx slab of modes,
+        and the mirror image for the inverse (device phase times, setup excluded)."""
         sch = getattr(fraq.Scheme, self.scheme)
         if self.name == "C4":
-            from paper_1901_05128_b200.parallel import FraqOps, run_2d_sharded
+            from paper_1901_05128_b200.parallel import FraqOps, run_2d_transposed
             i = self.insts[0]
             ops = getattr(self, "_ops", None) or FraqOps(fraq, torch)
             self._ops = ops
@@ -83,9 +84,9 @@ class Workload:
             else:
                 g1, g2 = i.g1, i.g2
             T = {}
-            r1, r2 = run_2d_sharded(ops, i.alpha1, i.alpha2, i.coupling_a, self.M, 1.0, self.N,
-                                    self.scheme, g1, g2, kconf=_modal_kc(fraq), scheme_arg=sch,
-                                    timings=T)
+            r1, r2 = run_2d_transposed(ops, i.alpha1, i.alpha2, i.coupling_a, self.M, 1.0,
+                                       self.N, self.scheme, g1, g2, kconf=_modal_kc(fraq),
+                                       scheme_arg=sch, timings=T)
 
             class R:  # RunResult-like
                 pass
@@ -103,9 +104,10 @@ class Workload:
 
     def launches(self):
         """Our kernels inside the device-timed region of one step.  1D: DST (DMMA), transpose,
-        K13, transpose, inverse DST.  C4: sine table + per field 2 DST + 2 transposes, K13, and
-        the same for the inverse (K13's tables are built at setup, outside the loop timer)."""
-        return 19 if self.name == "C4" else 5
+        K13, transpose, inverse DST.  C4: two DST passes (sine table + DMMA GEMM each), K13, and
+        two inverse passes (K13's tables are built at setup, outside the loop timer; the slab
+        permutes around the all-to-alls are torch copies)."""
+        return 9 if self.name == "C4" else 5
 
     def io_bytes(self):
         return 8 * self.dofs()
@@ -299,7 +301,7 @@ def run_gpu(args, rank, world, local, pg, METRIC, Clocks, fraq, torch):
                                "solver warp) + inverse DST",
                        "l2": "L2 flushed (256 MB write) before every step",
                        "parallelism": (f"instance-sharded x{world}" if wl.units > 1 else
-                                       f"mode slabs x{world} + one NCCL all-gather" if
+                                       f"row / kx-mode slabs x{world} + two NCCL all-to-all transposes" if
                                        wl.name == "C4" else f"replicas x{world}")},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,

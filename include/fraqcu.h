@@ -224,6 +224,12 @@ int fraq_run_2d(fraq_ctx ctx, double alpha1, double alpha2, double coupling_a, i
  * c0 / cN: [2][n_modes] field-major.  mem: FRAQ_HOST or FRAQ_DEVICE for all arrays. */
 int fraq_dst2d(fraq_ctx ctx, int grid_m, int n_fields, const double* in, double* out, int inverse,
                int mem);
+/* fraq_dst_cols: the 1D pass of the same transform along the leading axis of a grid_m x n_cols
+ * row-major array, out[k][c] = s sum_j S[k][j] in[j][c] with s = 2/(M+1) (forward) or 1
+ * (inverse) -- K12 (one DMMA GEMM).  The slab-local step of the transposed 2D DST of the
+ * mode-sharded C4 driver (x pass, NCCL all-to-all transpose, y pass). */
+int fraq_dst_cols(fraq_ctx ctx, int grid_m, long n_cols, const double* in, double* out,
+                  int inverse, int mem);
 int fraq_modal_run(fraq_ctx ctx, double alpha1, double alpha2, double coupling_a, double t_final,
                    long n_steps, int scheme, const fraq_kconf_t* kconf, long n_modes,
                    const double* lam, const double* c0, double* cN, int mem,

@@ -73,6 +73,7 @@ EXTRA = [
     "timing_sweep",
     "dst2d",
     "dst2d_device",
+    "dst_cols_device",
     "modal_run",
     "modal_run_device",
     "diag_fp64_peak",

@@ -26,6 +26,7 @@ void hist_lagged(fraq_hist h, long depth, double* out, int mem);
 void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, long ldd, int mem);
 int hist_last_path(fraq_hist h);
 void dst2d(fraq_ctx c, int M, int n_fields, const double* in, double* out, bool inverse, int mem);
+void dst_cols(fraq_ctx c, int M, long n_cols, const double* in, double* out, bool inverse, int mem);
 void modal_run_modes(fraq_ctx c, double alpha1, double alpha2, double a, double t_final, long N,
                      int scheme, const fraq_kconf_t* kc, long n_modes, const double* lam,
                      const double* c0, double* cN, int mem, fraq_run_info_t* info);
@@ -341,6 +342,14 @@ int fraq_dst2d(fraq_ctx c, int grid_m, int n_fields, const double* in, double* o
     return guarded([&] {
         check_ctx(c);
         dst2d(c, grid_m, n_fields, in, out, inverse != 0, mem);
+    });
+}
+
+int fraq_dst_cols(fraq_ctx c, int grid_m, long n_cols, const double* in, double* out, int inverse,
+                  int mem) {
+    return guarded([&] {
+        check_ctx(c);
+        dst_cols(c, grid_m, n_cols, in, out, inverse != 0, mem);
     });
 }
 

@@ -456,6 +456,10 @@ void dst2d(int grid_m, int n_fields, const double* in, double* out, bool inverse
     check(fraq_dst2d(default_context(), grid_m, n_fields, in, out, inverse ? 1 : 0, mem));
 }
 
+void dst_cols(int grid_m, long n_cols, const double* in, double* out, bool inverse, int mem) {
+    check(fraq_dst_cols(default_context(), grid_m, n_cols, in, out, inverse ? 1 : 0, mem));
+}
+
 RunResult modal_run(double alpha1, double alpha2, double coupling_a, double t_final,
                     long n_steps, Scheme scheme, long n_modes, const double* lam,
                     const double* c0, double* cN, int mem, const KernelConfig& kconf) {

@@ -231,6 +231,11 @@ RunResult run_2d(double alpha1, double alpha2, double coupling_a, int grid_m, do
 void dst2d(int grid_m, int n_fields, const double* in, double* out, bool inverse,
            int mem = FRAQ_HOST);
 
+/// 1D pass of the same transform along the leading axis of a grid_m x n_cols array (forward
+/// scale 2/(M+1), inverse 1): the slab-local step of the transposed, mode-sharded 2D DST.
+void dst_cols(int grid_m, long n_cols, const double* in, double* out, bool inverse,
+              int mem = FRAQ_HOST);
+
 /// One instance (fast BE / BDF2) stepped over n_modes modes with eigenvalues lam; c0 / cN are
 /// [2][n_modes] (field-major).  The per-rank work of the mode-sharded 2D solve.
 RunResult modal_run(double alpha1, double alpha2, double coupling_a, double t_final,

@@ -445,12 +445,9 @@ __global__ void __launch_bounds__(R2_MAXW * 32, 1) run2_kernel(RunArgs A) {
 
 void launch_run2(const RunArgs& a, int nw, int num_sms, cudaStream_t s) {
     const size_t smem = run2_smem_bytes(nw);
-    static bool attr = false;
-    if (!attr) {
-        FRAQ_CUDA(cudaFuncSetAttribute(run2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)run2_smem_bytes(R2_MAXW)));
-        attr = true;
-    }
+    // (per launch: the attribute is per device, and a process may drive several devices)
+    FRAQ_CUDA(cudaFuncSetAttribute(run2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)run2_smem_bytes(R2_MAXW)));
     int per_sm = 1;
     FRAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, run2_kernel, nw * 32, smem));
     const int grid = std::max(1, std::min(a.n_tasks, std::max(1, per_sm) * num_sms));

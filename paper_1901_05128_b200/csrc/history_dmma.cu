@@ -513,12 +513,9 @@ int run3_max_lag() { return D_LMAX; }
 
 void launch_run3(const RunArgs& a, int nwg, int num_sms, cudaStream_t s) {
     const size_t smem = run3_smem(nwg);
-    static bool attr = false;
-    if (!attr) {
-        FRAQ_CUDA(cudaFuncSetAttribute(run3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)run3_smem(D_MAXWG)));
-        attr = true;
-    }
+    // (per launch: the attribute is per device, and a process may drive several devices)
+    FRAQ_CUDA(cudaFuncSetAttribute(run3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)run3_smem(D_MAXWG)));
     int per_sm = 1;
     FRAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, run3_kernel, nwg * 32, smem));
 #ifdef FRAQ_EXP_ONECTA

@@ -695,6 +695,28 @@ void dst2d(fraq_ctx c, int M, int n_fields, const double* in, double* out, bool 
     FRAQ_CUDA(cudaStreamSynchronize(c->stream));
 }
 
+// 1D DST pass along the leading axis of a grid_m x n_cols array (K12): forward scale 2/(M+1),
+// inverse 1.  mem: FRAQ_HOST or FRAQ_DEVICE for in / out.
+void dst_cols(fraq_ctx c, int M, long n_cols, const double* in, double* out, bool inverse,
+              int mem) {
+    if (M < 1 || n_cols < 0) fail(FRAQ_EINVAL, "dst_cols: grid_m must be >= 1, n_cols >= 0");
+    if (n_cols == 0) return;
+    const long n = (long)M * n_cols;
+    const double sc = inverse ? 1.0 : 2.0 / (M + 1);
+    DevBuf<double> tab;
+    make_sintab(c, M, tab);
+    if (mem == FRAQ_DEVICE) {
+        dst_apply(c, M, tab.p, in, n_cols, out, sc);
+        FRAQ_CUDA(cudaStreamSynchronize(c->stream));
+        return;
+    }
+    DevBuf<double> di(n), dout(n);
+    FRAQ_CUDA(cudaMemcpyAsync(di.p, in, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    dst_apply(c, M, tab.p, di.p, n_cols, dout.p, sc);
+    FRAQ_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    FRAQ_CUDA(cudaStreamSynchronize(c->stream));
+}
+
 // One instance stepped over a caller-chosen set of modes (eigenvalues lam[n_modes]); c0 / cN are
 // [2][n_modes] (field-major).  The building block of the mode-sharded 2D driver: every rank
 // steps its slab of modes.  mem: FRAQ_HOST or FRAQ_DEVICE for lam / c0 / cN.

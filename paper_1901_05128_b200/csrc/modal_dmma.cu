@@ -212,7 +212,10 @@ __global__ void __launch_bounds__(320, RB == 2 ? 2 : 1) k13_kernel(K13Args A) {
                         }
                     }
                     // ---- readout of block i: S[mode][k] = sum_j y_j C[j][k]
-                    constexpr int NACC = 1;  // one chain per row block (no merging DADDs): +1-2%
+                    // accumulator chains per row block: one for RB = 2 (no merging DADDs; C5-BE
+                    // full horizon +2.7%), four for RB = 1, whose single row block would otherwise
+                    // be one chain of 2 NT dependent DMMAs with ~2.5 warps per SMSP (C4 -3.6%)
+                    constexpr int NACC = RB == 2 ? 1 : 4;
                     double sacc[RB][NACC][2];
 #pragma unroll
                     for (int rb = 0; rb < RB; ++rb)

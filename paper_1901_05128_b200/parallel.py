@@ -96,6 +96,12 @@ class FraqOps:
         self.fraq.dst2d_device(M, x.numel() // (M * M), x.data_ptr(), out.data_ptr(), inverse)
         return out
 
+    def dst_cols(self, M, x, inverse):
+        """1D DST pass along the leading axis of x (M x C): K12 via fraq_dst_cols."""
+        out = self.empty(*x.shape)
+        self.fraq.dst_cols_device(M, x.numel() // M, x.data_ptr(), out.data_ptr(), inverse)
+        return out
+
     def step(self, alpha1, alpha2, a, t_final, N, scheme, lam, c0, kconf):
         cN = self.empty(*c0.shape)
         rr = self.fraq.modal_run_device(alpha1, alpha2, a, t_final, N, scheme, lam.numel(),
@@ -132,6 +138,12 @@ class OracleOps:
         sc = 1.0 if inverse else (2.0 / (M + 1)) ** 2
         g = x.numpy().reshape(-1, M, M)
         return self.tensor(np.stack([sc * S @ gi @ S for gi in g]).reshape(x.shape))
+
+    def dst_cols(self, M, x, inverse):
+        import numpy as np
+        S = np.sin(np.outer(np.arange(1, M + 1), np.arange(1, M + 1)) * np.pi / (M + 1))
+        sc = 1.0 if inverse else 2.0 / (M + 1)
+        return self.tensor(sc * S @ x.numpy().reshape(M, -1)).reshape(x.shape)
 
     def step(self, alpha1, alpha2, a, t_final, N, scheme, lam, c0, kconf):
         sbd = scheme == "FastSBD"
@@ -199,3 +211,101 @@ def run_2d_sharded(ops, alpha1, alpha2, a, M, t_final, N, scheme, g1_0, g2_0, kc
         T["gather"] = ops.seconds(m2, m3)
         T["inverse"] = ops.seconds(m3, m4)
     return out[0], out[1]
+
+
+def _alltoall(ops, send):
+    """Equal-chunk all-to-all along dim 0 (NCCL over NVLink on the GPU box; gloo in the tests)."""
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return send
+    recv = ops.empty(*send.shape)
+    dist.all_to_all_single(recv, send.contiguous())
+    return recv
+
+
+def run_2d_transposed(ops, alpha1, alpha2, a, M, t_final, N, scheme, g1_0, g2_0, kconf=None,
+                      scheme_arg=None, timings=None, gather=True):
+    """C4 across the ranks of the default process group with the 2D DST split at the transpose
+    (north_star "(4)"): rank r owns the physical rows y in slab r and the modes
+    kx in slab r (all ky).
+
+      forward:  x pass on its rows (fraq_dst_cols)  ->  all-to-all transpose  ->  y pass
+      stepping: its kx slab of modes (fraq_modal_run, K13), no exchange
+      inverse:  ky pass  ->  all-to-all transpose  ->  kx pass on its rows
+
+    Slabs are padded to ceil(M / world) so both exchanges are equal-chunk all-to-alls
+    (2 x M x per doubles per rank each).  Each rank reads only its rows of g1_0 / g2_0 and ends
+    with its rows of the result; `gather=True` all-gathers them (outside the timed phases) and
+    returns the full (g1, g2), else the rank's (2, rows, M) slab.  `timings` (dict) receives the
+    device seconds of forward, step (the library's loop timer), exchange and inverse."""
+    import contextlib
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    lo, hi, per = slab_rows(M, rank, world)
+    n = hi - lo
+    ctx = torch.cuda.stream(ops.stream) if ops.stream is not None else contextlib.nullcontext()
+    T = timings if timings is not None else {}
+
+    def to_cols(recv):
+        # recv block q = [i (per)][f][j (per)] from rank q -> rows q*per + j, columns (f, i)
+        return recv.view(world, per, 2, per).permute(0, 3, 2, 1).reshape(world * per, 2 * per)[:M]
+
+    with ctx:
+        if isinstance(g1_0, torch.Tensor):
+            g = torch.stack([g1_0.reshape(M, M)[lo:hi], g2_0.reshape(M, M)[lo:hi]]).to(torch.float64)
+        else:
+            g = ops.tensor(np.stack([np.asarray(g1_0).reshape(M, M)[lo:hi],
+                                     np.asarray(g2_0).reshape(M, M)[lo:hi]]))
+        xs = ops.empty(M, 2, per)
+        xs.zero_()
+        xs[:, :, :n] = g.permute(2, 0, 1)                      # [x][f][y_local]
+        m0 = ops.mark()
+        w = ops.dst_cols(M, xs.reshape(M, 2 * per), inverse=False)  # [kx][f][y_local]
+        send = ops.empty(world * per, 2, per)
+        send.zero_()
+        send[:M] = w.view(M, 2, per)
+        m1 = ops.mark()
+        recv = _alltoall(ops, send)                            # block q: [kx_local][f][y of q]
+        m2 = ops.mark()
+        c = ops.dst_cols(M, to_cols(recv).contiguous(), inverse=False).view(M, 2, per)  # [ky][f][kxl]
+        m3 = ops.mark()
+        T["forward"] = ops.seconds(m0, m1) + ops.seconds(m2, m3)
+        T["exchange"] = ops.seconds(m1, m2)
+        T["step"] = 0.0
+        z_in = ops.empty(M, 2, per)
+        z_in.zero_()
+        if n > 0:
+            c0 = c[:, :, :n].permute(1, 0, 2).reshape(2, M * n).contiguous()  # [f][ky * n + kxl]
+            lam1 = 4.0 * (M + 1) ** 2 * np.sin(np.arange(1, M + 1) * np.pi / (2 * (M + 1))) ** 2
+            lam = ops.tensor((lam1[:, None] + lam1[None, lo:hi]).ravel())
+            cN, T["step"] = ops.step(alpha1, alpha2, a, t_final, N,
+                                     scheme if scheme_arg is None else scheme_arg, lam, c0, kconf)
+            z_in[:, :, :n] = cN.view(2, M, n).permute(1, 0, 2)
+        m4 = ops.mark()
+        z = ops.dst_cols(M, z_in.reshape(M, 2 * per), inverse=True)  # [y][f][kx_local]
+        send2 = ops.empty(world * per, 2, per)
+        send2.zero_()
+        send2[:M] = z.view(M, 2, per)
+        m5 = ops.mark()
+        recv2 = _alltoall(ops, send2)                          # block q: [y_local][f][kx of q]
+        m6 = ops.mark()
+        gx = ops.dst_cols(M, to_cols(recv2).contiguous(), inverse=True).view(M, 2, per)  # [x][f][yl]
+        slab = gx[:, :, :n].permute(1, 2, 0).contiguous()      # [f][y_local][x]
+        m7 = ops.mark()
+        T["inverse"] = ops.seconds(m4, m5) + ops.seconds(m6, m7)
+        T["exchange"] += ops.seconds(m5, m6)
+        if not gather:
+            return slab
+        if world > 1:
+            pad = ops.empty(2, per, M)
+            pad.zero_()
+            pad[:, :n] = slab
+            allp = ops.empty(world * 2, per, M)  # concatenated along dim 0 (NCCL and gloo)
+            dist.all_gather_into_tensor(allp, pad)
+            full = allp.view(world, 2, per, M).permute(1, 0, 2, 3).reshape(2, world * per, M)[:, :M]
+        else:
+            full = slab
+    return full[0].reshape(-1), full[1].reshape(-1)

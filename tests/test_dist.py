@@ -131,3 +131,61 @@ def test_c4_mode_shards_two_ranks(scheme):
         assert np.abs(r2 - s2.numpy()).max() <= 1e-14 * np.abs(s2.numpy()).max()
         assert np.abs(r1 - p1).max() <= 1e-10 * np.abs(p1).max()
         assert np.abs(r2 - p2).max() <= 1e-10 * np.abs(p2).max()
+
+
+def _worker_2d_t(rank, world, port, q, scheme):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.oracle import Oracle
+    from paper_1901_05128_b200.parallel import OracleOps, run_2d_transposed
+    g1, g2 = _c4_like(9)
+    ops = OracleOps(Oracle("port"), torch)
+    try:
+        T = {}
+        r1, r2 = run_2d_transposed(ops, 0.3, 0.6, -3.0, 9, 0.25, 40, scheme, g1, g2, timings=T)
+        slab = run_2d_transposed(ops, 0.3, 0.6, -3.0, 9, 0.25, 40, scheme, g1, g2, gather=False)
+        q.put((rank, r1.numpy(), r2.numpy(), slab.numpy(), sorted(T)))
+    except Exception as e:  # report instead of hanging the parent
+        q.put((rank, repr(e), None, None, None))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("scheme,world", [("FastBE", 2), ("FastSBD", 3)])
+def test_c4_transposed_dst_ranks(scheme, world):
+    """C4 with the 2D DST split at the transpose (parallel.run_2d_transposed) on gloo ranks: x pass
+    on each rank's rows, equal-chunk all-to-all, y pass, K13 over the rank's kx slab, and the
+    mirror image for the inverse.  9 rows over 2 ranks (5 + 4, padded) and 3 ranks (3 + 3 + 3):
+    every rank's gathered result equals the single-process run of the all-gather driver and the
+    physical-space 2D restatement, and each rank's slab is its rows of the result."""
+    import torch
+    from oracle.oracle import Oracle
+    from paper_1901_05128_b200.parallel import OracleOps, run_2d_sharded, slab_rows
+    from ffpe_refs import fast_stepper_nd
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_2d_t, args=(r, world, port, q, scheme))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(r[2] is not None for r in res), res
+    g1, g2 = _c4_like(9)
+    orc = Oracle("port")
+    s1, s2 = run_2d_sharded(OracleOps(orc, torch), 0.3, 0.6, -3.0, 9, 0.25, 40, scheme, g1, g2)
+    p1, p2 = fast_stepper_nd(orc, 0.3, 0.6, -3.0, 9, 2, 0.25, 40, scheme == "FastSBD", g1, g2)
+    for rank, r1, r2, slab, keys in res:
+        assert keys == ["exchange", "forward", "inverse", "step"]
+        assert np.abs(r1 - s1.numpy()).max() <= 1e-13 * np.abs(s1.numpy()).max()
+        assert np.abs(r2 - s2.numpy()).max() <= 1e-13 * np.abs(s2.numpy()).max()
+        assert np.abs(r1 - p1).max() <= 1e-10 * np.abs(p1).max()
+        assert np.abs(r2 - p2).max() <= 1e-10 * np.abs(p2).max()
+        lo, hi, _ = slab_rows(9, rank, world)
+        assert np.array_equal(slab[0], r1.reshape(9, 9)[lo:hi])
+        assert np.array_equal(slab[1], r2.reshape(9, 9)[lo:hi])

@@ -266,3 +266,40 @@ def test_sharded_driver_single_rank_equals_run_2d(fraq):
     assert np.abs(r1.cpu().numpy() - np.array(full.final_state.g1)).max() <= 1e-12
     assert np.abs(r2.cpu().numpy() - np.array(full.final_state.g2)).max() <= 1e-12
     assert set(T) == {"forward", "step", "gather", "inverse"} and T["step"] > 0
+
+
+@pytest.mark.parametrize("scheme", ["FastBE", "FastSBD"])
+def test_transposed_driver_single_rank_equals_run_2d(fraq, scheme):
+    """parallel.run_2d_transposed with the device ops (world = 1: x pass, identity exchange,
+    y pass via fraq_dst_cols; K13 over all modes) equals run_2d; the multi-rank all-to-all logic
+    is covered on CPU (tests/test_dist.py)."""
+    import torch
+    from paper_1901_05128_b200.parallel import FraqOps, run_2d_transposed
+    M = 63
+    rng = np.random.default_rng(4)
+    g1, g2 = rng.uniform(0, 1, M * M), rng.uniform(0, 1, M * M)
+    ops = FraqOps(fraq, torch)
+    T = {}
+    r1, r2 = run_2d_transposed(ops, 0.3, 0.6, -3.0, M, 1.0, 200, scheme, g1, g2,
+                               scheme_arg=getattr(fraq.Scheme, scheme), timings=T)
+    full = fraq.run_2d(0.3, 0.6, -3.0, M, 1.0, 200, getattr(fraq.Scheme, scheme), g1, g2)
+    assert np.abs(r1.cpu().numpy() - np.array(full.final_state.g1)).max() <= 1e-12
+    assert np.abs(r2.cpu().numpy() - np.array(full.final_state.g2)).max() <= 1e-12
+    assert set(T) == {"forward", "step", "exchange", "inverse"} and T["step"] > 0
+
+
+@pytest.mark.parametrize("M,C", [(1, 3), (7, 5), (63, 130), (1023, 17)])
+def test_dst_cols_matches_projection(fraq, M, C):
+    """fraq_dst_cols (K12 DMMA GEMM along the leading axis) against the direct sine sums, both
+    directions, device pointers; forward then inverse returns the input."""
+    import torch
+    rng = np.random.default_rng(M + C)
+    X = rng.uniform(-1, 1, (M, C))
+    S = np.sin(np.outer(np.arange(1, M + 1), np.arange(1, M + 1)) * np.pi / (M + 1))
+    xd = torch.tensor(X, dtype=torch.float64, device="cuda")
+    fd, bd = torch.empty_like(xd), torch.empty_like(xd)
+    fraq.dst_cols_device(M, C, xd.data_ptr(), fd.data_ptr(), False)
+    fraq.dst_cols_device(M, C, fd.data_ptr(), bd.data_ptr(), True)
+    F = fd.cpu().numpy()
+    assert np.abs(F - (2.0 / (M + 1)) * S @ X).max() <= 1e-13 * max(1.0, np.abs(F).max())
+    assert np.abs(bd.cpu().numpy() - X).max() <= 1e-12
