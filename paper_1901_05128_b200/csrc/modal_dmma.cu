@@ -125,13 +125,16 @@ __global__ void k13_tables_kernel(const K13TabSrc* src, int Jp, int delta, doubl
     }
 }
 
-// RB: 8-mode row blocks per CTA (modes = 8 RB); NT: 8-node tiles per GEMM warp.  At most 8 GEMM
-// warps + 1 solver warp per CTA, one CTA per SM (the register file is split per SM sub-partition:
-// 9 warps leave ~170 registers per thread for the state fragments and the table operands).
-template <int RB, int NT>
-// RB = 2 (J <= 256; ~90 KB of shared memory): two CTAs per SM, so one CTA's solver phase
-// overlaps the other's GEMMs and each SM sub-partition runs 4 GEMM warps.
-__global__ void __launch_bounds__(320, RB == 2 ? 2 : 1) k13_kernel(K13Args A) {
+// RB: 8-mode row blocks per CTA (modes = 8 RB); NT: 8-node tiles per GEMM warp; MAXT: threads.
+// * RB = 2, NT = 8, MAXT = 320 (J <= 256; ~90 KB of shared memory): two CTAs per SM, so one
+//   CTA's solver phase overlaps the other's GEMMs and each SM sub-partition runs 4 GEMM warps.
+// * RB = 2, NT = 8, MAXT = 576 (256 < J <= 512, "wide"): 16 modes x 64 nodes per GEMM warp,
+//   up to 8 GEMM warps per field + 2 solver warps, one CTA per SM (the tables of J = 512 take
+//   140 KB).  16 modes per task double the GEMM work behind each sequential 8-level solve.
+// * RB = 1 (NT = 12..16, MAXT = 320): 8 modes, 4 GEMM warps per field, one CTA per SM (~170
+//   registers per thread for the state fragments); kept as the FRAQ_K13_NARROW experiment path.
+template <int RB, int NT, int MAXT>
+__global__ void __launch_bounds__(MAXT, (MAXT == 320 && RB == 2) ? 2 : 1) k13_kernel(K13Args A) {
     constexpr int MODES = 8 * RB;
     extern __shared__ double ksm[];
     const int nwg = A.nwg, nwf = A.nwf, TS = A.TS, Jp = A.Jp;
@@ -285,7 +288,7 @@ __global__ void __launch_bounds__(320, RB == 2 ? 2 : 1) k13_kernel(K13Args A) {
                                            g * MODES + 8 * nt + 2 * t;
                         double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-                        for (int w = 0; w < 4; ++w)
+                        for (int w = 0; w < 8; ++w)
                             if (w < nwf) {
                                 const double2 v = *reinterpret_cast<const double2*>(pb + w * 8 * MODES);
                                 s0 += v.x;
@@ -411,15 +414,15 @@ size_t k13_smem(int TS, int nwg, int ring, int modes) {
            ((size_t)2 * TS + 2 * nwg * 8 * modes + 2 * ring * modes + 2 * 8 * modes + 2 * modes);
 }
 
-template <int RB, int NT>
+template <int RB, int NT, int MAXT>
 void k13_launch(const K13Args& a, size_t smem, int num_sms, cudaStream_t s) {
-    FRAQ_CUDA(cudaFuncSetAttribute(k13_kernel<RB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    FRAQ_CUDA(cudaFuncSetAttribute(k13_kernel<RB, NT, MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
     int per_sm = 1;
     const int threads = a.nwg * 32 + 64;
-    FRAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k13_kernel<RB, NT>, threads, smem));
+    FRAQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k13_kernel<RB, NT, MAXT>, threads, smem));
     const long grid = std::max(1L, std::min(a.n_tasks, (long)std::max(1, per_sm) * num_sms));
-    k13_kernel<RB, NT><<<(unsigned)grid, threads, smem, s>>>(a);
+    k13_kernel<RB, NT, MAXT><<<(unsigned)grid, threads, smem, s>>>(a);
     FRAQ_LAUNCH_CHECK();
 }
 
@@ -445,9 +448,11 @@ void k13_prepare(fraq_ctx c, const std::vector<K13Inst>& in, bool sbd, K13Plan& 
     P.n_inst = n_inst;
     P.sbd = sbd;
     P.delta = minL >= 8 ? 0 : 1;
-    // J <= 256: 16 modes x 64 nodes per GEMM warp; else 8 modes x 8 NT nodes per GEMM warp with
-    // the narrowest NT in {12, 13, 14, 16} that covers J in 4 warps (C4: 408 nodes -> NT = 13)
-    P.RB = maxJ <= 256 ? 2 : 1;
+    // 16 modes x 64 nodes per GEMM warp (J <= 256: two CTAs per SM; J <= 512: the wide CTA with
+    // up to 16 GEMM warps).  Experiment path: 8 modes x 8 NT nodes per GEMM warp with the
+    // narrowest NT in {12, 13, 14, 16} that covers J in 4 warps (C4: 408 nodes -> NT = 13)
+    const char* narrow = std::getenv("FRAQ_K13_NARROW");  // experiment switch: RB = 1 for J > 256
+    P.RB = (maxJ <= 256 || !(narrow && *narrow)) ? 2 : 1;
     P.NT = 8;
     if (P.RB == 1) {
         P.NT = 16;
@@ -512,16 +517,18 @@ void k13_exec(fraq_ctx c, K13Plan& P, const double* lam, int n_modes, long N, co
     A.counter = P.counter.p;
     FRAQ_CUDA(cudaMemsetAsync(P.counter.p, 0, sizeof(int), c->stream));
     const size_t smem = k13_smem(P.TS, P.nwg, P.ring, modes);
-    if (P.RB == 2)
-        k13_launch<2, 8>(A, smem, c->num_sms, c->stream);
+    if (P.RB == 2 && P.nwg <= 8)
+        k13_launch<2, 8, 320>(A, smem, c->num_sms, c->stream);
+    else if (P.RB == 2)
+        k13_launch<2, 8, 576>(A, smem, c->num_sms, c->stream);
     else if (P.NT == 12)
-        k13_launch<1, 12>(A, smem, c->num_sms, c->stream);
+        k13_launch<1, 12, 320>(A, smem, c->num_sms, c->stream);
     else if (P.NT == 13)
-        k13_launch<1, 13>(A, smem, c->num_sms, c->stream);
+        k13_launch<1, 13, 320>(A, smem, c->num_sms, c->stream);
     else if (P.NT == 14)
-        k13_launch<1, 14>(A, smem, c->num_sms, c->stream);
+        k13_launch<1, 14, 320>(A, smem, c->num_sms, c->stream);
     else
-        k13_launch<1, 16>(A, smem, c->num_sms, c->stream);
+        k13_launch<1, 16, 320>(A, smem, c->num_sms, c->stream);
 }
 
 }  // namespace fraqcu
