@@ -242,6 +242,18 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 320 && RB == 2) ? 2 : 1) k13_ke
                             for (int p = 1; p < NACC; ++p) v += sacc[rb][p][e];
                             pw[(2 * t + e) * MODES + 8 * rb + g] = v;
                         }
+#ifndef K13_SOLVER_REDUCE
+                    // the field's nwf partial tiles are summed here, in place into the field's
+                    // first tile (each element owned by one thread), so the solver warp's critical
+                    // path reads one tile instead of issuing 2 nwf RB DADDs behind the GEMM DMMAs
+                    asm volatile("bar.sync %0, %1;" ::"r"(2 + f), "r"(nwf * 32) : "memory");
+                    double* pf = part + ((size_t)(i & 1) * nwg + f * nwf) * 8 * MODES;
+                    for (int e = sl * 32 + lane; e < 8 * MODES; e += nwf * 32) {
+                        double v = pf[e];
+                        for (int w = 1; w < nwf; ++w) v += pf[w * 8 * MODES + e];
+                        pf[e] = v;
+                    }
+#endif
                 }
                 __syncthreads();
             }
@@ -286,6 +298,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 320 && RB == 2) ? 2 : 1) k13_ke
                     for (int nt = 0; nt < RB; ++nt) {
                         const double* pb = part + ((size_t)buf * nwg + sf * nwf) * 8 * MODES +
                                            g * MODES + 8 * nt + 2 * t;
+#ifdef K13_SOLVER_REDUCE
                         double s0 = 0.0, s1 = 0.0;
 #pragma unroll
                         for (int w = 0; w < 8; ++w)
@@ -296,6 +309,11 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 320 && RB == 2) ? 2 : 1) k13_ke
                             }
                         D[nt][0] = s0;
                         D[nt][1] = s1;
+#else
+                        const double2 v = *reinterpret_cast<const double2*>(pb);  // summed tile
+                        D[nt][0] = v.x;
+                        D[nt][1] = v.y;
+#endif
                     }
                     for (int j0 = 0; j0 < Lts; j0 += 4) {
                         const int j = j0 + t, lev = n0 - Lts + j;

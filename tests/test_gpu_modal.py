@@ -111,6 +111,26 @@ def test_k13_tensor_core_path_matches_k11(fraq, scheme, m, N, monkeypatch):
     assert rel(k13.final_state.g2, k11.final_state.g2) <= 1e-12
 
 
+@pytest.mark.parametrize("scheme,pts", [("FastBE", 300), ("FastBE", 509), ("FastSBD", 150),
+                                        ("FastSBD", 256)])
+def test_k13_wide_cta_matches_narrow_and_k11(fraq, scheme, pts, monkeypatch):
+    """Nodes per field in (256, 512]: the wide K13 CTA (16 modes, up to 16 GEMM warps of 64
+    nodes) against the 8-mode experiment path (FRAQ_K13_NARROW) and K11, on a ragged mode count
+    (1000) and level count (77); J = 300 and 509 (BE), 2 x 150 and 2 x 256 (SBD families)."""
+    spec = fraq.ProblemSpec(alpha1=0.35, alpha2=0.75, coupling_a=-2.5, grid_m=1000, t_final=0.7,
+                            n_steps=77, initial="poly_sin")
+    kc = modal_kc(fraq, auto_size=False, be_points=pts, sbd_points_1=pts, sbd_points_2=pts)
+    wide = fraq.run(spec, getattr(fraq.Scheme, scheme), kc)
+    monkeypatch.setenv("FRAQ_K13_NARROW", "1")
+    narrow = fraq.run(spec, getattr(fraq.Scheme, scheme), kc)
+    monkeypatch.setenv("FRAQ_MODAL_K11", "1")
+    k11 = fraq.run(spec, getattr(fraq.Scheme, scheme), kc)
+    for g in ("g1", "g2"):
+        w, n, k = (np.array(getattr(r.final_state, g)) for r in (wide, narrow, k11))
+        assert rel(w, n) <= 1e-12
+        assert rel(w, k) <= 1e-12
+
+
 def test_k13_batch_mixed_instances(fraq, orc):
     """C5-like batch through K13 with per-instance kernels (different J and L per field)."""
     from paper_1901_05128_b200.workloads import c5_instances
