@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <vector>
 
@@ -270,6 +271,11 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 320 && RB == 2) ? 2 : 1) k13_ke
                          m22 = lead * itau + h20 * al;
             const double idet = 1.0 / (m11 * m22 - m12 * m21);
             const double M11 = m11 * idet, M12 = m12 * idet, M21 = m21 * idet, M22 = m22 * idet;
+            // x = M^-1 r with r1 = -al s1 + a s2 + l1, r2 = a s1 - al s2 + l2 (M^-1 = [[M22, -M12],
+            // [-M21, M11]]), folded: x = P s + Q l;  l = itau gp (BE), itau (2 gp - gpp / 2) (SBD)
+            const double p11 = -fma(al, M22, a * M12), p12 = fma(a, M22, al * M12);
+            const double p21 = fma(a, M11, al * M21), p22 = -fma(al, M11, a * M21);
+            const double q11 = itau * M22, q12 = -itau * M12, q21 = -itau * M21, q22 = itau * M11;
             const double g10 = g0s[d], g20 = g0s[MODES + d];
             double gp1 = g10, gp2 = g20, gpp1 = 0.0, gpp2 = 0.0;
             const double* c1 = cwt[0];  // in-block weights c_1..c_7 (shared memory, broadcast)
@@ -334,8 +340,9 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 320 && RB == 2) ? 2 : 1) k13_ke
                         for (int nt = 0; nt < RB; ++nt) {
                             const double* g0f = g0s + sf * MODES + 8 * nt + 2 * t;
                             *reinterpret_cast<double2*>(sA + (sf * 8 + g) * MODES + 8 * nt + 2 * t) =
-                                make_double2(fma(corr_c, g0f[0], D[nt][0]),
-                                             fma(corr_c, g0f[1], D[nt][1]));
+                                A.sbd ? make_double2(fma(corr_c, g0f[0], D[nt][0]),
+                                                     fma(corr_c, g0f[1], D[nt][1]))
+                                      : make_double2(D[nt][0], D[nt][1]);
                         }
                     }
                     if (b + 1 < nb) corr_load(b + 1);  // latency hidden by the solve + barrier
@@ -348,27 +355,41 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 320 && RB == 2) ? 2 : 1) k13_ke
                             acc2[k] = sA[(8 + k) * MODES + d];
                         }
                         if (kmax == 8 && !(A.sbd && n0 == 1)) {
-                            // full block: no predicates; x = M r with M = inverse level matrix
+                            // full block, no predicates: x = P acc + (l terms of earlier levels),
+                            // coefficients folded per task (8 fp64 ops per level for BE, 12 SBD)
+                            auto full_block = [&](auto sbd_c) {
+                                constexpr bool SBD = decltype(sbd_c)::value;
 #pragma unroll
-                            for (int k = 0; k < 8; ++k) {
-                                const double l1 = A.sbd ? fma(2.0, gp1, -0.5 * gpp1) * itau : gp1 * itau;
-                                const double l2 = A.sbd ? fma(2.0, gp2, -0.5 * gpp2) * itau : gp2 * itau;
-                                const double r1 = fma(a, acc2[k], fma(-al, acc1[k], l1));
-                                const double r2 = fma(a, acc1[k], fma(-al, acc2[k], l2));
-                                const double x1 = fma(r1, M22, -(r2 * M12));
-                                const double x2 = fma(r2, M11, -(r1 * M21));
-                                ring[((n0 + k) & mask) * MODES + d] = x1;
-                                ring[(RING + ((n0 + k) & mask)) * MODES + d] = x2;
+                                for (int k = 0; k < 8; ++k) {
+                                    double h1, h2;
+                                    if constexpr (SBD) {
+                                        const double t1 = fma(2.0, gp1, -0.5 * gpp1),
+                                                     t2 = fma(2.0, gp2, -0.5 * gpp2);
+                                        h1 = fma(q11, t1, q12 * t2);
+                                        h2 = fma(q21, t1, q22 * t2);
+                                    } else {
+                                        h1 = fma(q11, gp1, q12 * gp2);
+                                        h2 = fma(q21, gp1, q22 * gp2);
+                                    }
+                                    const double x1 = fma(p11, acc1[k], fma(p12, acc2[k], h1));
+                                    const double x2 = fma(p21, acc1[k], fma(p22, acc2[k], h2));
+                                    ring[((n0 + k) & mask) * MODES + d] = x1;
+                                    ring[(RING + ((n0 + k) & mask)) * MODES + d] = x2;
 #pragma unroll
-                                for (int k2 = k + 1; k2 < 8; ++k2) {
-                                    acc1[k2] = fma(c1[k2 - k], x1, acc1[k2]);
-                                    acc2[k2] = fma(c2[k2 - k], x2, acc2[k2]);
+                                    for (int k2 = k + 1; k2 < 8; ++k2) {
+                                        acc1[k2] = fma(c1[k2 - k], x1, acc1[k2]);
+                                        acc2[k2] = fma(c2[k2 - k], x2, acc2[k2]);
+                                    }
+                                    gpp1 = gp1;
+                                    gpp2 = gp2;
+                                    gp1 = x1;
+                                    gp2 = x2;
                                 }
-                                gpp1 = gp1;
-                                gpp2 = gp2;
-                                gp1 = x1;
-                                gp2 = x2;
-                            }
+                            };
+                            if (A.sbd)
+                                full_block(std::true_type{});
+                            else
+                                full_block(std::false_type{});
                         } else {
 #pragma unroll
                         for (int k = 0; k < 8; ++k) {
@@ -389,17 +410,10 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 320 && RB == 2) ? 2 : 1) k13_ke
                                     x1 = (r1 * f22 - f12 * r2) * dt;
                                     x2 = (f11 * r2 - f21 * r1) * dt;
                                 } else {
-                                    const double s1 = acc1[k], s2 = acc2[k];
-                                    double r1, r2;
-                                    if (A.sbd) {
-                                        r1 = (2.0 * gp1 - 0.5 * gpp1) * itau - al * s1 + a * s2;
-                                        r2 = (2.0 * gp2 - 0.5 * gpp2) * itau - al * s2 + a * s1;
-                                    } else {
-                                        r1 = gp1 * itau - al * s1 + a * s2;
-                                        r2 = gp2 * itau - al * s2 + a * s1;
-                                    }
-                                    x1 = (r1 * m22 - m12 * r2) * idet;
-                                    x2 = (m11 * r2 - m21 * r1) * idet;
+                                    const double t1 = A.sbd ? fma(2.0, gp1, -0.5 * gpp1) : gp1;
+                                    const double t2 = A.sbd ? fma(2.0, gp2, -0.5 * gpp2) : gp2;
+                                    x1 = fma(p11, acc1[k], fma(p12, acc2[k], fma(q11, t1, q12 * t2)));
+                                    x2 = fma(p21, acc1[k], fma(p22, acc2[k], fma(q21, t1, q22 * t2)));
                                 }
                                 ring[(n & mask) * MODES + d] = x1;
                                 ring[(RING + (n & mask)) * MODES + d] = x2;
