@@ -110,6 +110,10 @@ struct fraq_ctx_s {
     // scratch reused by setup kernels
     fraqcu::DevBuf<double> scratch_d;
     fraqcu::DevBuf<long> scratch_l;
+    // DST sine table of the last grid size (modal.cu ctx_sintab): built once per M, so DST calls
+    // inside a caller's timed region do no cudaMalloc / cudaFree
+    fraqcu::DevBuf<double> sintab;
+    int sintab_m = 0;
     double* scratch(size_t n) {
         if (scratch_d.n < n) scratch_d.alloc(n);
         return scratch_d.p;

@@ -355,7 +355,8 @@ struct ModalPlan {
 
 struct Dst2D {
     int M = 0;
-    DevBuf<double> tab, A, B;
+    const double* tab = nullptr;
+    DevBuf<double> A, B;
     void init(fraq_ctx c, int m);
     void apply(fraq_ctx c, int n_fields, const double* in, double* out, bool inverse);
 };
@@ -374,10 +375,15 @@ void transpose_dev(fraq_ctx c, const double* in, long rows, long cols, double* o
     FRAQ_LAUNCH_CHECK();
 }
 
-void make_sintab(fraq_ctx c, int M, DevBuf<double>& tab) {
-    tab.alloc((size_t)2 * (M + 1));
-    sintab_kernel<<<64, 256, 0, c->stream>>>(tab.p, M);
-    FRAQ_LAUNCH_CHECK();
+// the context's sine table for grid size M (built on the context's stream on first use)
+const double* ctx_sintab(fraq_ctx c, int M) {
+    if (c->sintab_m != M || !c->sintab.p) {
+        c->sintab.alloc((size_t)2 * (M + 1));
+        sintab_kernel<<<64, 256, 0, c->stream>>>(c->sintab.p, M);
+        FRAQ_LAUNCH_CHECK();
+        c->sintab_m = M;
+    }
+    return c->sintab.p;
 }
 
 // Mode-space stepping of n_inst instances with per-instance kernels (device tables already in
@@ -450,7 +456,7 @@ void modal_exec(fraq_ctx c, ModalPlan& P, const double* lam, int n_modes, long N
 // along y and x with transposes in between.
 void Dst2D::init(fraq_ctx c, int m) {
     M = m;
-    make_sintab(c, M, tab);
+    tab = ctx_sintab(c, M);
     A.alloc((size_t)M * M);
     B.alloc((size_t)M * M);
 }
@@ -459,9 +465,9 @@ void Dst2D::apply(fraq_ctx c, int n_fields, const double* in, double* out, bool 
     const long MM = (long)M * M;
     const double sc = inverse ? 1.0 : 2.0 / (M + 1);
     for (int f = 0; f < n_fields; ++f) {
-        dst_apply(c, M, tab.p, in + f * MM, M, A.p, sc);   // A[k][x]
+        dst_apply(c, M, tab, in + f * MM, M, A.p, sc);   // A[k][x]
         transpose_dev(c, A.p, M, M, B.p);                  // B[x][k]
-        dst_apply(c, M, tab.p, B.p, M, A.p, sc);           // A[l][k]
+        dst_apply(c, M, tab, B.p, M, A.p, sc);           // A[l][k]
         transpose_dev(c, A.p, M, M, out + f * MM);         // out[k][l]
     }
 }
@@ -596,20 +602,20 @@ void ffpe_run_modal(fraq_ctx c, const fraq_spec_t* specs, int n_inst, bool sbd,
         lam[k] = 4.0 / (h * h) * sk * sk;
     }
     DevBuf<double> dlam(M), dG((size_t)M * C), dW((size_t)M * C), dc0((size_t)M * C),
-        dcN((size_t)M * C), tab;
+        dcN((size_t)M * C);
     FRAQ_CUDA(cudaMemcpyAsync(dlam.p, lam.data(), sizeof(double) * M, cudaMemcpyHostToDevice, c->stream));
     FRAQ_CUDA(cudaMemcpyAsync(dG.p, G0.data(), sizeof(double) * G0.size(), cudaMemcpyHostToDevice,
                               c->stream));
-    make_sintab(c, M, tab);
+    const double* tab = ctx_sintab(c, M);
     const double t1 = now_s2();
     EventTimer timer(c->stream);
     // forward DST (projection, 2/(M+1) S G): rows = modes; then [C][M] for the stepper
-    dst_apply(c, M, tab.p, dG.p, C, dW.p, 2.0 / (M + 1));
+    dst_apply(c, M, tab, dG.p, C, dW.p, 2.0 / (M + 1));
     transpose_dev(c, dW.p, M, C, dc0.p);
     modal_exec(c, S.plan, dlam.p, M, N, dc0.p, dcN.p);
     // inverse: g = S^T c (S symmetric)
     transpose_dev(c, dcN.p, C, M, dW.p);
-    dst_apply(c, M, tab.p, dW.p, C, dG.p, 1.0);
+    dst_apply(c, M, tab, dW.p, C, dG.p, 1.0);
     const double loop_s = timer.stop();
     FRAQ_CUDA(cudaMemcpy(G0.data(), dG.p, sizeof(double) * G0.size(), cudaMemcpyDeviceToHost));
     for (int i = 0; i < n_inst; ++i)
@@ -703,16 +709,15 @@ void dst_cols(fraq_ctx c, int M, long n_cols, const double* in, double* out, boo
     if (n_cols == 0) return;
     const long n = (long)M * n_cols;
     const double sc = inverse ? 1.0 : 2.0 / (M + 1);
-    DevBuf<double> tab;
-    make_sintab(c, M, tab);
+    const double* tab = ctx_sintab(c, M);
     if (mem == FRAQ_DEVICE) {
-        dst_apply(c, M, tab.p, in, n_cols, out, sc);
+        dst_apply(c, M, tab, in, n_cols, out, sc);
         FRAQ_CUDA(cudaStreamSynchronize(c->stream));
         return;
     }
     DevBuf<double> di(n), dout(n);
     FRAQ_CUDA(cudaMemcpyAsync(di.p, in, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
-    dst_apply(c, M, tab.p, di.p, n_cols, dout.p, sc);
+    dst_apply(c, M, tab, di.p, n_cols, dout.p, sc);
     FRAQ_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
     FRAQ_CUDA(cudaStreamSynchronize(c->stream));
 }
