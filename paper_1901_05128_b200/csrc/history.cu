@@ -575,14 +575,14 @@ struct fraq_hist_s {
     int n_run3_tasks = 0;
     int last_path = 0;
     // chunk staging for host-memory runs
-    DevBuf<double> ubuf[2], dbuf[2];
+    static constexpr int kMaxStages = 4;
+    DevBuf<double> ubuf[kMaxStages], dbuf[kMaxStages];
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
-    cudaEvent_t ev_u[2] = {nullptr, nullptr}, ev_c[2] = {nullptr, nullptr},
-                ev_d[2] = {nullptr, nullptr};
+    cudaEvent_t ev_u[kMaxStages] = {}, ev_c[kMaxStages] = {}, ev_d[kMaxStages] = {};
     ~fraq_hist_s() {
         if (s_h2d) cudaStreamDestroy(s_h2d);
         if (s_d2h) cudaStreamDestroy(s_d2h);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kMaxStages; ++i) {
             if (ev_u[i]) cudaEventDestroy(ev_u[i]);
             if (ev_c[i]) cudaEventDestroy(ev_c[i]);
             if (ev_d[i]) cudaEventDestroy(ev_d[i]);
@@ -878,7 +878,11 @@ void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, l
     rows = std::max<long>(1, std::min<long>(rows, std::max<long>(1, n_steps)));
     // a remainder under 32 rows joins the last chunk (keeps it on the blocked kernels)
     const long cap_rows = rows + 31;
-    for (int i = 0; i < 2; ++i) {
+    // staging depth: copies may run up to ns - 1 chunks ahead of / behind the kernel
+    int ns = 2;
+    if (const char* es = std::getenv("FRAQ_HOST_STAGES"))  // experiment override
+        if (*es) ns = std::max(2, std::min(fraq_hist_s::kMaxStages, std::atoi(es)));
+    for (int i = 0; i < ns; ++i) {
         if ((long)h->ubuf[i].n < cap_rows * dim) h->ubuf[i].alloc(cap_rows * dim);
         if (D && (long)h->dbuf[i].n < cap_rows * dim) h->dbuf[i].alloc(cap_rows * dim);
         if (!h->ev_u[i]) {
@@ -893,20 +897,20 @@ void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, l
     }
     cudaStream_t sc = h->ctx->stream;
     // copies may only start after earlier work on the compute stream (state + buffers)
-    FRAQ_CUDA(cudaEventRecord(h->ev_c[0], sc));
-    FRAQ_CUDA(cudaEventRecord(h->ev_c[1], sc));
-    FRAQ_CUDA(cudaEventRecord(h->ev_d[0], sc));
-    FRAQ_CUDA(cudaEventRecord(h->ev_d[1], sc));
+    for (int j = 0; j < ns; ++j) {
+        FRAQ_CUDA(cudaEventRecord(h->ev_c[j], sc));
+        FRAQ_CUDA(cudaEventRecord(h->ev_d[j], sc));
+    }
     long i = 0;
     for (long n0 = 0, nr = 0; n0 < n_steps; n0 += nr, ++i) {
-        const int b = (int)(i & 1);
+        const int b = (int)(i % ns);
         nr = (n_steps - n0 - rows < 32) ? n_steps - n0 : rows;
-        // H2D into ubuf[b] once the kernel that last read it (chunk i-2) finished
+        // H2D into ubuf[b] once the kernel that last read it (chunk i - ns) finished
         FRAQ_CUDA(cudaStreamWaitEvent(h->s_h2d, h->ev_c[b], 0));
         FRAQ_CUDA(cudaMemcpy2DAsync(h->ubuf[b].p, dim * 8, U + n0 * ldu, ldu * 8,
                                     h->d.total_dim * 8, nr, cudaMemcpyHostToDevice, h->s_h2d));
         FRAQ_CUDA(cudaEventRecord(h->ev_u[b], h->s_h2d));
-        // kernel on chunk i: needs its inputs and dbuf[b] drained by the D2H of chunk i-2
+        // kernel on chunk i: needs its inputs and dbuf[b] drained by the D2H of chunk i - ns
         FRAQ_CUDA(cudaStreamWaitEvent(sc, h->ev_u[b], 0));
         if (D) FRAQ_CUDA(cudaStreamWaitEvent(sc, h->ev_d[b], 0));
         run_device(h, h->ubuf[b].p, dim, nr, D ? h->dbuf[b].p : nullptr, dim);
