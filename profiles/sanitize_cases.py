@@ -1,0 +1,169 @@
+"""Tiny invocations of every kernel family, each cross-checked against a second path (another
+kernel, the per-level API, or a direct sum).  SURVEY.md §5 asks for compute-sanitizer runs on
+small configs.  compute-sanitizer is closed on this GPU pool (runs under it have left GPUs
+needing a reset), so these cases run plainly.  They exercise odd sizes and the edges of each
+kernel's shape range, and the same script runs under the sanitizer where it is allowed:
+
+    python profiles/sanitize_cases.py [case ...]
+    compute-sanitizer --tool memcheck python profiles/sanitize_cases.py   # where permitted
+
+Cases: setup (K1-K4, K7 auto sizing), k5 (per-level history, both variants), k5d (blocked,
+TMA-staged), k5c (head window > 32 levels), k10 (direct CQ), host (chunked host-buffer run),
+k13 (modal BE/SBD, two-CTA shape), k13w (wide CTA, J > 256), k11 (modal fallback), k6 (physical
+stepper), dst2d (2D DST + K13).
+"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1901_05128_b200 as fraq  # noqa: E402
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def case_setup():
+    b = fraq.KernelBudget(horizon=600, eps_tol=1e-12)
+    k = fraq.build_sbd_kernel_auto(0.6, 1.0 / 600, b)
+    e = fraq.KernelBudget(horizon=600, eps_tol=1e-12)
+    kb = fraq.build_be_kernel_auto(0.35, 1.0 / 600, e)
+    assert len(k.ratio1) > 0 and len(kb.ratios) > 0 and b.achieved_eps > 0
+
+
+def case_k5():
+    k = fraq.build_sbd_kernel(0.4, 0.05, 20, 20, 8)
+    rng = np.random.default_rng(1)
+    U = rng.uniform(-1, 1, (24, 5))
+    for var in (fraq.HistoryVariant.standalone, fraq.HistoryVariant.scheme):
+        h = fraq.SbdHistory(k, var, 5)
+        h2 = fraq.SbdHistory(k, var, 5)
+        out = []
+        for n in range(24):
+            h.push(list(U[n]))
+            if n >= 1:
+                out.append(np.array(h.derivative()))
+        D = h2.run(U)
+        assert rel(np.array(out), D[1:]) <= 1e-10
+
+
+def _blocked(points, dim, levels):
+    k = fraq.build_be_kernel(0.5, 1.0 / 4096, points)
+    rng = np.random.default_rng(2)
+    U = rng.uniform(-1, 1, (levels, dim))
+    h = fraq.BeHistory(k, fraq.HistoryVariant.standalone, dim)
+    D = h.run(U)
+    hs = fraq.BeHistory(k, fraq.HistoryVariant.standalone, dim)
+    ref = []
+    for n in range(levels):
+        hs.push(list(U[n]))
+        ref.append(np.array(hs.derivative()) if n >= 1 else np.full(dim, np.nan))
+    assert rel(D[1:], np.array(ref[1:])) <= 1e-10
+    return h.last_path
+
+
+def case_k5d():
+    assert _blocked(64, 16, 96) == 3
+
+
+def case_k5c():
+    k = fraq.build_sbd_kernel(0.7, 1.0 / 1024, 16, 16, 40)  # head window 40 > 32
+    rng = np.random.default_rng(3)
+    U = rng.uniform(-1, 1, (80, 8))
+    h = fraq.SbdHistory(k, fraq.HistoryVariant.standalone, 8)
+    D = h.run(U)
+    hs = fraq.SbdHistory(k, fraq.HistoryVariant.standalone, 8)
+    for n in range(80):
+        hs.push(list(U[n]))
+        if n >= 1:
+            assert rel(D[n], np.array(hs.derivative())) <= 1e-10
+
+
+def case_k10():
+    rng = np.random.default_rng(4)
+    U = rng.uniform(-1, 1, (130, 3))
+    Dd = fraq.direct_cq(True, 0.4, 1.0 / 512, U)
+    w = list(fraq.sbd_weights(0.4, 1.0 / 512, 129).weights)
+    ref = np.array([[sum(w[i] * U[n - i, j] for i in range(n + 1)) for j in range(3)]
+                    for n in range(130)])
+    assert rel(Dd, ref) <= 1e-10
+
+
+def case_host():
+    k = fraq.build_be_kernel(0.5, 1.0 / 4096, 64)
+    rng = np.random.default_rng(5)
+    U = rng.uniform(-1, 1, (200, 48))
+    h = fraq.BeHistory(k, fraq.HistoryVariant.standalone, 48)
+    os.environ["FRAQ_HOST_CHUNK"] = "32"
+    D = h.run(U)
+    os.environ["FRAQ_HOST_CHUNK"] = ""
+    h2 = fraq.BeHistory(k, fraq.HistoryVariant.standalone, 48)
+    assert rel(D[1:], h2.run(U)[1:]) <= 1e-12
+
+
+def _modal(scheme, m, N, **kw):
+    spec = fraq.ProblemSpec(alpha1=0.35, alpha2=0.75, coupling_a=-2.5, grid_m=m, t_final=0.7,
+                            n_steps=N, initial="poly_sin")
+    kc = fraq.KernelConfig()
+    kc.solver = fraq.SOLVER_MODAL
+    for a, v in kw.items():
+        setattr(kc, a, v)
+    return fraq.run(spec, getattr(fraq.Scheme, scheme), kc), spec, kc
+
+
+def case_k13():
+    for sc in ("FastBE", "FastSBD"):
+        r, spec, kc = _modal(sc, 37, 29)
+        os.environ["FRAQ_MODAL_K11"] = "1"
+        r11 = fraq.run(spec, getattr(fraq.Scheme, sc), kc)
+        os.environ["FRAQ_MODAL_K11"] = ""
+        assert rel(r.final_state.g1, r11.final_state.g1) <= 1e-12
+
+
+def case_k13w():
+    r, spec, kc = _modal("FastSBD", 40, 21, auto_size=False, be_points=64, sbd_points_1=150,
+                         sbd_points_2=150)
+    os.environ["FRAQ_MODAL_K11"] = "1"
+    r11 = fraq.run(spec, fraq.Scheme.FastSBD, kc)
+    os.environ["FRAQ_MODAL_K11"] = ""
+    assert rel(r.final_state.g2, r11.final_state.g2) <= 1e-12
+
+
+def case_k11():
+    os.environ["FRAQ_MODAL_K11"] = "1"
+    r, _, _ = _modal("FastBE", 21, 17)
+    os.environ["FRAQ_MODAL_K11"] = ""
+    assert np.all(np.isfinite(r.final_state.g1))
+
+
+def case_k6():
+    spec = fraq.ProblemSpec(alpha1=0.3, alpha2=0.6, coupling_a=2.0, grid_m=31, t_final=0.25,
+                            n_steps=20)
+    out = {}
+    for solver in (fraq.SOLVER_PHYSICAL, fraq.SOLVER_MODAL):
+        kc = fraq.KernelConfig()
+        kc.solver = solver
+        out[solver] = fraq.run(spec, fraq.Scheme.FastSBD, kc).final_state.g1
+    assert rel(out[fraq.SOLVER_PHYSICAL], out[fraq.SOLVER_MODAL]) <= 1e-9
+
+
+def case_dst2d():
+    m = 7
+    rng = np.random.default_rng(6)
+    g1 = rng.uniform(0, 1, m * m)
+    g2 = rng.uniform(0, 1, m * m)
+    out = fraq.run_2d(0.3, 0.6, -3.0, m, 0.25, 12, fraq.Scheme.FastSBD, g1, g2)
+    assert np.all(np.isfinite(out.final_state.g1))
+
+
+CASES = {n[5:]: f for n, f in globals().items() if n.startswith("case_")}
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(CASES)
+    for n in names:
+        CASES[n]()
+        print("ok", n, flush=True)
+    fraq.synchronize()
