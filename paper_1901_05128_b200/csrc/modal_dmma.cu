@@ -129,13 +129,15 @@ __global__ void k13_tables_kernel(const K13TabSrc* src, int Jp, int delta, doubl
 // RB: 8-mode row blocks per CTA (modes = 8 RB); NT: 8-node tiles per GEMM warp; MAXT: threads.
 // * RB = 2, NT = 8, MAXT = 320 (J <= 256; ~90 KB of shared memory): two CTAs per SM, so one
 //   CTA's solver phase overlaps the other's GEMMs and each SM sub-partition runs 4 GEMM warps.
-// * RB = 2, NT = 8, MAXT = 576 (256 < J <= 512, "wide"): 16 modes x 64 nodes per GEMM warp,
-//   up to 8 GEMM warps per field + 2 solver warps, one CTA per SM (the tables of J = 512 take
-//   140 KB).  16 modes per task double the GEMM work behind each sequential 8-level solve.
+// * RB = 2, NT = 9 / 11, MAXT = 448 (256 < J <= 432 / <= 512, "wide"): 16 modes x 72 / 88
+//   nodes per GEMM warp, up to 6 GEMM warps per field + 2 solver warps, one CTA per SM (the
+//   tables of J = 512 take 140 KB).  16 modes per task double the GEMM work behind each
+//   sequential 8-level solve; 3 GEMM warps per SM sub-partition leave the solver more of the
+//   fp64 pipe than 4.  (NT = 8, MAXT = 576: up to 8 GEMM warps per field, FRAQ_K13_NT=8.)
 // * RB = 1 (NT = 12..16, MAXT = 320): 8 modes, 4 GEMM warps per field, one CTA per SM (~170
 //   registers per thread for the state fragments); kept as the FRAQ_K13_NARROW experiment path.
 template <int RB, int NT, int MAXT>
-__global__ void __launch_bounds__(MAXT, (MAXT == 320 && RB == 2) ? 2 : 1) k13_kernel(K13Args A) {
+__global__ void __launch_bounds__(MAXT, (MAXT <= 320 && RB == 2) ? 2 : 1) k13_kernel(K13Args A) {
     constexpr int MODES = 8 * RB;
     extern __shared__ double ksm[];
     const int nwg = A.nwg, nwf = A.nwf, TS = A.TS, Jp = A.Jp;
@@ -486,6 +488,15 @@ void k13_prepare(fraq_ctx c, const std::vector<K13Inst>& in, bool sbd, K13Plan& 
     const char* narrow = std::getenv("FRAQ_K13_NARROW");  // experiment switch: RB = 1 for J > 256
     P.RB = (maxJ <= 256 || !(narrow && *narrow)) ? 2 : 1;
     P.NT = 8;
+    // J > 256: wider GEMM warps, at most 6 per field (448 threads, 128 registers): 72 nodes
+    // per warp up to J = 432 (C4: 408 nodes -> 432 instead of 448 padded, 3 GEMM warps per SM
+    // sub-partition instead of 4: C4 K13 loop -11%), 88 nodes beyond (C5-BDF2, 512: +2.9%)
+    if (P.RB == 2 && maxJ > 256) P.NT = maxJ <= 432 ? 9 : 11;
+    if (const char* ent = std::getenv("FRAQ_K13_NT")) {  // experiment override (8, 9, 11)
+        const int nt = std::atoi(ent);
+        if (P.RB == 2 && (nt == 8 || ((nt == 9 || nt == 11) && (maxJ + 8 * nt - 1) / (8 * nt) <= 6)))
+            P.NT = nt;
+    }
     if (P.RB == 1) {
         P.NT = 16;
         for (int cand : {12, 13, 14})
@@ -549,7 +560,11 @@ void k13_exec(fraq_ctx c, K13Plan& P, const double* lam, int n_modes, long N, co
     A.counter = P.counter.p;
     FRAQ_CUDA(cudaMemsetAsync(P.counter.p, 0, sizeof(int), c->stream));
     const size_t smem = k13_smem(P.TS, P.nwg, P.ring, modes);
-    if (P.RB == 2 && P.nwg <= 8)
+    if (P.RB == 2 && P.NT == 9)
+        k13_launch<2, 9, 448>(A, smem, c->num_sms, c->stream);
+    else if (P.RB == 2 && P.NT == 11)
+        k13_launch<2, 11, 448>(A, smem, c->num_sms, c->stream);
+    else if (P.RB == 2 && P.nwg <= 8)
         k13_launch<2, 8, 320>(A, smem, c->num_sms, c->stream);
     else if (P.RB == 2)
         k13_launch<2, 8, 576>(A, smem, c->num_sms, c->stream);
