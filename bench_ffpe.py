@@ -219,8 +219,14 @@ def run_gpu(args, rank, world, local, pg, METRIC, Clocks, fraq, torch):
     if pg:
         pg.barrier()
     torch.cuda.synchronize()
+    import gc
     with Clocks(local) as clk:
         for s in range(K):
+            # no Python garbage collection inside a step: a full collection stalls the host
+            # thread that issues the next phase's launches, and C4's device phase times
+            # (events around host-issued phases) then include 20-150 ms of idle GPU
+            gc.collect()
+            gc.disable()
             flush.zero_()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
@@ -230,6 +236,7 @@ def run_gpu(args, rank, world, local, pg, METRIC, Clocks, fraq, torch):
                 flush.zero_()
                 torch.cuda.synchronize()
                 loop, rs = wl.solve(fraq, specs[s], torch, device_inputs=True)
+            gc.enable()
             loops.append(loop)
         torch.cuda.synchronize()
     r0 = rs[0]

@@ -129,11 +129,11 @@ __global__ void k13_tables_kernel(const K13TabSrc* src, int Jp, int delta, doubl
 // RB: 8-mode row blocks per CTA (modes = 8 RB); NT: 8-node tiles per GEMM warp; MAXT: threads.
 // * RB = 2, NT = 8, MAXT = 320 (J <= 256; ~90 KB of shared memory): two CTAs per SM, so one
 //   CTA's solver phase overlaps the other's GEMMs and each SM sub-partition runs 4 GEMM warps.
-// * RB = 2, NT = 9 / 11, MAXT = 448 (256 < J <= 432 / <= 512, "wide"): 16 modes x 72 / 88
-//   nodes per GEMM warp, up to 6 GEMM warps per field + 2 solver warps, one CTA per SM (the
-//   tables of J = 512 take 140 KB).  16 modes per task double the GEMM work behind each
-//   sequential 8-level solve; 3 GEMM warps per SM sub-partition leave the solver more of the
-//   fp64 pipe than 4.  (NT = 8, MAXT = 576: up to 8 GEMM warps per field, FRAQ_K13_NT=8.)
+// * RB = 2, NT = 13 / 16, MAXT = 384 (256 < J <= 416 / <= 512, "wide"): 16 modes x 104 / 128
+//   nodes per GEMM warp, 4 GEMM warps per field + 2 solver warps, one CTA per SM (the tables
+//   of J = 512 take 140 KB).  16 modes per task double the GEMM work behind each sequential
+//   8-level solve; 2 GEMM warps per SM sub-partition beat 3 or 4 narrower ones.  (NT = 8,
+//   MAXT = 576, up to 8 GEMM warps per field: FRAQ_K13_NT=8.)
 // * RB = 1 (NT = 12..16, MAXT = 320): 8 modes, 4 GEMM warps per field, one CTA per SM (~170
 //   registers per thread for the state fragments); kept as the FRAQ_K13_NARROW experiment path.
 template <int RB, int NT, int MAXT>
@@ -488,13 +488,15 @@ void k13_prepare(fraq_ctx c, const std::vector<K13Inst>& in, bool sbd, K13Plan& 
     const char* narrow = std::getenv("FRAQ_K13_NARROW");  // experiment switch: RB = 1 for J > 256
     P.RB = (maxJ <= 256 || !(narrow && *narrow)) ? 2 : 1;
     P.NT = 8;
-    // J > 256: wider GEMM warps, at most 6 per field (448 threads, 128 registers): 72 nodes
-    // per warp up to J = 432 (C4: 408 nodes -> 432 instead of 448 padded, 3 GEMM warps per SM
-    // sub-partition instead of 4: C4 K13 loop -11%), 88 nodes beyond (C5-BDF2, 512: +2.9%)
-    if (P.RB == 2 && maxJ > 256) P.NT = maxJ <= 432 ? 9 : 11;
-    if (const char* ent = std::getenv("FRAQ_K13_NT")) {  // experiment override (8, 9, 11)
+    // J > 256: four GEMM warps per field of 104 nodes (J <= 416; C4: 408 -> 416) or 128 nodes
+    // (J <= 512; C5-BDF2: 512), 10 warps, ~168 registers.  Measured against 64 / 72 / 88-node
+    // warps (8 / 6 / 6 per field): C4 K13 loop 1406 (64) -> 1269 (72) -> 1171 ms (104);
+    // C5-shaped BDF2 1.112e10 (64) -> 1.144e10 (88) -> 1.234e10 DOF-steps/s (128).  Fewer GEMM
+    // warps per SM sub-partition (2 instead of 4) hold the same DMMA work.
+    if (P.RB == 2 && maxJ > 256) P.NT = maxJ <= 416 ? 13 : 16;
+    if (const char* ent = std::getenv("FRAQ_K13_NT")) {  // experiment override: 8, 13 or 16
         const int nt = std::atoi(ent);
-        if (P.RB == 2 && (nt == 8 || ((nt == 9 || nt == 11) && (maxJ + 8 * nt - 1) / (8 * nt) <= 6)))
+        if (P.RB == 2 && (nt == 8 || (nt == 13 && maxJ <= 416) || (nt == 16 && maxJ > 256)))
             P.NT = nt;
     }
     if (P.RB == 1) {
@@ -560,10 +562,10 @@ void k13_exec(fraq_ctx c, K13Plan& P, const double* lam, int n_modes, long N, co
     A.counter = P.counter.p;
     FRAQ_CUDA(cudaMemsetAsync(P.counter.p, 0, sizeof(int), c->stream));
     const size_t smem = k13_smem(P.TS, P.nwg, P.ring, modes);
-    if (P.RB == 2 && P.NT == 9)
-        k13_launch<2, 9, 448>(A, smem, c->num_sms, c->stream);
-    else if (P.RB == 2 && P.NT == 11)
-        k13_launch<2, 11, 448>(A, smem, c->num_sms, c->stream);
+    if (P.RB == 2 && P.NT == 13)
+        k13_launch<2, 13, 384>(A, smem, c->num_sms, c->stream);
+    else if (P.RB == 2 && P.NT == 16)
+        k13_launch<2, 16, 384>(A, smem, c->num_sms, c->stream);
     else if (P.RB == 2 && P.nwg <= 8)
         k13_launch<2, 8, 320>(A, smem, c->num_sms, c->stream);
     else if (P.RB == 2)

@@ -20,10 +20,14 @@ g1, g2 = ops.tensor(i.g1), ops.tensor(i.g2)
 drivers = (("sharded", run_2d_sharded), ("transposed", run_2d_transposed))
 if len(sys.argv) > 2:
     drivers = [d for d in drivers if d[0] == sys.argv[2]]
+import gc
 for rep in range(2):
     for name, fn in drivers:
+        gc.collect()
+        gc.disable()  # no collection pauses inside the timed phases
         T = {}
         r1, r2 = fn(ops, i.alpha1, i.alpha2, i.coupling_a, M, N / 8192, N, "FastSBD", g1, g2,
                     kconf=kc, scheme_arg=fraq.Scheme.FastSBD, timings=T)
+        gc.enable()
         print(name, {k: round(v * 1e3, 3) for k, v in T.items()}, "ms",
               float(r1.abs().sum()), float(r2.abs().sum()))
