@@ -127,8 +127,10 @@ __global__ void k13_tables_kernel(const K13TabSrc* src, int Jp, int delta, doubl
 }
 
 // RB: 8-mode row blocks per CTA (modes = 8 RB); NT: 8-node tiles per GEMM warp; MAXT: threads.
-// * RB = 2, NT = 8, MAXT = 320 (J <= 256; ~90 KB of shared memory): two CTAs per SM, so one
+// * RB = 2, NT = 8, MAXT = 320 (J <= 192; ~90 KB of shared memory): two CTAs per SM, so one
 //   CTA's solver phase overlaps the other's GEMMs and each SM sub-partition runs 4 GEMM warps.
+// * RB = 2, NT = 16, MAXT = 384 launched with 192 threads (192 < J <= 256): 2 GEMM warps per
+//   field, still two CTAs per SM (2 GEMM warps + 1 solver warp per SM sub-partition).
 // * RB = 2, NT = 13 / 16, MAXT = 384 (256 < J <= 416 / <= 512, "wide"): 16 modes x 104 / 128
 //   nodes per GEMM warp, 4 GEMM warps per field + 2 solver warps, one CTA per SM (the tables
 //   of J = 512 take 140 KB).  16 modes per task double the GEMM work behind each sequential
@@ -494,9 +496,12 @@ void k13_prepare(fraq_ctx c, const std::vector<K13Inst>& in, bool sbd, K13Plan& 
     // C5-shaped BDF2 1.112e10 (64) -> 1.144e10 (88) -> 1.234e10 DOF-steps/s (128).  Fewer GEMM
     // warps per SM sub-partition (2 instead of 4) hold the same DMMA work.
     if (P.RB == 2 && maxJ > 256) P.NT = maxJ <= 416 ? 13 : 16;
+    // J in (192, 256] (C3, C5-BE): 2 GEMM warps per field of 128 nodes, 6 warps per CTA, two
+    // CTAs per SM (168 registers x 192 threads x 2 fit): C5-shaped BE 2.360e10 -> 2.499e10
+    if (P.RB == 2 && maxJ > 192 && maxJ <= 256) P.NT = 16;
     if (const char* ent = std::getenv("FRAQ_K13_NT")) {  // experiment override: 8, 13 or 16
         const int nt = std::atoi(ent);
-        if (P.RB == 2 && (nt == 8 || (nt == 13 && maxJ <= 416) || (nt == 16 && maxJ > 256)))
+        if (P.RB == 2 && (nt == 8 || (nt == 13 && maxJ <= 416) || nt == 16))
             P.NT = nt;
     }
     if (P.RB == 1) {
