@@ -111,24 +111,31 @@ def test_k13_tensor_core_path_matches_k11(fraq, scheme, m, N, monkeypatch):
     assert rel(k13.final_state.g2, k11.final_state.g2) <= 1e-12
 
 
-@pytest.mark.parametrize("scheme,pts", [("FastBE", 300), ("FastBE", 509), ("FastSBD", 150),
+@pytest.mark.parametrize("scheme,pts", [("FastBE", 200), ("FastBE", 256), ("FastBE", 300),
+                                        ("FastBE", 509), ("FastSBD", 100), ("FastSBD", 150),
                                         ("FastSBD", 256)])
-def test_k13_wide_cta_matches_narrow_and_k11(fraq, scheme, pts, monkeypatch):
-    """Nodes per field in (256, 512]: the wide K13 CTA (16 modes, up to 16 GEMM warps of 64
-    nodes) against the 8-mode experiment path (FRAQ_K13_NARROW) and K11, on a ragged mode count
-    (1000) and level count (77); J = 300 and 509 (BE), 2 x 150 and 2 x 256 (SBD families)."""
+def test_k13_warp_shapes_agree(fraq, scheme, pts, monkeypatch):
+    """Every K13 CTA shape on a ragged mode count (1000) and level count (77): the default shape
+    for the node count (128-node GEMM warps for J in (192, 256], 104 / 128-node warps in the
+    wide CTA for J in (256, 416] / (416, 512]) against 64-node warps (FRAQ_K13_NT=8), the
+    8-mode path (FRAQ_K13_NARROW, J > 256) and K11.  J = 200, 256, 300, 509 (BE) and 2 x 100,
+    2 x 150, 2 x 256 (SBD families)."""
     spec = fraq.ProblemSpec(alpha1=0.35, alpha2=0.75, coupling_a=-2.5, grid_m=1000, t_final=0.7,
                             n_steps=77, initial="poly_sin")
     kc = modal_kc(fraq, auto_size=False, be_points=pts, sbd_points_1=pts, sbd_points_2=pts)
-    wide = fraq.run(spec, getattr(fraq.Scheme, scheme), kc)
+    sch = getattr(fraq.Scheme, scheme)
+    runs = [fraq.run(spec, sch, kc)]
+    monkeypatch.setenv("FRAQ_K13_NT", "8")
+    runs.append(fraq.run(spec, sch, kc))
+    monkeypatch.delenv("FRAQ_K13_NT")
     monkeypatch.setenv("FRAQ_K13_NARROW", "1")
-    narrow = fraq.run(spec, getattr(fraq.Scheme, scheme), kc)
+    runs.append(fraq.run(spec, sch, kc))
     monkeypatch.setenv("FRAQ_MODAL_K11", "1")
-    k11 = fraq.run(spec, getattr(fraq.Scheme, scheme), kc)
+    runs.append(fraq.run(spec, sch, kc))
     for g in ("g1", "g2"):
-        w, n, k = (np.array(getattr(r.final_state, g)) for r in (wide, narrow, k11))
-        assert rel(w, n) <= 1e-12
-        assert rel(w, k) <= 1e-12
+        ref = np.array(getattr(runs[-1].final_state, g))
+        for r in runs[:-1]:
+            assert rel(np.array(getattr(r.final_state, g)), ref) <= 1e-12
 
 
 def test_k13_batch_mixed_instances(fraq, orc):
