@@ -569,6 +569,8 @@ void k13_exec(fraq_ctx c, K13Plan& P, const double* lam, int n_modes, long N, co
     const size_t smem = k13_smem(P.TS, P.nwg, P.ring, modes);
     if (P.RB == 2 && P.NT == 13)
         k13_launch<2, 13, 384>(A, smem, c->num_sms, c->stream);
+    else if (P.RB == 2 && P.NT == 16 && P.nwg <= 4)  // J <= 256: two CTAs per SM
+        k13_launch<2, 16, 192>(A, smem, c->num_sms, c->stream);
     else if (P.RB == 2 && P.NT == 16)
         k13_launch<2, 16, 384>(A, smem, c->num_sms, c->stream);
     else if (P.RB == 2 && P.nwg <= 8)
