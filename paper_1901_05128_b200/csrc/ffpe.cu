@@ -502,8 +502,7 @@ void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
     DevBuf<double> corr(1);
     if (fast && sbd) {
         corr.alloc((size_t)2 * n_inst * (N + 1));
-        for (int t = 0; t < 2 * n_inst; ++t)
-            corr_sequence_dev(c, &ks[t], N, corr.p + (size_t)t * (N + 1));
+        corr_sequence_batch_dev(c, ks.data(), 2 * n_inst, N, corr.p, N + 1);
         for (int i = 0; i < n_inst; ++i) {
             inst[i].corr_off1 = (long)(2 * i) * (N + 1);
             inst[i].corr_off2 = (long)(2 * i + 1) * (N + 1);

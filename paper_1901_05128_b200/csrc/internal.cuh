@@ -144,6 +144,8 @@ void reconstruct_dev(fraq_ctx c, const fraq_kernel_t* k, long n, const long* idx
 // corr_d[e] = sum_j m_j p_j(e) with p_j(e) = r_j multiplied e times from 1 (fpfp.cpp:240-250),
 // for e = 0..e_max.  Device buffer out.
 void corr_sequence_dev(fraq_ctx c, const fraq_kernel_t* k, long e_max, double* corr_d);
+void corr_sequence_batch_dev(fraq_ctx c, const fraq_kernel_t* ks, int n, long e_max,
+                             double* corr_base, long stride);
 // direct.cu: classical O(N^2) CQ on DMMA (device pointers)
 void direct_cq_dev(fraq_ctx c, int sbd, double g, double tau, const double* U, long ldu,
                    long n_steps, long dim, double* D, long ldd);

@@ -511,10 +511,8 @@ void modal_prepare(fraq_ctx c, ModalSetup& S, const std::vector<double>& gam,
     S.corr_off.assign(ng, 0);
     if (sbd) {
         S.corr.alloc((size_t)ng * (N + 1));
-        for (int t = 0; t < ng; ++t) {
-            corr_sequence_dev(c, &S.ks[t], N, S.corr.p + (size_t)t * (N + 1));
-            S.corr_off[t] = (long)t * (N + 1);
-        }
+        corr_sequence_batch_dev(c, S.ks.data(), ng, N, S.corr.p, N + 1);
+        for (int t = 0; t < ng; ++t) S.corr_off[t] = (long)t * (N + 1);
     }
     const int n_inst = ng / 2;
     modal_plan(c, S.hd, a, std::vector<double>(n_inst, tau), sbd ? S.corr.p : nullptr, S.corr_off,
