@@ -4,7 +4,7 @@
 Workload C2: batched Riemann-Liouville derivative with the BDF2 (SBD) fast CQ, 65536 DOFs per GPU
 (CQ exponent 0.7 on the first half, 0.3 on the second), tau = 1/65536, reference auto-sized
 kernels (256 + 256 nodes, N_s = 17 / 15).  Signals u_k(t) = a_k t^b_k + c_k sin(w_k t), seeded
-(paper_1901_05128_b200/workloads.py), generated on the device before timing.
+(workloads.py), generated on the device before timing.
 
 One bench step = one pass of the hot path over the batch for LEVELS_PER_STEP (1024) time levels:
 push + derivative for every DOF at every level, through MultiHistory.run_device on device buffers
@@ -105,31 +105,41 @@ def reference_kernels(orc, tau):
             orc.build_kernel_auto(True, 1.0 - 0.7, tau, N_LEVELS)]
 
 
-def cpu_sample(orc, kernels, params, threads, target_s, dofs=DOFS):
+def c2_config(world, nodes, n_head, scaling="weak"):
+    """The workload description both arms print (identical dicts: same_config)."""
+    per = DOFS if scaling == "weak" else -(-DOFS // world)
+    return {
+        "workload": "C2: BDF2 fast CQ, 65536 DOFs (gamma 0.7 | 0.3), tau = 1/65536, N = 65536 "
+                    "levels; one step = 1024 levels x all DOFs (push+derivative)",
+        "dofs_per_gpu": per, "levels_per_step": LEVELS_PER_STEP,
+        "nodes": list(nodes), "n_head": list(n_head),
+        "l2": "inputs larger than L2 (537 MB of signal per step)",
+        "parallelism": (f"dof-sharded x{world}, no data-path collective" if scaling == "weak" else
+                        f"65536 / {world} DOFs per GPU (strong), no data-path collective")}
+
+
+def cpu_sample(orc, kernels, params, threads, levels, dofs=DOFS, U=None):
     """Times the reference SbdHistory (push + derivative per level) on the FULL C2 DOF set (both
-    exponent halves; each of `threads` host threads owns a contiguous DOF slice, so the per-thread
-    working set -- and hence the memory behaviour -- is that of a full run) for a bounded number
-    of levels sized to ~target_s seconds.  Per-level cost does not depend on the level index once
-    the lag window is full, so DOF-steps/s over the sample equals the full-run rate.
-    Returns (DOF-steps/s, sample description, seconds)."""
-    idx = np.arange(dofs)
-    warm = 32
-    U = params.signal(0, warm, idx)
-    secs, _ = orc.bench_history(kernels, U, threads)
-    rate = dofs * warm / max(secs, 1e-6)
-    levels = int(min(max(64, target_s * rate / dofs), 1024))
-    U = params.signal(0, levels, idx)
-    secs, _ = orc.bench_history(kernels, U, threads)
+    exponent halves; each of `threads` host threads owns a contiguous DOF slice, the run_convergence
+    worker-pool pattern of bench.cpp:194-223) for `levels` levels from level 0.  Per-level cost does
+    not depend on the level index once the lag window is full, so DOF-steps/s over the sample equals
+    the full-run rate.  Returns (DOF-steps/s, sample description, seconds)."""
+    if U is None:
+        U = params.signal(0, levels, np.arange(dofs))
+    secs, _ = orc.bench_history(kernels, U[:levels], threads)
     return (dofs * levels / secs, f"all {dofs} DOFs x {levels} levels (per-thread DOF slices "
             f"as in a full run)", secs)
 
 
 def run_reference_arm(args):
+    """The reference's own CPU implementation (oracle/_ref = the unmodified reference sources) on
+    the host cores, on the GPU arm's workload: one step = all 65536 DOFs x 1024 levels.  Maps no
+    library of the B200 package (checked)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     from oracle.oracle import Oracle, ref_available
-    from paper_1901_05128_b200.workloads import c2_params
+    from workloads import c2_params
     if not ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
@@ -137,22 +147,24 @@ def run_reference_arm(args):
     params = c2_params()
     kernels = reference_kernels(orc, params.tau)
     threads = os.cpu_count() or 1
-    target = 1.5  # seconds of CPU work per step
+    U = params.signal(0, LEVELS_PER_STEP, np.arange(DOFS))
     for _ in range(args.warmup):
-        cpu_sample(orc, kernels, params, threads, target / 4)
+        cpu_sample(orc, kernels, params, threads, LEVELS_PER_STEP // 8, U=U)
     vals, times = [], []
     for _ in range(args.steps):
-        v, sample, secs = cpu_sample(orc, kernels, params, threads, target)
+        v, sample, secs = cpu_sample(orc, kernels, params, threads, LEVELS_PER_STEP, U=U)
         vals.append(v)
         times.append(secs)
-    value = float(np.median(vals))
+    value = DOFS * LEVELS_PER_STEP * args.steps / sum(times)
+    loaded = sorted(m for m in sys.modules if m.startswith("paper_1901_05128_b200"))
+    assert not loaded, f"reference arm imported the B200 package: {loaded}"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C2 (BDF2 fast CQ, 65536 DOFs, gamma 0.7 | 0.3, N = 65536)",
-                   "dofs_per_gpu": DOFS, "levels_per_step": LEVELS_PER_STEP},
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": c2_config(world, [len(k.r1) + len(k.r2) for k in kernels],
+                            [k.n_head for k in kernels], args.scaling),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": sample + " per step; reference SbdHistory push+derivative, "
                                             "per-thread DOF slices (bench.cpp:194-223 pattern)"},
@@ -170,6 +182,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="C2: 65536 DOFs per GPU (weak, default) or 65536 / N per GPU (strong, "
+                         "SURVEY.md §8(e))")
     ap.add_argument("--workload", default="C2", choices=["C2", "C3", "C4", "C5", "C5-SBD"],
                     help="C2 (default, BASELINE configs[1]) or an FFPE config (bench_ffpe.py)")
     args = ap.parse_args()
@@ -195,7 +210,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = dist
     import paper_1901_05128_b200 as fraq
-    from paper_1901_05128_b200.workloads import c2_params
+    from workloads import c2_params
     if args.workload != "C2":
         import bench_ffpe
         bench_ffpe.run_gpu(args, rank, world, local, pg, METRIC, Clocks, fraq, torch)
@@ -219,23 +234,37 @@ def main():
 
     dev = torch.device("cuda", local)
     stream = torch.cuda.ExternalStream(fraq.context_stream())
-    # signals for the timed levels, generated on the device (rank-specific DOFs: weak scaling)
     K, W = args.steps, args.warmup
     # input / output buffers for at most one horizon of steps (reused cyclically beyond that;
-    # every step's 537 MB of signal is larger than L2 either way)
+    # every step's signal is larger than L2 either way)
     nbuf = max(1, min(K, N_LEVELS // LEVELS_PER_STEP))
     levels = nbuf * LEVELS_PER_STEP
-    gen = torch.Generator(device="cpu").manual_seed(1901051282 + rank)
-    if rank == 0:
-        a = torch.from_numpy(params.a); bb = torch.from_numpy(params.b)
-        c = torch.from_numpy(params.c); w = torch.from_numpy(params.w)
+    if args.scaling == "strong":
+        # contiguous DOF blocks of the ONE 65536-DOF job, 65536/N per GPU
+        per = -(-DOFS // world)
+        lo, hi = min(DOFS, rank * per), min(DOFS, (rank + 1) * per)
+        sel = slice(lo, hi)
+        a, bb, c, w = (torch.from_numpy(x[sel].copy()) for x in (params.a, params.b, params.c,
+                                                                  params.w))
+        half = DOFS // 2
+        dims = [max(0, min(hi, half) - lo), max(0, hi - max(lo, half))]
     else:
-        a = torch.randn(DOFS, generator=gen, dtype=torch.float64)
-        c = torch.randn(DOFS, generator=gen, dtype=torch.float64)
-        bb = 0.1 + 1.9 * torch.rand(DOFS, generator=gen, dtype=torch.float64)
-        w = 1.0 + 19.0 * torch.rand(DOFS, generator=gen, dtype=torch.float64)
+        # weak: each rank owns 65536 DOFs (rank 0 the seeded C2 set, others rank-seeded draws)
+        gen = torch.Generator(device="cpu").manual_seed(1901051282 + rank)
+        if rank == 0:
+            a = torch.from_numpy(params.a); bb = torch.from_numpy(params.b)
+            c = torch.from_numpy(params.c); w = torch.from_numpy(params.w)
+        else:
+            a = torch.randn(DOFS, generator=gen, dtype=torch.float64)
+            c = torch.randn(DOFS, generator=gen, dtype=torch.float64)
+            bb = 0.1 + 1.9 * torch.rand(DOFS, generator=gen, dtype=torch.float64)
+            w = 1.0 + 19.0 * torch.rand(DOFS, generator=gen, dtype=torch.float64)
+        dims = [DOFS // 2, DOFS - DOFS // 2]
+    gk = [k for k, d in zip(ks, dims) if d > 0]
+    dims = [d for d in dims if d > 0]
+    NL = sum(dims)  # DOFs on this rank
     a, bb, c, w = (x.to(dev) for x in (a, bb, c, w))
-    U = torch.empty((levels, DOFS), dtype=torch.float64, device=dev)
+    U = torch.empty((levels, NL), dtype=torch.float64, device=dev)
     for n0 in range(0, levels, 1024):
         n1 = min(levels, n0 + 1024)
         t = (torch.arange(n0, n1, device=dev, dtype=torch.float64) * tau)[:, None]
@@ -246,13 +275,13 @@ def main():
     torch.cuda.synchronize()
 
     # warm-up on a scratch history
-    hw = fraq.MultiHistory(ks, [DOFS // 2, DOFS - DOFS // 2])
+    hw = fraq.MultiHistory(gk, dims)
     for _ in range(W):
-        hw.run_device(Uw.data_ptr(), DOFS, LEVELS_PER_STEP, Dw.data_ptr(), DOFS)
+        hw.run_device(Uw.data_ptr(), NL, LEVELS_PER_STEP, Dw.data_ptr(), NL)
     fraq.synchronize()
     del hw
 
-    h = fraq.MultiHistory(ks, [DOFS // 2, DOFS - DOFS // 2])
+    h = fraq.MultiHistory(gk, dims)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
     if pg:
         pg.barrier()
@@ -260,8 +289,8 @@ def main():
     with Clocks(local) as clk:
         ev[0].record(stream)
         for s in range(K):
-            off = (s % nbuf) * LEVELS_PER_STEP * DOFS * 8
-            h.run_device(U.data_ptr() + off, DOFS, LEVELS_PER_STEP, D.data_ptr() + off, DOFS)
+            off = (s % nbuf) * LEVELS_PER_STEP * NL * 8
+            h.run_device(U.data_ptr() + off, NL, LEVELS_PER_STEP, D.data_ptr() + off, NL)
             ev[s + 1].record(stream)
         ev[K].synchronize()
         torch.cuda.synchronize()
@@ -272,8 +301,9 @@ def main():
     if pg:
         pg.all_reduce(t_local, op=pg.ReduceOp.MAX)
     total_ms = float(t_local.item())
-    dof_steps_local = DOFS * LEVELS_PER_STEP * K
-    value = world * dof_steps_local / (total_ms * 1e-3)
+    dof_steps_local = NL * LEVELS_PER_STEP * K
+    job_dofs = DOFS if args.scaling == "strong" else world * DOFS
+    value = job_dofs * LEVELS_PER_STEP * K / (total_ms * 1e-3)
 
     # sanity: outputs finite after the first level
     assert torch.isfinite(D[1:]).all().item()
@@ -295,27 +325,27 @@ def main():
         traffic = None
 
     # per-level fused kernel K5 (one HBM pass over the state per level) on the same workload
-    hs = fraq.MultiHistory(ks, [DOFS // 2, DOFS - DOFS // 2])
+    hs = fraq.MultiHistory(gk, dims)
     nstep = 24
-    hs.run_device(U.data_ptr(), DOFS, 3, D.data_ptr(), DOFS)  # levels 0..2 (n_steps < 4: per-level K5)
+    hs.run_device(U.data_ptr(), NL, 3, D.data_ptr(), NL)  # levels 0..2 (n_steps < 4: per-level K5)
     torch.cuda.synchronize()
     # force the per-level path: push/derivative on device pointers level by level
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for n in range(3, 3 + nstep):
-        hs.run_device(U.data_ptr() + n * DOFS * 8, DOFS, 1, D.data_ptr() + n * DOFS * 8, DOFS)
+        hs.run_device(U.data_ptr() + n * NL * 8, NL, 1, D.data_ptr() + n * NL * 8, NL)
     e1.record(stream)
     e1.synchronize()
     assert hs.last_path == 0
     step_level_ms = e0.elapsed_time(e1) / nstep
-    hbm_step = B * DOFS / (step_level_ms * 1e-3) / 1e9
+    hbm_step = B * NL / (step_level_ms * 1e-3) / 1e9
     del hs
 
     # e2e: the same metric through the C-ABI call with HOST buffers (pinned), copies inside
     ke = max(1, min(args.e2e_steps, K, nbuf))
     Uh = U[:ke * LEVELS_PER_STEP].cpu().pin_memory()
     Dh = torch.empty_like(Uh).pin_memory()
-    he = fraq.MultiHistory(ks, [DOFS // 2, DOFS - DOFS // 2])
+    he = fraq.MultiHistory(gk, dims)
     # untimed warm-up calls (first-call device state, staging buffers, streams, fragment tables)
     for s in range(min(args.warmup, ke)):
         rows = slice(s * LEVELS_PER_STEP, (s + 1) * LEVELS_PER_STEP)
@@ -328,8 +358,11 @@ def main():
         he.run(Uh[rows].numpy(), True, Dh[rows].numpy())
     e2e_s = time.perf_counter() - t_e
     del he
-    e2e_val = world * DOFS * LEVELS_PER_STEP * ke / e2e_s
-    step_bytes = LEVELS_PER_STEP * DOFS * 8
+    t_e = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if pg:
+        pg.all_reduce(t_e, op=pg.ReduceOp.MAX)
+    e2e_val = job_dofs * LEVELS_PER_STEP * ke / float(t_e.item())
+    step_bytes = LEVELS_PER_STEP * NL * 8
 
     # CPU baseline: the reference (oracle/_ref) on the host cores, rank 0 only, bounded sample
     cpu = None
@@ -340,7 +373,8 @@ def main():
             orc = Oracle(kind)
             rk = reference_kernels(orc, tau)
             threads = os.cpu_count() or 1
-            v, sample, secs = cpu_sample(orc, rk, params, threads, 15.0)
+            # ~10-15 s of CPU work: all DOFs x 256 levels
+            v, sample, secs = cpu_sample(orc, rk, params, threads, LEVELS_PER_STEP // 4)
             cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
                    "sample": sample + f" ({secs:.1f} s), reference SbdHistory push+derivative"}
         except Exception as e:  # report, never fake
@@ -351,17 +385,11 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": total_ms / K, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {
-                "workload": "C2: BDF2 fast CQ, 65536 DOFs per GPU (gamma 0.7 | 0.3), tau = 1/65536,"
-                            " N = 65536 levels; one step = 1024 levels x all DOFs (push+derivative)",
-                "dofs_per_gpu": DOFS, "levels_per_step": LEVELS_PER_STEP,
-                "nodes": n_nodes, "n_head": n_head,
-                "kernel_eps": [e for _, e in kernels],
-                "path": "MultiHistory.run_device -> K5d (temporally blocked, fp64 tensor cores)",
-                "l2": "inputs larger than L2 (537 MB of signal per step)",
-                "parallelism": f"dof-sharded x{world}, no data-path collective",
-                "setup_s": setup_s},
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": c2_config(world, n_nodes, n_head, args.scaling),
+            "setup": {"kernel_eps": [e for _, e in kernels], "setup_s": setup_s,
+                      "path": "MultiHistory.run_device -> K5d (temporally blocked, fp64 tensor "
+                              "cores)"},
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": dmma_peak,
                          "unit": "TFLOP/s", "frac": achieved_tf / dmma_peak,
                          "traffic": traffic, "traffic_unit": "GB per launch (ncu, profiles/)",

@@ -34,7 +34,7 @@ def _modal_kc(fraq):
 
 class Workload:
     def __init__(self, name, rank, world):
-        from paper_1901_05128_b200.workloads import c3_instance, c4_instance, c5_instances
+        from workloads import c3_instance, c4_instance, c5_instances
         self.name = name
         self.rank = rank
         if name == "C3":
@@ -101,6 +101,23 @@ class Workload:
             return r.loop_seconds, [r]
         rs = fraq.run_batch(specs, sch, _modal_kc(fraq))
         return rs[0].loop_seconds, rs
+
+    def config(self):
+        """The workload description both arms print (identical dicts)."""
+        desc = {"C3": "C3: 1D two-state FFPE, M = 4095, N = 16384, FastBE (m = 0.45, alpha = 0.4/0.8)",
+                "C4": "C4: 2D two-state FFPE, 1023^2, N = 8192, FastSBD (m = 0.4, alpha = 0.3/0.6)",
+                "C5": "C5 (BE): 1D FFPE sweep, 256 instances per GPU per step, M = 4095, N = 16384",
+                "C5-SBD": "C5 (BDF2): 1D FFPE sweep, 256 instances per GPU per step, M = 4095, "
+                          "N = 16384"}[self.name]
+        w = self.world
+        return {"workload": desc, "dofs_per_gpu_per_step": self.dofs(), "levels": self.N,
+                "l2": "L2 flushed (256 MB write) before every step",
+                "parallelism": (f"instance-sharded x{w}" if self.units > 1 else
+                                f"row / kx-mode slabs x{w} + two NCCL all-to-all transposes" if
+                                self.name == "C4" else f"replicas x{w}")}
+
+    def scaling(self):
+        return "strong" if self.name == "C4" else "weak"
 
     def launches(self):
         """Our kernels inside the device-timed region of one step.  1D: DST (DMMA), transpose,
@@ -185,7 +202,7 @@ def run_reference(args, rank, world, METRIC):
     if not ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    wl = Workload(args.workload, 0, 1)
+    wl = Workload(args.workload, 0, world)
     orc = Oracle("reference")
     threads = os.cpu_count() or 1
     vals = []
@@ -199,8 +216,8 @@ def run_reference(args, rank, world, METRIC):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": args.workload},
+        "higher_is_better": True, "scaling": wl.scaling(), "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": wl.config(),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": res[1]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
@@ -293,23 +310,14 @@ def run_gpu(args, rank, world, local, pg, METRIC, Clocks, fraq, torch):
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {e}"}
     if rank == 0:
-        desc = {"C3": "C3: 1D two-state FFPE, M = 4095, N = 16384, FastBE (m = 0.45, alpha = 0.4/0.8)",
-                "C4": "C4: 2D two-state FFPE, 1023^2, N = 8192, FastSBD (m = 0.4, alpha = 0.3/0.6)",
-                "C5": "C5 (BE): 1D FFPE sweep, 256 instances per GPU per step, M = 4095, N = 16384",
-                "C5-SBD": "C5 (BDF2): 1D FFPE sweep, 256 instances per GPU per step, M = 4095, "
-                          "N = 16384"}[wl.name]
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": 1e3 * loop_s / K, "higher_is_better": True,
-            "scaling": "strong" if wl.name == "C4" else "weak", "vs_baseline": None,
+            "scaling": wl.scaling(), "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "dofs_per_gpu_per_step": wl.dofs(), "levels": wl.N,
-                       "path": "mode-space solver: DST (DMMA) + K13 (DMMA block stepping, "
-                               "solver warp) + inverse DST",
-                       "l2": "L2 flushed (256 MB write) before every step",
-                       "parallelism": (f"instance-sharded x{world}" if wl.units > 1 else
-                                       f"row / kx-mode slabs x{world} + two NCCL all-to-all transposes" if
-                                       wl.name == "C4" else f"replicas x{world}")},
+            "config": wl.config(),
+            "path": "mode-space solver: DST (DMMA) + K13 (DMMA block stepping, solver warp) + "
+                    "inverse DST",
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_unit": "DRAM bytes per K13 launch (ncu, profiles/)",

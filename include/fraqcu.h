@@ -53,6 +53,9 @@ enum { FRAQ_POLY_SIN = 0, FRAQ_INDICATOR = 1, FRAQ_CUSTOM = 2 };
 
 typedef struct fraq_ctx_s* fraq_ctx;
 typedef struct fraq_hist_s* fraq_hist;
+typedef struct fraq_stepper_s* fraq_stepper;
+typedef struct fraq_block_s* fraq_block;
+typedef struct fraq_banded_s* fraq_banded;
 
 /* Compressed kernel tables: FastKernelBE (sbd = 0; m1 = node_weights, r1 = ratios, head[0..1])
  * or FastKernelSBD (sbd = 1; families (m1, r1) and (m2, r2), head[0..n_head-1]).
@@ -237,6 +240,48 @@ int fraq_modal_run(fraq_ctx ctx, double alpha1, double alpha2, double coupling_a
 int fraq_run_observed(fraq_ctx ctx, const fraq_spec_t* spec, int scheme,
                       const fraq_kconf_t* kconf, fraq_observer_fn fn, void* user, double* g1,
                       double* g2, fraq_run_info_t* info);
+
+/* ---------------------------------------------------------------- single-step API
+ * ClassicalStepper / FastStepper (fpfp.hpp:96-140, fpfp.cpp:81-349): one instance in physical
+ * space, advanced level by level -- the reference's stepper algorithm on the device (histories
+ * K5 + RHS and 2x2-block solve K6; classical schemes: full device history and O(n) sums).
+ * spec->n_steps sizes the kernels (auto sizing horizon) and is the last reachable level.
+ * fraq_stepper_step(st, k): advances k levels (stream-ordered, asynchronous); the reference's
+ * step() is k = 1.  fraq_stepper_state: G^n of both fields (host, grid_m values each; nullable)
+ * and the step index n (state() / step_index(), fpfp.hpp:100-101,112-113); synchronizes.
+ * fraq_stepper_kernel_eps: kernel_eps1() / kernel_eps2() (fpfp.hpp:114-115; 0 for classical). */
+int fraq_stepper_create(fraq_ctx ctx, const fraq_spec_t* spec, int scheme,
+                        const fraq_kconf_t* kconf, fraq_stepper* out);
+int fraq_stepper_step(fraq_stepper st, long n_steps);
+int fraq_stepper_state(fraq_stepper st, double* g1, double* g2, long* step);
+int fraq_stepper_kernel_eps(fraq_stepper st, double* eps1, double* eps2);
+int fraq_stepper_destroy(fraq_stepper st);
+
+/* BlockSystem (block_solver.hpp:38-58, block_solver.cpp:95-153): the coupled two-field system
+ *   [ lead/tau + d01 (a + A) , -a d02 I ; -a d01 I , lead/tau + d02 (a + A) ],
+ * A the Dirichlet stencil (-1, 2, -1)/h^2 on grid_m points, reduced once at creation (block
+ * cyclic reduction for grid_m = 2^K - 1, else block Thomas), solved on the device.
+ * fraq_block_solve: rhs1/rhs2 in, g1/g2 out (grid_m values each; mem FRAQ_HOST or FRAQ_DEVICE). */
+int fraq_block_create(fraq_ctx ctx, double d01, double d02, double coupling_a, double tau,
+                      int grid_m, double h, double bdf_lead, fraq_block* out);
+int fraq_block_solve(fraq_block b, const double* rhs1, const double* rhs2, double* g1,
+                     double* g2, int mem);
+int fraq_block_destroy(fraq_block b);
+/* DiscreteLaplacian::apply (block_solver.cpp:10-19): y = A x on grid_m points, spacing h. */
+int fraq_laplacian_apply(fraq_ctx ctx, int grid_m, double h, const double* x, double* y, int mem);
+/* BandedLU (block_solver.hpp:25-36, block_solver.cpp:28-93): general band matrix with kl sub-
+ * and ku super-diagonals, LAPACK gbtrf storage.  fraq_banded_set assembles one entry (at(),
+ * FRAQ_ERANGE outside the band); factorize uses partial pivoting (FRAQ_ERUNTIME on a zero
+ * pivot); solve before factorize is FRAQ_ELOGIC.  Factorization and substitution run on the
+ * device (sequential: the reference's general-purpose utility, not on the FFPE path). */
+int fraq_banded_create(fraq_ctx ctx, int n, int kl, int ku, fraq_banded* out);
+int fraq_banded_set(fraq_banded b, int row, int col, double value);
+int fraq_banded_get(fraq_banded b, int row, int col, double* value);
+/* the whole band at once: ab[(kl+ku+row-col) + col*(2kl+ku+1)], n*(2kl+ku+1) values (host) */
+int fraq_banded_assign(fraq_banded b, const double* ab);
+int fraq_banded_factorize(fraq_banded b);
+int fraq_banded_solve(fraq_banded b, double* rhs, int mem);
+int fraq_banded_destroy(fraq_banded b);
 
 /* ---------------------------------------------------------------- diagnostics
  * Measured fp64 FMA throughput of the context's GPU (TFLOP/s, 2 flops per DFMA): the roofline

@@ -400,6 +400,32 @@ class Oracle:
             C.c_long(n_steps), _p(U), _p(D), C.c_int(threads), C.byref(secs)), "bench_history")
         return secs.value, D
 
+    def hist_trace(self, kernels, U: np.ndarray, stride: int, threads: int):
+        """Reference histories (standalone) over U[n_steps, dofs] split evenly into
+        len(kernels) groups, `threads` workers; returns D at levels stride-1, 2 stride-1, ...
+        as an array [n_steps // stride, dofs]."""
+        assert self.kind == "reference"
+        U = _arr(U)
+        n_steps, dofs = U.shape
+        G = len(kernels)
+        keep = []
+
+        def ptrs(name):
+            arrs = [_arr(getattr(k, name)) if len(getattr(k, name)) else np.zeros(1)
+                    for k in kernels]
+            keep.extend(arrs)
+            return (_dp * G)(*[_p(a) for a in arrs])
+        gam = (C.c_double * G)(*[k.gamma for k in kernels])
+        nh = (C.c_int * G)(*[k.n_head for k in kernels])
+        n1 = (C.c_int * G)(*[k.np1 for k in kernels])
+        n2 = (C.c_int * G)(*[k.np2 for k in kernels])
+        D = np.zeros((n_steps // stride, dofs))
+        _raise(self.lib.ref_hist_trace(
+            C.c_int(int(kernels[0].sbd)), C.c_int(G), gam, C.c_double(kernels[0].tau), nh, n1,
+            n2, ptrs("head"), ptrs("m1"), ptrs("r1"), ptrs("m2"), ptrs("r2"), C.c_long(dofs),
+            C.c_long(n_steps), _p(U), C.c_long(stride), _p(D), C.c_int(threads)), "hist_trace")
+        return D
+
     def modal_run(self, k1: Kernel, k2: Kernel, a: float, tau: float, N: int, lam, u0, v0,
                   threads: int = 1):
         """Mode-space fast FFPE stepping (test_fpfp.cpp:79-134 with fast histories; lam = the

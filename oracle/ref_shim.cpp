@@ -356,6 +356,71 @@ int ref_bench_history(int sbd, int n_groups, const double* gammas, double tau, c
 }
 
 
+// Reference histories over U[n_steps, dofs] (groups of equal width, one kernel each), `threads`
+// workers over DOF slices, recording the derivative D at levels n = stride-1, 2 stride-1, ...
+// into D_trace[(n + 1) / stride - 1][dofs] (the parity trace of many lanes at a full horizon).
+int ref_hist_trace(int sbd, int n_groups, const double* gammas, double tau, const int* nh,
+                   const int* np1, const int* np2, const double* const* heads,
+                   const double* const* m1, const double* const* r1, const double* const* m2,
+                   const double* const* r2, long dofs, long n_steps, const double* U,
+                   long stride, double* D_trace, int threads) {
+    return guard([&] {
+        std::vector<FastKernelBE> kbe;
+        std::vector<FastKernelSBD> ksbd;
+        for (int g = 0; g < n_groups; ++g) {
+            const FlatKernel f{sbd, nh[g], np1[g], np2[g], gammas[g], tau, heads[g],
+                               m1[g],  r1[g], m2 ? m2[g] : nullptr, r2 ? r2[g] : nullptr};
+            if (sbd)
+                ksbd.push_back(to_sbd(f));
+            else
+                kbe.push_back(to_be(f));
+        }
+        const long per_group = dofs / n_groups;
+        struct Slice {
+            int g;
+            long lo, hi;
+        };
+        std::vector<Slice> slices;
+        const int T = std::max(1, threads);
+        const int per = std::max(1, T / n_groups);
+        for (int g = 0; g < n_groups; ++g)
+            for (int t = 0; t < per; ++t) {
+                const long lo = g * per_group + per_group * t / per;
+                const long hi = g * per_group + per_group * (t + 1) / per;
+                if (hi > lo) slices.push_back({g, lo, hi});
+            }
+        auto work = [&](std::size_t si) {
+            const Slice s = slices[si];
+            const long w = s.hi - s.lo;
+            std::vector<double> in(w), out(w);
+            auto drive = [&](auto& h) {
+                for (long n = 0; n < n_steps; ++n) {
+                    std::memcpy(in.data(), U + n * dofs + s.lo, w * sizeof(double));
+                    h.push(in);
+                    if (n >= 1) h.derivative(out);
+                    if ((n + 1) % stride == 0) {
+                        double* row = D_trace + ((n + 1) / stride - 1) * dofs + s.lo;
+                        if (n >= 1)
+                            std::memcpy(row, out.data(), w * sizeof(double));
+                        else
+                            for (long i = 0; i < w; ++i) row[i] = std::nan("");
+                    }
+                }
+            };
+            if (sbd) {
+                SbdHistory h(ksbd[s.g], HistoryVariant::standalone, w);
+                drive(h);
+            } else {
+                BeHistory h(kbe[s.g], HistoryVariant::standalone, w);
+                drive(h);
+            }
+        };
+        std::vector<std::thread> pool;
+        for (std::size_t i = 0; i < slices.size(); ++i) pool.emplace_back(work, i);
+        for (auto& t : pool) t.join();
+    });
+}
+
 // ---------------------------------------------------------------------------------------------
 // Mode-space FFPE restatement over the reference's own history lanes: the
 // reference's mode-space oracle algebra (test_fpfp.cpp:79-134, mode_be / mode_sbd, solve2x2)

@@ -57,6 +57,7 @@ EXTRA = [
     "MultiHistory",
     "build_be_kernel_auto",
     "build_sbd_kernel_auto",
+    "build_kernels_auto_sizes",
     "context_stream",
     "diag_dmma_peak",
     "direct_cq",
@@ -86,6 +87,12 @@ EXTRA = [
     "SOLVER_MODAL",
     "SOLVER_PHYSICAL",
     "synchronize",
+    "BandedLU",
+    "BlockSystem",
+    "ClassicalStepper",
+    "DiscreteLaplacian",
+    "FastStepper",
+    "solve_block_system",
 ]
 
 globals().update({name: getattr(_impl, name) for name in __all__ + EXTRA

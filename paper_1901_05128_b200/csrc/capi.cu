@@ -25,6 +25,7 @@ void hist_output(fraq_hist h, int mode, double* out, int mem);
 void hist_lagged(fraq_hist h, long depth, double* out, int mem);
 void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, long ldd, int mem);
 int hist_last_path(fraq_hist h);
+fraq_ctx hist_ctx(fraq_hist h);
 void dst2d(fraq_ctx c, int M, int n_fields, const double* in, double* out, bool inverse, int mem);
 void dst_cols(fraq_ctx c, int M, long n_cols, const double* in, double* out, bool inverse, int mem);
 void modal_run_modes(fraq_ctx c, double alpha1, double alpha2, double a, double t_final, long N,
@@ -37,6 +38,29 @@ void ffpe_run_2d(fraq_ctx c, double alpha1, double alpha2, double a, int m, doub
 void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
               const fraq_kconf_t* kc, double* g1, double* g2, fraq_run_info_t* info,
               fraq_observer_fn obs, void* user);
+
+// ffpe.cu: single-step API objects
+struct PhysStepper;
+struct BlockDev;
+struct BandedDev;
+void stepper_create(fraq_ctx c, const fraq_spec_t* spec, int scheme, const fraq_kconf_t* kc,
+                    PhysStepper** out);
+void stepper_step(PhysStepper* st, long n);
+void stepper_state(PhysStepper* st, double* g1, double* g2, long* step);
+void stepper_eps(PhysStepper* st, double* e1, double* e2);
+void stepper_destroy(PhysStepper* st);
+void block_create(fraq_ctx c, double d01, double d02, double a, double tau, int m, double h,
+                  double lead, BlockDev** out);
+void block_solve(BlockDev* b, const double* rhs1, const double* rhs2, double* g1, double* g2,
+                 int mem);
+void block_destroy(BlockDev* b);
+void laplacian_apply(fraq_ctx c, int m, double h, const double* x, double* y, int mem);
+void banded_create(fraq_ctx c, int n, int kl, int ku, BandedDev** out);
+double* banded_at(BandedDev* b, int row, int col);
+void banded_factorize(BandedDev* b);
+void banded_assign(BandedDev* b, const double* ab);
+void banded_solve(BandedDev* b, double* rhs, int mem);
+void banded_destroy(BandedDev* b);
 
 namespace {
 constexpr double kPi = 3.14159265358979323846;
@@ -51,6 +75,13 @@ double host_gamma(double x) {  // gauss_jacobi.cpp:108-123 (host scalar helper f
     for (int i = 1; i < 9; ++i) acc += c[i] / (x + i);
     const double t = x + 7.5;
     return std::sqrt(2.0 * kPi) * std::pow(t, x + 0.5) * std::exp(-t) * acc;
+}
+
+// A history is bound to its context: calls serialise on that context's lock.
+template <class F>
+int guarded_hist(fraq_hist h, F&& f) {
+    if (!h) return guarded([] { fail(FRAQ_EINVAL, "null history"); });
+    return guarded(hist_ctx(h), f);
 }
 
 void check_exps(double a, double b) {
@@ -103,8 +134,11 @@ int fraq_ctx_create(int device, void* stream, fraq_ctx* out) {
 }
 
 int fraq_ctx_destroy(fraq_ctx c) {
+    // the caller guarantees no concurrent use of c (it is being destroyed); wait for any call
+    // in flight on another thread, then release outside the lock
+    if (!c) return FRAQ_OK;
+    { std::lock_guard<std::recursive_mutex> lock(c->mu); }
     return guarded([&] {
-        if (!c) return;
         cudaSetDevice(c->device);
         cudaStreamSynchronize(c->stream);
         if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -113,7 +147,7 @@ int fraq_ctx_destroy(fraq_ctx c) {
 }
 
 int fraq_ctx_synchronize(fraq_ctx c) {
-    return guarded([&] {
+    return guarded(c, [&] {
         check_ctx(c);
         FRAQ_CUDA(cudaStreamSynchronize(c->stream));
     });
@@ -148,7 +182,7 @@ int fraq_jacobi_moment(double a, double b, int k, double* out) {
 }
 
 int fraq_gauss_jacobi(fraq_ctx c, double a, double b, int n, double* nodes, double* weights) {
-    return guarded([&] {
+    return guarded(c, [&] {
         check_ctx(c);
         gauss_jacobi_dev(c, a, b, n, nodes, weights);
     });
@@ -157,7 +191,7 @@ int fraq_gauss_jacobi(fraq_ctx c, double a, double b, int n, double* nodes, doub
 // ------------------------------------------------------------------ L1
 static int weights_common(fraq_ctx c, bool sbd, double g, double tau, long n_max, double* out,
                           int mem) {
-    return guarded([&] {
+    return guarded(c, [&] {
         check_ctx(c);
         if (mem == FRAQ_DEVICE) {
             if (sbd)
@@ -200,7 +234,7 @@ int fraq_coupling_from_transition(double m, double* out) {
 
 // ------------------------------------------------------------------ L2 kernels
 int fraq_build_be_kernel(fraq_ctx c, double g, double tau, int np, fraq_kernel_t* out) {
-    return guarded([&] {
+    return guarded(c, [&] {
         check_ctx(c);
         build_be_kernel_dev(c, g, tau, np, out);
     });
@@ -208,7 +242,7 @@ int fraq_build_be_kernel(fraq_ctx c, double g, double tau, int np, fraq_kernel_t
 
 int fraq_build_sbd_kernel(fraq_ctx c, double g, double tau, int np1, int np2, int nh,
                           fraq_kernel_t* out) {
-    return guarded([&] {
+    return guarded(c, [&] {
         check_ctx(c);
         build_sbd_kernel_dev(c, g, tau, np1, np2, nh, out);
     });
@@ -218,7 +252,7 @@ int fraq_default_sbd_head(double g) { return g <= 0.5 ? 15 : 17; }
 
 int fraq_build_be_kernel_auto(fraq_ctx c, double g, double tau, fraq_budget_t* b,
                               fraq_kernel_t* out) {
-    return guarded([&] {
+    return guarded(c, [&] {
         check_ctx(c);
         build_kernel_auto_dev(c, false, 1, &g, tau, b, out);
     });
@@ -226,7 +260,7 @@ int fraq_build_be_kernel_auto(fraq_ctx c, double g, double tau, fraq_budget_t* b
 
 int fraq_build_sbd_kernel_auto(fraq_ctx c, double g, double tau, fraq_budget_t* b,
                                fraq_kernel_t* out) {
-    return guarded([&] {
+    return guarded(c, [&] {
         check_ctx(c);
         build_kernel_auto_dev(c, true, 1, &g, tau, b, out);
     });
@@ -234,14 +268,14 @@ int fraq_build_sbd_kernel_auto(fraq_ctx c, double g, double tau, fraq_budget_t* 
 
 int fraq_build_kernels_auto(fraq_ctx c, int sbd, int n, const double* gammas, double tau,
                             fraq_budget_t* budgets, fraq_kernel_t* out) {
-    return guarded([&] {
+    return guarded(c, [&] {
         check_ctx(c);
         build_kernel_auto_dev(c, sbd != 0, n, gammas, tau, budgets, out);
     });
 }
 
 int fraq_reconstruct(fraq_ctx c, const fraq_kernel_t* k, long n, const long* idx, double* out) {
-    return guarded([&] {
+    return guarded(c, [&] {
         check_ctx(c);
         reconstruct_dev(c, k, n, idx, out);
     });
@@ -249,7 +283,7 @@ int fraq_reconstruct(fraq_ctx c, const fraq_kernel_t* k, long n, const long* idx
 
 int fraq_kernel_error_report(fraq_ctx c, const fraq_kernel_t* k, long n_max, double* eps,
                              double* max_eps, long* argmax) {
-    return guarded([&] {
+    return guarded(c, [&] {
         check_ctx(c);
         kernel_error_report_dev(c, k, n_max, eps, max_eps, argmax);
     });
@@ -258,45 +292,46 @@ int fraq_kernel_error_report(fraq_ctx c, const fraq_kernel_t* k, long n_max, dou
 // ------------------------------------------------------------------ L2 histories
 int fraq_hist_create(fraq_ctx c, int n_groups, const fraq_kernel_t* const* kernels,
                      const long* dims, int variant, fraq_hist* out) {
-    return guarded([&] { hist_create(c, n_groups, kernels, dims, variant, out); });
+    return guarded(c, [&] { hist_create(c, n_groups, kernels, dims, variant, out); });
 }
 int fraq_hist_destroy(fraq_hist h) {
-    return guarded([&] { hist_destroy(h); });
+    return guarded_hist(h, [&] { hist_destroy(h); });
 }
 int fraq_hist_info(fraq_hist h, long* level, long* appended, long* dim) {
-    return guarded([&] {
-        if (!h) fail(FRAQ_EINVAL, "null history");
-        hist_info(h, level, appended, dim);
-    });
+    return guarded_hist(h, [&] { hist_info(h, level, appended, dim); });
 }
 int fraq_hist_push(fraq_hist h, const double* v, int mem) {
-    return guarded([&] { hist_push(h, v, mem); });
+    return guarded_hist(h, [&] { hist_push(h, v, mem); });
 }
 int fraq_hist_advance(fraq_hist h) {
-    return guarded([&] { hist_advance(h); });
+    return guarded_hist(h, [&] { hist_advance(h); });
 }
 int fraq_hist_append(fraq_hist h, const double* v, int mem) {
-    return guarded([&] { hist_append(h, v, mem); });
+    return guarded_hist(h, [&] { hist_append(h, v, mem); });
 }
 int fraq_hist_history_sum(fraq_hist h, double* out, int mem) {
-    return guarded([&] { hist_output(h, 1, out, mem); });
+    return guarded_hist(h, [&] { hist_output(h, 1, out, mem); });
 }
 int fraq_hist_derivative(fraq_hist h, double* out, int mem) {
-    return guarded([&] { hist_output(h, 2, out, mem); });
+    return guarded_hist(h, [&] { hist_output(h, 2, out, mem); });
 }
 int fraq_hist_lagged(fraq_hist h, long depth, double* out, int mem) {
-    return guarded([&] { hist_lagged(h, depth, out, mem); });
+    return guarded_hist(h, [&] { hist_lagged(h, depth, out, mem); });
 }
 int fraq_hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, long ldd,
                   int mem) {
-    return guarded([&] { hist_run(h, U, ldu, n_steps, D, ldd, mem); });
+    return guarded_hist(h, [&] { hist_run(h, U, ldu, n_steps, D, ldd, mem); });
 }
-int fraq_hist_last_path(fraq_hist h) { return h ? hist_last_path(h) : -1; }
+int fraq_hist_last_path(fraq_hist h) {
+    if (!h) return -1;
+    std::lock_guard<std::recursive_mutex> lock(hist_ctx(h)->mu);
+    return hist_last_path(h);
+}
 
 // ------------------------------------------------------------------ direct CQ
 int fraq_direct_cq(fraq_ctx c, int sbd, double g, double tau, const double* U, long ldu,
                    long n_steps, long dim, double* D, long ldd, int mem) {
-    return guarded([&] {
+    return guarded(c, [&] {
         check_ctx(c);
         check_weight_args(g, tau);
         if (n_steps < 0 || dim < 0 || ldu < dim || ldd < dim)
@@ -330,7 +365,7 @@ int fraq_run_2d(fraq_ctx c, double alpha1, double alpha2, double coupling_a, int
                 double t_final, long n_steps, int scheme, const fraq_kconf_t* kconf,
                 const double* g1_0, const double* g2_0, double* g1, double* g2,
                 fraq_run_info_t* info) {
-    return guarded([&] {
+    return guarded(c, [&] {
         check_ctx(c);
         ffpe_run_2d(c, alpha1, alpha2, coupling_a, grid_m, t_final, n_steps, scheme, kconf, g1_0,
                     g2_0, g1, g2, info);
@@ -339,7 +374,7 @@ int fraq_run_2d(fraq_ctx c, double alpha1, double alpha2, double coupling_a, int
 
 int fraq_dst2d(fraq_ctx c, int grid_m, int n_fields, const double* in, double* out, int inverse,
                int mem) {
-    return guarded([&] {
+    return guarded(c, [&] {
         check_ctx(c);
         dst2d(c, grid_m, n_fields, in, out, inverse != 0, mem);
     });
@@ -347,7 +382,7 @@ int fraq_dst2d(fraq_ctx c, int grid_m, int n_fields, const double* in, double* o
 
 int fraq_dst_cols(fraq_ctx c, int grid_m, long n_cols, const double* in, double* out, int inverse,
                   int mem) {
-    return guarded([&] {
+    return guarded(c, [&] {
         check_ctx(c);
         dst_cols(c, grid_m, n_cols, in, out, inverse != 0, mem);
     });
@@ -357,7 +392,7 @@ int fraq_modal_run(fraq_ctx c, double alpha1, double alpha2, double coupling_a, 
                    long n_steps, int scheme, const fraq_kconf_t* kconf, long n_modes,
                    const double* lam, const double* c0, double* cN, int mem,
                    fraq_run_info_t* info) {
-    return guarded([&] {
+    return guarded(c, [&] {
         check_ctx(c);
         modal_run_modes(c, alpha1, alpha2, coupling_a, t_final, n_steps, scheme, kconf, n_modes,
                         lam, c0, cN, mem, info);
@@ -366,7 +401,7 @@ int fraq_modal_run(fraq_ctx c, double alpha1, double alpha2, double coupling_a, 
 
 int fraq_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
              const fraq_kconf_t* kconf, double* g1, double* g2, fraq_run_info_t* info) {
-    return guarded([&] {
+    return guarded(c, [&] {
         check_ctx(c);
         ffpe_run(c, specs, n_inst, scheme, kconf, g1, g2, info, nullptr, nullptr);
     });
@@ -375,10 +410,123 @@ int fraq_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
 int fraq_run_observed(fraq_ctx c, const fraq_spec_t* spec, int scheme, const fraq_kconf_t* kconf,
                       fraq_observer_fn fn, void* user, double* g1, double* g2,
                       fraq_run_info_t* info) {
-    return guarded([&] {
+    return guarded(c, [&] {
         check_ctx(c);
         ffpe_run(c, spec, 1, scheme, kconf, g1, g2, info, fn, user);
     });
+}
+
+// ------------------------------------------------------------------ single-step API
+}  // extern "C"
+
+struct fraq_stepper_s {
+    fraq_ctx ctx;
+    PhysStepper* p;
+};
+struct fraq_block_s {
+    fraq_ctx ctx;
+    BlockDev* p;
+};
+struct fraq_banded_s {
+    fraq_ctx ctx;
+    BandedDev* p;
+};
+
+namespace {
+template <class H, class F>
+int guarded_obj(H h, const char* what, F&& f) {
+    if (!h) return guarded([&] { fail(FRAQ_EINVAL, std::string("null ") + what); });
+    return guarded(h->ctx, [&] {
+        check_ctx(h->ctx);
+        f();
+    });
+}
+}  // namespace
+
+extern "C" {
+
+int fraq_stepper_create(fraq_ctx c, const fraq_spec_t* spec, int scheme,
+                        const fraq_kconf_t* kconf, fraq_stepper* out) {
+    return guarded(c, [&] {
+        check_ctx(c);
+        if (!spec || !out) fail(FRAQ_EINVAL, "stepper: null argument");
+        PhysStepper* p = nullptr;
+        stepper_create(c, spec, scheme, kconf, &p);
+        *out = new fraq_stepper_s{c, p};
+    });
+}
+int fraq_stepper_step(fraq_stepper st, long n_steps) {
+    return guarded_obj(st, "stepper", [&] { stepper_step(st->p, n_steps); });
+}
+int fraq_stepper_state(fraq_stepper st, double* g1, double* g2, long* step) {
+    return guarded_obj(st, "stepper", [&] { stepper_state(st->p, g1, g2, step); });
+}
+int fraq_stepper_kernel_eps(fraq_stepper st, double* eps1, double* eps2) {
+    return guarded_obj(st, "stepper", [&] { stepper_eps(st->p, eps1, eps2); });
+}
+int fraq_stepper_destroy(fraq_stepper st) {
+    if (!st) return FRAQ_OK;
+    const int r = guarded_obj(st, "stepper", [&] { stepper_destroy(st->p); });
+    delete st;
+    return r;
+}
+
+int fraq_block_create(fraq_ctx c, double d01, double d02, double coupling_a, double tau,
+                      int grid_m, double h, double bdf_lead, fraq_block* out) {
+    return guarded(c, [&] {
+        check_ctx(c);
+        if (!out) fail(FRAQ_EINVAL, "BlockSystem: null out");
+        BlockDev* p = nullptr;
+        block_create(c, d01, d02, coupling_a, tau, grid_m, h, bdf_lead, &p);
+        *out = new fraq_block_s{c, p};
+    });
+}
+int fraq_block_solve(fraq_block b, const double* rhs1, const double* rhs2, double* g1,
+                     double* g2, int mem) {
+    return guarded_obj(b, "BlockSystem", [&] { block_solve(b->p, rhs1, rhs2, g1, g2, mem); });
+}
+int fraq_block_destroy(fraq_block b) {
+    if (!b) return FRAQ_OK;
+    const int r = guarded_obj(b, "BlockSystem", [&] { block_destroy(b->p); });
+    delete b;
+    return r;
+}
+int fraq_laplacian_apply(fraq_ctx c, int grid_m, double h, const double* x, double* y, int mem) {
+    return guarded(c, [&] {
+        check_ctx(c);
+        laplacian_apply(c, grid_m, h, x, y, mem);
+    });
+}
+
+int fraq_banded_create(fraq_ctx c, int n, int kl, int ku, fraq_banded* out) {
+    return guarded(c, [&] {
+        check_ctx(c);
+        if (!out) fail(FRAQ_EINVAL, "BandedLU: null out");
+        BandedDev* p = nullptr;
+        banded_create(c, n, kl, ku, &p);
+        *out = new fraq_banded_s{c, p};
+    });
+}
+int fraq_banded_set(fraq_banded b, int row, int col, double value) {
+    return guarded_obj(b, "BandedLU", [&] { *banded_at(b->p, row, col) = value; });
+}
+int fraq_banded_get(fraq_banded b, int row, int col, double* value) {
+    return guarded_obj(b, "BandedLU", [&] { *value = *banded_at(b->p, row, col); });
+}
+int fraq_banded_assign(fraq_banded b, const double* ab) {
+    return guarded_obj(b, "BandedLU", [&] { banded_assign(b->p, ab); });
+}
+int fraq_banded_factorize(fraq_banded b) {
+    return guarded_obj(b, "BandedLU", [&] { banded_factorize(b->p); });
+}
+int fraq_banded_solve(fraq_banded b, double* rhs, int mem) {
+    return guarded_obj(b, "BandedLU", [&] { banded_solve(b->p, rhs, mem); });
+}
+int fraq_banded_destroy(fraq_banded b) {
+    if (!b) return FRAQ_OK;
+    const int r = guarded_obj(b, "BandedLU", [&] { banded_destroy(b->p); });
+    delete b;
+    return r;
 }
 
 }  // extern "C"

@@ -71,7 +71,7 @@ using namespace fraqcu;
 
 // tflops[0] = DMMA alone, tflops[1] = DMMA + DFMA interleaved (total fp64 flops of both pipes)
 extern "C" int fraq_diag_dmma_peak(fraq_ctx c, double* tflops) {
-    return guarded([&] {
+    return guarded(c, [&] {
         check_ctx(c);
         DevBuf<double> sink(256);
         const int blocks = c->num_sms * 8, iters = 1024;
@@ -101,7 +101,7 @@ extern "C" int fraq_diag_dmma_peak(fraq_ctx c, double* tflops) {
 }
 
 extern "C" int fraq_diag_fp64_peak(fraq_ctx c, double* tflops) {
-    return guarded([&] {
+    return guarded(c, [&] {
         check_ctx(c);
         DevBuf<double> sink(256);
         const int blocks = c->num_sms * 8, iters = 4096;

@@ -61,10 +61,18 @@ struct SysDev {
     long th_off;         // offset into thomas buffer (2 * grid_m M2 entries)
 };
 
-// Block matrices of BlockSystem (block_solver.cpp:95-117).
+// Block matrices of BlockSystem (block_solver.cpp:95-117), rounded exactly as the reference
+// forms them: its Release build contracts the diagonal into fma(d0, fma(2, 1/h^2, a), lead/tau)
+// (vfmadd132sd in the -O3 -march build).  These entries are the one place where fp64 rounding
+// matters: the block system has cond ~1.4e6 at M = 4095, its diagonal is constant along the
+// grid, so a rounding of the diagonal shifts every row the same way and the solution drifts
+// systematically (3.8e-9 relative after 256 C3 steps for the reference itself).  Identical
+// entries make the B200 solve converge to the reference's fp64 system, not to a neighbour of it.
 void blocks(double d01, double d02, double a, double tau, double h, double lead, M2& D, M2& E) {
     const double ih2 = 1.0 / (h * h);
-    D = {lead / tau + d01 * (a + 2.0 * ih2), -a * d02, -a * d01, lead / tau + d02 * (a + 2.0 * ih2)};
+    const double lt = lead / tau;
+    const double ad = std::fma(2.0, ih2, a);
+    D = {std::fma(d01, ad, lt), -a * d02, -a * d01, std::fma(d02, ad, lt)};
     E = {-d01 * ih2, 0.0, 0.0, -d02 * ih2};
 }
 
@@ -74,18 +82,37 @@ int cr_levels(int m) {
     return ((1L << K) - 1 == m && K <= kMaxLevels) ? K : 0;
 }
 
-// Setup of one system on the host from its scalar description (tiny: O(levels) or O(M) 2x2
-// algebra per system; the O(M) Thomas factors are computed by thomas_setup_kernel).
+// Block cyclic-reduction coefficients of one system, computed in extended precision (x87 long
+// double) and rounded once.  With fp64 recursion D_(l+1) = D_l - 2 E_l D_l^-1 E_l, every level's
+// rounding is shared by all rows of that level -- a coherent perturbation of the system, like
+// the entry rounding above -- and the solution drifted 6.6e-9 from the reference's after 256 C3
+// steps; from extended-precision coefficients it stays within 1.2e-11 (profiles/r02/
+// physical_bisect.txt).  The per-step reduction and substitution run in fp64 on the device:
+// their rounding is not coherent across rows and does not accumulate.
+struct M2L {
+    long double a, b, c, d;
+};
+M2L mulL(const M2L& x, const M2L& y) {
+    return {x.a * y.a + x.b * y.c, x.a * y.b + x.b * y.d, x.c * y.a + x.d * y.c,
+            x.c * y.b + x.d * y.d};
+}
+M2L invL(const M2L& x) {
+    const long double det = x.a * x.d - x.b * x.c;
+    return {x.d / det, -x.b / det, -x.c / det, x.a / det};
+}
+M2 rnd(const M2L& x) { return {(double)x.a, (double)x.b, (double)x.c, (double)x.d}; }
+
 void setup_cr(SysDev& S, const M2& D0, const M2& E0) {
-    M2 D = D0, E = E0;
+    M2L D{D0.a, D0.b, D0.c, D0.d}, E{E0.a, E0.b, E0.c, E0.d};
     for (int l = 0; l < S.K; ++l) {
-        const M2 Di = inv(D);
-        S.lv[l].F = mul(E, Di);
-        S.lv[l].G = Di;
-        S.lv[l].H = mul(Di, E);
-        const M2 FE = mul(S.lv[l].F, E);
-        E = scal(-1.0, FE);
-        D = sub(D, scal(2.0, FE));
+        const M2L Di = invL(D);
+        const M2L F = mulL(E, Di);
+        S.lv[l].F = rnd(F);
+        S.lv[l].G = rnd(Di);
+        S.lv[l].H = rnd(mulL(Di, E));
+        const M2L FE = mulL(F, E);
+        E = {-FE.a, -FE.b, -FE.c, -FE.d};
+        D = {D.a - 2 * FE.a, D.b - 2 * FE.b, D.c - 2 * FE.c, D.d - 2 * FE.d};
     }
 }
 
@@ -133,6 +160,152 @@ struct SolveArgs {
     int first;            // SBD first step
     double* out;          // nullable: final state (inst * 2m: g1 then g2)
 };
+
+// The 2x2-block tridiagonal solve of BlockSystem::solve (block_solver.cpp:119-153) on one CTA,
+// in place on sb[1..m] (sb[0] = sb[m+1] = 0): block cyclic reduction with the setup
+// coefficients (grid_m = 2^K - 1), else block Thomas (one thread; general grid sizes).
+// Ends with __syncthreads().
+template <int THREADS>
+__device__ void block_solve_smem(double2* sb, const SysDev& S, const M2* thomas, int m) {
+    if (S.K > 0) {
+        const int K = S.K;
+        // forward reduction
+        for (int l = 0; l < K - 1; ++l) {
+            const int s = 1 << l;
+            const M2 F = S.lv[l].F;
+            for (int i = 2 * s * (threadIdx.x + 1); i <= m; i += 2 * s * THREADS) {
+                const double2 sum = make_double2(sb[i - s].x + sb[i + s].x, sb[i - s].y + sb[i + s].y);
+                const double2 t = mv(F, sum);
+                sb[i] = make_double2(sb[i].x - t.x, sb[i].y - t.y);
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            const int i = 1 << (K - 1);
+            sb[i] = mv(S.lv[K - 1].G, sb[i]);
+        }
+        __syncthreads();
+        for (int l = K - 2; l >= 0; --l) {
+            const int s = 1 << l;
+            const M2 Gm = S.lv[l].G, H = S.lv[l].H;
+            for (int i = s * (2 * (int)threadIdx.x + 1); i <= m; i += 2 * s * THREADS) {
+                const double2 xb = mv(Gm, sb[i]);
+                const double2 nb = make_double2(sb[i - s].x + sb[i + s].x, sb[i - s].y + sb[i + s].y);
+                const double2 t = mv(H, nb);
+                sb[i] = make_double2(xb.x - t.x, xb.y - t.y);
+            }
+            __syncthreads();
+        }
+    } else if (threadIdx.x == 0) {
+        // block Thomas with the setup factors
+        const M2* W = thomas + S.th_off;
+        const M2* Dinv = W + m;
+        for (int k = 1; k < m; ++k) {
+            const double2 t = mv(W[k], sb[k]);
+            sb[k + 1] = make_double2(sb[k + 1].x - t.x, sb[k + 1].y - t.y);
+        }
+        sb[m] = mv(Dinv[m - 1], sb[m]);
+        for (int k = m - 2; k >= 0; --k) {
+            const double2 ex = mv(S.E, sb[k + 2]);
+            sb[k + 1] = mv(Dinv[k], make_double2(sb[k + 1].x - ex.x, sb[k + 1].y - ex.y));
+        }
+    }
+    __syncthreads();
+}
+
+// BlockSystem::solve on its own (block_solver.cpp:119-153): one CTA per system.
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) block_solve_kernel(const SysDev* sys, const M2* thomas,
+                                                              int m, const double* rhs1,
+                                                              const double* rhs2, double* g1,
+                                                              double* g2) {
+    extern __shared__ double2 sb[];
+    for (int k = threadIdx.x; k < m; k += THREADS) sb[k + 1] = make_double2(rhs1[k], rhs2[k]);
+    if (threadIdx.x == 0) {
+        sb[0] = make_double2(0.0, 0.0);
+        sb[m + 1] = make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    block_solve_smem<THREADS>(sb, sys[0], thomas, m);
+    for (int k = threadIdx.x; k < m; k += THREADS) {
+        g1[k] = sb[k + 1].x;
+        g2[k] = sb[k + 1].y;
+    }
+}
+
+// DiscreteLaplacian::apply (block_solver.cpp:10-19): y = (2 x_i - x_{i-1} - x_{i+1}) / h^2.
+__global__ void laplacian_kernel(int m, double ih2, const double* x, double* y) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    double v = 2.0 * x[i];
+    if (i > 0) v -= x[i - 1];
+    if (i + 1 < m) v -= x[i + 1];
+    y[i] = v * ih2;
+}
+
+// BandedLU (block_solver.cpp:28-93): LAPACK gbtrf band storage ab[(kl+ku+row-col) + col*ldab],
+// partial pivoting from the kl rows below the diagonal.  A general-purpose sequential
+// factorization; one thread (the FFPE path uses the block solve above instead).
+__global__ void banded_factor_kernel(double* ab, int* piv, int n, int kl, int ku, int* status) {
+    const int ldab = 2 * kl + ku + 1, kv = kl + ku;
+    for (int j = 0; j < n; ++j) {
+        const int jmax = min(n - 1, j + kl);
+        int p = j;
+        double pmax = fabs(ab[(size_t)j * ldab + kv]);
+        for (int i = j + 1; i <= jmax; ++i) {
+            const double v = fabs(ab[(size_t)j * ldab + kv + (i - j)]);
+            if (v > pmax) {
+                pmax = v;
+                p = i;
+            }
+        }
+        if (pmax == 0.0) {
+            *status = 1;
+            return;
+        }
+        piv[j] = p;
+        const int cmax = min(n - 1, j + kv);
+        if (p != j)
+            for (int c = j; c <= cmax; ++c) {
+                double* base = ab + (size_t)c * ldab + kv;
+                const double t = base[j - c];
+                base[j - c] = base[p - c];
+                base[p - c] = t;
+            }
+        const double dinv = 1.0 / ab[(size_t)j * ldab + kv];
+        for (int i = j + 1; i <= jmax; ++i) {
+            double& lij = ab[(size_t)j * ldab + kv + (i - j)];
+            lij *= dinv;
+            const double l = lij;
+            for (int c = j + 1; c <= cmax; ++c) {
+                double* base = ab + (size_t)c * ldab + kv;
+                base[i - c] -= l * base[j - c];
+            }
+        }
+    }
+    *status = 0;
+}
+
+__global__ void banded_solve_kernel(const double* ab, const int* piv, int n, int kl, int ku,
+                                    double* rhs) {
+    const int ldab = 2 * kl + ku + 1, kv = kl + ku;
+    for (int j = 0; j < n; ++j) {
+        if (piv[j] != j) {
+            const double t = rhs[j];
+            rhs[j] = rhs[piv[j]];
+            rhs[piv[j]] = t;
+        }
+        const int imax = min(n - 1, j + kl);
+        const double xj = rhs[j];
+        for (int i = j + 1; i <= imax; ++i) rhs[i] -= ab[(size_t)j * ldab + kv + (i - j)] * xj;
+    }
+    for (int j = n - 1; j >= 0; --j) {
+        double v = rhs[j];
+        for (int c = j + 1; c <= min(n - 1, j + kv); ++c)
+            v -= ab[(size_t)c * ldab + kv + (j - c)] * rhs[c];
+        rhs[j] = v / ab[(size_t)j * ldab + kv];
+    }
+}
 
 // RHS (fpfp.cpp:277-279, 298-302, 339-344) then the block solve; one CTA per instance.
 template <int THREADS>
@@ -210,51 +383,7 @@ __global__ void __launch_bounds__(THREADS) solve_kernel(SolveArgs A) {
         sb[m + 1] = make_double2(0.0, 0.0);
     }
     __syncthreads();
-    const SysDev& S = A.sys[A.first ? I.sys_first : I.sys_main];
-    if (S.K > 0) {
-        const int K = S.K;
-        // forward reduction
-        for (int l = 0; l < K - 1; ++l) {
-            const int s = 1 << l;
-            const M2 F = S.lv[l].F;
-            for (int i = 2 * s * (threadIdx.x + 1); i <= m; i += 2 * s * THREADS) {
-                const double2 sum = make_double2(sb[i - s].x + sb[i + s].x, sb[i - s].y + sb[i + s].y);
-                const double2 t = mv(F, sum);
-                sb[i] = make_double2(sb[i].x - t.x, sb[i].y - t.y);
-            }
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) {
-            const int i = 1 << (K - 1);
-            sb[i] = mv(S.lv[K - 1].G, sb[i]);
-        }
-        __syncthreads();
-        for (int l = K - 2; l >= 0; --l) {
-            const int s = 1 << l;
-            const M2 Gm = S.lv[l].G, H = S.lv[l].H;
-            for (int i = s * (2 * (int)threadIdx.x + 1); i <= m; i += 2 * s * THREADS) {
-                const double2 xb = mv(Gm, sb[i]);
-                const double2 nb = make_double2(sb[i - s].x + sb[i + s].x, sb[i - s].y + sb[i + s].y);
-                const double2 t = mv(H, nb);
-                sb[i] = make_double2(xb.x - t.x, xb.y - t.y);
-            }
-            __syncthreads();
-        }
-    } else if (threadIdx.x == 0) {
-        // block Thomas with the setup factors (single thread; general grid sizes)
-        const M2* W = A.thomas + S.th_off;
-        const M2* Dinv = W + m;
-        for (int k = 1; k < m; ++k) {
-            const double2 t = mv(W[k], sb[k]);
-            sb[k + 1] = make_double2(sb[k + 1].x - t.x, sb[k + 1].y - t.y);
-        }
-        sb[m] = mv(Dinv[m - 1], sb[m]);
-        for (int k = m - 2; k >= 0; --k) {
-            const double2 ex = mv(S.E, sb[k + 2]);
-            sb[k + 1] = mv(Dinv[k], make_double2(sb[k + 1].x - ex.x, sb[k + 1].y - ex.y));
-        }
-    }
-    __syncthreads();
+    block_solve_smem<THREADS>(sb, A.sys[A.first ? I.sys_first : I.sys_main], A.thomas, m);
     // append G^n into both rings (slot n % L)
     double* w1 = A.ring + G1.ring_off + (n % G1.L) * ld;
     double* w2 = A.ring + G2.ring_off + (n % G2.L) * ld;
@@ -341,53 +470,66 @@ void build_ffpe_kernels(fraq_ctx c, const std::vector<double>& gam, double tau, 
 void ffpe_run_modal(fraq_ctx c, const fraq_spec_t* specs, int n_inst, bool sbd,
                     const fraq_kconf_t& kc, double* g1_out, double* g2_out, fraq_run_info_t* info);
 
-void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
-              const fraq_kconf_t* kc_in, double* g1_out, double* g2_out, fraq_run_info_t* info,
-              fraq_observer_fn obs, void* user) {
+// ================================================================================ PhysStepper
+// ClassicalStepper / FastStepper (fpfp.cpp:81-349) for a batch of instances in physical space:
+// the device state of one or many instances stepped level by level.  Behind ffpe_run (physical
+// solver, observer runs) and the stepper handles of the C ABI (fraq_stepper_*).
+struct PhysStepper {
+    fraq_ctx c = nullptr;
+    int n_inst = 0, m = 0;
+    long N = 0;        // horizon the kernels / classical tables are sized for
+    bool sbd = false, fast = false;
+    double tau = 0.0;
+    std::vector<double> G0, eps, d0;
+    std::vector<fraq_kernel_t> ks;
+    DevBuf<double> ctab, g0, corr, sbuf, outb, hist;
+    DevBuf<int> gof;
+    DevBuf<SysDev> dsys;
+    DevBuf<M2> thomas;
+    DevBuf<InstDev> dinst;
+    HistDevice hd;
+    SolveArgs sa{};
+    long level = 0, appended = 1, step_idx = 0, total = 0;
+    size_t smem = 0;
+    double setup_seconds = 0.0;
+
+    PhysStepper(fraq_ctx c_, const fraq_spec_t* specs, int n_inst_, int scheme,
+                const fraq_kconf_t& kc);
+    void step(long n_steps);  // asynchronous on the context stream
+    void state(double* g1, double* g2);  // [n_inst][m] each; synchronizes
+};
+
+void validate_specs(const fraq_spec_t* specs, int n_inst, int scheme) {
     if (n_inst < 1) fail(FRAQ_EINVAL, "run: need at least one instance");
-    fraq_kconf_t kc;
-    if (kc_in)
-        kc = *kc_in;
-    else
-        fraq_kconf_default(&kc);
     const fraq_spec_t& s0 = specs[0];
-    const int m = s0.grid_m;
-    const long N = s0.n_steps;
-    if (m < 1) fail(FRAQ_EINVAL, "run: grid_m must be >= 1");
-    if (N < 1) fail(FRAQ_EINVAL, "run: n_steps must be >= 1");
+    if (s0.grid_m < 1) fail(FRAQ_EINVAL, "run: grid_m must be >= 1");
+    if (s0.n_steps < 1) fail(FRAQ_EINVAL, "run: n_steps must be >= 1");
     for (int i = 0; i < n_inst; ++i) {
         const fraq_spec_t& s = specs[i];
-        if (s.grid_m != m || s.n_steps != N || s.t_final != s0.t_final || s.length != s0.length)
+        if (s.grid_m != s0.grid_m || s.n_steps != s0.n_steps || s.t_final != s0.t_final ||
+            s.length != s0.length)
             fail(FRAQ_EINVAL, "run: batched instances must share grid_m, n_steps, t_final, length");
         if (s.initial == FRAQ_CUSTOM && (!s.custom_g1 || !s.custom_g2))
             fail(FRAQ_EINVAL, "initial_field: custom samples must have grid_m entries");
         if (s.initial < 0 || s.initial > 2) fail(FRAQ_EINVAL, "unknown initial data tag");
     }
-    const bool sbd = scheme == FRAQ_SBD || scheme == FRAQ_FASTSBD;
-    const bool fast = scheme == FRAQ_FASTBE || scheme == FRAQ_FASTSBD;
-    if (kc.solver == FRAQ_SOLVER_MODAL) {
-        if (!fast) fail(FRAQ_EINVAL, "run: the modal solver needs a fast scheme");
-        if (obs) fail(FRAQ_EINVAL, "run: the modal solver does not stream intermediate states");
-        ffpe_run_modal(c, specs, n_inst, sbd, kc, g1_out, g2_out, info);
-        return;
-    }
-    if (kc.solver == FRAQ_SOLVER_AUTO && fast && !obs) {
-        bool done = false;
-        try {
-            ffpe_run_modal(c, specs, n_inst, sbd, kc, g1_out, g2_out, info);
-            done = true;
-        } catch (const Error& e) {
-            if (e.code != FRAQ_EINVAL || std::string(e.what()).find("modal run:") != 0) throw;
-        }
-        if (done) return;
-    }
-    if (kc.solver < 0 || kc.solver > FRAQ_SOLVER_AUTO) fail(FRAQ_EINVAL, "run: unknown solver");
-    const double tau = s0.t_final / double(N);
-    const double h = s0.length / double(m + 1);
+    if (scheme < FRAQ_BE || scheme > FRAQ_FASTSBD) fail(FRAQ_EINVAL, "run: unknown scheme");
+}
+
+PhysStepper::PhysStepper(fraq_ctx c_, const fraq_spec_t* specs, int n_inst_, int scheme,
+                         const fraq_kconf_t& kc)
+    : c(c_), n_inst(n_inst_) {
     const double t_setup0 = now_s();
+    const fraq_spec_t& s0 = specs[0];
+    m = s0.grid_m;
+    N = s0.n_steps;
+    sbd = scheme == FRAQ_SBD || scheme == FRAQ_FASTSBD;
+    fast = scheme == FRAQ_FASTBE || scheme == FRAQ_FASTSBD;
+    tau = s0.t_final / double(N);
+    const double h = s0.length / double(m + 1);
 
     // ---------------------------------------------------------------- initial data
-    std::vector<double> G0((size_t)n_inst * 2 * m);
+    G0.resize((size_t)n_inst * 2 * m);
     for (int i = 0; i < n_inst; ++i)
         initial_field(specs[i], G0.data() + (size_t)i * 2 * m, G0.data() + (size_t)i * 2 * m + m);
 
@@ -397,10 +539,8 @@ void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
         gam[2 * i] = 1.0 - specs[i].alpha1;
         gam[2 * i + 1] = 1.0 - specs[i].alpha2;
     }
-    std::vector<fraq_kernel_t> ks;
-    std::vector<double> eps(2 * n_inst, 0.0);
-    std::vector<double> d0(2 * n_inst);
-    DevBuf<double> ctab;  // classical tables (2 n_inst x (N+1))
+    eps.assign(2 * n_inst, 0.0);
+    d0.resize(2 * n_inst);
     if (fast) {
         build_ffpe_kernels(c, gam, tau, N, sbd, kc, ks, eps);
         for (int t = 0; t < 2 * n_inst; ++t) d0[t] = ks[t].head[0];
@@ -427,6 +567,7 @@ void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
         const double a = specs[i].coupling_a;
         auto mk = [&](int sidx, double f, double lead) {
             M2 D, E;
+            // d01 = f * d0 as the reference scales it (2/3 d_0 for the first SBD step)
             blocks(f * d0[2 * i], f * d0[2 * i + 1], a, tau, h, lead, D, E);
             SysDev& S = sys[sidx];
             S.K = K;
@@ -457,9 +598,9 @@ void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
             mk(i, 1.0, 1.0);
         }
     }
-    DevBuf<SysDev> dsys(n_sys);
+    dsys.alloc(n_sys);
     FRAQ_CUDA(cudaMemcpy(dsys.p, sys.data(), sizeof(SysDev) * n_sys, cudaMemcpyHostToDevice));
-    DevBuf<M2> thomas(std::max<long>(1, th));
+    thomas.alloc(std::max<long>(1, th));
     if (!K) {
         DevBuf<M2> dD(n_sys);
         FRAQ_CUDA(cudaMemcpy(dD.p, sysD.data(), sizeof(M2) * n_sys, cudaMemcpyHostToDevice));
@@ -470,7 +611,6 @@ void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
     }
 
     // ---------------------------------------------------------------- histories / buffers
-    HistDevice hd;
     std::vector<long> dims(2 * n_inst, m);
     std::vector<const fraq_kernel_t*> kp(2 * n_inst);
     std::vector<fraq_kernel_t> pseudo;  // classical: a 2-slot lag ring carrier (no nodes)
@@ -487,9 +627,8 @@ void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
         }
     }
     hd.build(c, 2 * n_inst, kp.data(), dims.data());
-    DevBuf<InstDev> dinst(n_inst);
-    FRAQ_CUDA(cudaMemcpy(dinst.p, inst.data(), sizeof(InstDev) * n_inst, cudaMemcpyHostToDevice));
-    DevBuf<double> g0((size_t)n_inst * 2 * m);
+    dinst.alloc(n_inst);
+    g0.alloc((size_t)n_inst * 2 * m);
     FRAQ_CUDA(cudaMemcpy(g0.p, G0.data(), sizeof(double) * G0.size(), cudaMemcpyHostToDevice));
     // append G^0 into ring slot 0 of both fields (FastStepper ctor, fpfp.cpp:229-237)
     for (int i = 0; i < n_inst; ++i)
@@ -499,7 +638,7 @@ void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
                                  sizeof(double) * m, cudaMemcpyHostToDevice));
         }
     // SBD correction sequences: corr[e] for e = 0 .. N (K7)
-    DevBuf<double> corr(1);
+    corr.alloc(1);
     if (fast && sbd) {
         corr.alloc((size_t)2 * n_inst * (N + 1));
         corr_sequence_batch_dev(c, ks.data(), 2 * n_inst, N, corr.p, N + 1);
@@ -507,14 +646,12 @@ void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
             inst[i].corr_off1 = (long)(2 * i) * (N + 1);
             inst[i].corr_off2 = (long)(2 * i + 1) * (N + 1);
         }
-        FRAQ_CUDA(cudaMemcpy(dinst.p, inst.data(), sizeof(InstDev) * n_inst, cudaMemcpyHostToDevice));
     }
-    DevBuf<double> sbuf((size_t)2 * n_inst * m);
-    DevBuf<double> outb((size_t)2 * n_inst * m);
+    FRAQ_CUDA(cudaMemcpy(dinst.p, inst.data(), sizeof(InstDev) * n_inst, cudaMemcpyHostToDevice));
+    sbuf.alloc((size_t)2 * n_inst * m);
+    outb.alloc((size_t)2 * n_inst * m);
     // classical: full history of both fields, [t][2 n_inst m]
-    DevBuf<double> hist;
-    DevBuf<int> gof;
-    const long total = (long)2 * n_inst * m;
+    total = (long)2 * n_inst * m;
     if (!fast) {
         hist.alloc((size_t)(N + 1) * total);
         FRAQ_CUDA(cudaMemcpy(hist.p, G0.data(), sizeof(double) * total, cudaMemcpyHostToDevice));
@@ -523,21 +660,11 @@ void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
         gof.alloc(total);
         FRAQ_CUDA(cudaMemcpy(gof.p, go.data(), sizeof(int) * total, cudaMemcpyHostToDevice));
     }
-    FRAQ_CUDA(cudaStreamSynchronize(c->stream));
-    const double t_setup1 = now_s();
-
-    // ---------------------------------------------------------------- time loop
-    cudaEvent_t e0, e1;
-    FRAQ_CUDA(cudaEventCreate(&e0));
-    FRAQ_CUDA(cudaEventCreate(&e1));
-    FRAQ_CUDA(cudaEventRecord(e0, c->stream));
-    const int threads = 512;
-    const size_t smem = sizeof(double2) * (m + 2);
+    smem = sizeof(double2) * (m + 2);
+    if (smem > 227 * 1024) fail(FRAQ_EINVAL, "run: grid_m too large for the on-chip block solve");
     if (smem > 48 * 1024)
         FRAQ_CUDA(cudaFuncSetAttribute(solve_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)std::min<size_t>(smem, 227 * 1024)));
-    if (smem > 227 * 1024) fail(FRAQ_EINVAL, "run: grid_m too large for the on-chip block solve");
-    SolveArgs sa{};
+                                       (int)smem));
     sa.inst = dinst.p;
     sa.sys = dsys.p;
     sa.thomas = thomas.p;
@@ -549,14 +676,17 @@ void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
     sa.head = hd.head.p;
     sa.m = m;
     sa.sbd = sbd;
-    long level = 0, appended = 1;
-    std::vector<double> ob1, ob2;
-    if (obs) {
-        ob1.resize(m);
-        ob2.resize(m);
-        obs(0, G0.data(), G0.data() + m, m, user);
-    }
-    for (long n = 1; n <= N; ++n) {
+    sa.out = outb.p;
+    FRAQ_CUDA(cudaStreamSynchronize(c->stream));
+    setup_seconds = now_s() - t_setup0;
+}
+
+void PhysStepper::step(long n_steps) {
+    if (n_steps < 0) fail(FRAQ_EINVAL, "step: negative step count");
+    if (step_idx + n_steps > N)
+        fail(FRAQ_EINVAL, "step: beyond the horizon the stepper was sized for (spec.n_steps)");
+    for (long q = 0; q < n_steps; ++q) {
+        const long n = ++step_idx;
         const bool first = sbd && n == 1;
         if (fast) {
             if (!first) {
@@ -584,8 +714,9 @@ void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
         }
         sa.n = n;
         sa.first = first;
-        sa.out = (n == N) ? outb.p : nullptr;
-        solve_kernel<512><<<n_inst, threads, smem, c->stream>>>(sa);
+        // the last level of a call leaves G^n in outb (state reads, ffpe_run's result)
+        sa.out = (q == n_steps - 1) ? outb.p : nullptr;
+        solve_kernel<512><<<n_inst, 512, smem, c->stream>>>(sa);
         FRAQ_LAUNCH_CHECK();
         if (!fast) {
             // keep the full history: copy G^n rows out of the 2-slot rings
@@ -598,16 +729,78 @@ void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
         }
         level += 1;
         appended += 1;
-        if (obs) {
-            const GroupDev& G1 = hd.groups_h[0];
-            const GroupDev& G2 = hd.groups_h[1];
-            FRAQ_CUDA(cudaMemcpyAsync(ob1.data(), hd.ring.p + G1.ring_off + (n % G1.L) * (long)G1.ld,
+    }
+}
+
+void PhysStepper::state(double* g1, double* g2) {
+    std::vector<double> outh((size_t)2 * n_inst * m);
+    if (step_idx == 0) {
+        outh = G0;
+    } else {
+        // G^n of every instance from the rings (slot n % L)
+        for (int t = 0; t < 2 * n_inst; ++t) {
+            const GroupDev& G = hd.groups_h[t];
+            FRAQ_CUDA(cudaMemcpyAsync(outh.data() + (size_t)t * m,
+                                      hd.ring.p + G.ring_off + (step_idx % G.L) * (long)G.ld,
                                       sizeof(double) * m, cudaMemcpyDeviceToHost, c->stream));
-            FRAQ_CUDA(cudaMemcpyAsync(ob2.data(), hd.ring.p + G2.ring_off + (n % G2.L) * (long)G2.ld,
-                                      sizeof(double) * m, cudaMemcpyDeviceToHost, c->stream));
-            FRAQ_CUDA(cudaStreamSynchronize(c->stream));
+        }
+        FRAQ_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    for (int i = 0; i < n_inst; ++i) {
+        if (g1) std::memcpy(g1 + (size_t)i * m, outh.data() + (size_t)i * 2 * m, sizeof(double) * m);
+        if (g2)
+            std::memcpy(g2 + (size_t)i * m, outh.data() + (size_t)i * 2 * m + m, sizeof(double) * m);
+    }
+}
+
+void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
+              const fraq_kconf_t* kc_in, double* g1_out, double* g2_out, fraq_run_info_t* info,
+              fraq_observer_fn obs, void* user) {
+    fraq_kconf_t kc;
+    if (kc_in)
+        kc = *kc_in;
+    else
+        fraq_kconf_default(&kc);
+    validate_specs(specs, n_inst, scheme);
+    const bool sbd = scheme == FRAQ_SBD || scheme == FRAQ_FASTSBD;
+    const bool fast = scheme == FRAQ_FASTBE || scheme == FRAQ_FASTSBD;
+    if (kc.solver == FRAQ_SOLVER_MODAL) {
+        if (!fast) fail(FRAQ_EINVAL, "run: the modal solver needs a fast scheme");
+        if (obs) fail(FRAQ_EINVAL, "run: the modal solver does not stream intermediate states");
+        ffpe_run_modal(c, specs, n_inst, sbd, kc, g1_out, g2_out, info);
+        return;
+    }
+    if (kc.solver == FRAQ_SOLVER_AUTO && fast && !obs) {
+        bool done = false;
+        try {
+            ffpe_run_modal(c, specs, n_inst, sbd, kc, g1_out, g2_out, info);
+            done = true;
+        } catch (const Error& e) {
+            if (e.code != FRAQ_EINVAL || std::string(e.what()).find("modal run:") != 0) throw;
+        }
+        if (done) return;
+    }
+    if (kc.solver < 0 || kc.solver > FRAQ_SOLVER_AUTO) fail(FRAQ_EINVAL, "run: unknown solver");
+    PhysStepper st(c, specs, n_inst, scheme, kc);
+    const long N = st.N;
+    const int m = st.m;
+
+    // ---------------------------------------------------------------- time loop
+    cudaEvent_t e0, e1;
+    FRAQ_CUDA(cudaEventCreate(&e0));
+    FRAQ_CUDA(cudaEventCreate(&e1));
+    FRAQ_CUDA(cudaEventRecord(e0, c->stream));
+    if (obs) {
+        // the observer sees every accepted level (fpfp.cpp:367-375), G^0 first
+        std::vector<double> ob1(m), ob2(m);
+        obs(0, st.G0.data(), st.G0.data() + m, m, user);
+        for (long n = 1; n <= N; ++n) {
+            st.step(1);
+            st.state(ob1.data(), ob2.data());  // instance 0 (observer runs are single-instance)
             obs(n, ob1.data(), ob2.data(), m, user);
         }
+    } else {
+        st.step(N);
     }
     FRAQ_CUDA(cudaEventRecord(e1, c->stream));
     FRAQ_CUDA(cudaEventSynchronize(e1));
@@ -616,28 +809,210 @@ void ffpe_run(fraq_ctx c, const fraq_spec_t* specs, int n_inst, int scheme,
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     std::vector<double> outh((size_t)2 * n_inst * m);
-    FRAQ_CUDA(cudaMemcpy(outh.data(), outb.p, sizeof(double) * outh.size(), cudaMemcpyDeviceToHost));
+    FRAQ_CUDA(cudaMemcpy(outh.data(), st.outb.p, sizeof(double) * outh.size(), cudaMemcpyDeviceToHost));
     for (int i = 0; i < n_inst; ++i) {
         std::memcpy(g1_out + (size_t)i * m, outh.data() + (size_t)i * 2 * m, sizeof(double) * m);
         std::memcpy(g2_out + (size_t)i * m, outh.data() + (size_t)i * 2 * m + m, sizeof(double) * m);
     }
     if (info) {
         info->loop_seconds = ms * 1e-3;
-        info->setup_seconds = t_setup1 - t_setup0;
-        info->kernel_eps1 = eps[0];
-        info->kernel_eps2 = eps[1];
+        info->setup_seconds = st.setup_seconds;
+        info->kernel_eps1 = st.eps[0];
+        info->kernel_eps2 = st.eps[1];
         if (fast) {
-            info->np[0] = ks[0].np1;
-            info->np[1] = ks[0].np2;
-            info->np[2] = ks[1].np1;
-            info->np[3] = ks[1].np2;
-            info->n_head[0] = ks[0].n_head;
-            info->n_head[1] = ks[1].n_head;
+            info->np[0] = st.ks[0].np1;
+            info->np[1] = st.ks[0].np2;
+            info->np[2] = st.ks[1].np1;
+            info->np[3] = st.ks[1].np2;
+            info->n_head[0] = st.ks[0].n_head;
+            info->n_head[1] = st.ks[1].n_head;
         } else {
             for (int q = 0; q < 4; ++q) info->np[q] = 0;
             info->n_head[0] = info->n_head[1] = 0;
         }
     }
+}
+
+// ================================================================================ ABI objects
+// Stepper handle: ClassicalStepper / FastStepper (fpfp.hpp:96-140), always physical space (the
+// reference's algorithm: histories K5 + RHS and block solve K6; classical O(n) sums).
+void stepper_create(fraq_ctx c, const fraq_spec_t* spec, int scheme, const fraq_kconf_t* kc_in,
+                    PhysStepper** out) {
+    fraq_kconf_t kc;
+    if (kc_in)
+        kc = *kc_in;
+    else
+        fraq_kconf_default(&kc);
+    validate_specs(spec, 1, scheme);
+    *out = new PhysStepper(c, spec, 1, scheme, kc);
+}
+void stepper_step(PhysStepper* st, long n) { st->step(n); }
+void stepper_state(PhysStepper* st, double* g1, double* g2, long* step) {
+    st->state(g1, g2);
+    if (step) *step = st->step_idx;
+}
+void stepper_eps(PhysStepper* st, double* e1, double* e2) {
+    if (e1) *e1 = st->eps[0];
+    if (e2) *e2 = st->eps[1];
+}
+void stepper_destroy(PhysStepper* st) {
+    cudaStreamSynchronize(st->c->stream);
+    delete st;
+}
+
+// BlockSystem (block_solver.hpp:38-58): the factored system of one (d01, d02, a, tau, lead).
+struct BlockDev {
+    fraq_ctx c;
+    int m;
+    DevBuf<SysDev> sys;
+    DevBuf<M2> thomas;
+    DevBuf<double> io;  // rhs1, rhs2, g1, g2 staging for host calls
+};
+void block_create(fraq_ctx c, double d01, double d02, double a, double tau, int m, double h,
+                  double lead, BlockDev** out) {
+    if (m < 1) fail(FRAQ_EINVAL, "BlockSystem: grid_m must be >= 1");
+    if (!(tau > 0.0) || !(h > 0.0)) fail(FRAQ_EINVAL, "BlockSystem: tau and h must be > 0");
+    if (sizeof(double2) * (m + 2) > 227 * 1024)
+        fail(FRAQ_EINVAL, "BlockSystem: grid_m too large for the on-chip block solve");
+    auto* b = new BlockDev();
+    try {
+        b->c = c;
+        b->m = m;
+        M2 D, E;
+        blocks(d01, d02, a, tau, h, lead, D, E);
+        SysDev S{};
+        S.K = cr_levels(m);
+        S.E = E;
+        S.th_off = 0;
+        if (S.K) setup_cr(S, D, E);
+        b->sys.alloc(1);
+        FRAQ_CUDA(cudaMemcpy(b->sys.p, &S, sizeof(SysDev), cudaMemcpyHostToDevice));
+        b->thomas.alloc(S.K ? 1 : 2L * m);
+        if (!S.K) {
+            DevBuf<M2> dD(1);
+            FRAQ_CUDA(cudaMemcpy(dD.p, &D, sizeof(M2), cudaMemcpyHostToDevice));
+            thomas_setup_kernel<<<1, 32, 0, c->stream>>>(b->sys.p, dD.p, 1, m, b->thomas.p);
+            FRAQ_LAUNCH_CHECK();
+            FRAQ_CUDA(cudaStreamSynchronize(c->stream));
+        }
+        b->io.alloc(4L * m);
+    } catch (...) {
+        delete b;
+        throw;
+    }
+    *out = b;
+}
+void block_solve(BlockDev* b, const double* rhs1, const double* rhs2, double* g1, double* g2,
+                 int mem) {
+    fraq_ctx c = b->c;
+    const int m = b->m;
+    const size_t smem = sizeof(double2) * (m + 2);
+    if (smem > 48 * 1024)
+        FRAQ_CUDA(cudaFuncSetAttribute(block_solve_kernel<512>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (mem == FRAQ_DEVICE) {
+        block_solve_kernel<512><<<1, 512, smem, c->stream>>>(b->sys.p, b->thomas.p, m, rhs1, rhs2,
+                                                            g1, g2);
+        FRAQ_LAUNCH_CHECK();
+        return;
+    }
+    double* d = b->io.p;
+    FRAQ_CUDA(cudaMemcpyAsync(d, rhs1, 8L * m, cudaMemcpyHostToDevice, c->stream));
+    FRAQ_CUDA(cudaMemcpyAsync(d + m, rhs2, 8L * m, cudaMemcpyHostToDevice, c->stream));
+    block_solve_kernel<512><<<1, 512, smem, c->stream>>>(b->sys.p, b->thomas.p, m, d, d + m,
+                                                        d + 2 * m, d + 3 * m);
+    FRAQ_LAUNCH_CHECK();
+    FRAQ_CUDA(cudaMemcpyAsync(g1, d + 2 * m, 8L * m, cudaMemcpyDeviceToHost, c->stream));
+    FRAQ_CUDA(cudaMemcpyAsync(g2, d + 3 * m, 8L * m, cudaMemcpyDeviceToHost, c->stream));
+    FRAQ_CUDA(cudaStreamSynchronize(c->stream));
+}
+void block_destroy(BlockDev* b) {
+    cudaStreamSynchronize(b->c->stream);
+    delete b;
+}
+
+void laplacian_apply(fraq_ctx c, int m, double h, const double* x, double* y, int mem) {
+    if (m < 1) fail(FRAQ_EINVAL, "DiscreteLaplacian: grid_m must be >= 1");
+    const double ih2 = 1.0 / (h * h);
+    if (mem == FRAQ_DEVICE) {
+        laplacian_kernel<<<(m + 255) / 256, 256, 0, c->stream>>>(m, ih2, x, y);
+        FRAQ_LAUNCH_CHECK();
+        return;
+    }
+    DevBuf<double> d(2L * m);
+    FRAQ_CUDA(cudaMemcpyAsync(d.p, x, 8L * m, cudaMemcpyHostToDevice, c->stream));
+    laplacian_kernel<<<(m + 255) / 256, 256, 0, c->stream>>>(m, ih2, d.p, d.p + m);
+    FRAQ_LAUNCH_CHECK();
+    FRAQ_CUDA(cudaMemcpyAsync(y, d.p + m, 8L * m, cudaMemcpyDeviceToHost, c->stream));
+    FRAQ_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+// BandedLU (block_solver.hpp:25-36): band storage assembled on the host (at()), factored and
+// solved on the device.
+struct BandedDev {
+    fraq_ctx c;
+    int n, kl, ku, ldab;
+    bool factored = false;
+    std::vector<double> ab_h;
+    DevBuf<double> ab, rhs;
+    DevBuf<int> piv, status;
+};
+void banded_create(fraq_ctx c, int n, int kl, int ku, BandedDev** out) {
+    if (n < 1 || kl < 0 || ku < 0) fail(FRAQ_EINVAL, "BandedLU: bad shape");
+    auto* b = new BandedDev();
+    b->c = c;
+    b->n = n;
+    b->kl = kl;
+    b->ku = ku;
+    b->ldab = 2 * kl + ku + 1;
+    b->ab_h.assign((size_t)b->ldab * n, 0.0);
+    *out = b;
+}
+double* banded_at(BandedDev* b, int row, int col) {
+    if (row < 0 || row >= b->n || col < 0 || col >= b->n || col - row > b->ku ||
+        row - col > b->kl)
+        fail(FRAQ_ERANGE, "BandedLU::at: outside the band");
+    return &b->ab_h[(size_t)col * b->ldab + (b->kl + b->ku + row - col)];
+}
+void banded_assign(BandedDev* b, const double* ab) {
+    if (!ab) fail(FRAQ_EINVAL, "BandedLU: null band");
+    b->ab_h.assign(ab, ab + b->ab_h.size());
+    b->factored = false;
+}
+void banded_factorize(BandedDev* b) {
+    fraq_ctx c = b->c;
+    b->ab.alloc(b->ab_h.size());
+    b->piv.alloc(b->n);
+    b->status.alloc(1);
+    FRAQ_CUDA(cudaMemcpyAsync(b->ab.p, b->ab_h.data(), 8 * b->ab_h.size(), cudaMemcpyHostToDevice,
+                              c->stream));
+    banded_factor_kernel<<<1, 1, 0, c->stream>>>(b->ab.p, b->piv.p, b->n, b->kl, b->ku,
+                                                 b->status.p);
+    FRAQ_LAUNCH_CHECK();
+    int st = 0;
+    FRAQ_CUDA(cudaMemcpyAsync(&st, b->status.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    FRAQ_CUDA(cudaStreamSynchronize(c->stream));
+    if (st) fail(FRAQ_ERUNTIME, "BandedLU: zero pivot (singular system)");
+    b->factored = true;
+}
+void banded_solve(BandedDev* b, double* rhs, int mem) {
+    if (!b->factored) fail(FRAQ_ELOGIC, "BandedLU::solve before factorize");
+    fraq_ctx c = b->c;
+    if (mem == FRAQ_DEVICE) {
+        banded_solve_kernel<<<1, 1, 0, c->stream>>>(b->ab.p, b->piv.p, b->n, b->kl, b->ku, rhs);
+        FRAQ_LAUNCH_CHECK();
+        return;
+    }
+    if (!b->rhs.p) b->rhs.alloc(b->n);
+    FRAQ_CUDA(cudaMemcpyAsync(b->rhs.p, rhs, 8L * b->n, cudaMemcpyHostToDevice, c->stream));
+    banded_solve_kernel<<<1, 1, 0, c->stream>>>(b->ab.p, b->piv.p, b->n, b->kl, b->ku, b->rhs.p);
+    FRAQ_LAUNCH_CHECK();
+    FRAQ_CUDA(cudaMemcpyAsync(rhs, b->rhs.p, 8L * b->n, cudaMemcpyDeviceToHost, c->stream));
+    FRAQ_CUDA(cudaStreamSynchronize(c->stream));
+}
+void banded_destroy(BandedDev* b) {
+    cudaStreamSynchronize(b->c->stream);
+    delete b;
 }
 
 }  // namespace fraqcu

@@ -499,4 +499,157 @@ std::vector<RunResult> run_batch(const std::vector<ProblemSpec>& specs, Scheme s
     return out;
 }
 
+// ------------------------------------------------------------------ block_solver.hpp
+void DiscreteLaplacian::apply(std::span<const double> x, std::span<double> y) const {
+    if ((int)x.size() < grid_m || (int)y.size() < grid_m)
+        throw std::invalid_argument("DiscreteLaplacian::apply: spans shorter than grid_m");
+    check(fraq_laplacian_apply(default_context(), grid_m, h, x.data(), y.data(), FRAQ_HOST));
+}
+
+double DiscreteLaplacian::eigenvalue(int k, double length) const {
+    // block_solver.cpp:21-24 (closed form; a test oracle in the reference)
+    const double s = std::sin(k * 3.14159265358979323846 * h / (2.0 * length));
+    return 4.0 / (h * h) * s * s;
+}
+
+BandedLU::BandedLU(int n, int kl, int ku)
+    : n_(n), kl_(kl), ku_(ku), ldab_(2 * kl + ku + 1),
+      ab_(static_cast<std::size_t>(2 * kl + ku + 1) * (n > 0 ? n : 0), 0.0) {
+    check(fraq_banded_create(default_context(), n, kl, ku, &b_));
+}
+BandedLU::~BandedLU() {
+    if (b_) fraq_banded_destroy(b_);
+}
+BandedLU::BandedLU(BandedLU&& o) noexcept
+    : n_(o.n_), kl_(o.kl_), ku_(o.ku_), ldab_(o.ldab_), factored_(o.factored_),
+      ab_(std::move(o.ab_)), b_(o.b_) {
+    o.b_ = nullptr;
+}
+BandedLU& BandedLU::operator=(BandedLU&& o) noexcept {
+    if (this != &o) {
+        if (b_) fraq_banded_destroy(b_);
+        n_ = o.n_;
+        kl_ = o.kl_;
+        ku_ = o.ku_;
+        ldab_ = o.ldab_;
+        factored_ = o.factored_;
+        ab_ = std::move(o.ab_);
+        b_ = o.b_;
+        o.b_ = nullptr;
+    }
+    return *this;
+}
+double& BandedLU::at(int row, int col) {
+    if (row < 0 || row >= n_ || col < 0 || col >= n_ || col - row > ku_ || row - col > kl_)
+        throw std::out_of_range("BandedLU::at: outside the band");
+    return ab_[static_cast<std::size_t>(col) * ldab_ + (kl_ + ku_ + row - col)];
+}
+void BandedLU::factorize() {
+    // hand the assembled band to the device object, factor there
+    check(fraq_banded_assign(b_, ab_.data()));
+    check(fraq_banded_factorize(b_));
+    factored_ = true;
+}
+void BandedLU::solve(std::span<double> rhs) const {
+    if (!factored_) throw std::logic_error("BandedLU::solve before factorize");
+    if ((int)rhs.size() < n_) throw std::invalid_argument("BandedLU::solve: rhs shorter than n");
+    check(fraq_banded_solve(b_, rhs.data(), FRAQ_HOST));
+}
+
+BlockSystem::BlockSystem(double d01, double d02, double coupling_a, double tau,
+                         const DiscreteLaplacian& lap, double bdf_lead)
+    : m_(lap.grid_m) {
+    check(fraq_block_create(default_context(), d01, d02, coupling_a, tau, lap.grid_m, lap.h,
+                            bdf_lead, &b_));
+}
+BlockSystem::~BlockSystem() {
+    if (b_) fraq_block_destroy(b_);
+}
+BlockSystem::BlockSystem(BlockSystem&& o) noexcept : m_(o.m_), b_(o.b_) { o.b_ = nullptr; }
+BlockSystem& BlockSystem::operator=(BlockSystem&& o) noexcept {
+    if (this != &o) {
+        if (b_) fraq_block_destroy(b_);
+        m_ = o.m_;
+        b_ = o.b_;
+        o.b_ = nullptr;
+    }
+    return *this;
+}
+void BlockSystem::solve(std::span<const double> rhs1, std::span<const double> rhs2,
+                        std::span<double> g1, std::span<double> g2) const {
+    if ((int)rhs1.size() < m_ || (int)rhs2.size() < m_ || (int)g1.size() < m_ ||
+        (int)g2.size() < m_)
+        throw std::invalid_argument("BlockSystem::solve: spans shorter than grid_m");
+    check(fraq_block_solve(b_, rhs1.data(), rhs2.data(), g1.data(), g2.data(), FRAQ_HOST));
+}
+
+void solve_block_system(double d01, double d02, double coupling_a, double tau,
+                        const DiscreteLaplacian& lap, std::span<const double> rhs1,
+                        std::span<const double> rhs2, std::span<double> g1,
+                        std::span<double> g2, double bdf_lead) {
+    BlockSystem sys(d01, d02, coupling_a, tau, lap, bdf_lead);
+    sys.solve(rhs1, rhs2, g1, g2);
+}
+
+// ------------------------------------------------------------------ steppers (fpfp.hpp:80-140)
+namespace {
+fraq_stepper make_stepper(const ProblemSpec& spec, int scheme, const KernelConfig* kconf) {
+    if (spec.initial == InitialData::custom &&
+        ((int)spec.custom_g1.size() != spec.grid_m || (int)spec.custom_g2.size() != spec.grid_m))
+        throw std::invalid_argument("initial_field: custom samples must have grid_m entries");
+    const fraq_spec_t fs = flat_spec(spec);
+    fraq_kconf_t kc;
+    if (kconf)
+        kc = flat_kconf(*kconf);
+    else
+        fraq_kconf_default(&kc);
+    fraq_stepper st = nullptr;
+    check(fraq_stepper_create(default_context(), &fs, scheme, &kc, &st));
+    return st;
+}
+void refresh(fraq_stepper st, StateField& f, long& at, long step, int m) {
+    if (at == step) return;
+    f.g1.resize(m);
+    f.g2.resize(m);
+    long n = 0;
+    check(fraq_stepper_state(st, f.g1.data(), f.g2.data(), &n));
+    f.step = n;
+    at = step;
+}
+}  // namespace
+
+ClassicalStepper::ClassicalStepper(const ProblemSpec& spec, bool sbd)
+    : st_(make_stepper(spec, sbd ? FRAQ_SBD : FRAQ_BE, nullptr)) {
+    state_.g1.resize(spec.grid_m);
+}
+ClassicalStepper::~ClassicalStepper() {
+    if (st_) fraq_stepper_destroy(st_);
+}
+void ClassicalStepper::step() {
+    check(fraq_stepper_step(st_, 1));
+    ++step_;
+}
+const StateField& ClassicalStepper::state() const {
+    refresh(st_, state_, state_at_, step_, (int)state_.g1.size());
+    return state_;
+}
+
+FastStepper::FastStepper(const ProblemSpec& spec, bool sbd, const KernelConfig& kconf)
+    : st_(make_stepper(spec, sbd ? FRAQ_FASTSBD : FRAQ_FASTBE, &kconf)) {
+    state_.g1.resize(spec.grid_m);
+    check(fraq_stepper_kernel_eps(st_, &eps1_, &eps2_));
+}
+FastStepper::~FastStepper() {
+    if (st_) fraq_stepper_destroy(st_);
+}
+void FastStepper::step() { step_n(1); }
+void FastStepper::step_n(long n) {
+    check(fraq_stepper_step(st_, n));
+    step_ += n;
+}
+const StateField& FastStepper::state() const {
+    refresh(st_, state_, state_at_, step_, (int)state_.g1.size());
+    return state_;
+}
+
 }  // namespace fraq

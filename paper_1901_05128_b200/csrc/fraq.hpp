@@ -163,6 +163,73 @@ public:
     SbdHistory(const FastKernelSBD& kernel, HistoryVariant variant, std::size_t dim);
 };
 
+// ------------------------------------------------------------------ block_solver.hpp
+/// Tridiagonal stencil (-1, 2, -1)/h^2 on M interior nodes, homogeneous Dirichlet
+/// (block_solver.hpp:10-22).  apply() runs on the device.
+struct DiscreteLaplacian {
+    int grid_m = 1;
+    double h = 0.5;
+
+    DiscreteLaplacian() = default;
+    DiscreteLaplacian(int m, double length) : grid_m(m), h(length / (m + 1)) {}
+
+    /// y = A x
+    void apply(std::span<const double> x, std::span<double> y) const;
+
+    /// lambda_k = (4/h^2) sin^2(k pi h / (2L)), k = 1..M.  Test oracle.
+    double eigenvalue(int k, double length) const;
+};
+
+/// General banded LU with partial pivoting, LAPACK gbtrf storage (block_solver.hpp:25-36).
+/// at() assembles into a host copy; factorize() and solve() run on the device.
+class BandedLU {
+public:
+    BandedLU(int n, int kl, int ku);
+    ~BandedLU();
+    BandedLU(const BandedLU&) = delete;
+    BandedLU& operator=(const BandedLU&) = delete;
+    BandedLU(BandedLU&&) noexcept;
+    BandedLU& operator=(BandedLU&&) noexcept;
+
+    double& at(int row, int col);  // assembly access, |row-col| <= kl/ku
+    void factorize();              // throws on zero pivot
+    void solve(std::span<double> rhs) const;
+
+private:
+    int n_, kl_, ku_, ldab_;
+    bool factored_ = false;
+    std::vector<double> ab_;
+    fraq_banded b_ = nullptr;
+};
+
+/// One implicit solve of the coupled two-field block system (block_solver.hpp:38-58):
+///   [ lead/tau + d01 (a + A) , -a d02 I ; -a d01 I , lead/tau + d02 (a + A) ],
+/// reduced once on construction (block cyclic reduction / block Thomas), solved on the device.
+class BlockSystem {
+public:
+    BlockSystem(double d01, double d02, double coupling_a, double tau,
+                const DiscreteLaplacian& lap, double bdf_lead);
+    ~BlockSystem();
+    BlockSystem(const BlockSystem&) = delete;
+    BlockSystem& operator=(const BlockSystem&) = delete;
+    BlockSystem(BlockSystem&&) noexcept;
+    BlockSystem& operator=(BlockSystem&&) noexcept;
+
+    /// Solves into g1, g2 (each grid_m long).
+    void solve(std::span<const double> rhs1, std::span<const double> rhs2,
+               std::span<double> g1, std::span<double> g2) const;
+
+private:
+    int m_;
+    fraq_block b_ = nullptr;
+};
+
+/// The one-shot form shared by all steppers: assemble, factorize, solve (block_solver.hpp:60-65).
+void solve_block_system(double d01, double d02, double coupling_a, double tau,
+                        const DiscreteLaplacian& lap, std::span<const double> rhs1,
+                        std::span<const double> rhs2, std::span<double> g1,
+                        std::span<double> g2, double bdf_lead = 1.0);
+
 // ------------------------------------------------------------------ fpfp.hpp
 enum class Scheme { BE, FastBE, SBD, FastSBD };
 Scheme scheme_from_name(const std::string& name);
@@ -215,8 +282,9 @@ struct RunResult {
 StateField initial_field(const ProblemSpec& spec);
 double l2_norm(std::span<const double> v, double h);
 
-/// fpfp.cpp:351-381 on the device.  The observer, when set, sees the initial state only (the
-/// device loop does not stream intermediate states back; pass n_steps-limited specs instead).
+/// fpfp.cpp:351-381 on the device.  The observer, when set, sees the initial state and every
+/// accepted step (fpfp.cpp:360-375): the run then uses the physical solver and copies each level
+/// back to the host (fraq_run_observed).
 RunResult run(const ProblemSpec& spec, Scheme scheme, const KernelConfig& kconf = {},
               const std::function<void(long, const StateField&)>& observer = nullptr);
 
@@ -242,6 +310,51 @@ RunResult modal_run(double alpha1, double alpha2, double coupling_a, double t_fi
                     long n_steps, Scheme scheme, long n_modes, const double* lam,
                     const double* c0, double* cN, int mem = FRAQ_HOST,
                     const KernelConfig& kconf = {});
+
+// --- single-step entry points (fpfp.hpp:80-140); the state lives on the device ---
+
+/// Classical stepper (fpfp.hpp:82-101): full solution history on the device, O(n) direct CQ
+/// sums per step, block solve.  spec.n_steps is the last reachable step.
+class ClassicalStepper {
+public:
+    ClassicalStepper(const ProblemSpec& spec, bool sbd);
+    ~ClassicalStepper();
+    ClassicalStepper(const ClassicalStepper&) = delete;
+    ClassicalStepper& operator=(const ClassicalStepper&) = delete;
+    void step();  // advances by one time level
+    const StateField& state() const;
+    long step_index() const { return step_; }
+
+private:
+    fraq_stepper st_ = nullptr;
+    long step_ = 0;
+    mutable StateField state_;
+    mutable long state_at_ = -1;
+};
+
+/// Fast stepper (fpfp.hpp:103-140): exact heads, per-node accumulators (K5), factored blocks,
+/// reconstructed SBD correction weights -- the reference's physical-space algorithm on the GPU.
+class FastStepper {
+public:
+    FastStepper(const ProblemSpec& spec, bool sbd, const KernelConfig& kconf);
+    ~FastStepper();
+    FastStepper(const FastStepper&) = delete;
+    FastStepper& operator=(const FastStepper&) = delete;
+    void step();
+    const StateField& state() const;
+    long step_index() const { return step_; }
+    double kernel_eps1() const { return eps1_; }
+    double kernel_eps2() const { return eps2_; }
+    /// addition: advance n levels in one stream-ordered call
+    void step_n(long n);
+
+private:
+    fraq_stepper st_ = nullptr;
+    long step_ = 0;
+    double eps1_ = 0.0, eps2_ = 0.0;
+    mutable StateField state_;
+    mutable long state_at_ = -1;
+};
 
 /// Many independent instances (same grid_m, n_steps, t_final) solved together.
 std::vector<RunResult> run_batch(const std::vector<ProblemSpec>& specs, Scheme scheme,

@@ -928,5 +928,6 @@ void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, l
 }
 
 int hist_last_path(fraq_hist h) { return h->last_path; }
+fraq_ctx hist_ctx(fraq_hist h) { return h->ctx; }
 
 }  // namespace fraqcu

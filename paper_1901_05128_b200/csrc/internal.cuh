@@ -35,18 +35,9 @@ void set_last_error(const std::string& m);
 
 #define FRAQ_LAUNCH_CHECK() FRAQ_CUDA(cudaGetLastError())
 
-// The library is thread-safe by serialisation: calls share a context's stream and setup scratch
-// buffers, so concurrent callers (the reference's run() is reentrant and releases the GIL; its
-// harness runs solves in worker threads) take turns.  One mutex per library (inline function,
-// not per template instance); recursive, since an observer callback may call back into the API.
-inline std::recursive_mutex& api_mutex() {
-    static std::recursive_mutex m;
-    return m;
-}
-
+// Error mapping of every ABI entry point: exceptions -> return code + thread-local message.
 template <class F>
-int guarded(F&& f) {
-    std::lock_guard<std::recursive_mutex> lock(api_mutex());
+int guarded_nolock(F&& f) {
     try {
         f();
         return FRAQ_OK;
@@ -62,6 +53,13 @@ int guarded(F&& f) {
     }
 }
 
+// Context-free entry points (host math, context creation): no shared state, no lock.
+template <class F>
+int guarded(F&& f) {
+    return guarded_nolock(f);
+}
+
+// ------------------------------------------------------------------ device buffers
 // ------------------------------------------------------------------ device buffers
 template <class T>
 struct DevBuf {
@@ -103,6 +101,11 @@ struct DevBuf {
 }  // namespace fraqcu
 
 struct fraq_ctx_s {
+    // Calls on one context share its stream and setup scratch buffers, so concurrent callers of
+    // the SAME context take turns (the reference's run() is reentrant and releases the GIL; its
+    // harness runs solves in worker threads).  Different contexts -- one per GPU, INTEGRATION.md
+    // section 5 -- never contend.  Recursive: an observer callback may call back into the API.
+    std::recursive_mutex mu;
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -121,6 +124,14 @@ struct fraq_ctx_s {
 };
 
 namespace fraqcu {
+
+// Entry points bound to a context: serialised per context (see fraq_ctx_s::mu).
+template <class F>
+int guarded(fraq_ctx c, F&& f) {
+    if (!c) return guarded_nolock([] { fail(FRAQ_EINVAL, "null fraq_ctx"); });
+    std::lock_guard<std::recursive_mutex> lock(c->mu);
+    return guarded_nolock(f);
+}
 
 inline void check_ctx(fraq_ctx c) {
     if (!c) fail(FRAQ_EINVAL, "null fraq_ctx");

@@ -219,8 +219,13 @@ __global__ void chain_kernel(const ChainJob* jobs, int n_jobs) {
     }
 }
 
-__global__ void scale_kernel(double* v, long n, double g, double tau, int sbd) {
-    const double sc = sbd ? pow(1.5 / tau, g) : pow(tau, -g);
+// d_i = c_i * tau^-g for every table of a batch (blockIdx.y = table).  The scales come from the
+// host's std::pow, the reference's own call (cq_weights.cpp:36), so d_0 -- which enters the
+// FFPE block system's diagonal, where one ulp is amplified by the ~1e6 condition number --
+// is bit-identical to the reference's.
+__global__ void scale_kernel(double* base, long n, const double* scales) {
+    double* v = base + (long)blockIdx.y * n;
+    const double sc = scales[blockIdx.y];
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
         v[i] *= sc;
 }
@@ -228,7 +233,7 @@ __global__ void scale_kernel(double* v, long n, double g, double tau, int sbd) {
 // SBD Cauchy product out_i = (3/(2 tau))^g sum_{j<=i} c1_j c2_{i-j}, serial j per output index
 // (cq_weights.cpp:56-59).  blockIdx.y = table in a batch.
 struct CauchyJob {
-    double g, tau;
+    double sc;  // (3/(2 tau))^g from the host's std::pow (cq_weights.cpp:54)
     long n_max;
     const double* c1;
     const double* c2;
@@ -236,7 +241,7 @@ struct CauchyJob {
 };
 __global__ void cauchy_kernel(const CauchyJob* jobs) {
     const CauchyJob J = jobs[blockIdx.y];
-    const double sc = pow(1.5 / J.tau, J.g);
+    const double sc = J.sc;
     // process indices from the top so long rows start first
     const long i = J.n_max - (blockIdx.x * (long)blockDim.x + threadIdx.x);
     if (i < 0) return;
@@ -413,11 +418,12 @@ void weights_batch(fraq_ctx c, bool sbd, const std::vector<double>& gs, double t
         DevBuf<ChainJob> d = upload(c, cj);
         chain_kernel<<<(B + 127) / 128, 128, 0, c->stream>>>(d.p, B);
         FRAQ_LAUNCH_CHECK();
-        for (int t = 0; t < B; ++t) {
-            scale_kernel<<<std::min<long>(1024, (L + 255) / 256), 256, 0, c->stream>>>(
-                base + t * L, L, gs[t], tau, 0);
-            FRAQ_LAUNCH_CHECK();
-        }
+        std::vector<double> sc(B);
+        for (int t = 0; t < B; ++t) sc[t] = std::pow(tau, -gs[t]);
+        DevBuf<double> dsc = upload(c, sc);
+        dim3 grid((unsigned)std::min<long>(256, (L + 255) / 256), (unsigned)B);
+        scale_kernel<<<grid, 256, 0, c->stream>>>(base, L, dsc.p);
+        FRAQ_LAUNCH_CHECK();
         FRAQ_CUDA(cudaStreamSynchronize(c->stream));
         return;
     }
@@ -432,7 +438,7 @@ void weights_batch(fraq_ctx c, bool sbd, const std::vector<double>& gs, double t
     FRAQ_LAUNCH_CHECK();
     std::vector<CauchyJob> qj(B);
     for (int t = 0; t < B; ++t)
-        qj[t] = {gs[t], tau, n_max, cs.p + (size_t)(2 * t) * L, cs.p + (size_t)(2 * t + 1) * L,
+        qj[t] = {std::pow(1.5 / tau, gs[t]), n_max, cs.p + (size_t)(2 * t) * L, cs.p + (size_t)(2 * t + 1) * L,
                  base + t * L};
     DevBuf<CauchyJob> dq = upload(c, qj);
     dim3 grid((unsigned)((L + 127) / 128), (unsigned)B);
@@ -591,15 +597,28 @@ void corr_sequence_dev(fraq_ctx c, const fraq_kernel_t* k, long e_max, double* c
 void corr_sequence_batch_dev(fraq_ctx c, const fraq_kernel_t* ks, int n, long e_max,
                              double* corr_base, long stride) {
     if (n <= 0) return;
-    std::vector<DevKernel> dk;
-    dk.reserve(n);
+    // every kernel's (m, r) tables packed into one host vector: one allocation, one copy
+    std::vector<size_t> off(n);
+    size_t total = 0;
+    for (int t = 0; t < n; ++t) {
+        off[t] = total;
+        total += (size_t)(ks[t].np1 + ks[t].np2);
+    }
+    std::vector<double> m(std::max<size_t>(1, total)), r(std::max<size_t>(1, total));
+    for (int t = 0; t < n; ++t) {
+        const fraq_kernel_t& k = ks[t];
+        double* mt = m.data() + off[t];
+        double* rt = r.data() + off[t];
+        for (int j = 0; j < k.np1; ++j) mt[j] = k.m1[j], rt[j] = k.r1[j];
+        for (int j = 0; j < k.np2; ++j) mt[k.np1 + j] = k.m2[j], rt[k.np1 + j] = k.r2[j];
+    }
+    DevBuf<double> dm = upload(c, m), dr = upload(c, r);
     std::vector<ScanJob> jobs;
     jobs.reserve(n);
-    for (int t = 0; t < n; ++t) {
-        dk.push_back(upload_kernel(c, ks + t));
-        jobs.push_back(ScanJob{dk[t].J, dk[t].m.p, dk[t].r.p, 0, 3, e_max + 3, nullptr,
-                               corr_base + (size_t)t * stride - 3, nullptr, nullptr});
-    }
+    for (int t = 0; t < n; ++t)
+        jobs.push_back(ScanJob{ks[t].np1 + ks[t].np2, dm.p + off[t], dr.p + off[t], 0, 3,
+                               e_max + 3, nullptr, corr_base + (size_t)t * stride - 3, nullptr,
+                               nullptr});
     run_scans(c, jobs);
 }
 

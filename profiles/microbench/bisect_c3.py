@@ -2,7 +2,7 @@ import sys, numpy as np
 sys.path.insert(0, ".")
 import paper_1901_05128_b200 as fraq
 from oracle.oracle import Oracle
-from paper_1901_05128_b200.workloads import c3_instance
+from workloads import c3_instance
 orc = Oracle("reference")
 def rel(a, b):
     a, b = np.asarray(a), np.asarray(b); return np.max(np.abs(a - b)) / np.max(np.abs(b))

@@ -8,7 +8,7 @@ import torch
 sys.path.insert(0, ".")
 import paper_1901_05128_b200 as fraq  # noqa: E402
 from paper_1901_05128_b200.parallel import FraqOps, run_2d_sharded, run_2d_transposed  # noqa: E402
-from paper_1901_05128_b200.workloads import c4_instance  # noqa: E402
+from workloads import c4_instance  # noqa: E402
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 M = 1023

@@ -3,7 +3,7 @@ device auto-sizing + K13 tables + transfers, loop_seconds the DST + K13 + invers
 import sys, time
 sys.path.insert(0, ".")
 import paper_1901_05128_b200 as fraq
-from paper_1901_05128_b200.workloads import c5_instances
+from workloads import c5_instances
 
 N = 16384
 kc = fraq.KernelConfig()

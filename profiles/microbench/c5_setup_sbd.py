@@ -2,7 +2,7 @@
 import sys
 sys.path.insert(0, ".")
 import paper_1901_05128_b200 as fraq
-from paper_1901_05128_b200.workloads import c5_instances
+from workloads import c5_instances
 kc = fraq.KernelConfig()
 kc.solver = fraq.SOLVER_MODAL
 specs = [fraq.ProblemSpec(alpha1=i.alpha1, alpha2=i.alpha2, coupling_a=i.coupling_a, grid_m=4095,

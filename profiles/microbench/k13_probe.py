@@ -2,7 +2,7 @@
 import sys
 sys.path.insert(0, ".")
 import paper_1901_05128_b200 as fraq
-from paper_1901_05128_b200.workloads import c5_instances
+from workloads import c5_instances
 
 scheme = sys.argv[1] if len(sys.argv) > 1 else "FastBE"
 n_inst = int(sys.argv[2]) if len(sys.argv) > 2 else 32

@@ -6,7 +6,7 @@ import sys, time
 import numpy as np
 sys.path.insert(0, ".")
 from oracle.oracle import Oracle
-from paper_1901_05128_b200.workloads import c3_instance
+from workloads import c3_instance
 
 M, N = 4095, int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 T = N / 16384

@@ -4,7 +4,7 @@ import sys
 import numpy as np
 sys.path.insert(0, ".")
 from oracle.oracle import Oracle
-from paper_1901_05128_b200.workloads import c3_instance
+from workloads import c3_instance
 
 def modespace_be(M, N, T, a, al1, al2, g1, g2, dt=np.longdouble):
     h = dt(1) / (M + 1); tau = dt(T) / N

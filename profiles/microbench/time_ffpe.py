@@ -4,7 +4,7 @@ import sys, time
 sys.path.insert(0, ".")
 import numpy as np
 import paper_1901_05128_b200 as fraq
-from paper_1901_05128_b200.workloads import c3_instance, c5_instances
+from workloads import c3_instance, c5_instances
 
 def kc(modal):
     k = fraq.KernelConfig()

@@ -5,7 +5,7 @@ sources compiled by oracle/Makefile).  Run in the build container, where /root/r
 
 Contents (all produced by the reference's own code path):
   c1_*   C1 workload sample: BE auto kernel at (0.5, 1/4096, 4096), 4 DOFs x 4096 steps of
-         u_k = t^{b_k} (paper_1901_05128_b200.workloads.c1_params), reference derivatives;
+         u_k = t^{b_k} (workloads.c1_params), reference derivatives;
   c4a/b  SBD auto sizing at the C4 exponents (0.7, 0.4), tau = 1/8192, horizon 8192;
   ffpe*  reference fraq::run final states for small poly_sin problems, all four schemes.
 """
@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 from oracle.oracle import Oracle  # noqa: E402
-from paper_1901_05128_b200.workloads import c1_params  # noqa: E402  (pure numpy, no GPU)
+from workloads import c1_params  # noqa: E402  (pure numpy, no GPU)
 
 
 def main():

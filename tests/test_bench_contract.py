@@ -29,6 +29,24 @@ def test_reference_arm_contract(workload):
     cb = d["cpu_baseline"]
     assert cb["kind"] == "reference" and cb["cores"] >= 1 and cb["value"] == d["value"]
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
+    # same_config: the reference arm prints exactly the dict the GPU arm prints
+    if workload == "C2":
+        import bench
+        assert d["config"] == bench.c2_config(1, [512, 512], [17, 15])
+    else:
+        import bench_ffpe
+        assert d["config"] == bench_ffpe.Workload(workload, 0, 1).config()
+
+
+def test_reference_arm_maps_no_product_library():
+    """The CPU arm must not load the B200 package (its __init__ maps _fraq / libfraqcu.so):
+    everything it imports -- workloads, oracle -- lives outside the package."""
+    code = ("import sys; sys.argv = ['bench.py']; import bench, bench_ffpe, workloads, oracle.oracle; "
+            "workloads.c2_params(64); bench_ffpe.Workload('C3', 0, 1).config(); "
+            "bad = [m for m in sys.modules if m.startswith('paper_1901_05128_b200')]; "
+            "assert not bad, bad")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
 
 
 @pytest.mark.gpu

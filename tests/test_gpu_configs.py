@@ -7,7 +7,7 @@ Oracle: the reference compiled from its sources (oracle/_ref) when present, else
 import numpy as np
 import pytest
 
-from paper_1901_05128_b200.workloads import c1_params, c2_params, c3_instance, c5_instances
+from workloads import c1_params, c2_params, c3_instance, c5_instances
 
 pytestmark = pytest.mark.gpu
 
@@ -57,11 +57,14 @@ def test_c1_fast_and_direct(fraq, orc, port):
 
 @pytest.mark.slow
 def test_c2_sampled_dofs_full_horizon(fraq, orc, port):
-    """C2: BDF2, 65536 DOFs (gamma 0.7 | 0.3), N = 65536: 16 + 16 sampled DOFs through the full
-    horizon with the production tables; GPU fast == reference fast; direct sums on 2 DOFs."""
+    """C2: BDF2, 65536 DOFs (gamma 0.7 | 0.3), N = 65536, production tables: every 32nd DOF
+    (2048 lanes, 1024 per exponent) through the full horizon, GPU fast (K5d) == reference fast
+    (SbdHistory lanes, all host threads) at <= 1e-10 on 1024 checkpoints per lane; direct sums on
+    one lane per exponent (GPU K10 vs the oracle) with the fast-vs-direct gap reproduced."""
+    import os
     p = c2_params()
     half = 32768
-    idx = np.concatenate([np.arange(0, half, half // 16), half + np.arange(0, half, half // 16)])
+    idx = np.arange(0, 65536, 32)
     U = p.signal(0, p.n_steps, idx)
     ks, kos = [], []
     for g in (0.7, 0.3):
@@ -70,21 +73,119 @@ def test_c2_sampled_dofs_full_horizon(fraq, orc, port):
         kos.append(orc.build_kernel_auto(True, g, p.tau, p.n_steps))
         assert (len(ks[-1].ratio1), ks[-1].n_head) == (kos[-1].np1, kos[-1].n_head)
         assert b.achieved_eps == pytest.approx(kos[-1].achieved_eps, rel=1e-3)
-    h = fraq.MultiHistory(ks, [16, 16])
+    nl = len(idx) // 2
+    h = fraq.MultiHistory(ks, [nl, nl])
     D = h.run(U)
+    assert h.last_path >= 1
+    stride = 64
+    if orc.kind == "reference":
+        T = orc.hist_trace(kos, U, stride, os.cpu_count() or 1)
+    else:
+        T = np.hstack([orc.hist_run(kos[gi], U[:, gi * nl:(gi + 1) * nl])[stride - 1::stride]
+                       for gi in range(2)])
+    Dc = D[stride - 1::stride]
     for gi in range(2):
-        cols = slice(16 * gi, 16 * gi + 16)
-        D_ref = orc.hist_run(kos[gi], U[:, cols])
-        assert rel_linf(D[:, cols], D_ref) <= 1e-10
-        # direct O(N^2) sums on one DOF per exponent: GPU (DMMA) vs oracle, and the gap
-        c = 16 * gi
+        cols = slice(gi * nl, (gi + 1) * nl)
+        lane_err = np.max(np.abs(Dc[:, cols] - T[:, cols]), axis=0) / np.max(np.abs(T[:, cols]))
+        assert np.max(lane_err) <= 1e-10, (gi, np.argmax(lane_err), np.max(lane_err))
+    for gi in range(2):
+        c = gi * nl
         g = (0.7, 0.3)[gi]
         Dd = fraq.direct_cq(True, g, p.tau, U[:, c:c + 1])
         Dd_ref = port.direct_cq(True, g, p.tau, U[:, c:c + 1])
         assert rel_linf(Dd, Dd_ref) <= 1e-10
         gap_gpu = rel_linf(D[:, c:c + 1], Dd)
-        gap_ref = rel_linf(D_ref[:, :1], Dd_ref)
+        D_ref = orc.hist_run(kos[gi], U[:, c:c + 1])
+        gap_ref = rel_linf(D_ref, Dd_ref)
         assert gap_gpu == pytest.approx(gap_ref, rel=1e-2)  # reference accuracy at its 256 cap
+
+
+@pytest.mark.slow
+def test_c2_full_size_direct_all_lanes(fraq, port):
+    """C2 at full size on the device: fast CQ (K5d) and direct O(N^2) CQ (K10, DMMA Toeplitz
+    GEMM) on ALL 65536 lanes over the full horizon N = 65536 (the fast-vs-direct comparison of
+    test_fast_kernel.cpp:27-41 at the BASELINE size).  Per exponent: the fast-vs-direct gap of
+    every lane, compared with the reference-side gap (oracle direct sums, reference-pinned fast
+    port) on 8 sampled lanes to 2 significant digits, and the distribution over all lanes
+    recorded (profiles/r02/c2_direct_gaps.json when FRAQ_RECORD is set)."""
+    import json
+    import os
+    import torch
+    p = c2_params()
+    N, half = p.n_steps, 32768
+    dev = torch.device("cuda", 0)
+    out = {}
+    for gi, g in enumerate((0.7, 0.3)):
+        sl = slice(gi * half, (gi + 1) * half)
+        a, b, c, w = (torch.from_numpy(x[sl].copy()).to(dev) for x in (p.a, p.b, p.c, p.w))
+        U = torch.empty((N, half), dtype=torch.float64, device=dev)
+        for n0 in range(0, N, 2048):
+            t = (torch.arange(n0, n0 + 2048, device=dev, dtype=torch.float64) * p.tau)[:, None]
+            U[n0:n0 + 2048] = a * torch.pow(t, b) + c * torch.sin(w * t)
+        bud = fraq.KernelBudget(horizon=N, eps_tol=1e-12)
+        k = fraq.build_sbd_kernel_auto(g, p.tau, bud)
+        Df = torch.empty_like(U)
+        hh = fraq.MultiHistory([k], [half])
+        hh.run_device(U.data_ptr(), half, N, Df.data_ptr(), half)
+        Dd = torch.empty_like(U)
+        fraq.direct_cq_device(True, g, p.tau, U.data_ptr(), half, N, half, Dd.data_ptr(), half)
+        fraq.synchronize()
+        diff = torch.zeros(half, dtype=torch.float64, device=dev)
+        scale = torch.zeros(half, dtype=torch.float64, device=dev)
+        for n0 in range(1, N, 4096):
+            n1 = min(N, n0 + 4096)
+            diff = torch.maximum(diff, (Df[n0:n1] - Dd[n0:n1]).abs().amax(0))
+            scale = torch.maximum(scale, Dd[n0:n1].abs().amax(0))
+        gaps = (diff / scale).cpu().numpy()
+        assert np.all(np.isfinite(gaps))
+        lanes = np.arange(0, half, half // 8)
+        Us = U[:, lanes].cpu().numpy()
+        Dfs, Dds = Df[:, lanes].cpu().numpy(), Dd[:, lanes].cpu().numpy()
+        del U, Df, Dd
+        torch.cuda.empty_cache()
+        ko = port.build_kernel_auto(True, g, p.tau, N)
+        Fr = port.hist_run(ko, Us)
+        Dr = port.direct_cq(True, g, p.tau, Us)
+        for j in range(len(lanes)):
+            assert rel_linf(Dds[1:, j], Dr[1:, j]) <= 1e-10            # GPU direct == direct
+            assert rel_linf(Dfs[1:, j], Fr[1:, j]) <= 1e-10            # GPU fast == fast
+            ref_gap = rel_linf(Fr[1:, j], Dr[1:, j])
+            assert gaps[lanes[j]] == pytest.approx(ref_gap, rel=1e-2)  # the gap, 2 digits
+        out[str(g)] = {"lanes": half, "median": float(np.median(gaps)),
+                       "p99": float(np.quantile(gaps, 0.99)), "max": float(gaps.max()),
+                       "sampled_ref_gaps": [float(rel_linf(Fr[1:, j], Dr[1:, j]))
+                                            for j in range(len(lanes))]}
+        assert gaps.max() < 1e-2  # the reference's accuracy at its 256-point cap (SURVEY §8c)
+    if os.environ.get("FRAQ_RECORD"):
+        os.makedirs("profiles/r02", exist_ok=True)
+        json.dump(out, open("profiles/r02/c2_direct_gaps.json", "w"), indent=1)
+
+
+def test_c5_auto_sizes_all_instances(fraq):
+    """Every C5 exponent (4096 instances x 2 fields, tau = 1/16384, horizon 16384): the batched
+    device auto-sizer (fraq_build_kernels_auto, the path run_batch takes) reproduces the
+    reference's decisions (fast_kernel.cpp:182-256; tests/golden/c5_sizes.npz, generated from
+    oracle/_ref by tests/golden/make_c5_sizes.py): (N_p1, N_p2, n_head) exactly and the achieved
+    eps to 1e-6 relative, for BE and SBD."""
+    import os
+    d = np.load(os.path.join(os.path.dirname(__file__), "golden", "c5_sizes.npz"))
+    gam = d["gamma"]
+    tau, H = float(d["tau"]), int(d["horizon"])
+    bad = []
+    for sbd in (False, True):
+        got = []
+        for c0 in range(0, len(gam), 1024):
+            got += fraq.build_kernels_auto_sizes(sbd, list(gam[c0:c0 + 1024]), tau, H)
+        for t, (n1, n2, nh, eps) in enumerate(got):
+            if sbd:
+                want = tuple(int(x) for x in d["sbd_sizes"][t])
+                we = float(d["sbd_eps"][t])
+                have = (n1, n2, nh)
+            else:
+                want, we, have = (int(d["be_np"][t]),), float(d["be_eps"][t]), (n1,)
+            if have != want or abs(eps - we) > 1e-6 * we:
+                bad.append((sbd, t, float(gam[t]), have, want, eps, we))
+    assert not bad, bad[:20]
 
 
 def _modespace_be_truth(M, N, T, a, al1, al2, g1, g2):
@@ -126,10 +227,14 @@ def _modespace_be_truth(M, N, T, a, al1, al2, g1, g2):
 
 @pytest.mark.parametrize("N", [64, 256])
 def test_c3_grid_against_extended_precision_truth(fraq, orc, N):
-    """C3 grid (M = 4095, tau = 1/16384, a = -5.5, discontinuous data): both the reference and the
-    B200 path carry O(kappa eps) rounding per implicit step (cond of the block system ~1.4e6), so
-    each is compared with the extended-precision mode-space truth; the B200 result must be at
-    least as accurate as the reference's (measured: 8.5e-10 vs 1.4e-9 at N = 64)."""
+    """C3 grid (M = 4095, tau = 1/16384, a = -5.5, discontinuous data), classical BE.  The
+    reference's physical-space solve carries a systematic deviation from the exact discrete
+    solution: its block system (cond ~1.4e6) has a constant diagonal lead/tau + d0 (a + 2/h^2)
+    whose fp64 rounding shifts every row alike (profiles/r02/physical_bisect.txt).  The B200
+    physical path forms the same fp64 entries (bit-identical d0, the reference's fma) and reduces
+    them in extended precision, so it reproduces the reference's result -- deviation included --
+    to <= 1e-10, while the extended-precision mode-space evaluation is the truth both are
+    measured against."""
     inst = c3_instance()
     T = N / 16384
     t1, t2 = _modespace_be_truth(4095, N, T, -5.5, 0.4, 0.8, inst.g1, inst.g2)
@@ -138,10 +243,13 @@ def test_c3_grid_against_extended_precision_truth(fraq, orc, N):
                             custom_g2=list(inst.g2))
     rr = fraq.run(spec, fraq.Scheme.BE)
     g1, g2, _, _ = orc.run(0.4, 0.8, -5.5, 4095, T, N, "BE", "custom", inst.g1, inst.g2)
-    err_gpu = max(rel_linf(rr.final_state.g1, t1), rel_linf(rr.final_state.g2, t2))
-    err_ref = max(rel_linf(g1, t1), rel_linf(g2, t2))
-    assert err_gpu <= 1.5 * err_ref
-    assert err_gpu <= 1e-8
+    sc = max(np.max(np.abs(t1)), np.max(np.abs(t2)))
+    ad = lambda x, y: float(np.max(np.abs(np.asarray(x) - y))) / sc
+    err_gpu = max(ad(rr.final_state.g1, t1), ad(rr.final_state.g2, t2))
+    err_ref = max(ad(g1, t1), ad(g2, t2))
+    assert max(ad(rr.final_state.g1, g1), ad(rr.final_state.g2, g2)) <= 1e-10
+    assert err_gpu <= 1.05 * err_ref + 1e-12
+    assert err_ref < 1e-8
 
 
 def _modespace_fastbe(orc, inst, M, N, a, al1, al2):
@@ -181,11 +289,15 @@ def _modespace_fastbe(orc, inst, M, N, a, al1, al2):
 @pytest.mark.slow
 @pytest.mark.parametrize("solver", ["SOLVER_PHYSICAL", "SOLVER_AUTO"])
 def test_c3_full(fraq, orc, solver):
-    """C3 at full size: M = 4095, N = 16384, FastBE, alpha (0.4, 0.8), m = 0.45 (a = -5.5).
-    Same auto-sized kernels and certificates as the reference.  The physical-space scheme's
-    rounding drift on this grid is ~1e-7 absolute over 16384 implicit steps for ANY fp64
-    implementation (measured: reference vs the fp64 mode-space evaluation 6.8e-8, B200 4.3e-8);
-    the B200 state must be at least as close to the mode-space evaluation as the reference's."""
+    """C3 at full size: M = 4095, N = 16384, FastBE, alpha (0.4, 0.8), m = 0.45 (a = -5.5); the
+    reference's auto-sized kernels and certificates.
+    PHYSICAL (the reference's algorithm: histories + stencil + block solve) must reproduce the
+    reference's own result: <= 5e-9 of max|G| after 16384 steps of the cond ~1.4e6 system (fp64
+    LU rounding of the reference's per-step solves, not reproducible by a parallel solve;
+    profiles/r02/physical_bisect.txt: 2.1e-9 with the same entries, 2.0e-6 before).
+    AUTO (mode space, the default) steps the same discrete scheme without the ill-conditioned
+    solve: it must match the fp64 mode-space evaluation to 1e-10 and be closer to it than the
+    reference, whose own deviation (~1.2e-6 of max|G|) is recorded."""
     inst = c3_instance()
     spec = fraq.ProblemSpec(alpha1=inst.alpha1, alpha2=inst.alpha2, coupling_a=inst.coupling_a,
                             grid_m=4095, t_final=1.0, n_steps=16384, initial="custom",
@@ -195,35 +307,69 @@ def test_c3_full(fraq, orc, solver):
     rr = fraq.run(spec, fraq.Scheme.FastBE, kc)
     g1, g2, e1, e2 = orc.run(inst.alpha1, inst.alpha2, inst.coupling_a, 4095, 1.0, 16384,
                              "FastBE", "custom", inst.g1, inst.g2)
-    assert rr.kernel_eps1 == pytest.approx(e1, rel=1e-3)
-    assert rr.kernel_eps2 == pytest.approx(e2, rel=1e-3)
+    assert rr.kernel_eps1 == pytest.approx(e1, rel=1e-6)
+    assert rr.kernel_eps2 == pytest.approx(e2, rel=1e-6)
+    sc = max(np.max(np.abs(g1)), np.max(np.abs(g2)))
+    ad = lambda x, y: float(np.max(np.abs(np.asarray(x) - y))) / sc
+    vs_ref = max(ad(rr.final_state.g1, g1), ad(rr.final_state.g2, g2))
+    if solver == "SOLVER_PHYSICAL":
+        assert vs_ref <= 5e-9
+        return
     t1, t2 = _modespace_fastbe(orc, inst, 4095, 16384, inst.coupling_a, inst.alpha1, inst.alpha2)
-    ad = lambda x, y: float(np.max(np.abs(np.asarray(x) - y)))
     err_gpu = max(ad(rr.final_state.g1, t1), ad(rr.final_state.g2, t2))
     err_ref = max(ad(g1, t1), ad(g2, t2))
-    assert err_gpu <= err_ref
-    assert max(ad(rr.final_state.g1, g1), ad(rr.final_state.g2, g2)) <= 3e-7
+    assert err_gpu <= 1e-10
+    assert err_gpu < err_ref
+    assert 1e-7 < err_ref < 1e-5  # the reference's systematic deviation at full C3
 
 
 @pytest.mark.parametrize("solver", ["SOLVER_PHYSICAL", "SOLVER_AUTO"])
 @pytest.mark.parametrize("scheme", ["FastBE", "FastSBD"])
 def test_c5_sampled_instances(fraq, orc, scheme, solver):
-    """C5-style instances (random alpha, m, step-function data) at M = 4095 batched on the GPU;
-    each equals the reference's single-instance run (shortened horizon N = 512)."""
+    """C5-style instances (random alpha, m, step-function data) at M = 4095, batched on the GPU
+    (shortened horizon N = 512, tau = 1/16384).  PHYSICAL reproduces the reference's run to
+    1e-10 of max|G0|; AUTO (mode space) matches the mode-space restatement over the reference's
+    own history lanes (ref_modal_run, DST in extended precision) to 1e-10, and the reference
+    physical result within its own systematic deviation."""
     insts = c5_instances(6)[1:6:2]
     N = 512
+    tau = 1 / 16384
     specs = [fraq.ProblemSpec(alpha1=i.alpha1, alpha2=i.alpha2, coupling_a=i.coupling_a,
-                              grid_m=4095, t_final=N / 16384, n_steps=N, initial="custom",
+                              grid_m=4095, t_final=N * tau, n_steps=N, initial="custom",
                               custom_g1=list(i.g1), custom_g2=list(i.g2)) for i in insts]
     kc = fraq.KernelConfig()
     kc.solver = getattr(fraq, solver)
     outs = fraq.run_batch(specs, getattr(fraq.Scheme, scheme), kc)
+    sbd = scheme == "FastSBD"
+    M = 4095
     for i, o in zip(insts, outs):
-        g1, g2, _, _ = orc.run(i.alpha1, i.alpha2, i.coupling_a, 4095, N / 16384, N, scheme,
+        g1, g2, _, _ = orc.run(i.alpha1, i.alpha2, i.coupling_a, M, N * tau, N, scheme,
                                "custom", i.g1, i.g2)
-        # O(1) step-function data on the M = 4095 grid: agreement is limited by the scheme's
-        # rounding drift (~1e-8 absolute per 1000 implicit steps for any fp64 implementation,
-        # see test_c3_full / test_c3_grid_against_extended_precision_truth)
         scale = max(np.max(np.abs(i.g1)), np.max(np.abs(i.g2)))
-        assert np.max(np.abs(np.array(o.final_state.g1) - g1)) <= 2e-8 * scale
-        assert np.max(np.abs(np.array(o.final_state.g2) - g2)) <= 2e-8 * scale
+        d1 = np.max(np.abs(np.array(o.final_state.g1) - g1)) / scale
+        d2 = np.max(np.abs(np.array(o.final_state.g2) - g2)) / scale
+        if solver == "SOLVER_PHYSICAL":
+            assert max(d1, d2) <= 1e-10, (d1, d2)
+            continue
+        assert max(d1, d2) <= 1e-7  # the reference's own physical-space deviation
+        ks = [orc.build_kernel_auto(sbd, 1 - al, tau, N) for al in (i.alpha1, i.alpha2)]
+        u0, v0, lam, V = _dst_ld(M, i.g1, i.g2)
+        uN, vN, _ = orc.modal_run(ks[0], ks[1], i.coupling_a, tau, N, lam, u0, v0, threads=8)
+        t1 = (V.T @ uN.astype(np.longdouble)).astype(float)
+        t2 = (V.T @ vN.astype(np.longdouble)).astype(float)
+        e1 = np.max(np.abs(np.array(o.final_state.g1) - t1)) / scale
+        e2 = np.max(np.abs(np.array(o.final_state.g2) - t2)) / scale
+        assert max(e1, e2) <= 1e-10, (e1, e2)
+
+
+def _dst_ld(M, g1, g2):
+    """Sine-basis projection in extended precision (test_fpfp.cpp:39-54 normalisation)."""
+    dt = np.longdouble
+    h = dt(1) / (M + 1)
+    pi = np.arccos(dt(-1))
+    k = np.arange(1, M + 1, dtype=dt)
+    V = np.sin(np.outer(k, k) * pi * h)
+    lam = (4 / h ** 2 * np.sin(k * pi * h / 2) ** 2).astype(float)
+    u0 = (2 / dt(M + 1) * (V @ np.asarray(g1, dt))).astype(float)
+    v0 = (2 / dt(M + 1) * (V @ np.asarray(g2, dt))).astype(float)
+    return u0, v0, lam, V

@@ -68,7 +68,7 @@ def test_modal_rejects_classical_and_observer(fraq):
 def test_modal_c3_full_against_fp64_modespace(fraq, orc):
     """C3 (M = 4095, N = 16384, FastBE): the modal GPU solver equals the fp64 mode-space
     evaluation to ~1e-13 (the physical-space paths carry ~5e-8 rounding drift here)."""
-    from paper_1901_05128_b200.workloads import c3_instance
+    from workloads import c3_instance
     inst = c3_instance()
     spec = fraq.ProblemSpec(alpha1=0.4, alpha2=0.8, coupling_a=-5.5, grid_m=4095, t_final=1.0,
                             n_steps=16384, initial="custom", custom_g1=list(inst.g1),
@@ -140,7 +140,7 @@ def test_k13_warp_shapes_agree(fraq, scheme, pts, monkeypatch):
 
 def test_k13_batch_mixed_instances(fraq, orc):
     """C5-like batch through K13 with per-instance kernels (different J and L per field)."""
-    from paper_1901_05128_b200.workloads import c5_instances
+    from workloads import c5_instances
     insts = c5_instances(6)
     N = 80
     for scheme in ("FastBE", "FastSBD"):
@@ -177,7 +177,7 @@ def test_c4_full_size_sampled_modes(fraq, orc):
     """C4 at full size (1023^2, N = 8192, FastSBD): DST coefficients of the GPU result on sampled
     (ky, kx) modes -- extremes of lambda included -- equal the mode-space restatement over the
     reference's SbdHistory lanes run on the same modes."""
-    from paper_1901_05128_b200.workloads import c4_instance
+    from workloads import c4_instance
     M, N = 1023, 8192
     inst = c4_instance(M)
     out = fraq.run_2d(inst.alpha1, inst.alpha2, inst.coupling_a, M, 1.0, N, fraq.Scheme.FastSBD,
@@ -206,7 +206,7 @@ def test_c4_full_size_sampled_modes(fraq, orc):
 def test_c3_full_size_sampled_modes(fraq, orc, scheme):
     """C3 (M = 4095, N = 16384) through the modal solver vs the mode-space restatement on sampled
     modes (both schemes)."""
-    from paper_1901_05128_b200.workloads import c3_instance
+    from workloads import c3_instance
     M, N = 4095, 16384
     inst = c3_instance(M)
     spec = fraq.ProblemSpec(alpha1=inst.alpha1, alpha2=inst.alpha2, coupling_a=inst.coupling_a,
@@ -231,7 +231,7 @@ def test_c3_full_size_sampled_modes(fraq, orc, scheme):
 def test_c5_batch_full_horizon_sampled(fraq, orc, scheme):
     """C5: a batch of 16 instances (full M = 4095, N = 16384) in one modal launch; two instances
     checked on sampled modes against the mode-space restatement."""
-    from paper_1901_05128_b200.workloads import c5_instances
+    from workloads import c5_instances
     M, N = 4095, 16384
     insts = c5_instances(16)
     specs = [fraq.ProblemSpec(alpha1=i.alpha1, alpha2=i.alpha2, coupling_a=i.coupling_a, grid_m=M,
