@@ -137,4 +137,9 @@ int fo_modal_run(const fo_kernel* k1, const fo_kernel* k2, double a, double tau,
 #ifdef __cplusplus
 }
 #endif
+/* extended-precision mode-space anchor on sampled modes (fraq_anchor_ld.c) */
+int fo_anchor_ld(const fo_kernel* k1, const fo_kernel* k2, double a, double tau, long N, int M,
+                 long nm, const int* modes, const double* g1, const double* g2, double* uN,
+                 double* vN);
+
 #endif

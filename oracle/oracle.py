@@ -400,6 +400,23 @@ class Oracle:
             C.c_long(n_steps), _p(U), _p(D), C.c_int(threads), C.byref(secs)), "bench_history")
         return secs.value, D
 
+    def anchor_ld(self, k1: Kernel, k2: Kernel, a: float, tau: float, N: int, M: int, modes,
+                  g1, g2):
+        """Extended-precision mode-space evaluation of the 1D fast scheme on sampled DST modes
+        (oracle/fraq_anchor_ld.c; liboracle.so for either oracle kind).  modes are 1-based.
+        Returns the coefficients (uN, vN) after N levels."""
+        lib = self.lib if self.kind == "port" else C.CDLL(PORT_SO)
+        modes = np.ascontiguousarray(np.asarray(modes, dtype=np.int32))
+        g1, g2 = _arr(g1), _arr(g2)
+        nm = len(modes)
+        uN, vN = np.zeros(nm), np.zeros(nm)
+        f1, f2 = _to_fo(k1), _to_fo(k2)
+        _raise(lib.fo_anchor_ld(C.byref(f1), C.byref(f2), C.c_double(a), C.c_double(tau),
+                                C.c_long(N), C.c_int(M), C.c_long(nm),
+                                modes.ctypes.data_as(_ip), _p(g1), _p(g2), _p(uN), _p(vN)),
+               "anchor_ld")
+        return uN, vN
+
     def hist_trace(self, kernels, U: np.ndarray, stride: int, threads: int):
         """Reference histories (standalone) over U[n_steps, dofs] split evenly into
         len(kernels) groups, `threads` workers; returns D at levels stride-1, 2 stride-1, ...
