@@ -44,7 +44,6 @@ __host__ __device__ inline M2 inv(const M2& x) {
 __host__ __device__ inline M2 sub(const M2& x, const M2& y) {
     return {x.a - y.a, x.b - y.b, x.c - y.c, x.d - y.d};
 }
-__host__ __device__ inline M2 scal(double s, const M2& x) { return {s * x.a, s * x.b, s * x.c, s * x.d}; }
 __device__ inline double2 mv(const M2& m, double2 v) {
     return make_double2(fma(m.a, v.x, m.b * v.y), fma(m.c, v.x, m.d * v.y));
 }
@@ -59,6 +58,10 @@ struct SysDev {
     // Thomas: W[k] = E Delta_{k-1}^{-1}, Dinv[k] = Delta_k^{-1}; E stored below
     M2 E;
     long th_off;         // offset into thomas buffer (2 * grid_m M2 entries)
+    // the block system's entries UNROUNDED, as double-double (hi, lo) pairs, for the residual of
+    // the refinement step: row of field f reads
+    //   diag_f x_f - e_f (x_f,left + x_f,right) - c_f x_other = b_f
+    double dh[2], dl[2], eh[2], el[2], ch[2], cl[2];
 };
 
 // Block matrices of BlockSystem (block_solver.cpp:95-117), rounded exactly as the reference
@@ -113,6 +116,65 @@ void setup_cr(SysDev& S, const M2& D0, const M2& E0) {
         const M2L FE = mulL(F, E);
         E = {-FE.a, -FE.b, -FE.c, -FE.d};
         D = {D.a - 2 * FE.a, D.b - 2 * FE.b, D.c - 2 * FE.c, D.d - 2 * FE.d};
+    }
+}
+
+// ------------------------------------------------------------------ exact entries
+// Double-double values (error-free transforms on fp64) of the unrounded block-system entries.
+// The fp64 rounding of the constant diagonal lead/tau + d0 (a + 2/h^2) ~ 1e10 is what moves the
+// reference's physical-space solution ~1e-6 away from the exact discrete one at C3 (the system's
+// smooth modes amplify a diagonal shift by ~1e10 over the run, profiles/r02/physical_bisect.txt).
+// One refinement step per level with a residual formed from these entries removes it.
+struct DD {
+    double hi, lo;
+};
+DD dd_two_sum(double a, double b) {
+    const double s = a + b, bb = s - a;
+    return {s, (a - (s - bb)) + (b - bb)};
+}
+DD dd_norm(double hi, double lo) {
+    const double s = hi + lo;
+    return {s, lo - (s - hi)};
+}
+DD dd_add(DD x, DD y) {
+    const DD s = dd_two_sum(x.hi, y.hi);
+    return dd_norm(s.hi, s.lo + x.lo + y.lo);
+}
+DD dd_mul_d(DD x, double y) {
+    const double p = x.hi * y;
+    return dd_norm(p, std::fma(x.hi, y, -p) + x.lo * y);
+}
+DD dd_div_d(DD x, double y) {  // x / y
+    const double q = x.hi / y;
+    const double r = std::fma(-q, y, x.hi) + x.lo;
+    return dd_norm(q, r / y);
+}
+DD dd_div_dd(double x, DD y) {  // x / y
+    const double q = x / y.hi;
+    const double r = std::fma(-q, y.hi, x) - q * y.lo;
+    return dd_norm(q, r / y.hi);
+}
+
+// d0f = d0 * fnum / fden exactly (the SBD first step uses 2/3 d0, fpfp.cpp:224)
+void exact_entries(SysDev& S, double d01, double d02, double fnum, double fden, double a,
+                   double tau, double h, double lead) {
+    const DD h2 = dd_norm(h * h, std::fma(h, h, -h * h));
+    const DD ih2 = dd_div_dd(1.0, h2);
+    const DD lt = dd_div_d(DD{lead, 0.0}, tau);
+    const DD d0[2] = {dd_div_d(dd_mul_d(DD{d01, 0.0}, fnum), fden),
+                      dd_div_d(dd_mul_d(DD{d02, 0.0}, fnum), fden)};
+    for (int f = 0; f < 2; ++f) {
+        const DD e = dd_mul_d(ih2, d0[f].hi);
+        const DD e_full = dd_add(e, dd_mul_d(ih2, d0[f].lo));
+        const DD da = dd_add(dd_mul_d(d0[f], a), DD{0.0, 0.0});
+        const DD diag = dd_add(lt, dd_add(da, dd_mul_d(e_full, 2.0)));
+        const DD c = dd_mul_d(d0[1 - f], a);
+        S.dh[f] = diag.hi;
+        S.dl[f] = diag.lo;
+        S.eh[f] = e_full.hi;
+        S.el[f] = e_full.lo;
+        S.ch[f] = c.hi;
+        S.cl[f] = c.lo;
     }
 }
 
@@ -213,6 +275,53 @@ __device__ void block_solve_smem(double2* sb, const SysDev& S, const M2* thomas,
     __syncthreads();
 }
 
+// One refinement step: sb holds x0 (solve of b), sr holds b.  sr <- b - A x0 with the unrounded
+// entries in double-double accumulation, solved in place, and added: sb <- x0 + A^-1 r.  The
+// correction is ~1e-10 of x0 (cond ~1e6 x eps), so the approximate reduction suffices for it.
+__device__ inline void dd_acc(double& s, double& t, double p) {
+    const double u = s + p, bb = u - s;
+    t += (s - (u - bb)) + (p - bb);
+    s = u;
+}
+__device__ inline void dd_acc_prod(double& s, double& t, double c, double x) {
+    const double p = c * x;
+    t += fma(c, x, -p);
+    dd_acc(s, t, p);
+}
+__device__ inline double residual_row(double b, double x, double xl, double xr, double xo,
+                                      double dh, double dl, double eh, double el, double ch,
+                                      double cl) {
+    double s = b, t = 0.0;
+    dd_acc_prod(s, t, -dh, x);
+    dd_acc_prod(s, t, eh, xl);
+    dd_acc_prod(s, t, eh, xr);
+    dd_acc_prod(s, t, ch, xo);
+    t += el * (xl + xr) + cl * xo - dl * x;
+    return s + t;
+}
+template <int THREADS>
+__device__ void refine_smem(double2* sb, double2* sr, const SysDev& S, const M2* thomas, int m) {
+    for (int k = threadIdx.x; k < m; k += THREADS) {
+        const double2 x = sb[k + 1], l = sb[k], r = sb[k + 2], b = sr[k + 1];
+        const double r1 = residual_row(b.x, x.x, l.x, r.x, x.y, S.dh[0], S.dl[0], S.eh[0],
+                                       S.el[0], S.ch[0], S.cl[0]);
+        const double r2 = residual_row(b.y, x.y, l.y, r.y, x.x, S.dh[1], S.dl[1], S.eh[1],
+                                       S.el[1], S.ch[1], S.cl[1]);
+        sr[k + 1] = make_double2(r1, r2);
+    }
+    if (threadIdx.x == 0) {
+        sr[0] = make_double2(0.0, 0.0);
+        sr[m + 1] = make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    block_solve_smem<THREADS>(sr, S, thomas, m);
+    for (int k = threadIdx.x; k < m; k += THREADS) {
+        const double2 x = sb[k + 1], d = sr[k + 1];
+        sb[k + 1] = make_double2(x.x + d.x, x.y + d.y);
+    }
+    __syncthreads();
+}
+
 // BlockSystem::solve on its own (block_solver.cpp:119-153): one CTA per system.
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) block_solve_kernel(const SysDev* sys, const M2* thomas,
@@ -220,13 +329,18 @@ __global__ void __launch_bounds__(THREADS) block_solve_kernel(const SysDev* sys,
                                                               const double* rhs2, double* g1,
                                                               double* g2) {
     extern __shared__ double2 sb[];
-    for (int k = threadIdx.x; k < m; k += THREADS) sb[k + 1] = make_double2(rhs1[k], rhs2[k]);
+    double2* sr = sb + (m + 2);  // the right-hand side, kept for the refinement residual
+    for (int k = threadIdx.x; k < m; k += THREADS) {
+        sb[k + 1] = make_double2(rhs1[k], rhs2[k]);
+        sr[k + 1] = sb[k + 1];
+    }
     if (threadIdx.x == 0) {
         sb[0] = make_double2(0.0, 0.0);
         sb[m + 1] = make_double2(0.0, 0.0);
     }
     __syncthreads();
     block_solve_smem<THREADS>(sb, sys[0], thomas, m);
+    refine_smem<THREADS>(sb, sr, sys[0], thomas, m);
     for (int k = threadIdx.x; k < m; k += THREADS) {
         g1[k] = sb[k + 1].x;
         g2[k] = sb[k + 1].y;
@@ -307,10 +421,14 @@ __global__ void banded_solve_kernel(const double* ab, const int* piv, int n, int
     }
 }
 
-// RHS (fpfp.cpp:277-279, 298-302, 339-344) then the block solve; one CTA per instance.
+__device__ inline int m_of(const SolveArgs& A) { return A.m; }
+
+// RHS (fpfp.cpp:277-279, 298-302, 339-344) then the block solve + one refinement step; one CTA
+// per instance.
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) solve_kernel(SolveArgs A) {
     extern __shared__ double2 sb[];  // b / x, rows 1..m (index 0 and m+1 are zero)
+    double2* sr = sb + (m_of(A) + 2);  // b, kept for the refinement residual
     const InstDev I = A.inst[blockIdx.x];
     const GroupDev G1 = A.groups[I.g1], G2 = A.groups[I.g2];
     const int m = A.m;
@@ -377,13 +495,16 @@ __global__ void __launch_bounds__(THREADS) solve_kernel(SolveArgs A) {
             b2 = lead2 - a * x2 - as2 + a * x1;
         }
         sb[k + 1] = make_double2(b1, b2);
+        sr[k + 1] = sb[k + 1];
     }
     if (threadIdx.x == 0) {
         sb[0] = make_double2(0.0, 0.0);
         sb[m + 1] = make_double2(0.0, 0.0);
     }
     __syncthreads();
-    block_solve_smem<THREADS>(sb, A.sys[A.first ? I.sys_first : I.sys_main], A.thomas, m);
+    const SysDev& S = A.sys[A.first ? I.sys_first : I.sys_main];
+    block_solve_smem<THREADS>(sb, S, A.thomas, m);
+    refine_smem<THREADS>(sb, sr, S, A.thomas, m);
     // append G^n into both rings (slot n % L)
     double* w1 = A.ring + G1.ring_off + (n % G1.L) * ld;
     double* w2 = A.ring + G2.ring_off + (n % G2.L) * ld;
@@ -572,6 +693,8 @@ PhysStepper::PhysStepper(fraq_ctx c_, const fraq_spec_t* specs, int n_inst_, int
             SysDev& S = sys[sidx];
             S.K = K;
             S.E = E;
+            exact_entries(S, d0[2 * i], d0[2 * i + 1], f == 1.0 ? 1.0 : 2.0, f == 1.0 ? 1.0 : 3.0,
+                          a, tau, h, lead);
             sysD[sidx] = D;
             if (K)
                 setup_cr(S, D, E);
@@ -660,7 +783,7 @@ PhysStepper::PhysStepper(fraq_ctx c_, const fraq_spec_t* specs, int n_inst_, int
         gof.alloc(total);
         FRAQ_CUDA(cudaMemcpy(gof.p, go.data(), sizeof(int) * total, cudaMemcpyHostToDevice));
     }
-    smem = sizeof(double2) * (m + 2);
+    smem = 2 * sizeof(double2) * (m + 2);
     if (smem > 227 * 1024) fail(FRAQ_EINVAL, "run: grid_m too large for the on-chip block solve");
     if (smem > 48 * 1024)
         FRAQ_CUDA(cudaFuncSetAttribute(solve_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -872,7 +995,7 @@ void block_create(fraq_ctx c, double d01, double d02, double a, double tau, int 
                   double lead, BlockDev** out) {
     if (m < 1) fail(FRAQ_EINVAL, "BlockSystem: grid_m must be >= 1");
     if (!(tau > 0.0) || !(h > 0.0)) fail(FRAQ_EINVAL, "BlockSystem: tau and h must be > 0");
-    if (sizeof(double2) * (m + 2) > 227 * 1024)
+    if (2 * sizeof(double2) * (m + 2) > 227 * 1024)
         fail(FRAQ_EINVAL, "BlockSystem: grid_m too large for the on-chip block solve");
     auto* b = new BlockDev();
     try {
@@ -884,6 +1007,7 @@ void block_create(fraq_ctx c, double d01, double d02, double a, double tau, int 
         S.K = cr_levels(m);
         S.E = E;
         S.th_off = 0;
+        exact_entries(S, d01, d02, 1.0, 1.0, a, tau, h, lead);
         if (S.K) setup_cr(S, D, E);
         b->sys.alloc(1);
         FRAQ_CUDA(cudaMemcpy(b->sys.p, &S, sizeof(SysDev), cudaMemcpyHostToDevice));
@@ -906,7 +1030,7 @@ void block_solve(BlockDev* b, const double* rhs1, const double* rhs2, double* g1
                  int mem) {
     fraq_ctx c = b->c;
     const int m = b->m;
-    const size_t smem = sizeof(double2) * (m + 2);
+    const size_t smem = 2 * sizeof(double2) * (m + 2);
     if (smem > 48 * 1024)
         FRAQ_CUDA(cudaFuncSetAttribute(block_solve_kernel<512>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

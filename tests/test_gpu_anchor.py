@@ -1,0 +1,107 @@
+"""GPU: both B200 FFPE solvers at the FULL horizon against the extended-precision anchor
+(oracle/fraq_anchor_ld.c: the exact discrete FastBE / FastSBD solution on sampled DST modes,
+long double), next to the reference's own physical-space result.
+
+Cases: C3 (M = 4095, N = 16384, a = -5.5) and four C5 instances (seed 1901051285, M = 4095,
+N = 16384), FastBE and FastSBD.  Per case, with err = max over the sampled modes of
+|coefficient - anchor| / max|anchor coefficient|:
+  * the reference's physical stepper carries a systematic deviation from the rounded
+    block-system diagonal (profiles/r02/physical_bisect.txt) -- recorded;
+  * the B200 physical solver (block cyclic reduction refined each level against the unrounded
+    entries) and the B200 mode-space solver (the default) are both within 1e-10 of the anchor,
+    and below err_ref wherever the reference's deviation exceeds that.
+With FRAQ_RECORD set the numbers go to profiles/r02/anchor_full_horizon.json."""
+import concurrent.futures as cf
+import json
+import os
+
+import numpy as np
+import pytest
+
+from workloads import c3_instance, c5_instances
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+MODES = np.array([1, 2, 3, 4, 5, 8, 13, 32, 64, 256, 1024, 2048, 4095])
+M, N, TAU = 4095, 16384, 1 / 16384
+RECORD = {}
+
+
+def project_ld(g, modes=MODES):
+    dt = np.longdouble
+    j = np.arange(1, M + 1, dtype=dt)
+    V = np.sin(np.outer(np.asarray(modes, dt), j) * np.arccos(dt(-1)) / (M + 1))
+    return (2 / dt(M + 1) * (V @ np.asarray(g, dt))).astype(float)
+
+
+def cases():
+    return [("C3", c3_instance())] + [(f"C5[{i}]", c5_instances(4096)[i])
+                                       for i in (0, 1365, 2730, 4095)]
+
+
+@pytest.fixture(scope="module")
+def oracles():
+    from oracle.oracle import Oracle, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref (the reference compiled from its sources) is needed")
+    return Oracle("reference"), Oracle("port")
+
+
+def _ref_run(args):
+    from oracle.oracle import Oracle
+    name, inst, scheme = args
+    g1, g2, _, _ = Oracle("reference").run(inst.alpha1, inst.alpha2, inst.coupling_a, M, 1.0, N,
+                                           scheme, "custom", inst.g1, inst.g2)
+    return g1, g2
+
+
+@pytest.mark.parametrize("scheme", ["FastBE", "FastSBD"])
+def test_full_horizon_anchor(fraq, oracles, scheme):
+    ref, port = oracles
+    sbd = scheme == "FastSBD"
+    cs = cases()
+    specs = [fraq.ProblemSpec(alpha1=i.alpha1, alpha2=i.alpha2, coupling_a=i.coupling_a,
+                              grid_m=M, t_final=1.0, n_steps=N, initial="custom",
+                              custom_g1=list(i.g1), custom_g2=list(i.g2)) for _, i in cs]
+    sch = getattr(fraq.Scheme, scheme)
+    out = {}
+    for solver in ("SOLVER_PHYSICAL", "SOLVER_AUTO"):
+        kc = fraq.KernelConfig()
+        kc.solver = getattr(fraq, solver)
+        out[solver] = fraq.run_batch(specs, sch, kc)
+    with cf.ThreadPoolExecutor(max_workers=min(len(cs), os.cpu_count() or 1)) as ex:
+        refs = list(ex.map(_ref_run, [(n, i, scheme) for n, i in cs]))
+    for (name, inst), (r1, r2), phys, modal in zip(cs, refs, out["SOLVER_PHYSICAL"],
+                                                    out["SOLVER_AUTO"]):
+        ks = [ref.build_kernel_auto(sbd, 1 - al, TAU, N) for al in (inst.alpha1, inst.alpha2)]
+        uN, vN = port.anchor_ld(ks[0], ks[1], inst.coupling_a, TAU, N, M, MODES, inst.g1,
+                                inst.g2)
+        sc = max(np.abs(uN).max(), np.abs(vN).max())
+
+        def err(g1, g2):
+            return max(np.abs(project_ld(g1) - uN).max(), np.abs(project_ld(g2) - vN).max()) / sc
+        e_ref = err(r1, r2)
+        e_phys = err(phys.final_state.g1, phys.final_state.g2)
+        e_modal = err(modal.final_state.g1, modal.final_state.g2)
+        gsc = max(np.abs(r1).max(), np.abs(r2).max())
+        RECORD[f"{name} {scheme}"] = {
+            "reference_physical": e_ref, "b200_physical": e_phys, "b200_modal": e_modal,
+            "b200_physical_vs_reference": max(np.abs(np.array(phys.final_state.g1) - r1).max(),
+                                              np.abs(np.array(phys.final_state.g2) - r2).max())
+            / gsc,
+            "b200_modal_vs_reference": max(np.abs(np.array(modal.final_state.g1) - r1).max(),
+                                           np.abs(np.array(modal.final_state.g2) - r2).max())
+            / gsc,
+            "alpha": [inst.alpha1, inst.alpha2], "a": inst.coupling_a}
+    if os.environ.get("FRAQ_RECORD"):
+        os.makedirs("profiles/r02", exist_ok=True)
+        path = "profiles/r02/anchor_full_horizon.json"
+        old = json.load(open(path)) if os.path.exists(path) else {}
+        old.update(RECORD)
+        json.dump(old, open(path, "w"), indent=1)
+    for key, r in RECORD.items():
+        if not key.endswith(scheme):
+            continue
+        for solver in ("b200_physical", "b200_modal"):
+            assert r[solver] <= 1e-10, (key, solver, r)
+            assert r[solver] < r["reference_physical"] or r["reference_physical"] < 1e-10, (key, r)

@@ -25,10 +25,8 @@ def orc():
 def spec_of(fraq, alpha1, alpha2, a, m, t_final, n_steps, initial="poly_sin", g1=None, g2=None):
     s = fraq.ProblemSpec(alpha1=alpha1, alpha2=alpha2, coupling_a=a, grid_m=m, t_final=t_final,
                          n_steps=n_steps)
-    if initial == "indicator":
-        s.initial = fraq.InitialData.indicator
-    elif initial == "custom":
-        s.initial = fraq.InitialData.custom
+    s.initial = initial
+    if initial == "custom":
         s.custom_g1 = list(g1)
         s.custom_g2 = list(g2)
     return s
@@ -247,13 +245,16 @@ def test_be_vs_fastbe_trajectories(fraq):
 
 
 def test_fastsbd_equals_sbd_inside_head(fraq):
-    """test_fpfp.cpp:395-401: with n <= n_head FastSBD is the classical SBD scheme."""
+    """test_fpfp.cpp:395-401: with n <= n_head FastSBD is the classical SBD scheme (both in
+    physical space, as in the reference: 1e-13).  The mode-space solver steps the same scheme
+    without the stencil solve; against the physical classical run it differs by that solve's
+    rounding (measured 3.9e-13 on this grid)."""
     spec = spec_of(fraq, 0.3, 0.6, 2.0, 63, 1.0, 10)
-    for solver in (fraq.SOLVER_AUTO, fraq.SOLVER_PHYSICAL):
+    cls = fraq.run(spec, fraq.Scheme.SBD)
+    for solver, tol in ((fraq.SOLVER_PHYSICAL, 1e-13), (fraq.SOLVER_AUTO, 2e-12)):
         fst = fraq.run(spec, fraq.Scheme.FastSBD, kc_of(fraq, solver))
-        cls = fraq.run(spec, fraq.Scheme.SBD)
-        assert rel(fst.final_state.g1, cls.final_state.g1) < 1e-13
-        assert rel(fst.final_state.g2, cls.final_state.g2) < 1e-13
+        assert rel(fst.final_state.g1, cls.final_state.g1) < tol
+        assert rel(fst.final_state.g2, cls.final_state.g2) < tol
 
 
 @pytest.mark.parametrize("initial", ["poly_sin", "indicator"])
@@ -264,7 +265,7 @@ def test_temporal_order_bands(fraq, initial):
     cfg.alpha1, cfg.alpha2, cfg.coupling_a, cfg.grid_m, cfg.t_final = 0.3, 0.6, 2.0, 63, 1.0
     cfg.taus = [1 / 40, 1 / 80, 1 / 160]
     cfg.ref_tau = 1 / 1280
-    cfg.initial = getattr(fraq.InitialData, initial)
+    cfg.initial = initial
     for schemes, lo, hi in (([fraq.Scheme.BE, fraq.Scheme.FastBE], 0.9, 1.35),
                             ([fraq.Scheme.SBD, fraq.Scheme.FastSBD], 1.8, 2.45)):
         cfg.schemes = schemes
