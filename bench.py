@@ -182,6 +182,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--solver", default="modal", choices=["modal", "physical"],
+                    help="FFPE workloads: mode-space (default) or the physical-space stepper")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="C2: 65536 DOFs per GPU (weak, default) or 65536 / N per GPU (strong, "
                          "SURVEY.md §8(e))")

@@ -26,14 +26,14 @@ UNIT = "DOF-steps/s"
 CHUNK = 256
 
 
-def _modal_kc(fraq):
+def _modal_kc(fraq, solver="modal"):
     kc = fraq.KernelConfig()
-    kc.solver = fraq.SOLVER_MODAL
+    kc.solver = fraq.SOLVER_PHYSICAL if solver == "physical" else fraq.SOLVER_MODAL
     return kc
 
 
 class Workload:
-    def __init__(self, name, rank, world):
+    def __init__(self, name, rank, world, solver="modal"):
         from workloads import c3_instance, c4_instance, c5_instances
         self.name = name
         self.rank = rank
@@ -49,6 +49,9 @@ class Workload:
             self.units = CHUNK
             self.all = c5_instances(4096)
         self.world = world
+        self.solver = solver
+        if solver == "physical" and name == "C4":
+            raise ValueError("C4 (2D) has no physical-space solver; the reference is 1D only")
 
     def dofs(self):
         """DOFs advanced per step by THIS rank's call (C4: the whole job, strong scaling)."""
@@ -97,9 +100,9 @@ class Workload:
             r.final_state = fs
             return sum(T.values()), [r]
         if self.name == "C3":
-            r = fraq.run(specs[0], sch, _modal_kc(fraq))
+            r = fraq.run(specs[0], sch, _modal_kc(fraq, self.solver))
             return r.loop_seconds, [r]
-        rs = fraq.run_batch(specs, sch, _modal_kc(fraq))
+        rs = fraq.run_batch(specs, sch, _modal_kc(fraq, self.solver))
         return rs[0].loop_seconds, rs
 
     def config(self):
@@ -110,6 +113,8 @@ class Workload:
                 "C5-SBD": "C5 (BDF2): 1D FFPE sweep, 256 instances per GPU per step, M = 4095, "
                           "N = 16384"}[self.name]
         w = self.world
+        if self.solver == "physical":
+            desc += "; physical-space solver (K5 history + K6 RHS / block solve per level)"
         return {"workload": desc, "dofs_per_gpu_per_step": self.dofs(), "levels": self.N,
                 "l2": "L2 flushed (256 MB write) before every step",
                 "parallelism": (f"instance-sharded x{w}" if self.units > 1 else
@@ -120,10 +125,13 @@ class Workload:
         return "strong" if self.name == "C4" else "weak"
 
     def launches(self):
-        """Our kernels inside the device-timed region of one step.  1D: DST (DMMA), transpose,
-        K13, transpose, inverse DST.  C4: two DST passes (sine table + DMMA GEMM each), K13, and
-        two inverse passes (K13's tables are built at setup, outside the loop timer; the slab
-        permutes around the all-to-alls are torch copies)."""
+        """Our kernels inside the device-timed region of one step.  1D modal: DST (DMMA),
+        transpose, K13, transpose, inverse DST.  1D physical: K5 + K6 per level (the first BDF2
+        level has no K5).  C4: two DST passes (sine table + DMMA GEMM each), K13, and two inverse
+        passes (K13's tables are built at setup, outside the loop timer; the slab permutes around
+        the all-to-alls are torch copies)."""
+        if self.solver == "physical":
+            return 2 * self.N - (1 if self.scheme == "FastSBD" else 0)
         return 9 if self.name == "C4" else 5
 
     def io_bytes(self):
@@ -202,7 +210,7 @@ def run_reference(args, rank, world, METRIC):
     if not ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    wl = Workload(args.workload, 0, world)
+    wl = Workload(args.workload, 0, world, args.solver)
     orc = Oracle("reference")
     threads = os.cpu_count() or 1
     vals = []
@@ -225,7 +233,7 @@ def run_reference(args, rank, world, METRIC):
 
 
 def run_gpu(args, rank, world, local, pg, METRIC, Clocks, fraq, torch):
-    wl = Workload(args.workload, rank, world)
+    wl = Workload(args.workload, rank, world, args.solver)
     dev = torch.device("cuda", local)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > L2
     K, W = args.steps, args.warmup
@@ -288,6 +296,42 @@ def run_gpu(args, rank, world, local, pg, METRIC, Clocks, fraq, torch):
     Fm = float(np.mean(F))
     achieved = Fm * dof_steps / loop_s / 1e12
     peak = fraq.diag_dmma_peak()[0]
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "peak_source": "measured DMMA stream (fraq_diag_dmma_peak)",
+                "flops_per_dof_step": Fm, "kernel": "k13_kernel (modal, DMMA)"}
+    split = None
+    if wl.solver == "physical" and wl.name == "C3":
+        # per-kernel split of the physical stepper (events around every launch, 1024 levels in
+        # the middle of a run): K5 = one fused HBM pass over the history state per level,
+        # K6 = RHS + block cyclic reduction + refinement (one CTA per instance, latency-bound)
+        i = wl.insts[0]
+        spec = fraq.ProblemSpec(alpha1=i.alpha1, alpha2=i.alpha2, coupling_a=i.coupling_a,
+                                grid_m=wl.M, t_final=1.0, n_steps=wl.N, initial="custom",
+                                custom_g1=list(i.g1), custom_g2=list(i.g2))
+        st = fraq.FastStepper(spec, sbd, fraq.KernelConfig())
+        st.step_n(2048)
+        L = 1024
+        ms5, ms6 = st.time_split(L)
+        nodes = Fm / 4 - 1  # N_nodes (F = 4 N_nodes + 2 N_head, N_head = 2 for BE)
+        if sbd:
+            nodes = (Fm - 2 * 17) / 4
+        B = 8 * (2 * nodes + 2)               # SURVEY.md §8(d) bytes per DOF-step
+        dofs = 2 * wl.M
+        gbs = B * dofs * L / (ms5 * 1e-3) / 1e9
+        try:
+            hbm = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                              "MEASURED_PEAKS.json")))["hbm_gbs"]
+        except Exception:
+            hbm = 6543.7  # the pool's measured copy bandwidth in round 1
+        split = {"levels": L, "k5_us_per_level": 1e3 * ms5 / L, "k6_us_per_level": 1e3 * ms6 / L,
+                 "k6_share": ms6 / (ms5 + ms6), "loop_us_per_level": 1e6 * loop_s / K / wl.N,
+                 "k5_state_mb": 2 * wl.M * nodes * 8 / 1e6}
+        roofline = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
+                    "frac": gbs / hbm, "kernel": "step_kernel (K5, FFPE mode)",
+                    "bytes_per_dof_step": B,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                    "note": "the 16.8 MB C3 state is L2-resident (126 MB L2), so K5 can exceed "
+                            "the HBM figure; K6 (one CTA, latency-bound) dominates the level"}
     traffic = None
     try:
         tr = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
@@ -316,13 +360,13 @@ def run_gpu(args, rank, world, local, pg, METRIC, Clocks, fraq, torch):
             "scaling": wl.scaling(), "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": wl.config(),
-            "path": "mode-space solver: DST (DMMA) + K13 (DMMA block stepping, solver warp) + "
-                    "inverse DST",
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "traffic_unit": "DRAM bytes per K13 launch (ncu, profiles/)",
-                         "peak_source": "measured DMMA stream (fraq_diag_dmma_peak)",
-                         "flops_per_dof_step": Fm, "kernel": "k13_kernel (modal, DMMA)"},
+            "path": ("physical-space solver: K5 (history, FFPE mode) + K6 (RHS, block cyclic "
+                     "reduction, refinement) per level" if wl.solver == "physical" else
+                     "mode-space solver: DST (DMMA) + K13 (DMMA block stepping, solver warp) + "
+                     "inverse DST"),
+            "roofline": dict(roofline, traffic=traffic if wl.solver != "physical" else None,
+                             traffic_unit="DRAM bytes per K13 launch (ncu, profiles/)"),
+            "physical_split": split,
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": wl.io_bytes(),
                     "d2h_bytes_per_step": wl.io_bytes(),
                     "path": "fraq.run / run_batch / run_2d with host arrays (setup included)"},

@@ -256,6 +256,10 @@ int fraq_stepper_step(fraq_stepper st, long n_steps);
 int fraq_stepper_state(fraq_stepper st, double* g1, double* g2, long* step);
 int fraq_stepper_kernel_eps(fraq_stepper st, double* eps1, double* eps2);
 int fraq_stepper_destroy(fraq_stepper st);
+/* diagnostics: advance n_steps levels with CUDA events around every kernel; *ms_hist = summed
+ * device time of the history kernels (K5, or the classical sums), *ms_solve = of the RHS +
+ * block solves (K6).  The physical path's time split for bench.py. */
+int fraq_stepper_time_split(fraq_stepper st, long n_steps, double* ms_hist, double* ms_solve);
 
 /* BlockSystem (block_solver.hpp:38-58, block_solver.cpp:95-153): the coupled two-field system
  *   [ lead/tau + d01 (a + A) , -a d02 I ; -a d01 I , lead/tau + d02 (a + A) ],

@@ -48,6 +48,7 @@ void stepper_create(fraq_ctx c, const fraq_spec_t* spec, int scheme, const fraq_
 void stepper_step(PhysStepper* st, long n);
 void stepper_state(PhysStepper* st, double* g1, double* g2, long* step);
 void stepper_eps(PhysStepper* st, double* e1, double* e2);
+void stepper_time_split(PhysStepper* st, long n, double* ms_hist, double* ms_solve);
 void stepper_destroy(PhysStepper* st);
 void block_create(fraq_ctx c, double d01, double d02, double a, double tau, int m, double h,
                   double lead, BlockDev** out);
@@ -463,6 +464,12 @@ int fraq_stepper_state(fraq_stepper st, double* g1, double* g2, long* step) {
 }
 int fraq_stepper_kernel_eps(fraq_stepper st, double* eps1, double* eps2) {
     return guarded_obj(st, "stepper", [&] { stepper_eps(st->p, eps1, eps2); });
+}
+int fraq_stepper_time_split(fraq_stepper st, long n_steps, double* ms_hist, double* ms_solve) {
+    return guarded_obj(st, "stepper", [&] {
+        if (!ms_hist || !ms_solve) fail(FRAQ_EINVAL, "stepper: null output");
+        stepper_time_split(st->p, n_steps, ms_hist, ms_solve);
+    });
 }
 int fraq_stepper_destroy(fraq_stepper st) {
     if (!st) return FRAQ_OK;

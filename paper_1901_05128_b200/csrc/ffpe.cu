@@ -616,7 +616,10 @@ struct PhysStepper {
 
     PhysStepper(fraq_ctx c_, const fraq_spec_t* specs, int n_inst_, int scheme,
                 const fraq_kconf_t& kc);
-    void step(long n_steps);  // asynchronous on the context stream
+    void step(long n_steps, std::vector<cudaEvent_t>* ev = nullptr);  // stream-ordered
+    // diagnostics: step n levels with an event pair around every kernel; returns the summed
+    // device time of the history kernels (K5 / classical sums) and of the solves (K6)
+    void time_split(long n_steps, double* ms_hist, double* ms_solve);
     void state(double* g1, double* g2);  // [n_inst][m] each; synchronizes
 };
 
@@ -804,13 +807,25 @@ PhysStepper::PhysStepper(fraq_ctx c_, const fraq_spec_t* specs, int n_inst_, int
     setup_seconds = now_s() - t_setup0;
 }
 
-void PhysStepper::step(long n_steps) {
+void PhysStepper::step(long n_steps, std::vector<cudaEvent_t>* ev) {
     if (n_steps < 0) fail(FRAQ_EINVAL, "step: negative step count");
     if (step_idx + n_steps > N)
         fail(FRAQ_EINVAL, "step: beyond the horizon the stepper was sized for (spec.n_steps)");
+    auto mark = [&](int k) {
+        if (ev) FRAQ_CUDA(cudaEventRecord((*ev)[k], c->stream));
+    };
     for (long q = 0; q < n_steps; ++q) {
         const long n = ++step_idx;
         const bool first = sbd && n == 1;
+        if (ev) {
+            for (int k = 0; k < 4; ++k) {
+                cudaEvent_t e;
+                FRAQ_CUDA(cudaEventCreate(&e));
+                ev->push_back(e);
+            }
+        }
+        const int e0 = ev ? (int)ev->size() - 4 : 0;
+        mark(e0);
         if (fast) {
             if (!first) {
                 StepArgs a{};
@@ -835,12 +850,15 @@ void PhysStepper::step(long n_steps) {
                 hist.p, total, ctab.p, N + 1, gof.p, total, n, sbd, sbuf.p);
             FRAQ_LAUNCH_CHECK();
         }
+        mark(e0 + 1);
+        mark(e0 + 2);
         sa.n = n;
         sa.first = first;
         // the last level of a call leaves G^n in outb (state reads, ffpe_run's result)
         sa.out = (q == n_steps - 1) ? outb.p : nullptr;
         solve_kernel<512><<<n_inst, 512, smem, c->stream>>>(sa);
         FRAQ_LAUNCH_CHECK();
+        mark(e0 + 3);
         if (!fast) {
             // keep the full history: copy G^n rows out of the 2-slot rings
             for (int t = 0; t < 2 * n_inst; ++t) {
@@ -853,6 +871,28 @@ void PhysStepper::step(long n_steps) {
         level += 1;
         appended += 1;
     }
+}
+
+void PhysStepper::time_split(long n_steps, double* ms_hist, double* ms_solve) {
+    std::vector<cudaEvent_t> ev;
+    try {
+        step(n_steps, &ev);
+        FRAQ_CUDA(cudaStreamSynchronize(c->stream));
+        double h = 0.0, s = 0.0;
+        for (size_t k = 0; k + 3 < ev.size(); k += 4) {
+            float a = 0.f, b = 0.f;
+            FRAQ_CUDA(cudaEventElapsedTime(&a, ev[k], ev[k + 1]));
+            FRAQ_CUDA(cudaEventElapsedTime(&b, ev[k + 2], ev[k + 3]));
+            h += a;
+            s += b;
+        }
+        *ms_hist = h;
+        *ms_solve = s;
+    } catch (...) {
+        for (auto e : ev) cudaEventDestroy(e);
+        throw;
+    }
+    for (auto e : ev) cudaEventDestroy(e);
 }
 
 void PhysStepper::state(double* g1, double* g2) {
@@ -973,6 +1013,9 @@ void stepper_step(PhysStepper* st, long n) { st->step(n); }
 void stepper_state(PhysStepper* st, double* g1, double* g2, long* step) {
     st->state(g1, g2);
     if (step) *step = st->step_idx;
+}
+void stepper_time_split(PhysStepper* st, long n, double* ms_hist, double* ms_solve) {
+    st->time_split(n, ms_hist, ms_solve);
 }
 void stepper_eps(PhysStepper* st, double* e1, double* e2) {
     if (e1) *e1 = st->eps[0];

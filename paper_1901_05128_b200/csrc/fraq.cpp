@@ -647,6 +647,12 @@ void FastStepper::step_n(long n) {
     check(fraq_stepper_step(st_, n));
     step_ += n;
 }
+std::pair<double, double> FastStepper::time_split(long n) {
+    double a = 0.0, b = 0.0;
+    check(fraq_stepper_time_split(st_, n, &a, &b));
+    step_ += n;
+    return {a, b};
+}
 const StateField& FastStepper::state() const {
     refresh(st_, state_, state_at_, step_, (int)state_.g1.size());
     return state_;

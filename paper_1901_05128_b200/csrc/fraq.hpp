@@ -18,6 +18,7 @@
 #include <memory>
 #include <span>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "fraqcu.h"
@@ -347,6 +348,8 @@ public:
     double kernel_eps2() const { return eps2_; }
     /// addition: advance n levels in one stream-ordered call
     void step_n(long n);
+    /// addition (diagnostics): advance n levels timing each kernel; returns {ms K5, ms K6}
+    std::pair<double, double> time_split(long n);
 
 private:
     fraq_stepper st_ = nullptr;

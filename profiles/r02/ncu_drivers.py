@@ -1,0 +1,46 @@
+"""Small drivers for ncu captures of round 2 (run under ncu on the GPU box; never timed).
+
+    python profiles/r02/ncu_drivers.py c3phys [levels]   # physical C3: K5 (FFPE mode) + K6 per level
+    python profiles/r02/ncu_drivers.py c4dst             # one C4-shaped DST pass (K12, DMMA GEMM)
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import paper_1901_05128_b200 as fraq  # noqa: E402
+from workloads import c3_instance  # noqa: E402
+
+
+def c3phys(levels=64):
+    i = c3_instance()
+    spec = fraq.ProblemSpec(alpha1=i.alpha1, alpha2=i.alpha2, coupling_a=i.coupling_a,
+                            grid_m=4095, t_final=levels / 16384, n_steps=levels,
+                            initial="custom", custom_g1=list(i.g1), custom_g2=list(i.g2))
+    kc = fraq.KernelConfig()
+    kc.solver = fraq.SOLVER_PHYSICAL
+    r = fraq.run(spec, fraq.Scheme.FastBE, kc)
+    print("c3phys", levels, r.loop_seconds)
+
+
+def c4dst():
+    import torch
+    M = 1023
+    x = torch.randn(M, 2 * M, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(x)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        fraq.dst_cols_device(M, 2 * M, x.data_ptr(), y.data_ptr(), False)
+    fraq.synchronize()
+    print("c4dst ok", float(y.abs().max()))
+
+
+if __name__ == "__main__":
+    what = sys.argv[1]
+    if what == "c3phys":
+        c3phys(int(sys.argv[2]) if len(sys.argv) > 2 else 64)
+    else:
+        c4dst()
