@@ -243,25 +243,14 @@ def main():
     levels = nbuf * LEVELS_PER_STEP
     if args.scaling == "strong":
         # contiguous DOF blocks of the ONE 65536-DOF job, 65536/N per GPU
-        per = -(-DOFS // world)
-        lo, hi = min(DOFS, rank * per), min(DOFS, (rank + 1) * per)
+        from paper_1901_05128_b200.parallel import c2_strong_slice
+        lo, hi, groups = c2_strong_slice(rank, world, DOFS)
         sel = slice(lo, hi)
         a, bb, c, w = (torch.from_numpy(x[sel].copy()) for x in (params.a, params.b, params.c,
                                                                   params.w))
-        half = DOFS // 2
-        dims = [max(0, min(hi, half) - lo), max(0, hi - max(lo, half))]
-    else:
-        # weak: each rank owns 65536 DOFs (rank 0 the seeded C2 set, others rank-seeded draws)
-        gen = torch.Generator(device="cpu").manual_seed(1901051282 + rank)
-        if rank == 0:
-            a = torch.from_numpy(params.a); bb = torch.from_numpy(params.b)
-            c = torch.from_numpy(params.c); w = torch.from_numpy(params.w)
-        else:
-            a = torch.randn(DOFS, generator=gen, dtype=torch.float64)
-            c = torch.randn(DOFS, generator=gen, dtype=torch.float64)
-            bb = 0.1 + 1.9 * torch.rand(DOFS, generator=gen, dtype=torch.float64)
-            w = 1.0 + 19.0 * torch.rand(DOFS, generator=gen, dtype=torch.float64)
-        dims = [DOFS // 2, DOFS - DOFS // 2]
+        dims = [0, 0]
+        for g, cnt in groups:
+            dims[g] = cnt
     gk = [k for k, d in zip(ks, dims) if d > 0]
     dims = [d for d in dims if d > 0]
     NL = sum(dims)  # DOFs on this rank

@@ -32,15 +32,16 @@ void check(int st) {
     }
 }
 
+int default_device() {
+    const char* e = std::getenv("FRAQ_DEVICE");
+    return e ? std::atoi(e) : 0;
+}
+
 fraq_ctx default_context() {
     static std::mutex mu;
     static fraq_ctx ctx = nullptr;
     std::lock_guard<std::mutex> lock(mu);
-    if (!ctx) {
-        int dev = 0;
-        if (const char* e = std::getenv("FRAQ_DEVICE")) dev = std::atoi(e);
-        check(fraq_ctx_create(dev, nullptr, &ctx));
-    }
+    if (!ctx) check(fraq_ctx_create(default_device(), nullptr, &ctx));
     return ctx;
 }
 
@@ -403,8 +404,8 @@ void obs_tramp(long n, const double* g1, const double* g2, int m, void* user) {
 }
 }  // namespace
 
-RunResult run(const ProblemSpec& spec, Scheme scheme, const KernelConfig& kconf,
-              const std::function<void(long, const StateField&)>& observer) {
+RunResult run_on(fraq_ctx ctx, const ProblemSpec& spec, Scheme scheme, const KernelConfig& kconf,
+                 const std::function<void(long, const StateField&)>& observer) {
     if (spec.initial == InitialData::custom &&
         ((int)spec.custom_g1.size() != spec.grid_m || (int)spec.custom_g2.size() != spec.grid_m))
         throw std::invalid_argument("initial_field: custom samples must have grid_m entries");
@@ -416,10 +417,10 @@ RunResult run(const ProblemSpec& spec, Scheme scheme, const KernelConfig& kconf,
     fraq_run_info_t info{};
     if (observer) {
         ObsCtx oc{&observer, {}};
-        check(fraq_run_observed(default_context(), &fs, flat_scheme(scheme), &kc, obs_tramp, &oc,
+        check(fraq_run_observed(ctx, &fs, flat_scheme(scheme), &kc, obs_tramp, &oc,
                                 rr.final_state.g1.data(), rr.final_state.g2.data(), &info));
     } else {
-        check(fraq_run(default_context(), &fs, 1, flat_scheme(scheme), &kc, rr.final_state.g1.data(),
+        check(fraq_run(ctx, &fs, 1, flat_scheme(scheme), &kc, rr.final_state.g1.data(),
                        rr.final_state.g2.data(), &info));
     }
     rr.final_state.step = spec.n_steps;
@@ -428,6 +429,11 @@ RunResult run(const ProblemSpec& spec, Scheme scheme, const KernelConfig& kconf,
     rr.kernel_eps1 = info.kernel_eps1;
     rr.kernel_eps2 = info.kernel_eps2;
     return rr;
+}
+
+RunResult run(const ProblemSpec& spec, Scheme scheme, const KernelConfig& kconf,
+              const std::function<void(long, const StateField&)>& observer) {
+    return run_on(default_context(), spec, scheme, kconf, observer);
 }
 
 RunResult run_2d(double alpha1, double alpha2, double coupling_a, int grid_m, double t_final,

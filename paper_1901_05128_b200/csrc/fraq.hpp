@@ -26,7 +26,9 @@
 namespace fraq {
 
 // ------------------------------------------------------------------ runtime
-/// Process-wide context on the current device (FRAQ_DEVICE env overrides), created lazily.
+/// Device of the process-wide context: FRAQ_DEVICE, else 0.
+int default_device();
+/// Process-wide context on default_device(), created lazily.
 fraq_ctx default_context();
 /// Throws the reference exception type matching a fraqcu status code.
 void check(int status);
@@ -288,6 +290,12 @@ double l2_norm(std::span<const double> v, double h);
 /// back to the host (fraq_run_observed).
 RunResult run(const ProblemSpec& spec, Scheme scheme, const KernelConfig& kconf = {},
               const std::function<void(long, const StateField&)>& observer = nullptr);
+
+/// addition: run() on a caller-owned context (its own stream), e.g. one per worker thread --
+/// calls on different contexts proceed concurrently on the device.
+RunResult run_on(fraq_ctx ctx, const ProblemSpec& spec, Scheme scheme,
+                 const KernelConfig& kconf = {},
+                 const std::function<void(long, const StateField&)>& observer = nullptr);
 
 /// 2D FFPE on the unit square (grid_m^2 interior points, five-point Laplacian), fast schemes,
 /// stepped in the 2D DST eigenbasis.  Data row-major (x fastest).  No reference counterpart.

@@ -9,7 +9,6 @@
 #include <functional>
 #include <iostream>
 #include <map>
-#include <memory>
 #include <set>
 #include <stdexcept>
 #include <string>
@@ -87,135 +86,180 @@ void parse_args(int argc, char** argv, std::string& config, std::string& cmd, Op
     }
 }
 
-std::unique_ptr<std::ofstream> open_out(const std::string& path) {
-    if (path.empty() || path == "-") return nullptr;
-    auto f = std::make_unique<std::ofstream>(path);
-    if (!*f) throw std::runtime_error("cannot open output file: " + path);
-    return f;
-}
+// Options of one invocation: command line over config file over the per-subcommand default.
+struct Args {
+    Opts cli, file;
+    std::string get(const std::string& key, const std::string& fallback) const {
+        for (const Opts* src : {&cli, &file})
+            if (const auto it = src->find(key); it != src->end()) return it->second;
+        return fallback;
+    }
+    double number(const std::string& key, const std::string& fallback) const {
+        return fraq::parse_fraction(get(key, fallback));
+    }
+    long count(const std::string& key, const std::string& fallback) const {
+        return std::lround(number(key, fallback));
+    }
+    // the CQ family of weights / kernel-error: "be" or "sbd" only
+    bool sbd_family() const {
+        const std::string s = get("scheme", "be");
+        if (s == "be" || s == "sbd") return s == "sbd";
+        throw std::invalid_argument("scheme must be 'be' or 'sbd', got '" + s + "'");
+    }
+    fraq::ExperimentConfig experiment() const {
+        Opts no_out(cli);
+        no_out.erase("out");
+        return fraq::resolve_config(file, no_out);
+    }
+};
 
+// Output sink: the --out file, or stdout when absent / "-".
+class Sink {
+public:
+    explicit Sink(const std::string& path) {
+        if (path.empty() || path == "-") return;
+        file_.open(path);
+        if (!file_) throw std::runtime_error("cannot open output file: " + path);
+    }
+    std::ostream& stream() { return file_.is_open() ? static_cast<std::ostream&>(file_) : std::cout; }
+
+private:
+    std::ofstream file_;
+};
+
+// meta.txt of a convergence study: the resolved configuration, one `key = value` per line.
 void write_meta(const std::string& dir, const fraq::ExperimentConfig& c) {
-    std::ofstream m(std::filesystem::path(dir) / "meta.txt");
     using fraq::format_double;
-    m << "alpha1 = " << format_double(c.alpha1) << "\nalpha2 = " << format_double(c.alpha2)
-      << "\na = " << format_double(c.coupling_a) << "\ngrid-m = " << c.grid_m
-      << "\nt-final = " << format_double(c.t_final) << "\nref-tau = " << format_double(c.ref_tau)
-      << "\ninit = " << (c.initial == fraq::InitialData::poly_sin ? "poly_sin" : "indicator")
-      << "\nnp = " << c.kernel.be_points << "\nnp1 = " << c.kernel.sbd_points_1
-      << "\nnp2 = " << c.kernel.sbd_points_2 << "\nns = " << c.kernel.sbd_head
-      << "\neps-tol = " << format_double(c.kernel.eps_tol)
-      << "\nauto-kernel = " << (c.kernel.auto_size ? "1" : "0") << "\ntaus =";
-    for (double t : c.taus) m << ' ' << format_double(t);
-    m << "\nschemes =";
-    for (auto s : c.schemes) m << ' ' << fraq::scheme_name(s);
-    m << "\n";
+    std::string taus, schemes;
+    for (double t : c.taus) taus += " " + format_double(t);
+    for (fraq::Scheme s : c.schemes) schemes += " " + fraq::scheme_name(s);
+    const std::vector<std::pair<const char*, std::string>> lines = {
+        {"alpha1", " " + format_double(c.alpha1)},
+        {"alpha2", " " + format_double(c.alpha2)},
+        {"a", " " + format_double(c.coupling_a)},
+        {"grid-m", " " + std::to_string(c.grid_m)},
+        {"t-final", " " + format_double(c.t_final)},
+        {"ref-tau", " " + format_double(c.ref_tau)},
+        {"init", c.initial == fraq::InitialData::poly_sin ? " poly_sin" : " indicator"},
+        {"np", " " + std::to_string(c.kernel.be_points)},
+        {"np1", " " + std::to_string(c.kernel.sbd_points_1)},
+        {"np2", " " + std::to_string(c.kernel.sbd_points_2)},
+        {"ns", " " + std::to_string(c.kernel.sbd_head)},
+        {"eps-tol", " " + format_double(c.kernel.eps_tol)},
+        {"auto-kernel", c.kernel.auto_size ? " 1" : " 0"},
+        {"taus", taus},
+        {"schemes", schemes},
+    };
+    std::ofstream meta(std::filesystem::path(dir) / "meta.txt");
+    for (const auto& [key, value] : lines) meta << key << " =" << value << "\n";
 }
 
-int run(const std::string& config, const std::string& cmd, Opts opts) {
-    Opts file;
+int cmd_weights(const Args& a) {
+    const bool sbd = a.sbd_family();
+    const double alpha = a.number("alpha", "0.5"), tau = a.number("tau", "1");
+    const long n = a.count("n", "10");
+    Sink out(a.get("out", ""));
+    fraq::write_weights_csv(out.stream(), sbd ? fraq::sbd_weights(alpha, tau, n)
+                                              : fraq::be_weights(alpha, tau, n));
+    return 0;
+}
+
+int cmd_kernel_error(const Args& a) {
+    const bool sbd = a.sbd_family();
+    const double alpha = a.number("alpha", "0.5"), tau = a.number("tau", "0.001");
+    const long n_max = a.count("n-max", "1000");
+    fraq::KernelErrorReport rep;
+    if (sbd) {
+        const long ns = a.count("ns", "0");
+        const int head = ns > 0 ? static_cast<int>(ns) : fraq::default_sbd_head(alpha);
+        rep = fraq::kernel_error_report(
+            fraq::build_sbd_kernel(alpha, tau, static_cast<int>(a.count("np1", "41")),
+                                   static_cast<int>(a.count("np2", "41")), head),
+            n_max);
+    } else {
+        rep = fraq::kernel_error_report(
+            fraq::build_be_kernel(alpha, tau, static_cast<int>(a.count("np", "64"))), n_max);
+    }
+    Sink out(a.get("out", ""));
+    fraq::write_kernel_error_csv(out.stream(), rep);
+    return 0;
+}
+
+int cmd_solve(const Args& a) {
+    const fraq::ExperimentConfig cfg = a.experiment();
+    fraq::ProblemSpec spec;
+    spec.alpha1 = cfg.alpha1;
+    spec.alpha2 = cfg.alpha2;
+    spec.coupling_a = cfg.coupling_a;
+    spec.grid_m = cfg.grid_m;
+    spec.t_final = cfg.t_final;
+    spec.initial = cfg.initial;
+    // step count: --n-steps, else t-final / --tau, else 100 steps
+    const double tau = a.number("tau", "0"), n_steps = a.number("n-steps", "0");
+    spec.n_steps = n_steps > 0 ? std::lround(n_steps)
+                               : (tau > 0 ? std::lround(cfg.t_final / tau) : 100L);
+    const fraq::Scheme scheme = fraq::scheme_from_name(a.get("scheme", "be"));
+    std::set<long> snap_levels;
+    for (double t : fraq::parse_fraction_list(a.get("snapshot-times", "")))
+        snap_levels.insert(std::lround(t / spec.tau()));
+    const std::filesystem::path snap_dir = a.get("out-dir", ".");
+    std::function<void(long, const fraq::StateField&)> observer;
+    if (!snap_levels.empty()) {
+        std::filesystem::create_directories(snap_dir);
+        observer = [&](long n, const fraq::StateField& f) {
+            if (!snap_levels.count(n)) return;
+            std::ofstream snap(snap_dir / ("snapshot_n" + std::to_string(n) + ".csv"));
+            fraq::write_snapshot_csv(snap, spec, f);
+        };
+    }
+    const fraq::RunResult rr = fraq::run(spec, scheme, cfg.kernel, observer);
+    Sink out(a.get("out", ""));
+    fraq::write_snapshot_csv(out.stream(), spec, rr.final_state);
+    std::cerr << "loop_seconds=" << fraq::format_double(rr.loop_seconds)
+              << " setup_seconds=" << fraq::format_double(rr.setup_seconds) << "\n";
+    return 0;
+}
+
+int cmd_convergence(const Args& a) {
+    const fraq::ExperimentConfig cfg = a.experiment();
+    cfg.validate();
+    const std::filesystem::path dir = cfg.out_dir;
+    std::filesystem::create_directories(dir);
+    const std::vector<fraq::ConvergenceReport> reports = fraq::run_convergence(cfg);
+    write_meta(cfg.out_dir, cfg);
+    for (const fraq::ConvergenceReport& rep : reports) {
+        const auto path = dir / ("convergence_" + fraq::scheme_name(rep.scheme) + ".csv");
+        std::ofstream csv(path);
+        fraq::write_convergence_csv(csv, rep);
+        std::cout << path.string() << "\n";
+    }
+    return 0;
+}
+
+int cmd_bench(const Args& a) {
+    const fraq::ExperimentConfig cfg = a.experiment();
+    std::vector<long> counts;
+    for (double v : fraq::parse_fraction_list(a.get("n-list", "100,200,400,800,1600")))
+        counts.push_back(std::lround(v));
+    Sink out(a.get("out", ""));
+    fraq::write_bench_csv(out.stream(), fraq::timing_sweep(cfg, counts));
+    return 0;
+}
+
+int run(const std::string& config, const std::string& cmd, const Opts& opts) {
+    Args a;
+    a.cli = opts;
     if (!config.empty()) {
         std::ifstream in(config);
         if (!in) throw std::runtime_error("cannot open config file: " + config);
-        file = fraq::parse_config_text(in);
+        a.file = fraq::parse_config_text(in);
     }
-    const std::string out_path = opts.count("out") ? opts["out"] : "";
-    opts.erase("out");
-    auto merged = [&](const std::string& k, const std::string& dflt) {
-        if (auto it = opts.find(k); it != opts.end()) return it->second;
-        if (auto it = file.find(k); it != file.end()) return it->second;
-        return dflt;
+    static const std::map<std::string, int (*)(const Args&)> table = {
+        {"weights", cmd_weights},         {"kernel-error", cmd_kernel_error},
+        {"solve", cmd_solve},             {"convergence", cmd_convergence},
+        {"bench", cmd_bench},
     };
-    auto num = [&](const std::string& k, const std::string& dflt) {
-        return fraq::parse_fraction(merged(k, dflt));
-    };
-    auto cq_scheme = [&]() {
-        const std::string s = merged("scheme", "be");
-        if (s != "be" && s != "sbd")
-            throw std::invalid_argument("scheme must be 'be' or 'sbd', got '" + s + "'");
-        return s;
-    };
-    if (cmd == "weights") {
-        const std::string s = cq_scheme();
-        const double alpha = num("alpha", "0.5"), tau = num("tau", "1");
-        const long n = std::lround(num("n", "10"));
-        const fraq::WeightTable t =
-            s == "sbd" ? fraq::sbd_weights(alpha, tau, n) : fraq::be_weights(alpha, tau, n);
-        auto f = open_out(out_path);
-        fraq::write_weights_csv(f ? *f : std::cout, t);
-    } else if (cmd == "kernel-error") {
-        const std::string s = cq_scheme();
-        const double alpha = num("alpha", "0.5"), tau = num("tau", "0.001");
-        const long n_max = std::lround(num("n-max", "1000"));
-        fraq::KernelErrorReport rep;
-        if (s == "sbd") {
-            int ns = int(num("ns", "0"));
-            if (ns <= 0) ns = fraq::default_sbd_head(alpha);
-            rep = fraq::kernel_error_report(
-                fraq::build_sbd_kernel(alpha, tau, int(num("np1", "41")), int(num("np2", "41")), ns),
-                n_max);
-        } else {
-            rep = fraq::kernel_error_report(fraq::build_be_kernel(alpha, tau, int(num("np", "64"))),
-                                            n_max);
-        }
-        auto f = open_out(out_path);
-        fraq::write_kernel_error_csv(f ? *f : std::cout, rep);
-    } else if (cmd == "solve") {
-        const fraq::ExperimentConfig cfg = fraq::resolve_config(file, opts);
-        const double tau = num("tau", "0");
-        fraq::ProblemSpec spec;
-        spec.alpha1 = cfg.alpha1;
-        spec.alpha2 = cfg.alpha2;
-        spec.coupling_a = cfg.coupling_a;
-        spec.grid_m = cfg.grid_m;
-        spec.t_final = cfg.t_final;
-        spec.initial = cfg.initial;
-        spec.n_steps = std::lround(cfg.t_final / (tau > 0 ? tau : cfg.t_final / 100.0));
-        if (const double n = num("n-steps", "0"); n > 0) spec.n_steps = std::lround(n);
-        const fraq::Scheme scheme = fraq::scheme_from_name(merged("scheme", "be"));
-        std::vector<long> snaps;
-        if (const std::string times = merged("snapshot-times", ""); !times.empty())
-            for (double t : fraq::parse_fraction_list(times)) snaps.push_back(std::lround(t / spec.tau()));
-        const std::string out_dir = merged("out-dir", ".");
-        std::function<void(long, const fraq::StateField&)> observer;
-        if (!snaps.empty()) {
-            std::filesystem::create_directories(out_dir);
-            observer = [&](long n, const fraq::StateField& f) {
-                for (long s : snaps)
-                    if (s == n) {
-                        std::ofstream snap(std::filesystem::path(out_dir) /
-                                           ("snapshot_n" + std::to_string(n) + ".csv"));
-                        fraq::write_snapshot_csv(snap, spec, f);
-                    }
-            };
-        }
-        const fraq::RunResult rr = fraq::run(spec, scheme, cfg.kernel, observer);
-        auto f = open_out(out_path);
-        fraq::write_snapshot_csv(f ? *f : std::cout, spec, rr.final_state);
-        std::cerr << "loop_seconds=" << fraq::format_double(rr.loop_seconds)
-                  << " setup_seconds=" << fraq::format_double(rr.setup_seconds) << "\n";
-    } else if (cmd == "convergence") {
-        fraq::ExperimentConfig cfg = fraq::resolve_config(file, opts);
-        cfg.validate();
-        std::filesystem::create_directories(cfg.out_dir);
-        const auto reports = fraq::run_convergence(cfg);
-        write_meta(cfg.out_dir, cfg);
-        for (const auto& rep : reports) {
-            const auto path = std::filesystem::path(cfg.out_dir) /
-                              ("convergence_" + fraq::scheme_name(rep.scheme) + ".csv");
-            std::ofstream f(path);
-            fraq::write_convergence_csv(f, rep);
-            std::cout << path.string() << "\n";
-        }
-    } else {  // bench
-        const fraq::ExperimentConfig cfg = fraq::resolve_config(file, opts);
-        std::vector<long> ns;
-        for (double v : fraq::parse_fraction_list(merged("n-list", "100,200,400,800,1600")))
-            ns.push_back(std::lround(v));
-        const auto rows = fraq::timing_sweep(cfg, ns);
-        auto f = open_out(out_path);
-        fraq::write_bench_csv(f ? *f : std::cout, rows);
-    }
-    return 0;
+    return table.at(cmd)(a);
 }
 
 }  // namespace

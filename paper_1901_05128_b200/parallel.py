@@ -25,6 +25,23 @@ def shard(n: int, rank: int, world: int) -> tuple[int, int]:
     return lo, lo + base + (1 if rank < extra else 0)
 
 
+def c2_groups(lo: int, hi: int, n_dofs: int = 65536) -> list[tuple[int, int]]:
+    """C2 has two CQ exponents: DOFs [0, n/2) use gamma 0.7, [n/2, n) gamma 0.3.  For a
+    contiguous DOF block [lo, hi) returns the (group index, DOF count) pairs it spans, empty
+    groups dropped -- the MultiHistory groups a rank builds."""
+    half = n_dofs // 2
+    counts = [max(0, min(hi, half) - lo), max(0, hi - max(lo, half))]
+    return [(g, c) for g, c in enumerate(counts) if c > 0]
+
+
+def c2_strong_slice(rank: int, world: int, n_dofs: int = 65536):
+    """SURVEY.md §8(e) strong scaling of C2: rank r owns the contiguous DOF block
+    shard(n_dofs, r, world) of the ONE 65536-DOF job (the exponent halves map to rank halves when
+    world is even).  Returns (lo, hi, groups)."""
+    lo, hi = shard(n_dofs, rank, world)
+    return lo, hi, c2_groups(lo, hi, n_dofs)
+
+
 def max_over_ranks(value: float, device=None) -> float:
     """Max of a scalar over all ranks (the job time is the slowest rank's device time)."""
     import torch
@@ -108,52 +125,6 @@ class FraqOps:
                                         lam.data_ptr(), c0.data_ptr(), cN.data_ptr(),
                                         kconf if kconf is not None else self.fraq.KernelConfig())
         return cN, rr.loop_seconds
-
-
-class OracleOps:
-    """CPU stand-in with the same interface (numpy DST + the mode-space oracle), for the gloo
-    tests of the sharding logic.  TEST INFRASTRUCTURE: uses oracle/."""
-
-    def __init__(self, orc, torch):
-        self.orc, self.torch = orc, torch
-        self.stream = None
-
-    def tensor(self, x):
-        return self.torch.as_tensor(x, dtype=self.torch.float64).contiguous()
-
-    def empty(self, *shape):
-        return self.torch.empty(*shape, dtype=self.torch.float64)
-
-    def mark(self):
-        import time
-        return time.perf_counter()
-
-    @staticmethod
-    def seconds(a, b):
-        return b - a
-
-    def dst2d(self, M, x, inverse):
-        import numpy as np
-        S = np.sin(np.outer(np.arange(1, M + 1), np.arange(1, M + 1)) * np.pi / (M + 1))
-        sc = 1.0 if inverse else (2.0 / (M + 1)) ** 2
-        g = x.numpy().reshape(-1, M, M)
-        return self.tensor(np.stack([sc * S @ gi @ S for gi in g]).reshape(x.shape))
-
-    def dst_cols(self, M, x, inverse):
-        import numpy as np
-        S = np.sin(np.outer(np.arange(1, M + 1), np.arange(1, M + 1)) * np.pi / (M + 1))
-        sc = 1.0 if inverse else 2.0 / (M + 1)
-        return self.tensor(sc * S @ x.numpy().reshape(M, -1)).reshape(x.shape)
-
-    def step(self, alpha1, alpha2, a, t_final, N, scheme, lam, c0, kconf):
-        sbd = scheme == "FastSBD"
-        tau = t_final / N
-        k1 = self.orc.build_kernel_auto(sbd, 1 - alpha1, tau, N)
-        k2 = self.orc.build_kernel_auto(sbd, 1 - alpha2, tau, N)
-        u, v, secs = self.orc.modal_run(k1, k2, a, tau, N, lam.numpy(), c0[0].numpy(),
-                                        c0[1].numpy())
-        import numpy as np
-        return self.tensor(np.stack([u, v])), secs
 
 
 def run_2d_sharded(ops, alpha1, alpha2, a, M, t_final, N, scheme, g1_0, g2_0, kconf=None,

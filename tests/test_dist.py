@@ -82,7 +82,8 @@ def _worker_2d(rank, world, port, q, scheme):
                       WORLD_SIZE=str(world))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle.oracle import Oracle
-    from paper_1901_05128_b200.parallel import OracleOps, run_2d_sharded
+    from oracle_ops import OracleOps
+    from paper_1901_05128_b200.parallel import run_2d_sharded
     g1, g2 = _c4_like(9)
     ops = OracleOps(Oracle("port"), torch)
     try:
@@ -109,7 +110,8 @@ def test_c4_mode_shards_two_ranks(scheme):
     single-process run of the same driver and the physical-space 2D restatement to 1e-10."""
     import torch
     from oracle.oracle import Oracle
-    from paper_1901_05128_b200.parallel import OracleOps, run_2d_sharded
+    from oracle_ops import OracleOps
+    from paper_1901_05128_b200.parallel import run_2d_sharded
     from ffpe_refs import fast_stepper_nd
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -140,7 +142,8 @@ def _worker_2d_t(rank, world, port, q, scheme):
                       WORLD_SIZE=str(world))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle.oracle import Oracle
-    from paper_1901_05128_b200.parallel import OracleOps, run_2d_transposed
+    from oracle_ops import OracleOps
+    from paper_1901_05128_b200.parallel import run_2d_transposed
     g1, g2 = _c4_like(9)
     ops = OracleOps(Oracle("port"), torch)
     try:
@@ -162,7 +165,8 @@ def test_c4_transposed_dst_ranks(scheme, world):
     physical-space 2D restatement, and each rank's slab is its rows of the result."""
     import torch
     from oracle.oracle import Oracle
-    from paper_1901_05128_b200.parallel import OracleOps, run_2d_sharded, slab_rows
+    from oracle_ops import OracleOps
+    from paper_1901_05128_b200.parallel import run_2d_sharded, slab_rows
     from ffpe_refs import fast_stepper_nd
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -189,3 +193,65 @@ def test_c4_transposed_dst_ranks(scheme, world):
         lo, hi, _ = slab_rows(9, rank, world)
         assert np.array_equal(slab[0], r1.reshape(9, 9)[lo:hi])
         assert np.array_equal(slab[1], r2.reshape(9, 9)[lo:hi])
+
+
+def _strong_worker(rank, world, port, q):
+    """One rank of the C2 strong split: its DOF block and exponent groups, evaluated with the
+    oracle on a shortened horizon, and the all-gathered coverage of the job."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.oracle import Oracle
+    from paper_1901_05128_b200.parallel import c2_strong_slice
+    from workloads import c2_params
+    n = 96  # a scaled-down C2 job: 96 DOFs, exponent halves 0.7 | 0.3
+    lo, hi, groups = c2_strong_slice(rank, world, n)
+    p = c2_params(n)
+    orc = Oracle("port")
+    ks = [orc.build_sbd_kernel(g, 1e-3, 24, 24, 12) for g in (0.7, 0.3)]
+    U = p.signal(0, 64, np.arange(lo, hi))
+    cols, off = [], 0
+    for g, cnt in groups:
+        cols.append(orc.hist_run(ks[g], U[:, off:off + cnt]))
+        off += cnt
+    D = np.concatenate(cols, axis=1) if cols else np.zeros((64, 0))
+    cover = torch.tensor([lo, hi], dtype=torch.int64)
+    allc = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(allc, cover)
+    q.put((rank, lo, hi, D, [tuple(x.tolist()) for x in allc]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_c2_strong_split(world):
+    """bench.py --scaling strong: the ranks' DOF blocks tile the one 65536-DOF job (here a
+    96-DOF stand-in), each block picks the right exponent per DOF, and the stitched result equals
+    the single-process evaluation bitwise."""
+    from paper_1901_05128_b200.parallel import c2_groups, c2_strong_slice
+    assert c2_strong_slice(0, 8)[2] == [(0, 8192)] and c2_strong_slice(7, 8)[2] == [(1, 8192)]
+    assert c2_groups(30000, 40000) == [(0, 2768), (1, 7232)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_strong_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted([q.get(timeout=120) for _ in procs], key=lambda x: x[0])
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    cover = res[0][4]
+    assert cover[0][0] == 0 and cover[-1][1] == 96
+    assert all(a[1] == b[0] for a, b in zip(cover, cover[1:]))
+    from oracle.oracle import Oracle
+    from workloads import c2_params
+    orc = Oracle("port")
+    p = c2_params(96)
+    U = p.signal(0, 64, np.arange(96))
+    ks = [orc.build_sbd_kernel(g, 1e-3, 24, 24, 12) for g in (0.7, 0.3)]
+    full = np.concatenate([orc.hist_run(ks[0], U[:, :48]), orc.hist_run(ks[1], U[:, 48:])], axis=1)
+    stitched = np.concatenate([r[3] for r in res], axis=1)
+    assert np.array_equal(stitched, full)

@@ -16,8 +16,11 @@ def _blocks(lang):
     return re.findall(r"```" + lang + r"\n(.*?)```", txt, re.S)
 
 
-def test_cpp_call_sites_compile_and_link(tmp_path):
-    body = _blocks("cpp")[0]
+@pytest.mark.parametrize("block", [0, 1])
+def test_cpp_call_sites_compile_and_link(tmp_path, block):
+    """Block 0: histories / run / batches; block 1: the single-step API and the block-solver
+    types (a test_fpfp.cpp-style call site)."""
+    body = _blocks("cpp")[block]
     include = [l for l in body.splitlines() if l.startswith("#include")]
     code = "\n".join(l for l in body.splitlines() if not l.startswith("#include"))
     src = "\n".join(include) + """
