@@ -251,6 +251,18 @@ def main():
         dims = [0, 0]
         for g, cnt in groups:
             dims[g] = cnt
+    else:
+        # weak: each rank owns 65536 DOFs (rank 0 the seeded C2 set, others rank-seeded draws)
+        gen = torch.Generator(device="cpu").manual_seed(1901051282 + rank)
+        if rank == 0:
+            a = torch.from_numpy(params.a); bb = torch.from_numpy(params.b)
+            c = torch.from_numpy(params.c); w = torch.from_numpy(params.w)
+        else:
+            a = torch.randn(DOFS, generator=gen, dtype=torch.float64)
+            c = torch.randn(DOFS, generator=gen, dtype=torch.float64)
+            bb = 0.1 + 1.9 * torch.rand(DOFS, generator=gen, dtype=torch.float64)
+            w = 1.0 + 19.0 * torch.rand(DOFS, generator=gen, dtype=torch.float64)
+        dims = [DOFS // 2, DOFS - DOFS // 2]
     gk = [k for k, d in zip(ks, dims) if d > 0]
     dims = [d for d in dims if d > 0]
     NL = sum(dims)  # DOFs on this rank
