@@ -256,6 +256,8 @@ __global__ void __launch_bounds__(128) dst_kernel(const double* __restrict__ sin
     const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
     const int g = lane >> 2, t = lane & 3;
     const long period = 2L * (M + 1);
+    const unsigned pmask = (period & (period - 1)) == 0 ? (unsigned)period - 1u : 0u;
+    const bool small = M < 46340;  // (k+1)(j+1) fits 32 bits
     double acc[4][4][2];
 #pragma unroll
     for (int x = 0; x < 4; ++x)
@@ -266,7 +268,13 @@ __global__ void __launch_bounds__(128) dst_kernel(const double* __restrict__ sin
         for (int idx = tid; idx < ST_M * ST_K; idx += 128) {
             const int r = idx / ST_K, cc = idx % ST_K;
             const long k = k0 + r, j = j0 + cc;
-            sA[r][cc] = (k < M && j < M) ? sintab[((k + 1) * (j + 1)) % period] : 0.0;
+            // (k+1)(j+1) < 2^31 for every grid this path takes (M < 46340); the period
+            // 2(M+1) is a power of two on the BASELINE grids (mask instead of a division)
+            const long kj = (k + 1) * (j + 1);
+            const long ix = small ? (long)(pmask ? ((unsigned)kj & pmask)
+                                                 : (unsigned)kj % (unsigned)period)
+                                  : kj % period;
+            sA[r][cc] = (k < M && j < M) ? sintab[ix] : 0.0;
         }
         for (int idx = tid; idx < ST_K * ST_N; idx += 128) {
             const int r = idx / ST_N, cc = idx % ST_N;
@@ -304,6 +312,55 @@ __global__ void sintab_kernel(double* tab, int M) {
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < period;
          i += (long)gridDim.x * blockDim.x)
         tab[i] = sin(pi * (double)i / (double)(M + 1));
+}
+
+// K12s: the same transform for few columns (C <= CT; the 1D instances' two fields): a GEMV with
+// the sine gathered from a shared-memory copy of the table.  CTA = 32 outputs (lane = output k) x
+// 8 warps splitting the sum over j; the x row is a warp-uniform broadcast load.  The DMMA tile
+// kernel above would spend a 64-column tile on 2 columns and run a 4095-long k chain in 64 CTAs
+// (0.7 ms per C3 transform, 18% of the C3 run); this one is latency-light (128 CTAs, M/8 terms
+// per thread).
+template <int CT>
+__global__ void __launch_bounds__(256) dst_skinny_kernel(const double* __restrict__ sintab, int M,
+                                                         const double* __restrict__ In, long ldi,
+                                                         int C, double* Out, long ldo,
+                                                         double scale) {
+    extern __shared__ double smem[];
+    const int period = 2 * (M + 1);
+    double* tab = smem;                   // period values
+    double* part = smem + period;         // [8][32][CT]
+    for (int i = threadIdx.x; i < period; i += 256) tab[i] = sintab[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int k = blockIdx.x * 32 + lane;
+    const int kk = k < M ? k + 1 : 0;
+    const int per = (M + 7) / 8, j0 = warp * per, j1 = min(M, j0 + per);
+    double acc[CT];
+#pragma unroll
+    for (int c = 0; c < CT; ++c) acc[c] = 0.0;
+    // idx = (k+1)(j+1) mod period, advanced by k+1 per j
+    int idx = (int)(((long)kk * (j0 + 1)) % period);
+    for (int j = j0; j < j1; ++j) {
+        const double sv = tab[idx];
+        const double* x = In + (long)j * ldi;
+#pragma unroll
+        for (int c = 0; c < CT; ++c)
+            if (c < C) acc[c] = fma(sv, __ldg(x + c), acc[c]);
+        idx += kk;
+        if (idx >= period) idx -= period;
+    }
+#pragma unroll
+    for (int c = 0; c < CT; ++c) part[(warp * 32 + lane) * CT + c] = acc[c];
+    __syncthreads();
+    if (warp == 0 && k < M) {
+#pragma unroll
+        for (int c = 0; c < CT; ++c) {
+            if (c >= C) break;
+            double v = 0.0;
+            for (int w = 0; w < 8; ++w) v += part[(w * 32 + lane) * CT + c];
+            Out[(long)k * ldo + c] = scale * v;
+        }
+    }
 }
 
 __global__ void transpose_kernel(const double* in, long rows, long cols, double* out) {
@@ -364,6 +421,25 @@ struct Dst2D {
 // Apply the DST along the mode axis: Out (M x C) = scale * S In (M x C).
 void dst_apply(fraq_ctx c, int M, const double* sintab, const double* In, long C, double* Out,
                double scale) {
+    const size_t skinny_smem = sizeof(double) * (2 * (M + 1) + 8 * 32 * 8);
+    if (C <= 8 && skinny_smem <= 227 * 1024) {
+        const unsigned grid = (unsigned)((M + 31) / 32);
+        if (C <= 2) {
+            const size_t sm = sizeof(double) * (2 * (M + 1) + 8 * 32 * 2);
+            FRAQ_CUDA(cudaFuncSetAttribute(dst_skinny_kernel<2>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            dst_skinny_kernel<2><<<grid, 256, sm, c->stream>>>(sintab, M, In, C, (int)C, Out, C,
+                                                               scale);
+        } else {
+            FRAQ_CUDA(cudaFuncSetAttribute(dst_skinny_kernel<8>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)skinny_smem));
+            dst_skinny_kernel<8><<<grid, 256, skinny_smem, c->stream>>>(sintab, M, In, C, (int)C,
+                                                                       Out, C, scale);
+        }
+        FRAQ_LAUNCH_CHECK();
+        return;
+    }
     dim3 grid((unsigned)((C + ST_N - 1) / ST_N), (unsigned)((M + ST_M - 1) / ST_M));
     dst_kernel<<<grid, 128, 0, c->stream>>>(sintab, M, In, C, C, Out, C, scale);
     FRAQ_LAUNCH_CHECK();

@@ -489,6 +489,8 @@ void k13_prepare(fraq_ctx c, const std::vector<K13Inst>& in, bool sbd, K13Plan& 
     // narrowest NT in {12, 13, 14, 16} that covers J in 4 warps (C4: 408 nodes -> NT = 13)
     const char* narrow = std::getenv("FRAQ_K13_NARROW");  // experiment switch: RB = 1 for J > 256
     P.RB = (maxJ <= 256 || !(narrow && *narrow)) ? 2 : 1;
+    if (const char* rb1 = std::getenv("FRAQ_K13_RB1"); rb1 && *rb1 && maxJ <= 256)
+        P.RB = 1;  // experiment switch: 8-mode tasks for J <= 256
     P.NT = 8;
     // J > 256: four GEMM warps per field of 104 nodes (J <= 416; C4: 408 -> 416) or 128 nodes
     // (J <= 512; C5-BDF2: 512), 10 warps, ~168 registers.  Measured against 64 / 72 / 88-node

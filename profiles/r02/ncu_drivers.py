@@ -42,5 +42,22 @@ if __name__ == "__main__":
     what = sys.argv[1]
     if what == "c3phys":
         c3phys(int(sys.argv[2]) if len(sys.argv) > 2 else 64)
-    else:
+    elif what == "c4dst":
         c4dst()
+
+
+def c3modal():
+    from workloads import c3_instance as _c3
+    i = _c3()
+    spec = fraq.ProblemSpec(alpha1=i.alpha1, alpha2=i.alpha2, coupling_a=i.coupling_a,
+                            grid_m=4095, t_final=1.0, n_steps=16384, initial="custom",
+                            custom_g1=list(i.g1), custom_g2=list(i.g2))
+    kc = fraq.KernelConfig()
+    kc.solver = fraq.SOLVER_MODAL
+    for _ in range(2):
+        r = fraq.run(spec, fraq.Scheme.FastBE, kc)
+    print("c3modal", r.loop_seconds)
+
+
+if __name__ == "__main__" and sys.argv[1] == "c3modal":
+    c3modal()
