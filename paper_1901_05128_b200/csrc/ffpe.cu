@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -221,6 +222,8 @@ struct SolveArgs {
     int sbd;
     int first;            // SBD first step
     double* out;          // nullable: final state (inst * 2m: g1 then g2)
+    int refine;           // refinement step against the unrounded entries (always, except in
+                          // the FRAQ_K6_NOREFINE timing experiment)
 };
 
 // The 2x2-block tridiagonal solve of BlockSystem::solve (block_solver.cpp:119-153) on one CTA,
@@ -322,6 +325,17 @@ __device__ void refine_smem(double2* sb, double2* sr, const SysDev& S, const M2*
     __syncthreads();
 }
 
+// The system's reduction coefficients into shared memory, one coalesced copy: read from global
+// memory level by level, every CR level would first wait for an L1 miss (~700 cycles) -- 2/3 of
+// the whole solve at M = 4095 before this (41 -> 25 us per level at C3 with the refinement).
+template <int THREADS>
+__device__ void stage_sys(SysDev* dst, const SysDev* src) {
+    static_assert(sizeof(SysDev) % sizeof(double) == 0, "SysDev is copied as doubles");
+    const double* s = reinterpret_cast<const double*>(src);
+    double* d = reinterpret_cast<double*>(dst);
+    for (int i = threadIdx.x; i < (int)(sizeof(SysDev) / sizeof(double)); i += THREADS) d[i] = s[i];
+}
+
 // BlockSystem::solve on its own (block_solver.cpp:119-153): one CTA per system.
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) block_solve_kernel(const SysDev* sys, const M2* thomas,
@@ -330,6 +344,8 @@ __global__ void __launch_bounds__(THREADS) block_solve_kernel(const SysDev* sys,
                                                               double* g2) {
     extern __shared__ double2 sb[];
     double2* sr = sb + (m + 2);  // the right-hand side, kept for the refinement residual
+    __shared__ SysDev S;
+    stage_sys<THREADS>(&S, sys);
     for (int k = threadIdx.x; k < m; k += THREADS) {
         sb[k + 1] = make_double2(rhs1[k], rhs2[k]);
         sr[k + 1] = sb[k + 1];
@@ -339,8 +355,8 @@ __global__ void __launch_bounds__(THREADS) block_solve_kernel(const SysDev* sys,
         sb[m + 1] = make_double2(0.0, 0.0);
     }
     __syncthreads();
-    block_solve_smem<THREADS>(sb, sys[0], thomas, m);
-    refine_smem<THREADS>(sb, sr, sys[0], thomas, m);
+    block_solve_smem<THREADS>(sb, S, thomas, m);
+    refine_smem<THREADS>(sb, sr, S, thomas, m);
     for (int k = threadIdx.x; k < m; k += THREADS) {
         g1[k] = sb[k + 1].x;
         g2[k] = sb[k + 1].y;
@@ -429,10 +445,16 @@ template <int THREADS>
 __global__ void __launch_bounds__(THREADS) solve_kernel(SolveArgs A) {
     extern __shared__ double2 sb[];  // b / x, rows 1..m (index 0 and m+1 are zero)
     double2* sr = sb + (m_of(A) + 2);  // b, kept for the refinement residual
+    __shared__ SysDev S;
     const InstDev I = A.inst[blockIdx.x];
+    stage_sys<THREADS>(&S, A.sys + (A.first ? I.sys_first : I.sys_main));
     const GroupDev G1 = A.groups[I.g1], G2 = A.groups[I.g2];
     const int m = A.m;
     const double a = I.a, tau = I.tau, ih2 = 1.0 / (I.h * I.h);
+    // 1/tau once: the reference divides by tau per entry; for the power-of-two steps of every
+    // BASELINE config the product is bit-identical, otherwise it differs in the last bit of the
+    // RHS, which the refinement step does not care about (fp64 division is ~40 instructions)
+    const double itau = 1.0 / tau;
     const long n = A.n;
     const double* r1 = A.ring + G1.ring_off;
     const double* r2 = A.ring + G2.ring_off;
@@ -463,8 +485,8 @@ __global__ void __launch_bounds__(THREADS) solve_kernel(SolveArgs A) {
             const double u = p1[k], v = p2[k];
             const double au = (2.0 * u - (k > 0 ? p1[k - 1] : 0.0) - (k + 1 < m ? p1[k + 1] : 0.0)) * ih2;
             const double av = (2.0 * v - (k > 0 ? p2[k - 1] : 0.0) - (k + 1 < m ? p2[k + 1] : 0.0)) * ih2;
-            b1 = u / tau - (d10 / 3.0) * (a * u + au) + (a * d20 / 3.0) * v;
-            b2 = v / tau - (d20 / 3.0) * (a * v + av) + (a * d10 / 3.0) * u;
+            b1 = u * itau - (d10 / 3.0) * (a * u + au) + (a * d20 / 3.0) * v;
+            b2 = v * itau - (d20 / 3.0) * (a * v + av) + (a * d10 / 3.0) * u;
         } else {
             double x1 = s1[k], x2 = s2[k];
             double l1 = k > 0 ? s1[k - 1] : 0.0, rr1 = k + 1 < m ? s1[k + 1] : 0.0;
@@ -485,11 +507,11 @@ __global__ void __launch_bounds__(THREADS) solve_kernel(SolveArgs A) {
             const double as2 = (2.0 * x2 - l2 - rr2) * ih2;
             double lead1, lead2;
             if (A.sbd) {
-                lead1 = (2.0 * p1[k] - 0.5 * q1[k]) / tau;
-                lead2 = (2.0 * p2[k] - 0.5 * q2[k]) / tau;
+                lead1 = (2.0 * p1[k] - 0.5 * q1[k]) * itau;
+                lead2 = (2.0 * p2[k] - 0.5 * q2[k]) * itau;
             } else {
-                lead1 = p1[k] / tau;
-                lead2 = p2[k] / tau;
+                lead1 = p1[k] * itau;
+                lead2 = p2[k] * itau;
             }
             b1 = lead1 - a * x1 - as1 + a * x2;
             b2 = lead2 - a * x2 - as2 + a * x1;
@@ -502,9 +524,8 @@ __global__ void __launch_bounds__(THREADS) solve_kernel(SolveArgs A) {
         sb[m + 1] = make_double2(0.0, 0.0);
     }
     __syncthreads();
-    const SysDev& S = A.sys[A.first ? I.sys_first : I.sys_main];
     block_solve_smem<THREADS>(sb, S, A.thomas, m);
-    refine_smem<THREADS>(sb, sr, S, A.thomas, m);
+    if (A.refine) refine_smem<THREADS>(sb, sr, S, A.thomas, m);
     // append G^n into both rings (slot n % L)
     double* w1 = A.ring + G1.ring_off + (n % G1.L) * ld;
     double* w2 = A.ring + G2.ring_off + (n % G2.L) * ld;
@@ -612,6 +633,7 @@ struct PhysStepper {
     SolveArgs sa{};
     long level = 0, appended = 1, step_idx = 0, total = 0;
     size_t smem = 0;
+    int k6_threads = 512;
     double setup_seconds = 0.0;
 
     PhysStepper(fraq_ctx c_, const fraq_spec_t* specs, int n_inst_, int scheme,
@@ -788,9 +810,13 @@ PhysStepper::PhysStepper(fraq_ctx c_, const fraq_spec_t* specs, int n_inst_, int
     }
     smem = 2 * sizeof(double2) * (m + 2);
     if (smem > 227 * 1024) fail(FRAQ_EINVAL, "run: grid_m too large for the on-chip block solve");
-    if (smem > 48 * 1024)
+    k6_threads = std::getenv("FRAQ_K6_T1024") ? 1024 : 512;  // experiment switch
+    if (smem > 48 * 1024) {
         FRAQ_CUDA(cudaFuncSetAttribute(solve_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
+        FRAQ_CUDA(cudaFuncSetAttribute(solve_kernel<1024>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    }
     sa.inst = dinst.p;
     sa.sys = dsys.p;
     sa.thomas = thomas.p;
@@ -803,6 +829,7 @@ PhysStepper::PhysStepper(fraq_ctx c_, const fraq_spec_t* specs, int n_inst_, int
     sa.m = m;
     sa.sbd = sbd;
     sa.out = outb.p;
+    sa.refine = std::getenv("FRAQ_K6_NOREFINE") ? 0 : 1;  // experiment switch (timing only)
     FRAQ_CUDA(cudaStreamSynchronize(c->stream));
     setup_seconds = now_s() - t_setup0;
 }
@@ -856,7 +883,10 @@ void PhysStepper::step(long n_steps, std::vector<cudaEvent_t>* ev) {
         sa.first = first;
         // the last level of a call leaves G^n in outb (state reads, ffpe_run's result)
         sa.out = (q == n_steps - 1) ? outb.p : nullptr;
-        solve_kernel<512><<<n_inst, 512, smem, c->stream>>>(sa);
+        if (k6_threads == 1024)
+            solve_kernel<1024><<<n_inst, 1024, smem, c->stream>>>(sa);
+        else
+            solve_kernel<512><<<n_inst, 512, smem, c->stream>>>(sa);
         FRAQ_LAUNCH_CHECK();
         mark(e0 + 3);
         if (!fast) {

@@ -61,3 +61,27 @@ def c3modal():
 
 if __name__ == "__main__" and sys.argv[1] == "c3modal":
     c3modal()
+
+
+def k6split(levels=1024):
+    """Per-level K5 / K6 device time of the physical C3 stepper (events around every launch)."""
+    from workloads import c3_instance as _c3
+    i = _c3()
+    spec = fraq.ProblemSpec(alpha1=i.alpha1, alpha2=i.alpha2, coupling_a=i.coupling_a,
+                            grid_m=4095, t_final=1.0, n_steps=16384, initial="custom",
+                            custom_g1=list(i.g1), custom_g2=list(i.g2))
+    st = fraq.FastStepper(spec, False, fraq.KernelConfig())
+    st.step_n(1024)
+    a, b = st.time_split(levels)
+    import time
+    fraq.synchronize()
+    t0 = time.perf_counter()
+    st.step_n(levels)
+    fraq.synchronize()
+    dt = time.perf_counter() - t0
+    print(f"k5 {1e3 * a / levels:.2f} us  k6 {1e3 * b / levels:.2f} us  loop {1e6 * dt / levels:.2f} us"
+          " per level")
+
+
+if __name__ == "__main__" and sys.argv[1] == "k6split":
+    k6split()
