@@ -224,6 +224,9 @@ struct SolveArgs {
     double* out;          // nullable: final state (inst * 2m: g1 then g2)
     int refine;           // refinement step against the unrounded entries (always, except in
                           // the FRAQ_K6_NOREFINE timing experiment)
+    int tap1;             // add the newest head tap d_1 G^(n-1) here (K5 ran with first_tap 2)
+    const long* n_dev;    // CUDA-graph replays: n = *n_dev + n_off, first step never inside
+    int n_off;
 };
 
 // The 2x2-block tridiagonal solve of BlockSystem::solve (block_solver.cpp:119-153) on one CTA,
@@ -447,7 +450,7 @@ __global__ void __launch_bounds__(THREADS) solve_kernel(SolveArgs A) {
     double2* sr = sb + (m_of(A) + 2);  // b, kept for the refinement residual
     __shared__ SysDev S;
     const InstDev I = A.inst[blockIdx.x];
-    stage_sys<THREADS>(&S, A.sys + (A.first ? I.sys_first : I.sys_main));
+    stage_sys<THREADS>(&S, A.sys + (A.sbd && !A.n_dev && A.first ? I.sys_first : I.sys_main));
     const GroupDev G1 = A.groups[I.g1], G2 = A.groups[I.g2];
     const int m = A.m;
     const double a = I.a, tau = I.tau, ih2 = 1.0 / (I.h * I.h);
@@ -455,7 +458,8 @@ __global__ void __launch_bounds__(THREADS) solve_kernel(SolveArgs A) {
     // BASELINE config the product is bit-identical, otherwise it differs in the last bit of the
     // RHS, which the refinement step does not care about (fp64 division is ~40 instructions)
     const double itau = 1.0 / tau;
-    const long n = A.n;
+    const long n = A.n_dev ? *A.n_dev + A.n_off : A.n;
+    const int first = A.n_dev ? 0 : A.first;
     const double* r1 = A.ring + G1.ring_off;
     const double* r2 = A.ring + G2.ring_off;
     const long ld = G1.ld;
@@ -466,7 +470,7 @@ __global__ void __launch_bounds__(THREADS) solve_kernel(SolveArgs A) {
     const double* s2 = A.s + G2.dof0;
     const double* q1 = nullptr;
     const double* q2 = nullptr;
-    if (A.sbd && !A.first) {
+    if (A.sbd && !first) {
         q1 = r1 + ((n - 2) % G1.L) * ld;  // G^{n-2}
         q2 = r2 + ((n - 2) % G2.L) * ld;
         if (A.corr) {
@@ -478,9 +482,12 @@ __global__ void __launch_bounds__(THREADS) solve_kernel(SolveArgs A) {
     const double* g01 = A.g0 + I.g0_off;
     const double* g02 = g01 + m;
     const double d10 = A.head[G1.hd_off], d20 = A.head[G2.hd_off];
+    // newest head tap (fpfp.cpp:270-275 BE, 313-324 SBD i = 1), when the history pass left it
+    const bool tap = A.tap1 && n >= 2;
+    const double d11 = tap ? A.head[G1.hd_off + 1] : 0.0, d21 = tap ? A.head[G2.hd_off + 1] : 0.0;
     for (int k = threadIdx.x; k < m; k += THREADS) {
         double b1, b2;
-        if (A.sbd && A.first) {
+        if (A.sbd && first) {
             // 2/3-1/3 first step from G^0 (fpfp.cpp:293-303)
             const double u = p1[k], v = p2[k];
             const double au = (2.0 * u - (k > 0 ? p1[k - 1] : 0.0) - (k + 1 < m ? p1[k + 1] : 0.0)) * ih2;
@@ -491,6 +498,18 @@ __global__ void __launch_bounds__(THREADS) solve_kernel(SolveArgs A) {
             double x1 = s1[k], x2 = s2[k];
             double l1 = k > 0 ? s1[k - 1] : 0.0, rr1 = k + 1 < m ? s1[k + 1] : 0.0;
             double l2 = k > 0 ? s2[k - 1] : 0.0, rr2 = k + 1 < m ? s2[k + 1] : 0.0;
+            if (tap) {
+                x1 = fma(d11, p1[k], x1);
+                x2 = fma(d21, p2[k], x2);
+                if (k > 0) {
+                    l1 = fma(d11, p1[k - 1], l1);
+                    l2 = fma(d21, p2[k - 1], l2);
+                }
+                if (k + 1 < m) {
+                    rr1 = fma(d11, p1[k + 1], rr1);
+                    rr2 = fma(d21, p2[k + 1], rr2);
+                }
+            }
             if (A.sbd && A.corr) {
                 x1 += 0.5 * c1 * g01[k];
                 x2 += 0.5 * c2 * g02[k];
@@ -635,9 +654,23 @@ struct PhysStepper {
     size_t smem = 0;
     int k6_threads = 512;
     double setup_seconds = 0.0;
+    // CUDA graph of kGraphLevels levels of the fast schemes: the history pass of level n+1 (K5,
+    // side stream) overlaps the solve of level n (K6, context stream); the level comes from a
+    // device counter that the graph's last node advances, so one instantiated graph replays
+    // for the whole run.  Built on first use.
+    static constexpr int kGraphLevels = 64;
+    cudaGraphExec_t gexec = nullptr;
+    cudaStream_t s5 = nullptr;
+    std::vector<cudaEvent_t> gev;
+    DevBuf<long> ndev;
+    bool use_graph = true;
 
     PhysStepper(fraq_ctx c_, const fraq_spec_t* specs, int n_inst_, int scheme,
                 const fraq_kconf_t& kc);
+    ~PhysStepper();
+    StepArgs k5_args(long n) const;
+    void launch_k6(long n, bool last, cudaStream_t stream, const long* n_dev, int n_off);
+    void build_graph();
     void step(long n_steps, std::vector<cudaEvent_t>* ev = nullptr);  // stream-ordered
     // diagnostics: step n levels with an event pair around every kernel; returns the summed
     // device time of the history kernels (K5 / classical sums) and of the solves (K6)
@@ -796,7 +829,7 @@ PhysStepper::PhysStepper(fraq_ctx c_, const fraq_spec_t* specs, int n_inst_, int
         }
     }
     FRAQ_CUDA(cudaMemcpy(dinst.p, inst.data(), sizeof(InstDev) * n_inst, cudaMemcpyHostToDevice));
-    sbuf.alloc((size_t)2 * n_inst * m);
+    sbuf.alloc((size_t)(fast ? 2 : 1) * 2 * n_inst * m);  // fast: one buffer per level parity
     outb.alloc((size_t)2 * n_inst * m);
     // classical: full history of both fields, [t][2 n_inst m]
     total = (long)2 * n_inst * m;
@@ -830,8 +863,98 @@ PhysStepper::PhysStepper(fraq_ctx c_, const fraq_spec_t* specs, int n_inst_, int
     sa.sbd = sbd;
     sa.out = outb.p;
     sa.refine = std::getenv("FRAQ_K6_NOREFINE") ? 0 : 1;  // experiment switch (timing only)
+    sa.tap1 = fast ? 1 : 0;
+    use_graph = fast && !std::getenv("FRAQ_PHYS_NOGRAPH");  // experiment switch
     FRAQ_CUDA(cudaStreamSynchronize(c->stream));
     setup_seconds = now_s() - t_setup0;
+}
+
+__global__ void counter_kernel(long* ctr, long value, int add) {
+    if (add)
+        *ctr += value;
+    else
+        *ctr = value;
+}
+
+PhysStepper::~PhysStepper() {
+    if (c && c->stream) cudaStreamSynchronize(c->stream);
+    if (gexec) cudaGraphExecDestroy(gexec);
+    for (cudaEvent_t e : gev) cudaEventDestroy(e);
+    if (s5) cudaStreamDestroy(s5);
+}
+
+// History pass (K5, FFPE mode) of level n: advance to n, sum, head taps i >= 2 -> sbuf[n & 1].
+StepArgs PhysStepper::k5_args(long n) const {
+    StepArgs a{};
+    a.groups = hd.groups.p;
+    a.tiles = hd.tiles.p;
+    a.state = hd.state.p;
+    a.ring = hd.ring.p;
+    a.cr = hd.cr.p;
+    a.cf = hd.cf.p;
+    a.head = hd.head.p;
+    a.level = n - 1;
+    a.appended = n;
+    a.lo = 1;
+    a.adv = 1;
+    a.mode = MODE_FFPE;
+    a.first_tap = 2;
+    a.out = sbuf.p + (size_t)(n & 1) * total;
+    return a;
+}
+
+void PhysStepper::launch_k6(long n, bool last, cudaStream_t stream, const long* n_dev, int n_off) {
+    SolveArgs a = sa;
+    a.n = n;
+    a.first = sbd && n == 1;
+    a.n_dev = n_dev;
+    a.n_off = n_off;
+    if (fast) a.s = sbuf.p + (size_t)(n & 1) * total;
+    // the last level of a call leaves G^n in outb (state reads, ffpe_run's result); graph
+    // replays write it every level
+    a.out = (last || n_dev) ? outb.p : nullptr;
+    if (k6_threads == 1024)
+        solve_kernel<1024><<<n_inst, 1024, smem, stream>>>(a);
+    else
+        solve_kernel<512><<<n_inst, 512, smem, stream>>>(a);
+    FRAQ_LAUNCH_CHECK();
+}
+
+void PhysStepper::build_graph() {
+    const int G = kGraphLevels;
+    FRAQ_CUDA(cudaStreamCreateWithFlags(&s5, cudaStreamNonBlocking));
+    gev.resize(2 * G + 1);
+    for (auto& e : gev) FRAQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ndev.alloc(1);
+    cudaStream_t s6 = c->stream;
+    cudaGraph_t graph = nullptr;
+    FRAQ_CUDA(cudaStreamBeginCapture(s6, cudaStreamCaptureModeThreadLocal));
+    try {
+        FRAQ_CUDA(cudaEventRecord(gev[2 * G], s6));  // fork
+        FRAQ_CUDA(cudaStreamWaitEvent(s5, gev[2 * G], 0));
+        // chunk levels n0 + q, n0 even (replays start on even levels): parity of n = q & 1
+        for (int q = 0; q < G; ++q) {
+            if (q >= 2) FRAQ_CUDA(cudaStreamWaitEvent(s5, gev[G + q - 2], 0));  // K6(n-2) done
+            StepArgs a = k5_args(q);  // parity slot of level n0 + q
+            a.n_dev = ndev.p;
+            a.n_off = q;
+            hd.launch_step(c, a, s5);
+            FRAQ_CUDA(cudaEventRecord(gev[q], s5));
+            FRAQ_CUDA(cudaStreamWaitEvent(s6, gev[q], 0));  // K5(n) done
+            launch_k6(q, false, s6, ndev.p, q);
+            FRAQ_CUDA(cudaEventRecord(gev[G + q], s6));
+        }
+        counter_kernel<<<1, 1, 0, s6>>>(ndev.p, G, 1);
+        FRAQ_LAUNCH_CHECK();
+    } catch (...) {
+        cudaStreamEndCapture(s6, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+    }
+    FRAQ_CUDA(cudaStreamEndCapture(s6, &graph));
+    const cudaError_t e = cudaGraphInstantiate(&gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    FRAQ_CUDA(e);
 }
 
 void PhysStepper::step(long n_steps, std::vector<cudaEvent_t>* ev) {
@@ -841,8 +964,27 @@ void PhysStepper::step(long n_steps, std::vector<cudaEvent_t>* ev) {
     auto mark = [&](int k) {
         if (ev) FRAQ_CUDA(cudaEventRecord((*ev)[k], c->stream));
     };
-    for (long q = 0; q < n_steps; ++q) {
-        const long n = ++step_idx;
+    const long end = step_idx + n_steps;
+    bool counter_set = false;
+    while (step_idx < end) {
+        const long n = step_idx + 1;
+        // graph replay: whole chunks of levels >= 2 starting on an even level (not under the
+        // per-kernel timing of time_split)
+        if (use_graph && !ev && n >= 2 && (n & 1) == 0 && end - step_idx >= kGraphLevels) {
+            if (!gexec) build_graph();
+            if (!counter_set) {
+                counter_kernel<<<1, 1, 0, c->stream>>>(ndev.p, n, 0);
+                FRAQ_LAUNCH_CHECK();
+                counter_set = true;
+            }
+            FRAQ_CUDA(cudaGraphLaunch(gexec, c->stream));
+            step_idx += kGraphLevels;
+            level += kGraphLevels;
+            appended += kGraphLevels;
+            continue;
+        }
+        counter_set = false;
+        ++step_idx;
         const bool first = sbd && n == 1;
         if (ev) {
             for (int k = 0; k < 4; ++k) {
@@ -854,24 +996,8 @@ void PhysStepper::step(long n_steps, std::vector<cudaEvent_t>* ev) {
         const int e0 = ev ? (int)ev->size() - 4 : 0;
         mark(e0);
         if (fast) {
-            if (!first) {
-                StepArgs a{};
-                a.groups = hd.groups.p;
-                a.tiles = hd.tiles.p;
-                a.state = hd.state.p;
-                a.ring = hd.ring.p;
-                a.cr = hd.cr.p;
-                a.cf = hd.cf.p;
-                a.head = hd.head.p;
-                a.level = level;
-                a.appended = appended;
-                a.lo = 1;
-                a.adv = 1;
-                a.mode = MODE_FFPE;
-                a.out = sbuf.p;
-                hd.launch_step(c, a);
-            }
             // first SBD step: advance() only decays zero accumulators (no feed: 1 - n_head < 1)
+            if (!first) hd.launch_step(c, k5_args(n));
         } else if (!first) {
             classical_sum_kernel<<<(unsigned)((total + 255) / 256), 256, 0, c->stream>>>(
                 hist.p, total, ctab.p, N + 1, gof.p, total, n, sbd, sbuf.p);
@@ -879,15 +1005,7 @@ void PhysStepper::step(long n_steps, std::vector<cudaEvent_t>* ev) {
         }
         mark(e0 + 1);
         mark(e0 + 2);
-        sa.n = n;
-        sa.first = first;
-        // the last level of a call leaves G^n in outb (state reads, ffpe_run's result)
-        sa.out = (q == n_steps - 1) ? outb.p : nullptr;
-        if (k6_threads == 1024)
-            solve_kernel<1024><<<n_inst, 1024, smem, c->stream>>>(sa);
-        else
-            solve_kernel<512><<<n_inst, 512, smem, c->stream>>>(sa);
-        FRAQ_LAUNCH_CHECK();
+        launch_k6(n, step_idx == end, c->stream, nullptr, 0);
         mark(e0 + 3);
         if (!fast) {
             // keep the full history: copy G^n rows out of the 2-slot rings

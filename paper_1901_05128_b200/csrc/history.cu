@@ -73,10 +73,15 @@ __global__ void __launch_bounds__(LANES* S, 6) step_kernel(StepArgs A) {
     const int m = 4 * (tile.y + lane);  // first DOF of this thread's quad (within the group)
     const bool live = m < G.dim;
     __shared__ d4 s_part[S][LANES];
+    long level = A.level, appended = A.appended;
+    if (A.n_dev) {
+        level = *A.n_dev + A.n_off - 1;
+        appended = level + 1;
+    }
 
     // feed value u_{level+1-L} from the ring (read by every slice before the barrier below)
-    const long fi = A.level + 1 - G.L;
-    const bool feed = A.adv && fi >= A.lo && fi <= A.appended - 1;
+    const long fi = level + 1 - G.L;
+    const bool feed = A.adv && fi >= A.lo && fi <= appended - 1;
     const long ld = G.ld;
     d4 v = {0.0, 0.0, 0.0, 0.0};
     if (feed && live) v = ld4(A.ring + G.ring_off + (fi % G.L) * ld + m);
@@ -150,7 +155,6 @@ __global__ void __launch_bounds__(LANES* S, 6) step_kernel(StepArgs A) {
     if (!live) return;
     const int nv = min(4, G.dim - m);  // valid DOFs of this quad
     double* ring = A.ring + G.ring_off + m;
-    long appended = A.appended;
     if (A.app) {
         const double* u = A.u + G.dof0 + m;
         d4 x;
@@ -181,7 +185,8 @@ __global__ void __launch_bounds__(LANES* S, 6) step_kernel(StepArgs A) {
             top = n >= 2 ? 1 : 0;
         else
             top = min((long)G.L - 1, n - 1);
-        for (long i = 1; i <= top; ++i) fma4(acc, hd[i], ld4(ring + ((n - i) % G.L) * ld));
+        for (long i = A.first_tap > 1 ? A.first_tap : 1; i <= top; ++i)
+            fma4(acc, hd[i], ld4(ring + ((n - i) % G.L) * ld));
     }
     double* o = A.out + G.dof0 + m;
     o[0] = acc.x;
@@ -545,12 +550,14 @@ void HistDevice::zero(fraq_ctx c) {
     FRAQ_CUDA(cudaMemsetAsync(ring.p, 0, ring.n * sizeof(double), c->stream));
 }
 
-void HistDevice::launch_step(fraq_ctx c, const StepArgs& a) {
+void HistDevice::launch_step(fraq_ctx c, const StepArgs& a) { launch_step(c, a, c->stream); }
+
+void HistDevice::launch_step(fraq_ctx, const StepArgs& a, cudaStream_t stream) {
     if (n_tiles == 0) return;
     if (lanes == 32)
-        step_kernel<32, 4><<<n_tiles, 128, 0, c->stream>>>(a);
+        step_kernel<32, 4><<<n_tiles, 128, 0, stream>>>(a);
     else
-        step_kernel<8, 16><<<n_tiles, 128, 0, c->stream>>>(a);
+        step_kernel<8, 16><<<n_tiles, 128, 0, stream>>>(a);
     FRAQ_LAUNCH_CHECK();
 }
 

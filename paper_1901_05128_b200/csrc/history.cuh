@@ -40,6 +40,13 @@ struct StepArgs {
     int mode;        // 0: none, 1: history_sum, 2: derivative, 3: FFPE history term
     const double* u; // append input (device, user layout dof0-relative)
     double* out;     // output (device, user layout)
+    // FFPE stepper extras (zero = off): the level from a device counter (CUDA-graph replays:
+    // level = *n_dev + n_off - 1, appended = level + 1), and the first head tap of MODE_FFPE
+    // (2: tap 1 -- the newest level, d_1 G^(n-1) -- is left to the solve kernel, so the
+    // history pass of level n+1 can overlap the solve of level n)
+    const long* n_dev;
+    int n_off;
+    int first_tap;
 };
 
 enum { MODE_NONE = 0, MODE_SUM = 1, MODE_DERIV = 2, MODE_FFPE = 3 };
@@ -94,6 +101,7 @@ struct HistDevice {
     void build(fraq_ctx c, int n_groups, const fraq_kernel_t* const* ks, const long* dims,
                bool tables_only = false);
     void launch_step(fraq_ctx c, const StepArgs& a);
+    void launch_step(fraq_ctx c, const StepArgs& a, cudaStream_t stream);
     // reset state/ring to zero
     void zero(fraq_ctx c);
 };
