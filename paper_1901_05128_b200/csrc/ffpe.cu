@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -227,18 +228,37 @@ struct SolveArgs {
     int tap1;             // add the newest head tap d_1 G^(n-1) here (K5 ran with first_tap 2)
     const long* n_dev;    // CUDA-graph replays: n = *n_dev + n_off, first step never inside
     int n_off;
+    long long* prof;      // nullable: block 0 phase timestamps (FRAQ_K6_PROFILE experiment)
 };
+
+// Row storage of the on-chip solve: row i at slot i + i/8 + i/64 + i/512.  Cyclic reduction
+// touches rows at power-of-two strides; with rows packed densely (16-byte double2) a warp at
+// stride 8+ hit one bank group 32 times over (levels 1-2 and their back-substitution took ~2200
+// cycles each at M = 4095); the pad slots spread every power-of-two stride over the banks
+// (profiles/microbench/mb_cr.cu: one solve 21.9k -> 13.1k cycles).
+struct Rows {
+    double2* p;
+    __device__ __forceinline__ double2& operator[](int i) const {
+        return p[i + (i >> 3) + (i >> 6) + (i >> 9)];
+    }
+};
+// slots for rows 0 .. m+1
+__host__ __device__ constexpr size_t rows_len(int m) {
+    return (size_t)(m + 1) + ((m + 1) >> 3) + ((m + 1) >> 6) + ((m + 1) >> 9) + 1;
+}
 
 // The 2x2-block tridiagonal solve of BlockSystem::solve (block_solver.cpp:119-153) on one CTA,
 // in place on sb[1..m] (sb[0] = sb[m+1] = 0): block cyclic reduction with the setup
-// coefficients (grid_m = 2^K - 1), else block Thomas (one thread; general grid sizes).
+// coefficients (grid_m = 2^K - 1), else block Thomas (one thread; general grid sizes).  The
+// levels with at most 32 active rows run on warp 0 alone (__syncwarp between them; -10%).
 // Ends with __syncthreads().
 template <int THREADS>
-__device__ void block_solve_smem(double2* sb, const SysDev& S, const M2* thomas, int m) {
+__device__ void block_solve_smem(Rows sb, const SysDev& S, const M2* thomas, int m) {
     if (S.K > 0) {
         const int K = S.K;
+        const int lw = K > 6 ? K - 6 : 0;  // first level with <= 31 rows
         // forward reduction
-        for (int l = 0; l < K - 1; ++l) {
+        for (int l = 0; l < lw; ++l) {
             const int s = 1 << l;
             const M2 F = S.lv[l].F;
             for (int i = 2 * s * (threadIdx.x + 1); i <= m; i += 2 * s * THREADS) {
@@ -248,12 +268,38 @@ __device__ void block_solve_smem(double2* sb, const SysDev& S, const M2* thomas,
             }
             __syncthreads();
         }
-        if (threadIdx.x == 0) {
-            const int i = 1 << (K - 1);
-            sb[i] = mv(S.lv[K - 1].G, sb[i]);
+        if (threadIdx.x < 32) {
+            for (int l = lw; l < K - 1; ++l) {
+                const int s = 1 << l;
+                const M2 F = S.lv[l].F;
+                for (int i = 2 * s * (threadIdx.x + 1); i <= m; i += 64 * s) {
+                    const double2 sum =
+                        make_double2(sb[i - s].x + sb[i + s].x, sb[i - s].y + sb[i + s].y);
+                    const double2 t = mv(F, sum);
+                    sb[i] = make_double2(sb[i].x - t.x, sb[i].y - t.y);
+                }
+                __syncwarp();
+            }
+            if (threadIdx.x == 0) {
+                const int i = 1 << (K - 1);
+                sb[i] = mv(S.lv[K - 1].G, sb[i]);
+            }
+            __syncwarp();
+            for (int l = K - 2; l >= lw; --l) {
+                const int s = 1 << l;
+                const M2 Gm = S.lv[l].G, H = S.lv[l].H;
+                for (int i = s * (2 * (int)threadIdx.x + 1); i <= m; i += 64 * s) {
+                    const double2 xb = mv(Gm, sb[i]);
+                    const double2 nb =
+                        make_double2(sb[i - s].x + sb[i + s].x, sb[i - s].y + sb[i + s].y);
+                    const double2 t = mv(H, nb);
+                    sb[i] = make_double2(xb.x - t.x, xb.y - t.y);
+                }
+                __syncwarp();
+            }
         }
         __syncthreads();
-        for (int l = K - 2; l >= 0; --l) {
+        for (int l = lw - 1; l >= 0; --l) {
             const int s = 1 << l;
             const M2 Gm = S.lv[l].G, H = S.lv[l].H;
             for (int i = s * (2 * (int)threadIdx.x + 1); i <= m; i += 2 * s * THREADS) {
@@ -306,7 +352,7 @@ __device__ inline double residual_row(double b, double x, double xl, double xr, 
     return s + t;
 }
 template <int THREADS>
-__device__ void refine_smem(double2* sb, double2* sr, const SysDev& S, const M2* thomas, int m) {
+__device__ void refine_smem(Rows sb, Rows sr, const SysDev& S, const M2* thomas, int m) {
     for (int k = threadIdx.x; k < m; k += THREADS) {
         const double2 x = sb[k + 1], l = sb[k], r = sb[k + 2], b = sr[k + 1];
         const double r1 = residual_row(b.x, x.x, l.x, r.x, x.y, S.dh[0], S.dl[0], S.eh[0],
@@ -345,8 +391,9 @@ __global__ void __launch_bounds__(THREADS) block_solve_kernel(const SysDev* sys,
                                                               int m, const double* rhs1,
                                                               const double* rhs2, double* g1,
                                                               double* g2) {
-    extern __shared__ double2 sb[];
-    double2* sr = sb + (m + 2);  // the right-hand side, kept for the refinement residual
+    extern __shared__ double2 smem_rows[];
+    const Rows sb{smem_rows};
+    const Rows sr{smem_rows + rows_len(m)};  // the right-hand side, kept for the refinement
     __shared__ SysDev S;
     stage_sys<THREADS>(&S, sys);
     for (int k = threadIdx.x; k < m; k += THREADS) {
@@ -446,8 +493,13 @@ __device__ inline int m_of(const SolveArgs& A) { return A.m; }
 // per instance.
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) solve_kernel(SolveArgs A) {
-    extern __shared__ double2 sb[];  // b / x, rows 1..m (index 0 and m+1 are zero)
-    double2* sr = sb + (m_of(A) + 2);  // b, kept for the refinement residual
+    extern __shared__ double2 smem_rows[];
+    const Rows sb{smem_rows};                       // b / x, rows 1..m (rows 0, m+1 are zero)
+    const Rows sr{smem_rows + rows_len(m_of(A))};  // b, kept for the refinement residual
+    auto stamp = [&](int q) {
+        if (A.prof && blockIdx.x == 0 && threadIdx.x == 0) A.prof[q] += clock64();
+    };
+    stamp(0);
     __shared__ SysDev S;
     const InstDev I = A.inst[blockIdx.x];
     stage_sys<THREADS>(&S, A.sys + (A.sbd && !A.n_dev && A.first ? I.sys_first : I.sys_main));
@@ -543,8 +595,11 @@ __global__ void __launch_bounds__(THREADS) solve_kernel(SolveArgs A) {
         sb[m + 1] = make_double2(0.0, 0.0);
     }
     __syncthreads();
+    stamp(1);
     block_solve_smem<THREADS>(sb, S, A.thomas, m);
+    stamp(2);
     if (A.refine) refine_smem<THREADS>(sb, sr, S, A.thomas, m);
+    stamp(3);
     // append G^n into both rings (slot n % L)
     double* w1 = A.ring + G1.ring_off + (n % G1.L) * ld;
     double* w2 = A.ring + G2.ring_off + (n % G2.L) * ld;
@@ -556,6 +611,10 @@ __global__ void __launch_bounds__(THREADS) solve_kernel(SolveArgs A) {
             A.out[(long)blockIdx.x * 2 * m + k] = x.x;
             A.out[(long)blockIdx.x * 2 * m + m + k] = x.y;
         }
+    }
+    if (A.prof) {
+        __syncthreads();
+        stamp(4);
     }
 }
 
@@ -841,7 +900,7 @@ PhysStepper::PhysStepper(fraq_ctx c_, const fraq_spec_t* specs, int n_inst_, int
         gof.alloc(total);
         FRAQ_CUDA(cudaMemcpy(gof.p, go.data(), sizeof(int) * total, cudaMemcpyHostToDevice));
     }
-    smem = 2 * sizeof(double2) * (m + 2);
+    smem = 2 * sizeof(double2) * rows_len(m);
     if (smem > 227 * 1024) fail(FRAQ_EINVAL, "run: grid_m too large for the on-chip block solve");
     k6_threads = std::getenv("FRAQ_K6_T1024") ? 1024 : 512;  // experiment switch
     if (smem > 48 * 1024) {
@@ -1022,6 +1081,12 @@ void PhysStepper::step(long n_steps, std::vector<cudaEvent_t>* ev) {
 }
 
 void PhysStepper::time_split(long n_steps, double* ms_hist, double* ms_solve) {
+    DevBuf<long long> prof;
+    if (std::getenv("FRAQ_K6_PROFILE")) {  // experiment: K6 phase cycles (block 0)
+        prof.alloc(8);
+        FRAQ_CUDA(cudaMemset(prof.p, 0, 8 * sizeof(long long)));
+        sa.prof = prof.p;
+    }
     std::vector<cudaEvent_t> ev;
     try {
         step(n_steps, &ev);
@@ -1036,6 +1101,15 @@ void PhysStepper::time_split(long n_steps, double* ms_hist, double* ms_solve) {
         }
         *ms_hist = h;
         *ms_solve = s;
+        if (prof.p) {
+            long long v[8];
+            FRAQ_CUDA(cudaMemcpy(v, prof.p, sizeof(v), cudaMemcpyDeviceToHost));
+            std::fprintf(stderr, "K6 phases (cycles per level): rhs %.0f solve %.0f refine %.0f "
+                         "store %.0f\n", double(v[1] - v[0]) / n_steps,
+                         double(v[2] - v[1]) / n_steps, double(v[3] - v[2]) / n_steps,
+                         double(v[4] - v[3]) / n_steps);
+            sa.prof = nullptr;
+        }
     } catch (...) {
         for (auto e : ev) cudaEventDestroy(e);
         throw;
@@ -1186,7 +1260,7 @@ void block_create(fraq_ctx c, double d01, double d02, double a, double tau, int 
                   double lead, BlockDev** out) {
     if (m < 1) fail(FRAQ_EINVAL, "BlockSystem: grid_m must be >= 1");
     if (!(tau > 0.0) || !(h > 0.0)) fail(FRAQ_EINVAL, "BlockSystem: tau and h must be > 0");
-    if (2 * sizeof(double2) * (m + 2) > 227 * 1024)
+    if (2 * sizeof(double2) * rows_len(m) > 227 * 1024)
         fail(FRAQ_EINVAL, "BlockSystem: grid_m too large for the on-chip block solve");
     auto* b = new BlockDev();
     try {
@@ -1221,7 +1295,7 @@ void block_solve(BlockDev* b, const double* rhs1, const double* rhs2, double* g1
                  int mem) {
     fraq_ctx c = b->c;
     const int m = b->m;
-    const size_t smem = 2 * sizeof(double2) * (m + 2);
+    const size_t smem = 2 * sizeof(double2) * rows_len(m);
     if (smem > 48 * 1024)
         FRAQ_CUDA(cudaFuncSetAttribute(block_solve_kernel<512>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
