@@ -246,11 +246,14 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
 
 constexpr int ST_M = 64, ST_N = 64, ST_K = 16;
 
+// CTA tile 64 (k) x 64 (c), 4 warps of 32 x 32, K tile 16.  The next K tile's operands (8 sine
+// gathers + 8 input loads per thread) are fetched into registers while the tensor pipe works on
+// the current one, and land in shared memory behind a single barrier per K tile.
 __global__ void __launch_bounds__(128) dst_kernel(const double* __restrict__ sintab, int M,
                                                   const double* __restrict__ In, long ldi,
                                                   long C, double* Out, long ldo, double scale) {
-    __shared__ double sA[ST_M][ST_K + 1];
-    __shared__ double sB[ST_K][ST_N + 1];
+    __shared__ double sA[2][ST_M][ST_K + 1];
+    __shared__ double sB[2][ST_K][ST_N + 1];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const long k0 = (long)blockIdx.y * ST_M, c0 = (long)blockIdx.x * ST_N;
     const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
@@ -258,42 +261,65 @@ __global__ void __launch_bounds__(128) dst_kernel(const double* __restrict__ sin
     const long period = 2L * (M + 1);
     const unsigned pmask = (period & (period - 1)) == 0 ? (unsigned)period - 1u : 0u;
     const bool small = M < 46340;  // (k+1)(j+1) fits 32 bits
+    constexpr int PA = ST_M * ST_K / 128, PB = ST_K * ST_N / 128;  // 8 + 8 per thread
+    double ra[PA], rb[PB];
+    auto fetch = [&](long j0) {
+#pragma unroll
+        for (int q = 0; q < PA; ++q) {
+            const int idx = tid + 128 * q, r = idx / ST_K, cc = idx % ST_K;
+            const long k = k0 + r, j = j0 + cc;
+            const long kj = (k + 1) * (j + 1);
+            const long ix = small ? (long)(pmask ? ((unsigned)kj & pmask)
+                                                 : (unsigned)kj % (unsigned)period)
+                                  : kj % period;
+            ra[q] = (k < M && j < M) ? __ldg(sintab + ix) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < PB; ++q) {
+            const int idx = tid + 128 * q, r = idx / ST_N, cc = idx % ST_N;
+            const long j = j0 + r, c = c0 + cc;
+            rb[q] = (j < M && c < C) ? __ldg(In + j * ldi + c) : 0.0;
+        }
+    };
+    auto put = [&](int buf) {
+#pragma unroll
+        for (int q = 0; q < PA; ++q) {
+            const int idx = tid + 128 * q;
+            sA[buf][idx / ST_K][idx % ST_K] = ra[q];
+        }
+#pragma unroll
+        for (int q = 0; q < PB; ++q) {
+            const int idx = tid + 128 * q;
+            sB[buf][idx / ST_N][idx % ST_N] = rb[q];
+        }
+    };
     double acc[4][4][2];
 #pragma unroll
     for (int x = 0; x < 4; ++x)
 #pragma unroll
         for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    fetch(0);
+    put(0);
+    __syncthreads();
+    int buf = 0;
     for (long j0 = 0; j0 < M; j0 += ST_K) {
-        __syncthreads();
-        for (int idx = tid; idx < ST_M * ST_K; idx += 128) {
-            const int r = idx / ST_K, cc = idx % ST_K;
-            const long k = k0 + r, j = j0 + cc;
-            // (k+1)(j+1) < 2^31 for every grid this path takes (M < 46340); the period
-            // 2(M+1) is a power of two on the BASELINE grids (mask instead of a division)
-            const long kj = (k + 1) * (j + 1);
-            const long ix = small ? (long)(pmask ? ((unsigned)kj & pmask)
-                                                 : (unsigned)kj % (unsigned)period)
-                                  : kj % period;
-            sA[r][cc] = (k < M && j < M) ? sintab[ix] : 0.0;
-        }
-        for (int idx = tid; idx < ST_K * ST_N; idx += 128) {
-            const int r = idx / ST_N, cc = idx % ST_N;
-            const long j = j0 + r, c = c0 + cc;
-            sB[r][cc] = (j < M && c < C) ? In[j * ldi + c] : 0.0;
-        }
-        __syncthreads();
+        const bool more = j0 + ST_K < M;
+        if (more) fetch(j0 + ST_K);  // in flight during this tile's DMMAs
 #pragma unroll
         for (int kk = 0; kk < ST_K; kk += 4) {
             double af[4], bf[4];
 #pragma unroll
-            for (int x = 0; x < 4; ++x) af[x] = sA[wm + 8 * x + g][kk + t];
+            for (int x = 0; x < 4; ++x) af[x] = sA[buf][wm + 8 * x + g][kk + t];
 #pragma unroll
-            for (int y = 0; y < 4; ++y) bf[y] = sB[kk + t][wn + 8 * y + g];
+            for (int y = 0; y < 4; ++y) bf[y] = sB[buf][kk + t][wn + 8 * y + g];
 #pragma unroll
             for (int x = 0; x < 4; ++x)
 #pragma unroll
                 for (int y = 0; y < 4; ++y) dmma884(acc[x][y], af[x], bf[y]);
         }
+        if (more) put(buf ^ 1);  // the other buffer: last read one tile ago, behind a barrier
+        __syncthreads();
+        buf ^= 1;
     }
 #pragma unroll
     for (int x = 0; x < 4; ++x)
