@@ -366,6 +366,7 @@ __global__ void __launch_bounds__(256) dst_skinny_kernel(const double* __restric
     for (int c = 0; c < CT; ++c) acc[c] = 0.0;
     // idx = (k+1)(j+1) mod period, advanced by k+1 per j
     int idx = (int)(((long)kk * (j0 + 1)) % period);
+#pragma unroll 4
     for (int j = j0; j < j1; ++j) {
         const double sv = tab[idx];
         const double* x = In + (long)j * ldi;

@@ -207,14 +207,31 @@ struct ChainJob {
     long n_max;
     double* out;
 };
+// One CTA per chain: the ratios q_i = (i-1-g)/i do not depend on the chain, so the CTA computes
+// them in parallel into the output first (an fp64 division is a ~40-instruction sequence; inside
+// the serial loop it set the pace), then one thread runs the product c_i = (c_(i-1) q_i) x in the
+// reference's order -- bitwise the reference's chain (cq_weights.cpp:19-25).
 __global__ void chain_kernel(const ChainJob* jobs, int n_jobs) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n_jobs) return;
-    const ChainJob J = jobs[t];
+    const ChainJob J = jobs[blockIdx.x];
+    for (long i = 1 + threadIdx.x; i <= J.n_max; i += blockDim.x) J.out[i] = (i - 1 - J.g) / i;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
     double c = 1.0;
     J.out[0] = c;
-    for (long i = 1; i <= J.n_max; ++i) {
-        c = c * ((i - 1 - J.g) / i) * J.x;
+    // batches of 16 ratios in registers: the loads of a batch are in flight together
+    long i = 1;
+    for (; i + 15 <= J.n_max; i += 16) {
+        double q[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) q[t] = J.out[i + t];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+            c = c * q[t] * J.x;
+            J.out[i + t] = c;
+        }
+    }
+    for (; i <= J.n_max; ++i) {
+        c = c * J.out[i] * J.x;
         J.out[i] = c;
     }
 }
@@ -402,7 +419,12 @@ void run_rules(fraq_ctx c, const std::vector<RuleJob>& jobs) {
 void run_scans(fraq_ctx c, const std::vector<ScanJob>& jobs) {
     if (jobs.empty()) return;
     DevBuf<ScanJob> dj = upload(c, jobs);
-    scan_kernel<<<(unsigned)jobs.size(), kScanThreads, 0, c->stream>>>(dj.p);
+    // one node per thread; with J <= 256 the upper 256 threads would only add zeros (dropping
+    // them leaves every sum bitwise the same and halves the cross-warp pass)
+    int maxJ = 0;
+    for (const ScanJob& j : jobs) maxJ = std::max(maxJ, j.J);
+    const int threads = maxJ <= 256 ? 256 : kScanThreads;
+    scan_kernel<<<(unsigned)jobs.size(), threads, 0, c->stream>>>(dj.p);
     FRAQ_LAUNCH_CHECK();
     FRAQ_CUDA(cudaStreamSynchronize(c->stream));
 }
@@ -416,7 +438,7 @@ void weights_batch(fraq_ctx c, bool sbd, const std::vector<double>& gs, double t
         std::vector<ChainJob> cj(B);
         for (int t = 0; t < B; ++t) cj[t] = {gs[t], 1.0, n_max, base + t * L};
         DevBuf<ChainJob> d = upload(c, cj);
-        chain_kernel<<<(B + 127) / 128, 128, 0, c->stream>>>(d.p, B);
+        chain_kernel<<<B, 256, 0, c->stream>>>(d.p, B);
         FRAQ_LAUNCH_CHECK();
         std::vector<double> sc(B);
         for (int t = 0; t < B; ++t) sc[t] = std::pow(tau, -gs[t]);
@@ -434,7 +456,7 @@ void weights_batch(fraq_ctx c, bool sbd, const std::vector<double>& gs, double t
         cj[2 * t + 1] = {gs[t], 1.0 / 3.0, n_max, cs.p + (size_t)(2 * t + 1) * L};
     }
     DevBuf<ChainJob> d = upload(c, cj);
-    chain_kernel<<<(2 * B + 127) / 128, 128, 0, c->stream>>>(d.p, 2 * B);
+    chain_kernel<<<2 * B, 256, 0, c->stream>>>(d.p, 2 * B);
     FRAQ_LAUNCH_CHECK();
     std::vector<CauchyJob> qj(B);
     for (int t = 0; t < B; ++t)
