@@ -57,6 +57,9 @@ def dist_env():
 
 # ----------------------------------------------------------------------------- clocks sampling
 class Clocks:
+    """nvidia-smi samples (SM clock, throttle reasons) during a timed region.  The sampler is
+    started and its first line awaited before the region begins, and it polls every 50 ms, so
+    even a ~100 ms region (C2: 20 steps x 5 ms) gets samples; the pre-region line is dropped."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
@@ -64,13 +67,18 @@ class Clocks:
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.proc = None
+        self.out = ""
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import select
+            ready, _, _ = select.select([self.proc.stdout], [], [], 5.0)
+            if ready:
+                self.proc.stdout.readline()  # sampler is up; this line predates the region
         except Exception:
             self.proc = None
         return self
