@@ -329,7 +329,7 @@ def main():
     B = 0.5 * sum(8 * (2 * nn + 2) for nn in n_nodes)
     pk = peaks()
     try:  # DRAM traffic per K5d launch from the committed ncu --set full capture (profiles/)
-        tr = json.load(open(os.path.join(ROOT, "profiles", "r01b_traffic.json")))
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r02", "k5d_traffic.json")))
         assert tr["levels_per_launch"] == LEVELS_PER_STEP
         traffic = tr["dram_bytes_per_launch"] / 1e9  # GB per launch (one step)
     except Exception:
