@@ -66,6 +66,29 @@ def test_fast_stepper_equals_run_physical(fraq, sbd):
     assert st.kernel_eps1() == rr.kernel_eps1 and st.kernel_eps2() == rr.kernel_eps2
 
 
+@pytest.mark.parametrize("sbd", [False, True])
+def test_graph_replays_equal_single_steps(fraq, sbd):
+    """run() steps the physical scheme through the 64-level CUDA graph (K5 of level n+1 on a side
+    stream overlapping K6 of level n, device level counter); single steps launch eagerly.  Both
+    must give the same bits, including the eager remainder after the last whole graph chunk."""
+    N = 64 * 3 + 13
+    spec = spec_of(fraq, 0.45, 0.65, 1.3, 127, 0.3, N, "indicator")
+    st = fraq.FastStepper(spec, sbd, kc_of(fraq))
+    for n in range(N):
+        st.step()
+    rr = fraq.run(spec, fraq.Scheme.FastSBD if sbd else fraq.Scheme.FastBE,
+                  kc_of(fraq, fraq.SOLVER_PHYSICAL))
+    assert np.array_equal(st.state().g1, rr.final_state.g1)
+    assert np.array_equal(st.state().g2, rr.final_state.g2)
+    # a stepper that mixes both: graph chunks inside step_n, eager steps around them
+    st2 = fraq.FastStepper(spec, sbd, kc_of(fraq))
+    st2.step()
+    st2.step_n(150)
+    st2.step_n(N - 151)
+    assert np.array_equal(st2.state().g1, rr.final_state.g1)
+    assert np.array_equal(st2.state().g2, rr.final_state.g2)
+
+
 @pytest.mark.parametrize("scheme", SCHEMES)
 def test_stepper_trajectory_matches_reference(fraq, orc, scheme):
     """State after every k steps vs the reference's run() to level k (fixed-size kernels, so the
