@@ -648,6 +648,17 @@ void corr_sequence_batch_dev(fraq_ctx c, const fraq_kernel_t* ks, int n, long e_
 // up to max_points until eps <= eps_tol tau^-g; SBD then grows the head by x1.5 while the argmax
 // of the error lies below 8 head0.  All exponents of the batch advance together; each round is
 // one rule launch + one scan launch over the still-active exponents.
+// chosen ladder rung of exponent t -> its table slot (1024 doubles of m and of r)
+__global__ void gather_tables_kernel(const double* lm, const double* lr, const long* pick,
+                                     double* mt, double* rt) {
+    const double* m = lm + (size_t)pick[blockIdx.x] * 1024;
+    const double* r = lr + (size_t)pick[blockIdx.x] * 1024;
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
+        mt[(size_t)blockIdx.x * 1024 + i] = m[i];
+        rt[(size_t)blockIdx.x * 1024 + i] = r[i];
+    }
+}
+
 void build_kernel_auto_dev(fraq_ctx c, bool sbd, int n, const double* gammas, double tau,
                            fraq_budget_t* budgets, fraq_kernel_t* out) {
     if (n <= 0) return;
@@ -683,23 +694,6 @@ void build_kernel_auto_dev(fraq_ctx c, bool sbd, int n, const double* gammas, do
     DevBuf<long> am((size_t)n);
     std::vector<double> hmx(n);
     std::vector<long> ham(n);
-    auto build_round = [&](const std::vector<int>& which) {
-        std::vector<RuleJob> rj;
-        for (int t : which) {
-            const int p = std::min(np[t], budgets[t].max_points);
-            np[t] = p;
-            check_rule_args(gammas[t], sbd ? 2.0 - 2.0 * gammas[t] : 1.0 - gammas[t], p);
-            double* m = mt.p + (size_t)t * 1024;
-            double* r = rt.p + (size_t)t * 1024;
-            if (sbd)
-                rj.push_back({gammas[t], 2.0 - 2.0 * gammas[t], p, 4, gammas[t], tau, r, m, r + p,
-                              m + p});
-            else
-                rj.push_back({gammas[t], 1.0 - gammas[t], p, 1, gammas[t], tau, r, m, nullptr,
-                              nullptr});
-        }
-        run_rules(c, rj);
-    };
     auto scan_round = [&](const std::vector<int>& which, const std::vector<long>& from) {
         std::vector<ScanJob> sj;
         for (size_t q = 0; q < which.size(); ++q) {
@@ -713,24 +707,66 @@ void build_kernel_auto_dev(fraq_ctx c, bool sbd, int n, const double* gammas, do
         FRAQ_CUDA(cudaMemcpy(hmx.data(), mx.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
         FRAQ_CUDA(cudaMemcpy(ham.data(), am.p, sizeof(long) * n, cudaMemcpyDeviceToHost));
     };
-    // phase 1: point counts
-    for (;;) {
-        std::vector<int> act;
-        for (int t = 0; t < n; ++t)
-            if (!done[t]) act.push_back(t);
-        if (act.empty()) break;
-        build_round(act);
-        std::vector<long> from;
-        for (int t : act)
-            from.push_back(sbd ? std::min<long>(budgets[t].horizon, 8L * head[t]) : 2L);
-        scan_round(act, from);
-        for (int t : act) {
-            if (!sbd) budgets[t].achieved_eps = hmx[t];
-            if (hmx[t] <= tol[t] || np[t] >= budgets[t].max_points)
-                done[t] = 1;
-            else
-                np[t] = np[t] + np[t] / 2;
+    // phase 1: point counts.  The reference grows N_p by x1.5 from 64 (BE) / 41 (SBD) up to the
+    // cap, stopping at the first size whose eps meets the tolerance (fast_kernel.cpp:182-235).
+    // Every size on that ladder is independent of the others (its own rule, its own scan from
+    // the same start index), so all of them are evaluated at once -- one rule launch and one
+    // scan launch instead of one round per size -- and the first passing size is picked on the
+    // host: the same decisions and tables, bitwise, at the latency of a single round.
+    struct Rung {
+        int t, p;
+    };
+    std::vector<Rung> rungs;
+    std::vector<int> first_rung(n);
+    for (int t = 0; t < n; ++t) {
+        first_rung[t] = (int)rungs.size();
+        int p = np[t];
+        for (;;) {
+            p = std::min(p, budgets[t].max_points);
+            check_rule_args(gammas[t], sbd ? 2.0 - 2.0 * gammas[t] : 1.0 - gammas[t], p);
+            rungs.push_back({t, p});
+            if (p >= budgets[t].max_points) break;
+            p = p + p / 2;
         }
+    }
+    const size_t R = rungs.size();
+    DevBuf<double> lm(R * 1024), lr(R * 1024), lmx(R);
+    DevBuf<long> lam(R);
+    {
+        std::vector<RuleJob> rj;
+        std::vector<ScanJob> sj;
+        for (size_t q = 0; q < R; ++q) {
+            const int t = rungs[q].t, p = rungs[q].p;
+            double* m = lm.p + q * 1024;
+            double* r = lr.p + q * 1024;
+            if (sbd)
+                rj.push_back({gammas[t], 2.0 - 2.0 * gammas[t], p, 4, gammas[t], tau, r, m, r + p,
+                              m + p});
+            else
+                rj.push_back({gammas[t], 1.0 - gammas[t], p, 1, gammas[t], tau, r, m, nullptr,
+                              nullptr});
+            const long from = sbd ? std::min<long>(budgets[t].horizon, 8L * head[t]) : 2L;
+            sj.push_back({sbd ? 2 * p : p, m, r, sbd ? 1 : 0, from, budgets[t].horizon,
+                          tables.p + (size_t)t * L, nullptr, lmx.p + q, lam.p + q});
+        }
+        run_rules(c, rj);
+        run_scans(c, sj);
+    }
+    std::vector<double> rmx(R);
+    FRAQ_CUDA(cudaMemcpy(rmx.data(), lmx.p, sizeof(double) * R, cudaMemcpyDeviceToHost));
+    std::vector<long> pick(n);
+    for (int t = 0; t < n; ++t) {
+        size_t q = first_rung[t];
+        while (q + 1 < R && rungs[q + 1].t == t && !(rmx[q] <= tol[t])) ++q;
+        pick[t] = (long)q;
+        np[t] = rungs[q].p;
+        if (!sbd) budgets[t].achieved_eps = rmx[q];
+    }
+    {
+        DevBuf<long> dpick = upload(c, pick);
+        gather_tables_kernel<<<n, 256, 0, c->stream>>>(lm.p, lr.p, dpick.p, mt.p, rt.p);
+        FRAQ_LAUNCH_CHECK();
+        FRAQ_CUDA(cudaStreamSynchronize(c->stream));
     }
     if (sbd) {
         // phase 2: head growth on the final node tables
