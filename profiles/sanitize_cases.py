@@ -10,7 +10,9 @@ kernel's shape range, and the same script runs under the sanitizer where it is a
 Cases: setup (K1-K4, K7 auto sizing), k5 (per-level history, both variants), k5d (blocked,
 TMA-staged), k5c (head window > 32 levels), k10 (direct CQ), host (chunked host-buffer run),
 k13 (modal BE/SBD, two-CTA shape), k13w (wide CTA, J > 256), k11 (modal fallback), k6 (physical
-stepper), dst2d (2D DST + K13).
+stepper), dst2d (2D DST + K13); round 2: graph (the physical stepper's 64-level CUDA graph, K5 and
+K6 on two streams), blocks (BlockSystem CR + Thomas + refinement, BandedLU, Laplacian), dsts
+(the skinny DST K12s against the tile DST K12).
 """
 import os
 import sys
@@ -157,6 +159,55 @@ def case_dst2d():
     g2 = rng.uniform(0, 1, m * m)
     out = fraq.run_2d(0.3, 0.6, -3.0, m, 0.25, 12, fraq.Scheme.FastSBD, g1, g2)
     assert np.all(np.isfinite(out.final_state.g1))
+
+
+def case_graph():
+    # 2 graph replays + an eager remainder (odd grid: Thomas-free CR grid 63; and 21: Thomas)
+    for m in (63, 21):
+        spec = fraq.ProblemSpec(alpha1=0.35, alpha2=0.7, coupling_a=-1.5, grid_m=m,
+                                t_final=0.3, n_steps=141)
+        kc = fraq.KernelConfig()
+        kc.solver = fraq.SOLVER_PHYSICAL
+        for sch, sbd in ((fraq.Scheme.FastBE, False), (fraq.Scheme.FastSBD, True)):
+            rr = fraq.run(spec, sch, kc)
+            st = fraq.FastStepper(spec, sbd, fraq.KernelConfig())
+            for _ in range(141):
+                st.step()
+            assert np.array_equal(st.state().g1, rr.final_state.g1)
+
+
+def case_blocks():
+    for m in (1, 3, 7, 20, 63):
+        lap = fraq.DiscreteLaplacian(m, 1.0)
+        rng = np.random.default_rng(m)
+        x1, x2 = rng.uniform(-1, 1, m), rng.uniform(-1, 1, m)
+        ax1, ax2 = np.array(lap.apply(list(x1))), np.array(lap.apply(list(x2)))
+        d01, d02, a, tau, lead = 1.7, 0.4, -1.3, 0.02, 1.5
+        r1 = lead / tau * x1 + d01 * (a * x1 + ax1) - a * d02 * x2
+        r2 = lead / tau * x2 + d02 * (a * x2 + ax2) - a * d01 * x1
+        y1, y2 = fraq.BlockSystem(d01, d02, a, tau, lap, lead).solve(list(r1), list(r2))
+        assert rel(y1, x1) < 1e-12 and rel(y2, x2) < 1e-12
+    lu = fraq.BandedLU(5, 1, 2)
+    for i in range(5):
+        lu.set(i, i, 3.0)
+        if i + 1 < 5:
+            lu.set(i, i + 1, 1.0)
+            lu.set(i + 1, i, -1.0)
+    lu.factorize()
+    assert np.all(np.isfinite(lu.solve([1.0] * 5)))
+
+
+def case_dsts():
+    import torch
+    for M, C in ((7, 1), (31, 2), (63, 8), (63, 9)):
+        x = torch.randn(M, C, dtype=torch.float64, device="cuda")
+        y = torch.empty_like(x)
+        torch.cuda.synchronize()
+        fraq.dst_cols_device(M, C, x.data_ptr(), y.data_ptr(), False)
+        k = torch.arange(1, M + 1, dtype=torch.float64, device="cuda")
+        S = torch.sin(torch.outer(k, k) * torch.pi / (M + 1))
+        ref = (2.0 / (M + 1)) * S @ x
+        assert float((y - ref).abs().max() / ref.abs().max()) < 1e-13
 
 
 CASES = {n[5:]: f for n, f in globals().items() if n.startswith("case_")}
