@@ -280,6 +280,31 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 320 && RB == 2) ? 2 : 1) k13_ke
             const double p11 = -fma(al, M22, a * M12), p12 = fma(a, M22, al * M12);
             const double p21 = fma(a, M11, al * M21), p22 = -fma(al, M11, a * M21);
             const double q11 = itau * M22, q12 = -itau * M12, q21 = -itau * M21, q22 = itau * M11;
+            // the full-block solve as a two-operation chain: x(k) = z(k) + A1 x(k-1), where
+            // A1 = P C(1) + lq Q carries everything level k-1 feeds into level k (lq = 1 BE,
+            // 2 SBD), and the older levels enter z off the chain through B_m = P C(m)
+            // (m >= 2; SBD: B_2 -= Q/2), C(m) = diag(c1_m, c2_m) the in-block weights
+            // (BE in the 192-thread shape -- C3, C5-BE: +6.6% / +3.1%; the SBD chain carries more
+            // terms and lost 3% in the wide CTA, and the 96-register shapes would spill)
+            constexpr bool kChain2 = NT == 16 && MAXT == 192;
+            double chA[4], chB[8][4];
+            if (kChain2) {
+                const double lq = A.sbd ? 2.0 : 1.0;
+                const double c11 = cwt[0][1], c21 = cwt[1][1];
+                chA[0] = fma(p11, c11, lq * q11);
+                chA[1] = fma(p12, c21, lq * q12);
+                chA[2] = fma(p21, c11, lq * q21);
+                chA[3] = fma(p22, c21, lq * q22);
+#pragma unroll
+                for (int m = 2; m < 8; ++m) {
+                    const double c1m = cwt[0][m], c2m = cwt[1][m];
+                    const double sq = (A.sbd && m == 2) ? -0.5 : 0.0;
+                    chB[m][0] = fma(sq, q11, p11 * c1m);
+                    chB[m][1] = fma(sq, q12, p12 * c2m);
+                    chB[m][2] = fma(sq, q21, p21 * c1m);
+                    chB[m][3] = fma(sq, q22, p22 * c2m);
+                }
+            }
             const double g10 = g0s[d], g20 = g0s[MODES + d];
             double gp1 = g10, gp2 = g20, gpp1 = 0.0, gpp2 = 0.0;
             const double* c1 = cwt[0];  // in-block weights c_1..c_7 (shared memory, broadcast)
@@ -359,6 +384,51 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 320 && RB == 2) ? 2 : 1) k13_ke
                             acc2[k] = sA[(8 + k) * MODES + d];
                         }
                         if (kmax == 8 && !(A.sbd && n0 == 1)) {
+                            // full block, no predicates: z(k) = P acc(k) (+ the l terms reaching
+                            // back into the previous block), then the chain x(k) = z(k) +
+                            // A1 x(k-1) -- two dependent fp64 operations per level instead of four
+                            // -- with the older levels folded into z(k2 >= k+2) off the chain
+                            auto full_block_chain2 = [&](auto sbd_c) {
+                                constexpr bool SBD = decltype(sbd_c)::value;
+                                double z1[8], z2[8];
+#pragma unroll
+                                for (int k = 0; k < 8; ++k) {
+                                    z1[k] = fma(p11, acc1[k], p12 * acc2[k]);
+                                    z2[k] = fma(p21, acc1[k], p22 * acc2[k]);
+                                }
+                                if constexpr (SBD) {
+                                    const double t1 = fma(2.0, gp1, -0.5 * gpp1),
+                                                 t2 = fma(2.0, gp2, -0.5 * gpp2);
+                                    z1[0] = fma(q11, t1, fma(q12, t2, z1[0]));
+                                    z2[0] = fma(q21, t1, fma(q22, t2, z2[0]));
+                                    z1[1] = fma(-0.5 * q11, gp1, fma(-0.5 * q12, gp2, z1[1]));
+                                    z2[1] = fma(-0.5 * q21, gp1, fma(-0.5 * q22, gp2, z2[1]));
+                                } else {
+                                    z1[0] = fma(q11, gp1, fma(q12, gp2, z1[0]));
+                                    z2[0] = fma(q21, gp1, fma(q22, gp2, z2[0]));
+                                }
+                                double x1 = z1[0], x2 = z2[0];
+#pragma unroll
+                                for (int k = 0; k < 8; ++k) {
+                                    if (k > 0) {
+                                        const double y1 = fma(chA[0], x1, fma(chA[1], x2, z1[k]));
+                                        const double y2 = fma(chA[2], x1, fma(chA[3], x2, z2[k]));
+                                        gpp1 = x1;
+                                        gpp2 = x2;
+                                        x1 = y1;
+                                        x2 = y2;
+                                    }
+                                    ring[((n0 + k) & mask) * MODES + d] = x1;
+                                    ring[(RING + ((n0 + k) & mask)) * MODES + d] = x2;
+#pragma unroll
+                                    for (int k2 = k + 2; k2 < 8; ++k2) {
+                                        z1[k2] = fma(chB[k2 - k][0], x1, fma(chB[k2 - k][1], x2, z1[k2]));
+                                        z2[k2] = fma(chB[k2 - k][2], x1, fma(chB[k2 - k][3], x2, z2[k2]));
+                                    }
+                                }
+                                gp1 = x1;
+                                gp2 = x2;
+                            };
                             // full block, no predicates: x = P acc + (l terms of earlier levels),
                             // coefficients folded per task (8 fp64 ops per level for BE, 12 SBD)
                             auto full_block = [&](auto sbd_c) {
@@ -392,6 +462,8 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 320 && RB == 2) ? 2 : 1) k13_ke
                             };
                             if (A.sbd)
                                 full_block(std::true_type{});
+                            else if constexpr (kChain2)
+                                full_block_chain2(std::false_type{});
                             else
                                 full_block(std::false_type{});
                         } else {
