@@ -113,15 +113,15 @@ static void ld_solve2(LD a11, LD a12, LD a21, LD a22, LD r1, LD r2, LD* x1, LD* 
     *x2 = (a11 * r2 - a21 * r1) / det;
 }
 
+static int anchor_steps(const fo_kernel* k1, const fo_kernel* k2, LD a, LD tau, long N, long nm,
+                        const LD* lam, const LD* u0, const LD* v0, double* uN, double* vN);
+
 int fo_anchor_ld(const fo_kernel* k1, const fo_kernel* k2, double a_, double tau_, long N, int M,
                  long nm, const int* modes, const double* g1, const double* g2, double* uN,
                  double* vN) {
     if (N < 1 || nm < 1 || M < 1 || k1->sbd != k2->sbd) return FO_EINVAL;
-    const int sbd = k1->sbd;
-    const LD a = a_, tau = tau_, pi = acosl(-1.0L), Mp1 = (LD)(M + 1);
+    const LD pi = acosl(-1.0L), Mp1 = (LD)(M + 1);
     LD *lam = malloc(sizeof(LD) * nm), *u0 = malloc(sizeof(LD) * nm), *v0 = malloc(sizeof(LD) * nm);
-    LD *s1 = malloc(sizeof(LD) * nm), *s2 = malloc(sizeof(LD) * nm);
-    LD *x1 = malloc(sizeof(LD) * nm), *x2 = malloc(sizeof(LD) * nm);
     for (long q = 0; q < nm; ++q) {
         const int k = modes[q];
         const LD s = sinl((LD)k * pi / (2.0L * Mp1));
@@ -135,6 +135,38 @@ int fo_anchor_ld(const fo_kernel* k1, const fo_kernel* k2, double a_, double tau
         u0[q] = 2.0L / Mp1 * c1;
         v0[q] = 2.0L / Mp1 * c2;
     }
+    const int st = anchor_steps(k1, k2, a_, tau_, N, nm, lam, u0, v0, uN, vN);
+    free(lam);
+    free(u0);
+    free(v0);
+    return st;
+}
+
+/* The same stepping for caller-given modes: eigenvalues lam (e.g. lambda_k + lambda_l of the 2D
+ * five-point stencil) and initial coefficients u0 / v0, each given as a (hi, lo) pair of doubles
+ * (value = hi + lo, so an extended-precision projection passes through unrounded). */
+int fo_anchor_modes_ld(const fo_kernel* k1, const fo_kernel* k2, double a_, double tau_, long N,
+                       long nm, const double* lam2, const double* u02, const double* v02,
+                       double* uN, double* vN) {
+    if (N < 1 || nm < 1 || k1->sbd != k2->sbd) return FO_EINVAL;
+    LD *lam = malloc(sizeof(LD) * nm), *u0 = malloc(sizeof(LD) * nm), *v0 = malloc(sizeof(LD) * nm);
+    for (long q = 0; q < nm; ++q) {
+        lam[q] = (LD)lam2[2 * q] + (LD)lam2[2 * q + 1];
+        u0[q] = (LD)u02[2 * q] + (LD)u02[2 * q + 1];
+        v0[q] = (LD)v02[2 * q] + (LD)v02[2 * q + 1];
+    }
+    const int st = anchor_steps(k1, k2, a_, tau_, N, nm, lam, u0, v0, uN, vN);
+    free(lam);
+    free(u0);
+    free(v0);
+    return st;
+}
+
+static int anchor_steps(const fo_kernel* k1, const fo_kernel* k2, LD a, LD tau, long N, long nm,
+                        const LD* lam, const LD* u0, const LD* v0, double* uN, double* vN) {
+    const int sbd = k1->sbd;
+    LD *s1 = malloc(sizeof(LD) * nm), *s2 = malloc(sizeof(LD) * nm);
+    LD *x1 = malloc(sizeof(LD) * nm), *x2 = malloc(sizeof(LD) * nm);
     ld_hist h1, h2;
     int st = ld_init(&h1, k1, nm);
     if (!st) st = ld_init(&h2, k2, nm);
@@ -207,9 +239,6 @@ int fo_anchor_ld(const fo_kernel* k1, const fo_kernel* k2, double a_, double tau
         }
     ld_free(&h1);
     ld_free(&h2);
-    free(lam);
-    free(u0);
-    free(v0);
     free(s1);
     free(s2);
     free(x1);

@@ -141,5 +141,8 @@ int fo_modal_run(const fo_kernel* k1, const fo_kernel* k2, double a, double tau,
 int fo_anchor_ld(const fo_kernel* k1, const fo_kernel* k2, double a, double tau, long N, int M,
                  long nm, const int* modes, const double* g1, const double* g2, double* uN,
                  double* vN);
+int fo_anchor_modes_ld(const fo_kernel* k1, const fo_kernel* k2, double a, double tau, long N,
+                       long nm, const double* lam2, const double* u02, const double* v02,
+                       double* uN, double* vN);
 
 #endif

@@ -417,6 +417,25 @@ class Oracle:
                "anchor_ld")
         return uN, vN
 
+    def anchor_modes_ld(self, k1: Kernel, k2: Kernel, a: float, tau: float, N: int, lam, u0, v0):
+        """anchor_ld for caller-given modes: lam, u0, v0 as numpy longdouble (or float) arrays,
+        passed through unrounded as (hi, lo) double pairs.  Returns (uN, vN)."""
+        lib = self.lib if self.kind == "port" else C.CDLL(PORT_SO)
+
+        def split(x):
+            x = np.asarray(x, dtype=np.longdouble)
+            hi = x.astype(np.float64)
+            lo = (x - hi.astype(np.longdouble)).astype(np.float64)
+            return np.ascontiguousarray(np.stack([hi, lo], axis=1).ravel())
+        L2, U2, V2 = split(lam), split(u0), split(v0)
+        nm = len(L2) // 2
+        uN, vN = np.zeros(nm), np.zeros(nm)
+        f1, f2 = _to_fo(k1), _to_fo(k2)
+        _raise(lib.fo_anchor_modes_ld(C.byref(f1), C.byref(f2), C.c_double(a), C.c_double(tau),
+                                      C.c_long(N), C.c_long(nm), _p(L2), _p(U2), _p(V2), _p(uN),
+                                      _p(vN)), "anchor_modes_ld")
+        return uN, vN
+
     def hist_trace(self, kernels, U: np.ndarray, stride: int, threads: int):
         """Reference histories (standalone) over U[n_steps, dofs] split evenly into
         len(kernels) groups, `threads` workers; returns D at levels stride-1, 2 stride-1, ...

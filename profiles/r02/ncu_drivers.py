@@ -85,3 +85,20 @@ def k6split(levels=1024):
 
 if __name__ == "__main__" and sys.argv[1] == "k6split":
     k6split()
+
+
+def c5batch(scheme="FastSBD", n_inst=37, N=4096):
+    """A C5-shaped K13 launch (instances of workloads.c5_instances, M = 4095)."""
+    from workloads import c5_instances as _c5
+    insts = _c5(n_inst)
+    specs = [fraq.ProblemSpec(alpha1=i.alpha1, alpha2=i.alpha2, coupling_a=i.coupling_a,
+                              grid_m=4095, t_final=N / 16384, n_steps=N, initial="custom",
+                              custom_g1=list(i.g1), custom_g2=list(i.g2)) for i in insts]
+    kc = fraq.KernelConfig()
+    kc.solver = fraq.SOLVER_MODAL
+    rs = fraq.run_batch(specs, getattr(fraq.Scheme, scheme), kc)
+    print("c5batch", scheme, rs[0].loop_seconds)
+
+
+if __name__ == "__main__" and sys.argv[1] == "c5batch":
+    c5batch(sys.argv[2] if len(sys.argv) > 2 else "FastSBD")

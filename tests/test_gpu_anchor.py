@@ -105,3 +105,43 @@ def test_full_horizon_anchor(fraq, oracles, scheme):
         for solver in ("b200_physical", "b200_modal"):
             assert r[solver] <= 1e-10, (key, solver, r)
             assert r[solver] < r["reference_physical"] or r["reference_physical"] < 1e-10, (key, r)
+
+
+def test_c4_full_horizon_anchor(fraq, oracles):
+    """C4 (2D, 1023^2, N = 8192, FastSBD; no reference capability -- the reference is 1D only):
+    the B200 result on 144 sampled (ky, kx) modes, extremes of lambda_ky + lambda_kx included,
+    against the extended-precision anchor (2D projection and eigenvalues in long double, mode
+    stepping in long double with the reference's node tables), to 1e-10 of the largest
+    coefficient."""
+    from workloads import c4_instance
+    ref, port = oracles
+    M2, N2 = 1023, 8192
+    inst = c4_instance(M2)
+    out = fraq.run_2d(inst.alpha1, inst.alpha2, inst.coupling_a, M2, 1.0, N2,
+                      fraq.Scheme.FastSBD, inst.g1, inst.g2)
+    dt = np.longdouble
+    pi = np.arccos(dt(-1))
+    ks = np.array([1, 2, 3, 5, 17, 100, 256, 511, 700, 900, 1022, 1023])
+    j = np.arange(1, M2 + 1, dtype=dt)
+    S = np.sin(np.outer(ks.astype(dt), j) * pi / (M2 + 1))
+    sc = (2 / dt(M2 + 1)) ** 2
+
+    def coef(g):
+        return (sc * (S @ np.asarray(g, dt).reshape(M2, M2) @ S.T)).ravel()  # [ky][kx]
+    lam1 = 4 * (M2 + 1) ** 2 * np.sin(ks.astype(dt) * pi / (2 * (M2 + 1))) ** 2
+    lam = (lam1[:, None] + lam1[None, :]).ravel()
+    tau = 1.0 / N2
+    k1 = ref.build_kernel_auto(True, 1 - inst.alpha1, tau, N2)
+    k2 = ref.build_kernel_auto(True, 1 - inst.alpha2, tau, N2)
+    u0, v0 = coef(inst.g1), coef(inst.g2)
+    uN, vN = port.anchor_modes_ld(k1, k2, inst.coupling_a, tau, N2, lam, u0, v0)
+    s = max(np.abs(uN).max(), np.abs(vN).max())
+    e1 = float(np.abs(coef(out.final_state.g1).astype(float) - uN).max() / s)
+    e2 = float(np.abs(coef(out.final_state.g2).astype(float) - vN).max() / s)
+    if os.environ.get("FRAQ_RECORD"):
+        os.makedirs("profiles/r02", exist_ok=True)
+        path = "profiles/r02/anchor_full_horizon.json"
+        old = json.load(open(path)) if os.path.exists(path) else {}
+        old["C4 FastSBD (2D, 144 modes)"] = {"b200_modal": max(e1, e2)}
+        json.dump(old, open(path, "w"), indent=1)
+    assert max(e1, e2) <= 1e-10, (e1, e2)
