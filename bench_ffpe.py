@@ -300,6 +300,23 @@ def run_gpu(args, rank, world, local, pg, METRIC, Clocks, fraq, torch):
                 "frac": achieved / peak, "peak_source": "measured DMMA stream (fraq_diag_dmma_peak)",
                 "flops_per_dof_step": Fm, "kernel": "k13_kernel (modal, DMMA)"}
     split = None
+    if wl.solver == "physical" and wl.name != "C3":
+        # C5 physical: the history pass of every instance is one HBM-bound K5 launch per level
+        # (state 256 inst x 2 fields x 4095 x N_nodes x 8 B read + written); the K6 solves of a
+        # level run beside the next level's K5 (CUDA graph), so the whole loop time is charged
+        # to K5 here -- a lower bound on its bandwidth
+        nodes = Fm / 4 - 1 if not sbd else (Fm - 2 * 17) / 4
+        B = 8 * (2 * nodes + 2)
+        gbs = B * dof_steps / loop_s / 1e9
+        try:
+            hbm = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                              "MEASURED_PEAKS.json")))["hbm_gbs"]
+        except Exception:
+            hbm = 6543.7
+        roofline = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
+                    "frac": gbs / hbm, "kernel": "step_kernel (K5, FFPE mode) + K6 overlapped",
+                    "bytes_per_dof_step": B, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                    "note": "whole loop time charged to K5 (lower bound)"}
     if wl.solver == "physical" and wl.name == "C3":
         # per-kernel split of the physical stepper (events around every launch, 1024 levels in
         # the middle of a run): K5 = one fused HBM pass over the history state per level,
