@@ -19,6 +19,8 @@
 // integer-indexed table), forward (x 2/(M+1)) and inverse.
 #include <cuda_runtime.h>
 
+#include <cstdio>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -605,12 +607,23 @@ struct ModalSetup {
 void modal_prepare(fraq_ctx c, ModalSetup& S, const std::vector<double>& gam,
                    const std::vector<double>& a, double tau, long N, bool sbd,
                    const fraq_kconf_t& kc) {
+    const bool trace = std::getenv("FRAQ_SETUP_TRACE") != nullptr;  // diagnostics
+    double tt = now_s2();
+    auto lap = [&](const char* what) {
+        if (!trace) return;
+        cudaStreamSynchronize(c->stream);
+        const double t = now_s2();
+        std::fprintf(stderr, "setup %-14s %8.2f ms\n", what, 1e3 * (t - tt));
+        tt = t;
+    };
     build_ffpe_kernels(c, gam, tau, N, sbd, kc, S.ks, S.eps);
+    lap("kernels");
     const int ng = (int)gam.size();
     std::vector<const fraq_kernel_t*> kp(ng);
     std::vector<long> dims(ng, 1);
     for (int t = 0; t < ng; ++t) kp[t] = &S.ks[t];
     S.hd.build(c, ng, kp.data(), dims.data(), /*tables_only=*/true);
+    lap("hist tables");
     S.corr_off.assign(ng, 0);
     if (sbd) {
         S.corr.alloc((size_t)ng * (N + 1));
@@ -618,8 +631,10 @@ void modal_prepare(fraq_ctx c, ModalSetup& S, const std::vector<double>& gam,
         for (int t = 0; t < ng; ++t) S.corr_off[t] = (long)t * (N + 1);
     }
     const int n_inst = ng / 2;
+    lap("corr");
     modal_plan(c, S.hd, a, std::vector<double>(n_inst, tau), sbd ? S.corr.p : nullptr, S.corr_off,
                n_inst, sbd, S.plan);
+    lap("plan");
 }
 
 struct EventTimer {
@@ -669,31 +684,35 @@ void ffpe_run_modal(fraq_ctx c, const fraq_spec_t* specs, int n_inst, bool sbd,
     const double tau = specs[0].t_final / double(N);
     const double h = specs[0].length / double(M + 1);
     const long C = 2L * n_inst;
-    // initial data, column c = 2 inst + field, row = grid point
+    // initial data, instance-major rows (row c = 2 inst + field): contiguous host writes; the
+    // device transposes to the [grid point][c] layout the DST takes
     std::vector<double> G0((size_t)M * C);
     std::vector<double> gam(C), av(n_inst), tv(n_inst, tau);
     for (int i = 0; i < n_inst; ++i) {
         const fraq_spec_t& s = specs[i];
-        for (int j = 0; j < M; ++j) {
-            const double x = (j + 1) * h;
-            double v1, v2;
-            if (s.initial == FRAQ_POLY_SIN) {
-                v1 = x * (1.0 - x);
-                v2 = std::sin(x);
-            } else if (s.initial == FRAQ_INDICATOR) {
-                v1 = x > 0.5 ? 1.0 - x : 0.0;
-                v2 = x < 0.5 ? x : 0.0;
-            } else {
-                v1 = s.custom_g1[j];
-                v2 = s.custom_g2[j];
+        double* r1 = G0.data() + (size_t)(2 * i) * M;
+        double* r2 = r1 + M;
+        if (s.initial == FRAQ_CUSTOM) {
+            std::memcpy(r1, s.custom_g1, sizeof(double) * M);
+            std::memcpy(r2, s.custom_g2, sizeof(double) * M);
+        } else {
+            for (int j = 0; j < M; ++j) {
+                const double x = (j + 1) * h;
+                if (s.initial == FRAQ_POLY_SIN) {
+                    r1[j] = x * (1.0 - x);
+                    r2[j] = std::sin(x);
+                } else {
+                    r1[j] = x > 0.5 ? 1.0 - x : 0.0;
+                    r2[j] = x < 0.5 ? x : 0.0;
+                }
             }
-            G0[(size_t)j * C + 2 * i] = v1;
-            G0[(size_t)j * C + 2 * i + 1] = v2;
         }
         gam[2 * i] = 1.0 - s.alpha1;
         gam[2 * i + 1] = 1.0 - s.alpha2;
         av[i] = s.coupling_a;
     }
+    if (std::getenv("FRAQ_SETUP_TRACE"))
+        std::fprintf(stderr, "setup %-14s %8.2f ms\n", "initial data", 1e3 * (now_s2() - t0));
     ModalSetup S;
     modal_prepare(c, S, gam, av, tau, N, sbd, kc);
     // eigenvalues lambda_k = (4/h^2) sin^2(k pi h / (2 L)) (block_solver.cpp:21-24)
@@ -705,10 +724,13 @@ void ffpe_run_modal(fraq_ctx c, const fraq_spec_t* specs, int n_inst, bool sbd,
     DevBuf<double> dlam(M), dG((size_t)M * C), dW((size_t)M * C), dc0((size_t)M * C),
         dcN((size_t)M * C);
     FRAQ_CUDA(cudaMemcpyAsync(dlam.p, lam.data(), sizeof(double) * M, cudaMemcpyHostToDevice, c->stream));
-    FRAQ_CUDA(cudaMemcpyAsync(dG.p, G0.data(), sizeof(double) * G0.size(), cudaMemcpyHostToDevice,
+    FRAQ_CUDA(cudaMemcpyAsync(dW.p, G0.data(), sizeof(double) * G0.size(), cudaMemcpyHostToDevice,
                               c->stream));
+    transpose_dev(c, dW.p, C, M, dG.p);  // [c][grid point] -> [grid point][c]
     const double* tab = ctx_sintab(c, M);
     const double t1 = now_s2();
+    if (std::getenv("FRAQ_SETUP_TRACE"))
+        std::fprintf(stderr, "setup %-14s %8.2f ms\n", "total", 1e3 * (t1 - t0));
     EventTimer timer(c->stream);
     // forward DST (projection, 2/(M+1) S G): rows = modes; then [C][M] for the stepper
     dst_apply(c, M, tab, dG.p, C, dW.p, 2.0 / (M + 1));
@@ -718,12 +740,14 @@ void ffpe_run_modal(fraq_ctx c, const fraq_spec_t* specs, int n_inst, bool sbd,
     transpose_dev(c, dcN.p, C, M, dW.p);
     dst_apply(c, M, tab, dW.p, C, dG.p, 1.0);
     const double loop_s = timer.stop();
-    FRAQ_CUDA(cudaMemcpy(G0.data(), dG.p, sizeof(double) * G0.size(), cudaMemcpyDeviceToHost));
-    for (int i = 0; i < n_inst; ++i)
-        for (int j = 0; j < M; ++j) {
-            g1_out[(size_t)i * M + j] = G0[(size_t)j * C + 2 * i];
-            g2_out[(size_t)i * M + j] = G0[(size_t)j * C + 2 * i + 1];
-        }
+    // back to instance-major rows on the device, then contiguous copies out
+    transpose_dev(c, dG.p, M, C, dW.p);
+    FRAQ_CUDA(cudaMemcpy(G0.data(), dW.p, sizeof(double) * G0.size(), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n_inst; ++i) {
+        std::memcpy(g1_out + (size_t)i * M, G0.data() + (size_t)(2 * i) * M, sizeof(double) * M);
+        std::memcpy(g2_out + (size_t)i * M, G0.data() + (size_t)(2 * i + 1) * M,
+                    sizeof(double) * M);
+    }
     fill_info(info, S, loop_s, t1 - t0);
 }
 

@@ -804,8 +804,13 @@ void build_kernel_auto_dev(fraq_ctx c, bool sbd, int n, const double* gammas, do
     std::vector<double> hm((size_t)n * 1024), hr((size_t)n * 1024);
     FRAQ_CUDA(cudaMemcpy(hm.data(), mt.p, sizeof(double) * n * 1024, cudaMemcpyDeviceToHost));
     FRAQ_CUDA(cudaMemcpy(hr.data(), rt.p, sizeof(double) * n * 1024, cudaMemcpyDeviceToHost));
-    std::vector<double> ht((size_t)n * L);
-    FRAQ_CUDA(cudaMemcpy(ht.data(), tables.p, sizeof(double) * n * L, cudaMemcpyDeviceToHost));
+    // only the heads leave the device (a C5 batch's full tables are 67 MB)
+    int HW = 1;
+    for (int t = 0; t < n; ++t) HW = std::max(HW, head[t]);
+    HW = (int)std::min<long>(HW, L);
+    std::vector<double> ht((size_t)n * HW);
+    FRAQ_CUDA(cudaMemcpy2D(ht.data(), sizeof(double) * HW, tables.p, sizeof(double) * L,
+                           sizeof(double) * HW, n, cudaMemcpyDeviceToHost));
     for (int t = 0; t < n; ++t) {
         fraq_kernel_t* k = out + t;
         std::memset(k, 0, sizeof(*k));
@@ -827,7 +832,7 @@ void build_kernel_auto_dev(fraq_ctx c, bool sbd, int n, const double* gammas, do
                 k->r2[j] = r[np[t] + j];
             }
         // head = classical weights d_0 .. d_{head-1} (prefix of the sizing table)
-        for (int i = 0; i < head[t]; ++i) k->head[i] = ht[(size_t)t * L + i];
+        for (int i = 0; i < head[t]; ++i) k->head[i] = ht[(size_t)t * HW + i];
     }
 }
 
