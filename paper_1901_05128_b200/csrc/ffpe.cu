@@ -229,6 +229,8 @@ struct SolveArgs {
     const long* n_dev;    // CUDA-graph replays: n = *n_dev + n_off, first step never inside
     int n_off;
     long long* prof;      // nullable: block 0 phase timestamps (FRAQ_K6_PROFILE experiment)
+    double* hist_out;     // classical schemes: G^n also into the full history row n
+    long hist_total;
 };
 
 // Row storage of the on-chip solve: row i at slot i + i/8 + i/64 + i/512.  Cyclic reduction
@@ -611,6 +613,11 @@ __global__ void __launch_bounds__(THREADS) solve_kernel(SolveArgs A) {
             A.out[(long)blockIdx.x * 2 * m + k] = x.x;
             A.out[(long)blockIdx.x * 2 * m + m + k] = x.y;
         }
+        if (A.hist_out) {
+            double* row = A.hist_out + n * A.hist_total;
+            row[G1.dof0 + k] = x.x;
+            row[G2.dof0 + k] = x.y;
+        }
     }
     if (A.prof) {
         __syncthreads();
@@ -618,16 +625,92 @@ __global__ void __launch_bounds__(THREADS) solve_kernel(SolveArgs A) {
     }
 }
 
-// Classical direct sums (fpfp.cpp:114-122, 150-164): s[k] = (SBD: 0.5 d_{n-1} G^0) +
-// sum_{i=1}^{n-1} d_i G^{n-i}, serial in i like the reference.  Full history hist[t][group dof].
-__global__ void classical_sum_kernel(const double* hist, long hist_ld, const double* d, long d_ld,
-                                     const int* group_of_dof, long total, long n, int sbd,
-                                     double* s) {
+// Classical direct sums (fpfp.cpp:114-122, 150-164):
+//   s_n[k] = (SBD: 0.5 d_(n-1) G^0[k]) + sum_(i=1)^(n-1) d_i G^(n-i)[k]
+// over the full device history hist[t][k] (k = group * m + j; group g = field of an instance,
+// weights d of group g at ctab + g * (N + 1)).  Evaluated per block of kCB levels: the levels
+// before the block enter once per block as a Toeplitz GEMM on the fp64 tensor cores (K10's tile
+// scheme, per-group weights), the levels inside the block per level.  The direct per-level sum
+// re-read the whole history every level (O(N^2 M) memory traffic: ~1400 s for C3's shape,
+// slower than the reference's CPU loop); blocked, the history is read once per kCB levels.
+constexpr int kCB = 64;            // classical block (levels) == GEMM M tile
+constexpr int CT_N = 64, CT_K = 16;
+
+__device__ __forceinline__ void cdmma(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+// S_old[r][k] = sum_(q<n0) A_g[r][q] hist[q][k], level n = n0 + r, A_g[r][q] = d_g[n - q] for
+// q >= 1, the SBD correction 0.5 d_g[n - 1] for q = 0 (BE: 0).  grid.x = (group, 64-DOF tile).
+__global__ void __launch_bounds__(128) classical_old_kernel(const double* __restrict__ hist,
+                                                           long total, const double* __restrict__ ctab,
+                                                           long d_ld, int m, int tiles_per_group,
+                                                           long n0, int rows, int sbd, double* Sold) {
+    __shared__ double sA[kCB][CT_K + 1];
+    __shared__ double sB[CT_K][CT_N + 1];
+    const int grp = blockIdx.x / tiles_per_group, tile = blockIdx.x % tiles_per_group;
+    const double* w = ctab + (size_t)grp * d_ld;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+    const int g = lane >> 2, t = lane & 3;
+    const long j0c = (long)tile * CT_N;          // first DOF of the tile within the group
+    const long k0 = (long)grp * m + j0c;         // history column
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (long q0 = 0; q0 < n0; q0 += CT_K) {
+        __syncthreads();
+        for (int idx = tid; idx < kCB * CT_K; idx += 128) {
+            const int r = idx / CT_K, cq = idx % CT_K;
+            const long q = q0 + cq, n = n0 + r;
+            double v = 0.0;
+            if (r < rows && q < n0) v = q == 0 ? (sbd ? 0.5 * w[n - 1] : 0.0) : w[n - q];
+            sA[r][cq] = v;
+        }
+        for (int idx = tid; idx < CT_K * CT_N; idx += 128) {
+            const int r = idx / CT_N, cc = idx % CT_N;
+            const long q = q0 + r;
+            sB[r][cc] = (q < n0 && j0c + cc < m) ? hist[q * total + k0 + cc] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < CT_K; kk += 4) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) af[a] = sA[wm + 8 * a + g][kk + t];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) bf[b] = sB[kk + t][wn + 8 * b + g];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) cdmma(acc[a][b], af[a], bf[b]);
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int r = wm + 8 * a + g;
+                const long jj = j0c + wn + 8 * b + 2 * t + e;
+                if (r < rows && jj < m) Sold[(long)r * total + (long)grp * m + jj] = acc[a][b][e];
+            }
+}
+
+// s_n[k] = S_old[n - n0][k] + sum_(q = n0)^(n-1) d[n - q] hist[q][k]  (levels of the block)
+__global__ void classical_inblock_kernel(const double* hist, long total, const double* ctab,
+                                         long d_ld, int m, long n0, long n, const double* Sold,
+                                         double* s) {
     const long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
     if (k >= total) return;
-    const double* w = d + group_of_dof[k] * d_ld;
-    double acc = sbd ? 0.5 * w[n - 1] * hist[k] : 0.0;
-    for (long i = 1; i <= n - 1; ++i) acc += w[i] * hist[(n - i) * hist_ld + k];
+    const double* w = ctab + (k / m) * d_ld;
+    double acc = Sold[(n - n0) * total + k];
+    for (long q = n0; q < n; ++q) acc = fma(w[n - q], hist[q * total + k], acc);
     s[k] = acc;
 }
 
@@ -702,8 +785,7 @@ struct PhysStepper {
     double tau = 0.0;
     std::vector<double> G0, eps, d0;
     std::vector<fraq_kernel_t> ks;
-    DevBuf<double> ctab, g0, corr, sbuf, outb, hist;
-    DevBuf<int> gof;
+    DevBuf<double> ctab, g0, corr, sbuf, outb, hist, sold;
     DevBuf<SysDev> dsys;
     DevBuf<M2> thomas;
     DevBuf<InstDev> dinst;
@@ -895,10 +977,7 @@ PhysStepper::PhysStepper(fraq_ctx c_, const fraq_spec_t* specs, int n_inst_, int
     if (!fast) {
         hist.alloc((size_t)(N + 1) * total);
         FRAQ_CUDA(cudaMemcpy(hist.p, G0.data(), sizeof(double) * total, cudaMemcpyHostToDevice));
-        std::vector<int> go(total);
-        for (long k = 0; k < total; ++k) go[k] = (int)(k / m);
-        gof.alloc(total);
-        FRAQ_CUDA(cudaMemcpy(gof.p, go.data(), sizeof(int) * total, cudaMemcpyHostToDevice));
+        sold.alloc((size_t)kCB * total);
     }
     smem = 2 * sizeof(double2) * rows_len(m);
     if (smem > 227 * 1024) fail(FRAQ_EINVAL, "run: grid_m too large for the on-chip block solve");
@@ -923,6 +1002,8 @@ PhysStepper::PhysStepper(fraq_ctx c_, const fraq_spec_t* specs, int n_inst_, int
     sa.out = outb.p;
     sa.refine = std::getenv("FRAQ_K6_NOREFINE") ? 0 : 1;  // experiment switch (timing only)
     sa.tap1 = fast ? 1 : 0;
+    sa.hist_out = fast ? nullptr : hist.p;
+    sa.hist_total = total;
     use_graph = fast && !std::getenv("FRAQ_PHYS_NOGRAPH");  // experiment switch
     FRAQ_CUDA(cudaStreamSynchronize(c->stream));
     setup_seconds = now_s() - t_setup0;
@@ -1057,24 +1138,25 @@ void PhysStepper::step(long n_steps, std::vector<cudaEvent_t>* ev) {
         if (fast) {
             // first SBD step: advance() only decays zero accumulators (no feed: 1 - n_head < 1)
             if (!first) hd.launch_step(c, k5_args(n));
-        } else if (!first) {
-            classical_sum_kernel<<<(unsigned)((total + 255) / 256), 256, 0, c->stream>>>(
-                hist.p, total, ctab.p, N + 1, gof.p, total, n, sbd, sbuf.p);
-            FRAQ_LAUNCH_CHECK();
+        } else {
+            const long n0 = n - (n - 1) % kCB;  // first level of this classical block
+            if (n == n0) {  // (also at the first SBD level: the block's later levels need it)
+                const int tpg = (m + CT_N - 1) / CT_N;
+                const int rows = (int)std::min<long>(kCB, N - n0 + 1);
+                classical_old_kernel<<<(unsigned)(tpg * 2 * n_inst), 128, 0, c->stream>>>(
+                    hist.p, total, ctab.p, N + 1, m, tpg, n0, rows, sbd, sold.p);
+                FRAQ_LAUNCH_CHECK();
+            }
+            if (!first) {
+                classical_inblock_kernel<<<(unsigned)((total + 255) / 256), 256, 0, c->stream>>>(
+                    hist.p, total, ctab.p, N + 1, m, n0, n, sold.p, sbuf.p);
+                FRAQ_LAUNCH_CHECK();
+            }
         }
         mark(e0 + 1);
         mark(e0 + 2);
         launch_k6(n, step_idx == end, c->stream, nullptr, 0);
         mark(e0 + 3);
-        if (!fast) {
-            // keep the full history: copy G^n rows out of the 2-slot rings
-            for (int t = 0; t < 2 * n_inst; ++t) {
-                const GroupDev& G = hd.groups_h[t];
-                FRAQ_CUDA(cudaMemcpyAsync(hist.p + n * total + (long)t * m,
-                                          hd.ring.p + G.ring_off + (n % G.L) * (long)G.ld,
-                                          sizeof(double) * m, cudaMemcpyDeviceToDevice, c->stream));
-            }
-        }
         level += 1;
         appended += 1;
     }
