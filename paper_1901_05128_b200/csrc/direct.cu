@@ -31,8 +31,8 @@ __global__ void __launch_bounds__(128) toeplitz_kernel(const double* __restrict_
                                                        const double* __restrict__ U, long ldu,
                                                        long n_steps, long dim, double* D,
                                                        long ldd) {
-    __shared__ double sA[DT_M][DT_K + 1];  // Toeplitz tile A[n][j] = w[n - j] (0 above diagonal)
-    __shared__ double sB[DT_K][DT_N + 1];  // signal tile B[j][m]
+    __shared__ double sA[2][DT_M][DT_K + 1];  // Toeplitz tile A[n][j] = w[n - j] (0 above diag)
+    __shared__ double sB[2][DT_K][DT_N + 1];  // signal tile B[j][m]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const long n0 = (long)blockIdx.y * DT_M, m0 = (long)blockIdx.x * DT_N;
     const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;  // warp sub-tile origin
@@ -42,32 +42,59 @@ __global__ void __launch_bounds__(128) toeplitz_kernel(const double* __restrict_
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-    const long kend = min(n0 + DT_M, n_steps);  // source levels j < kend (lower triangle)
-    for (long j0 = 0; j0 < kend; j0 += DT_K) {
-        __syncthreads();
-        for (int idx = tid; idx < DT_M * DT_K; idx += 128) {
-            const int r = idx / DT_K, c = idx % DT_K;
+    // the next K-tile's operands are fetched into registers while the current tile's DMMAs run
+    // (as K12 does); one barrier per K-tile
+    constexpr int PA = DT_M * DT_K / 128, PB = DT_K * DT_N / 128;
+    double ra[PA], rb[PB];
+    auto fetch = [&](long j0) {
+#pragma unroll
+        for (int q = 0; q < PA; ++q) {
+            const int idx = tid + 128 * q, r = idx / DT_K, c = idx % DT_K;
             const long n = n0 + r, j = j0 + c;
-            sA[r][c] = (j <= n && n < n_steps) ? w[n - j] : 0.0;
+            ra[q] = (j <= n && n < n_steps) ? __ldg(w + (n - j)) : 0.0;
         }
-        for (int idx = tid; idx < DT_K * DT_N; idx += 128) {
-            const int r = idx / DT_N, c = idx % DT_N;
+#pragma unroll
+        for (int q = 0; q < PB; ++q) {
+            const int idx = tid + 128 * q, r = idx / DT_N, c = idx % DT_N;
             const long j = j0 + r, m = m0 + c;
-            sB[r][c] = (j < n_steps && m < dim) ? U[j * ldu + m] : 0.0;
+            rb[q] = (j < n_steps && m < dim) ? __ldg(U + j * ldu + m) : 0.0;
         }
-        __syncthreads();
+    };
+    auto put = [&](int buf) {
+#pragma unroll
+        for (int q = 0; q < PA; ++q) {
+            const int idx = tid + 128 * q;
+            sA[buf][idx / DT_K][idx % DT_K] = ra[q];
+        }
+#pragma unroll
+        for (int q = 0; q < PB; ++q) {
+            const int idx = tid + 128 * q;
+            sB[buf][idx / DT_N][idx % DT_N] = rb[q];
+        }
+    };
+    const long kend = min(n0 + DT_M, n_steps);  // source levels j < kend (lower triangle)
+    fetch(0);
+    put(0);
+    __syncthreads();
+    int buf = 0;
+    for (long j0 = 0; j0 < kend; j0 += DT_K) {
+        const bool more = j0 + DT_K < kend;
+        if (more) fetch(j0 + DT_K);
 #pragma unroll
         for (int kk = 0; kk < DT_K; kk += 4) {
             double af[4], bf[4];
 #pragma unroll
-            for (int a = 0; a < 4; ++a) af[a] = sA[wm + 8 * a + g][kk + t];   // A: row g, col t
+            for (int a = 0; a < 4; ++a) af[a] = sA[buf][wm + 8 * a + g][kk + t];  // A: row g, col t
 #pragma unroll
-            for (int b = 0; b < 4; ++b) bf[b] = sB[kk + t][wn + 8 * b + g];   // B: row t, col g
+            for (int b = 0; b < 4; ++b) bf[b] = sB[buf][kk + t][wn + 8 * b + g];  // B: row t, col g
 #pragma unroll
             for (int a = 0; a < 4; ++a)
 #pragma unroll
                 for (int b = 0; b < 4; ++b) dmma884(acc[a][b], af[a], bf[b]);
         }
+        if (more) put(buf ^ 1);
+        __syncthreads();
+        buf ^= 1;
     }
     // C/D fragment: row g, cols 2t, 2t+1
 #pragma unroll
