@@ -529,3 +529,15 @@ def test_concurrent_runs_from_threads(fraq):
         t.join()
     for a, b in zip(out, seq):
         assert list(a.final_state.g1) == list(b.final_state.g1)
+
+
+@pytest.mark.parametrize("sbd", [False, True])
+@pytest.mark.parametrize("n,dim", [(1, 1), (17, 3), (65, 67), (130, 5), (200, 129)])
+def test_direct_cq_ragged_matches_oracle(fraq, orc, sbd, n, dim):
+    """K10 (direct CQ, Toeplitz GEMM on DMMA) on ragged shapes -- partial level and DOF tiles,
+    single level / single lane -- against the oracle's direct sum (test_fast_kernel.cpp:27-41)."""
+    rng = np.random.default_rng(n * 1000 + dim)
+    U = rng.uniform(-1, 1, (n, dim))
+    D = fraq.direct_cq(sbd, 0.37, 0.01, U)
+    Dr = orc.direct_cq(sbd, 0.37, 0.01, U)
+    assert np.max(np.abs(D - Dr)) <= 1e-12 * max(np.max(np.abs(Dr)), 1e-300)
