@@ -384,21 +384,31 @@ __global__ void __launch_bounds__(256, 2)
                     // deferred reduction of the previous pair: its LDS / DADD / STG latency
                     // overlaps the readout DMMAs just issued (asynchronous tensor pipe)
                     if (mid_reduce) reduce_pair();
-                    // ---- state GEMM: Y <- r^8 (.) Y + V R
+                    // ---- state GEMM: Y <- r^8 (.) Y + V R.  All rescale DMULs first, then the
+                    // DMMAs K half by K half: a DMUL queued between DMMAs waits for the shared
+                    // fp64 pipe (23% of K5d's stall samples sat on DMULs), and no two
+                    // consecutive DMMAs share an accumulator.  +1.1% at C2
+                    // (profiles/r02/k5d_variants.sh); every element sees the same operations in
+                    // the same order as before
 #pragma unroll
                     for (int ntl = 0; ntl < D_NT; ++ntl) {
                         const double ra = r8w[(ntl * 2) * 32], rbv = r8w[(ntl * 2 + 1) * 32];
-                        const double b0 = rw[(ntl * 2) * 32], b1 = rw[(ntl * 2 + 1) * 32];
 #pragma unroll
                         for (int rb = 0; rb < 2; ++rb) {
 #ifndef FRAQ_EXP_NODMUL
                             Y[rb][ntl][0] *= ra;
                             Y[rb][ntl][1] *= rbv;
 #endif
-                            dmma(Y[rb][ntl], vf[rb][0], b0);
-                            dmma(Y[rb][ntl], vf[rb][1], b1);
                         }
                     }
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+#pragma unroll
+                        for (int ntl = 0; ntl < D_NT; ++ntl) {
+                            const double b = rw[(ntl * 2 + h) * 32];
+#pragma unroll
+                            for (int rb = 0; rb < 2; ++rb) dmma(Y[rb][ntl], vf[rb][h], b);
+                        }
                     // partial readout (DOF g, levels 2t, 2t+1) -> shared memory
 #pragma unroll
                     for (int rb = 0; rb < 2; ++rb) {
