@@ -22,7 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CUDA_HOME = os.path.dirname(os.path.dirname(NVCC))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CLI = os.path.join(os.path.dirname(os.path.abspath(__file__)), "fraq")
-CU_SOURCES = ["setup.cu", "history.cu", "history_dmma.cu", "ffpe.cu", "modal.cu", "modal_dmma.cu", "direct.cu",
+CU_SOURCES = ["setup.cu", "history.cu", "history_dmma.cu", "history_fir.cu", "ffpe.cu", "modal.cu", "modal_dmma.cu", "direct.cu",
               "capi.cu", "diag.cu"]
 
 CUDA_LIB = os.path.join(HERE, "libfraqcu.so")

@@ -21,8 +21,15 @@ namespace fraqcu {
 
 // history_dmma.cu
 void build_frag_tables(fraq_ctx c, HistDevice& d);
-void launch_run3(const RunArgs& a, int nwg, int num_sms, cudaStream_t s);
+void launch_run3(const RunArgs& a, int nwg, int num_sms, cudaStream_t s, bool allow_tma);
 int run3_max_lag();
+// history_fir.cu (K5e)
+void build_fir_plan(fraq_ctx c, HistDevice& d);
+void fir_note_inputs(fraq_ctx c, HistDevice& d, long A0, const double* U, long ldu, long n_steps);
+bool fir_eligible(const HistDevice& d, long A0, const double* U, long ldu, long n_steps);
+void launch_run4(fraq_ctx c, HistDevice& d, const int2* tasks, int n_tasks, int* counter, long A0,
+                 const double* U, long ldu, long n_steps, double* D, long ldd);
+void fir_materialize(fraq_ctx c, HistDevice& d, long A1);
 
 namespace {
 
@@ -540,6 +547,8 @@ void HistDevice::build(fraq_ctx c, int n_groups, const fraq_kernel_t* const* ks,
     up(tiles.p, tiles_h.data(), tiles_h.size() * sizeof(int2));
     up(cr.p, hr.data(), hr.size() * sizeof(double));
     up(cf.p, hf.data(), hf.size() * sizeof(double));
+    cr_h = hr;
+    cf_h = hf;
     up(head.p, hh.data(), hh.size() * sizeof(double));
     zero(c);
     FRAQ_CUDA(cudaStreamSynchronize(c->stream));
@@ -652,6 +661,8 @@ void flush(fraq_hist h, int mode, double* out_d) {
     a.mode = mode;
     a.out = out_d;
     if (!a.adv && !a.app && mode == MODE_NONE) return;
+    fir_materialize(h->ctx, h->d, h->appended);  // K5 reads every node's state
+    if (h->pending) fir_note_inputs(h->ctx, h->d, h->appended, h->stage.p, h->d.total_dim, 1);
     h->d.launch_step(h->ctx, a);
     if (h->pending) {
         if (h->appended > 0) h->level += 1;
@@ -733,6 +744,7 @@ void hist_advance(fraq_hist h) {
     check_advance(h);
     StepArgs a = base_args(h);
     a.adv = 1;
+    fir_materialize(h->ctx, h->d, h->appended);
     h->d.launch_step(h->ctx, a);
     h->level += 1;
 }
@@ -744,6 +756,7 @@ void hist_append(fraq_hist h, const double* v, int mem) {
     StepArgs a = base_args(h);
     a.app = 1;
     a.u = h->stage.p;
+    fir_note_inputs(h->ctx, h->d, h->appended, h->stage.p, h->d.total_dim, 1);
     h->d.launch_step(h->ctx, a);
     h->appended += 1;
 }
@@ -804,35 +817,70 @@ void run_device(fraq_hist h, const double* U, long ldu, long n_steps, double* D,
         a.cr = h->d.cr.p;
         a.cf = h->d.cf.p;
         a.head = h->d.head.p;
-        a.A0 = h->appended;
         a.lo = (int)h->lo;
-        a.n_steps = n_steps;
-        a.U = U;
         a.ldu = ldu;
-        a.D = D;
         a.ldd = ldd;
         const int P = (h->d.max_J + 31) / 32;
-        FRAQ_CUDA(cudaMemsetAsync(h->counter.p, 0, sizeof(int), h->ctx->stream));
         static const bool k5c = std::getenv("FRAQ_K5C") != nullptr;
-        if (!k5c && h->d.max_L <= run3_max_lag()) {
-            // K5d (DMMA block formulation), default
-            h->last_path = 3;
-            build_frag_tables(h->ctx, h->d);
-            a.tasks = h->run3_tasks.p;
-            a.n_tasks = h->n_run3_tasks;
-            a.frag = h->d.frag.p;
-            launch_run3(a, std::max(1, (h->d.max_J + 63) / 64), h->ctx->num_sms, h->ctx->stream);
-        } else {
-            h->last_path = 2;
-            a.tasks = h->run2_tasks.p;
-            a.n_tasks = h->n_run2_tasks;
-            launch_run2(a, std::max(1, P), h->ctx->num_sms, h->ctx->stream);
+        const bool k5d = !k5c && h->d.max_L <= run3_max_lag();
+        if (k5d) build_fir_plan(h->ctx, h->d);
+        // TMA boxes start at a group's first DOF + 16 i: 16-byte aligned only for even starts
+        bool even_groups = true;
+        for (const GroupDev& G : h->d.groups_h) even_groups = even_groups && (G.dof0 % 2 == 0);
+        const FirPlan& fp = h->d.fir;
+        // The call runs as up to three launches: K5d until the steady-state form is valid (the
+        // first levels of a history), K5e on whole 8-level blocks, K5d on a ragged tail.
+        for (long done = 0; done < n_steps;) {
+            const long A0 = h->appended, rest = n_steps - done;
+            const double* Uc = U + done * ldu;
+            double* Dc = D ? D + done * ldd : nullptr;
+            long m = rest;
+            FRAQ_CUDA(cudaMemsetAsync(h->counter.p, 0, sizeof(int), h->ctx->stream));
+            if (k5d && even_groups && fir_eligible(h->d, A0, Uc, ldu, rest & ~7L)) {
+                // K5e: short nodes as an exact FIR, long nodes in K5d's block form
+                m = rest & ~7L;
+                h->last_path = 4;
+                launch_run4(h->ctx, h->d, h->run3_tasks.p, h->n_run3_tasks, h->counter.p, A0, Uc,
+                            ldu, m, Dc, ldd);
+            } else {
+                if (k5d && fp.ok) {
+                    // K5d up to the level K5e can take over from: past min_level, with the last
+                    // kw_max input rows on record
+                    const long s = std::max<long>(std::max(fp.min_level, fp.kw_max),
+                                                  A0 + (fp.xh_valid >= fp.kw_max ? 0 : fp.kw_max));
+                    const long pre = (s - A0 + 31) / 32 * 32;
+                    if (pre > 0 && pre + 64 <= rest) m = pre;
+                }
+                fir_materialize(h->ctx, h->d, A0);
+                a.A0 = A0;
+                a.n_steps = m;
+                a.U = Uc;
+                a.D = Dc;
+                if (k5d) {
+                    // K5d (DMMA block formulation)
+                    h->last_path = 3;
+                    build_frag_tables(h->ctx, h->d);
+                    a.tasks = h->run3_tasks.p;
+                    a.n_tasks = h->n_run3_tasks;
+                    a.frag = h->d.frag.p;
+                    launch_run3(a, std::max(1, (h->d.max_J + 63) / 64), h->ctx->num_sms,
+                                h->ctx->stream, even_groups);
+                } else {
+                    h->last_path = 2;
+                    a.tasks = h->run2_tasks.p;
+                    a.n_tasks = h->n_run2_tasks;
+                    launch_run2(a, std::max(1, P), h->ctx->num_sms, h->ctx->stream);
+                }
+            }
+            fir_note_inputs(h->ctx, h->d, A0, Uc, ldu, m);
+            h->appended += m;
+            h->level = h->appended - 1;
+            done += m;
         }
-        h->appended += n_steps;
-        h->level = h->appended - 1;
         return;
     }
     h->last_path = 0;
+    fir_materialize(h->ctx, h->d, h->appended);
     for (long n = 0; n < n_steps; ++n) {
         if (h->appended > 0) check_advance(h);
         StepArgs a = base_args(h);
@@ -844,6 +892,7 @@ void run_device(fraq_hist h, const double* U, long ldu, long n_steps, double* D,
             if (!G.sbd && h->appended + 1 < 2) ok = false;
         a.mode = (D && ok) ? MODE_DERIV : MODE_NONE;
         a.out = D ? D + n * ldd : nullptr;
+        fir_note_inputs(h->ctx, h->d, h->appended, a.u, h->d.total_dim, 1);
         h->d.launch_step(h->ctx, a);
         if (D && !ok) {
             // derivative undefined on the first BE push: NaN row (the reference throws)

@@ -78,6 +78,39 @@ struct RunArgs {
 constexpr int kFragC = 0, kFragR = 4096, kFragR8 = 8192, kFragRF = 8704, kFragW = 9728;
 constexpr int kFragDoubles = 9792;
 
+// K5e (history_fir.cu): the blocked evaluation with the fast-decaying nodes folded into an exact
+// FIR over the last M inputs.  Per group: the slow ("long") nodes keep their state recurrence;
+// a node j is "short" when |r_j|^M <= 2^-70, so everything it remembers lies within M levels
+// and its contribution is the Toeplitz sum  sum_{m<M} (sum_j f_j r_j^m) v(n-m).
+constexpr int E_MAXWG = 8;   // warps per CTA (node slices of up to 64 long nodes)
+struct FirGroup {
+    int JL, TL;              // long nodes, their 8-node tiles
+    int M;                   // FIR length of the short nodes (0: none)
+    int KW, nkk;             // combined window over the input rows (multiple of 4), k-steps
+    int NTW;                 // tiles per warp (warp w owns tiles [w NTW, (w+1) NTW))
+    int kk0[E_MAXWG + 1];    // FIR k-steps of warp w: [kk0[w], kk0[w+1])
+    long tab_off;            // tables: C[TL*64], R[TL*64], H[nkk*32] (doubles)
+    int perm_off;            // original node index of long position p (-1: padding)
+    int short_off, n_short;  // original node indices of the short nodes
+};
+struct FirPlan {
+    bool built = false, ok = false;
+    std::vector<FirGroup> groups_h;
+    DevBuf<FirGroup> groups;
+    DevBuf<double> tabs;
+    DevBuf<int> perm;        // long positions, then short lists
+    int nwg = 1;             // warps per CTA
+    int capC = 64, capH = 32;  // shared-memory table capacities (doubles)
+    int kw_max = 0;          // input rows a call needs from before its first level
+    int min_level = 0;       // first level index the steady-state form is valid from
+    int ring_rows = 128;     // shared-memory input ring (power of two)
+    // input history ring in HBM (rows = level & (xh_rows - 1)), valid trailing rows
+    DevBuf<double> xh;
+    int xh_rows = 0;
+    long xh_valid = 0;
+    bool short_stale = false;  // short-node states in `state` lag behind (rebuilt on demand)
+};
+
 // Device-resident tables + state of a set of groups.
 struct HistDevice {
     std::vector<GroupDev> groups_h;
@@ -97,6 +130,10 @@ struct HistDevice {
     // DMMA fragment tables for K5d (built on first use): per group kFragDoubles doubles
     DevBuf<double> frag;
     bool frag_built = false;
+    // host copies of the per-node ratios / feeds (cr, cf) for the K5e table builder
+    std::vector<double> cr_h, cf_h;
+    // K5e plan (history_fir.cu; built on first use)
+    FirPlan fir;
 
     void build(fraq_ctx c, int n_groups, const fraq_kernel_t* const* ks, const long* dims,
                bool tables_only = false);

@@ -168,7 +168,15 @@ __global__ void __launch_bounds__(256, 2)
     const int nwg = blockDim.x >> 5;  // warps = node slices of 64
     const int sl = warp;
     const double qnan = __longlong_as_double(0x7ff8000000000000LL);
-    if (tid == 0) s_group = -1;
+    // completion barriers of the input tiles: initialised once per CTA (re-initialising a live
+    // barrier per task hung K5e after an odd number of completions); a task's chunk k uses
+    // mbar[k & 1] and the phase each barrier is in carries over from task to task
+    unsigned phases = 0;
+    if (tid == 0) {
+        s_group = -1;
+        mbar_init(&S.mbar[0]);
+        mbar_init(&S.mbar[1]);
+    }
     for (;;) {
         __syncthreads();
         if (tid == 0) s_task = atomicAdd(A.counter, 1);
@@ -247,11 +255,8 @@ __global__ void __launch_bounds__(256, 2)
         };
         const bool tma = A.use_tma && blockDim.x == 256;
         if (tma) {
-            if (tid == 0) {
-                mbar_init(&S.mbar[0]);
-                mbar_init(&S.mbar[1]);
+            if (tid == 0)
                 tma_tile(&umap, &S.X[0][0], &S.mbar[0], (int)(G.dof0 + tk.y), 0, D_TC * 16 * 8);
-            }
         } else if (blockDim.x == 256) {
             prefetch(0);
         }
@@ -314,7 +319,8 @@ __global__ void __launch_bounds__(256, 2)
                              (int)(G.dof0 + tk.y), (int)(c0 + D_TC), D_TC * 16 * 8);
                 // this chunk's tile landed (TMA, zero-filled past the ends of U); the mbarrier
                 // completion makes it visible to every waiting thread
-                mbar_wait(&S.mbar[ck & 1], (ck >> 1) & 1);
+                mbar_wait(&S.mbar[ck & 1], (phases >> (ck & 1)) & 1u);
+                phases ^= 1u << (ck & 1);
             } else {
                 if (blockDim.x == 256) {
 #pragma unroll
@@ -521,7 +527,7 @@ void build_frag_tables(fraq_ctx c, HistDevice& d) {
 
 int run3_max_lag() { return D_LMAX; }
 
-void launch_run3(const RunArgs& a, int nwg, int num_sms, cudaStream_t s) {
+void launch_run3(const RunArgs& a, int nwg, int num_sms, cudaStream_t s, bool allow_tma) {
     const size_t smem = run3_smem(nwg);
     // (per launch: the attribute is per device, and a process may drive several devices)
     FRAQ_CUDA(cudaFuncSetAttribute(run3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -549,7 +555,8 @@ void launch_run3(const RunArgs& a, int nwg, int num_sms, cudaStream_t s) {
     const bool aligned = (reinterpret_cast<uintptr_t>(a.U) % 16 == 0) && (a.ldu % 2 == 0) &&
                          a.ldu >= 16 && a.n_steps >= 1 && a.n_steps < (1L << 31) &&
                          a.ldu < (1L << 31) && !std::getenv("FRAQ_NO_TMA");
-    if (encode && aligned && nwg == D_MAXWG) {
+    // (allow_tma: every group starts at an even DOF, so each box starts 16-byte aligned)
+    if (encode && aligned && allow_tma && nwg == D_MAXWG) {
         const cuuint64_t dims[2] = {(cuuint64_t)a.ldu, (cuuint64_t)a.n_steps};
         const cuuint64_t strides[1] = {(cuuint64_t)a.ldu * 8};
         const cuuint32_t box[2] = {16, (cuuint32_t)D_TC}, estr[2] = {1, 1};

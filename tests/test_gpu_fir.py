@@ -1,0 +1,184 @@
+"""GPU parity of K5e (history_fir.cu): the blocked history evaluation with the fast-decaying
+nodes folded into an exact FIR, against the CPU oracle (the reference compiled from its own
+sources when present) and against K5d on the same inputs.
+
+K5e takes over a blocked run once the history is past its first levels (path 4); K5d (path 3)
+runs the first levels and ragged tails, and the per-level kernel K5 the single pushes.  The
+short-node states K5e skips are rebuilt before any of those reads them, so every mix of the
+three paths must equal the reference's push/derivative sequence (fast_kernel.cpp:261-409).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def orc():
+    from oracle.oracle import Oracle, ref_available
+    return Oracle("reference" if ref_available() else "port")
+
+
+def kernel_from_oracle(fraq, k):
+    if k.sbd:
+        return fraq.make_sbd_kernel(k.gamma, k.tau, list(k.head), list(k.m1), list(k.r1),
+                                    list(k.m2), list(k.r2))
+    return fraq.make_be_kernel(k.gamma, k.tau, list(k.head), list(k.m1), list(k.r1))
+
+
+def make(fraq, o, variant, dim):
+    k = kernel_from_oracle(fraq, o)
+    cls = fraq.SbdHistory if o.sbd else fraq.BeHistory
+    return cls(k, getattr(fraq.HistoryVariant, variant), dim)
+
+
+def check(D, D_ref, scale, tol):
+    D, D_ref = np.asarray(D, dtype=float), np.asarray(D_ref, dtype=float)
+    assert np.array_equal(np.isnan(D), np.isnan(D_ref))
+    ok = ~np.isnan(D_ref)
+    err = np.max(np.abs(D[ok] - D_ref[ok]) / np.maximum(np.abs(D_ref[ok]), scale))
+    assert err <= tol, err
+
+
+C2_TAU = 1.0 / 65536
+
+
+@pytest.fixture(scope="module")
+def c2_kernels(orc):
+    # the C2 tables: the reference's auto-sized 256 + 256 nodes, heads 17 / 15
+    return [orc.build_kernel_auto(True, g, C2_TAU, 65536, 1e-12) for g in (0.7, 0.3)]
+
+
+@pytest.mark.parametrize("variant", ["standalone", "scheme"])
+def test_k5e_c2_tables_match_reference(fraq, orc, c2_kernels, variant):
+    """C2's kernels, 40 + 24 DOFs, 720 levels in one call: K5d on the first levels, K5e on the
+    rest; every level equals the reference history to 1e-12 of the output scale."""
+    rng = np.random.default_rng(41)
+    dims = [40, 24]
+    n = 720
+    U = rng.uniform(-1, 1, (n, sum(dims)))
+    ks = [kernel_from_oracle(fraq, o) for o in c2_kernels]
+    sch = variant == "scheme"
+    ref = np.concatenate([orc.hist_run(c2_kernels[0], U[:, :40], sch),
+                          orc.hist_run(c2_kernels[1], U[:, 40:], sch)], axis=1)
+    h = fraq.MultiHistory(ks, dims) if not sch else None
+    if sch:
+        # (MultiHistory is the standalone variant; the scheme variant through SbdHistory)
+        for c0, c1, o in ((0, 40, c2_kernels[0]), (40, 64, c2_kernels[1])):
+            hh = make(fraq, o, variant, c1 - c0)
+            D = hh.run(np.ascontiguousarray(U[:, c0:c1]))
+            assert hh.last_path == 4
+            check(D, ref[:, c0:c1], C2_TAU ** -o.gamma, 1e-12)
+        return
+    D = h.run(U)
+    assert h.last_path == 4
+    check(D[:, :40], ref[:, :40], C2_TAU ** -0.7, 1e-12)
+    check(D[:, 40:], ref[:, 40:], C2_TAU ** -0.3, 1e-12)
+
+
+def test_k5e_equals_k5d(fraq, orc, c2_kernels, monkeypatch):
+    """The same calls with K5e switched off (FRAQ_NO_K5E: everything on K5d): the two blocked
+    forms agree to a few ulps of the output scale, and so do the states they leave behind
+    (one further per-level push + derivative after the runs reads every node's state)."""
+    rng = np.random.default_rng(43)
+    o = c2_kernels[0]
+    dim, n = 32, 512
+    U = rng.uniform(-1, 1, (n + 1, dim))
+    outs, paths = [], []
+    for off in (False, True):
+        if off:
+            monkeypatch.setenv("FRAQ_NO_K5E", "1")
+        else:
+            monkeypatch.delenv("FRAQ_NO_K5E", raising=False)
+        h = make(fraq, o, "standalone", dim)
+        D = np.concatenate([h.run(U[:256]), h.run(U[256:n])])
+        paths.append(h.last_path)
+        h.push(list(U[n]))
+        D = np.concatenate([D, np.array(h.derivative())[None, :]])
+        outs.append(D)
+    assert paths == [4, 3]
+    scale = C2_TAU ** -o.gamma
+    assert np.max(np.abs(outs[0] - outs[1])) <= 2e-14 * scale * 4
+
+
+@pytest.mark.parametrize("sbd", [False, True])
+def test_k5e_mixed_with_pushes_and_ragged_calls(fraq, orc, sbd):
+    """Blocked runs of ragged lengths (K5e on the 8-level blocks, K5d on the remainders)
+    interleaved with single pushes (K5, which needs the short states rebuilt and keeps the
+    input ring current): the whole sequence equals the reference history."""
+    rng = np.random.default_rng(47 + sbd)
+    tau = 1.0 / 16384
+    o = orc.build_kernel_auto(sbd, 0.6, tau, 16384, 1e-12)
+    dim = 24
+    n = 900
+    U = rng.uniform(-1, 1, (n, dim))
+    ref = orc.hist_run(o, U)
+    h = make(fraq, o, "standalone", dim)
+    out = []
+    pos = 0
+    seen = set()
+    for ln in (200, -3, 136, 77, -2, 64, 203, -1, 214):
+        if ln < 0:
+            for _ in range(-ln):
+                h.push(list(U[pos]))
+                out.append(np.array(h.derivative())[None, :])
+                pos += 1
+        else:
+            out.append(np.asarray(h.run(U[pos:pos + ln]), dtype=float))
+            seen.add(h.last_path)
+            pos += ln
+    assert pos == n
+    assert 4 in seen
+    check(np.concatenate(out), ref, tau ** -0.6, 1e-12)
+
+
+def test_k5e_small_kernels_and_ragged_groups(fraq, orc):
+    """Groups of ragged sizes with small kernels (some with no short node at all, some with no
+    long tile per warp): tasks straddle no group boundary and every group equals its own
+    reference history.  The same with odd group starts, which TMA cannot address (boxes must
+    start 16-byte aligned): those histories stay on K5d's register-staged path."""
+    rng = np.random.default_rng(53)
+    dims = [2, 4, 16, 18, 34, 6]  # (even group starts: K5e stages its inputs by TMA)
+    taus = [1e-3, 1e-4, 1e-5, 1e-3, 1e-5, 1e-4]
+    os_ = [orc.build_be_kernel(0.25 + 0.1 * i, taus[i], 24 + 37 * i) for i in range(len(dims))]
+    ks = [kernel_from_oracle(fraq, o) for o in os_]
+    h = fraq.MultiHistory(ks, dims)
+    n = 480
+    U = rng.uniform(-1, 1, (n, sum(dims)))
+    D = np.concatenate([np.asarray(h.run(U[:200]), dtype=float),
+                        np.asarray(h.run(U[200:]), dtype=float)])
+    assert h.last_path == 4
+    c = 0
+    for o, dm, tau in zip(os_, dims, taus):
+        D_ref = orc.hist_run(o, np.ascontiguousarray(U[:, c:c + dm]))
+        check(D[:, c:c + dm], D_ref, tau ** -o.gamma, 1e-12)
+        c += dm
+    odd = [1, 3, 16, 17, 33, 6]  # total 76 (even leading dimension), odd group starts
+    h = fraq.MultiHistory(ks, odd)
+    D = np.asarray(h.run(U[:, :sum(odd)]), dtype=float)
+    assert h.last_path == 3
+    c = 0
+    for o, dm, tau in zip(os_, odd, taus):
+        D_ref = orc.hist_run(o, np.ascontiguousarray(U[:, c:c + dm]))
+        check(D[:, c:c + dm], D_ref, tau ** -o.gamma, 1e-12)
+        c += dm
+
+
+def test_k5e_long_run_device(fraq, orc, c2_kernels):
+    """run_device (device buffers, torch) in 256-level calls over 2048 levels, compared on the
+    last levels with the reference history: no drift between the FIR form and the recurrences."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(59)
+    o = c2_kernels[1]
+    dim, n = 32, 2048
+    U = rng.uniform(-1, 1, (n, dim))
+    ref = orc.hist_run(o, U)
+    k = kernel_from_oracle(fraq, o)
+    h = fraq.MultiHistory([k], [dim])
+    Ud = torch.from_numpy(U).cuda()
+    Dd = torch.empty_like(Ud)
+    for s in range(0, n, 256):
+        h.run_device(Ud.data_ptr() + s * dim * 8, dim, 256, Dd.data_ptr() + s * dim * 8, dim)
+    fraq.synchronize()
+    assert h.last_path == 4
+    check(Dd.cpu().numpy(), ref, C2_TAU ** -0.3, 1e-12)

@@ -309,7 +309,7 @@ def test_blocked_input_staging_tma_and_registers(fraq, orc, sbd, monkeypatch):
             monkeypatch.delenv("FRAQ_NO_TMA", raising=False)
         h = fraq.MultiHistory([k1, k2], [20, 28])
         D = np.concatenate([h.run(U[:300]), h.run(U[300:337]), h.run(U[337:])])
-        assert h.last_path == 3
+        assert h.last_path in (3, 4)  # K5d, or K5e once past the first levels
         outs.append(D)
     assert np.array_equal(outs[0], outs[1], equal_nan=True)
     assert np.array_equal(np.isnan(outs[0]), np.isnan(ref))
