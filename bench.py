@@ -8,10 +8,10 @@ kernels (256 + 256 nodes, N_s = 17 / 15).  Signals u_k(t) = a_k t^b_k + c_k sin(
 
 One bench step = one pass of the hot path over the batch for LEVELS_PER_STEP (1024) time levels:
 push + derivative for every DOF at every level, through MultiHistory.run_device on device buffers
-(temporally blocked kernel K5d, fp64 tensor cores).  K timed steps advance a fresh history from
-level 0; the default K = 64 covers the whole C2 horizon N = 65536.  Warm-up steps run on a
-separate history.  Each K5d launch reads and writes the 268 MB history state once (a fixed
-~0.15 ms per launch: 3% of a 1024-level step, 6% of a 512-level one).
+(temporally blocked kernels on the fp64 tensor cores: K5d for the first 96 levels of a history,
+K5e -- the fast-decaying nodes folded into an exact FIR window -- from there on).  K timed steps
+advance a fresh history from level 0; the default K = 64 covers the whole C2 horizon N = 65536.
+Warm-up steps run on a separate history.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
                     [--workload C2 | C3 | C4 | C5 | C5-SBD]     (FFPE configs: bench_ffpe.py)
@@ -319,17 +319,32 @@ def main():
     # sanity: outputs finite after the first level
     assert torch.isfinite(D[1:]).all().item()
 
-    # roofline of the dominant kernel (K5d): fp64 tensor-pipe bound; algorithmic flops per DOF-step
-    # F = 4 N_nodes + 2 N_head, averaged over the two exponent halves
+    # roofline of the dominant kernel (K5e): fp64 tensor-pipe bound; algorithmic flops per DOF-step
+    # F = 4 N_nodes + 2 N_head, averaged over the two exponent halves.  K5e
+    # EXECUTES fewer: per 16 DOFs x 8 levels 8 DMMAs per tile of 8 slow nodes + 2 per 4 rows of the
+    # combined input window (head taps + the FIR of the fast-decaying nodes); both are reported.
     F = 0.5 * sum(4 * nn + 2 * hh for nn, hh in zip(n_nodes, n_head))
     achieved_tf = F * dof_steps_local / (total_ms * 1e-3) / 1e12
+    launches = list(h.launches)
+    fir = list(h.fir_info)
+    fir_groups = [{"fir_levels": fir[3 * i], "recurrence_nodes": fir[3 * i + 1],
+                   "window_rows": fir[3 * i + 2]} for i in range(len(dims))]
+    k5e = h.last_path == 4 and all(fg["window_rows"] > 0 for fg in fir_groups)
+    if k5e:
+        dmma_blk = [8 * ((fg["recurrence_nodes"] + 7) // 8) + 2 * (fg["window_rows"] // 4)
+                    for fg in fir_groups]
+        F_exec = sum(d * 512.0 / 128.0 * dm for d, dm in zip(dmma_blk, dims)) / NL
+    else:
+        F_exec = F
+    executed_tf = F_exec * dof_steps_local / (total_ms * 1e-3) / 1e12
     dmma_peak = fraq.diag_dmma_peak()[0]   # fp64 tensor core (DMMA) stream, measured live
     fp64_peak = fraq.diag_fp64_peak()      # DFMA stream, for reference
     # HBM figures: algorithmic bytes of one state pass per level, B = 8 (2 N_nodes + 2)
     B = 0.5 * sum(8 * (2 * nn + 2) for nn in n_nodes)
     pk = peaks()
     try:  # DRAM traffic per K5d launch from the committed ncu --set full capture (profiles/)
-        tr = json.load(open(os.path.join(ROOT, "profiles", "r02", "k5d_traffic.json")))
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r02",
+                                         "k5e_traffic.json" if k5e else "k5d_traffic.json")))
         assert tr["levels_per_launch"] == LEVELS_PER_STEP
         traffic = tr["dram_bytes_per_launch"] / 1e9  # GB per launch (one step)
     except Exception:
@@ -399,15 +414,30 @@ def main():
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": c2_config(world, n_nodes, n_head, args.scaling),
             "setup": {"kernel_eps": [e for _, e in kernels], "setup_s": setup_s,
-                      "path": "MultiHistory.run_device -> K5d (temporally blocked, fp64 tensor "
-                              "cores)"},
+                      "path": "MultiHistory.run_device -> " +
+                              ("K5e (temporally blocked, fp64 tensor cores; fast-decaying nodes "
+                               "as an exact FIR window; K5d on a history's first 96 levels)"
+                               if k5e else "K5d (temporally blocked, fp64 tensor cores)"),
+                      "k5e_groups": fir_groups,
+                      "launches_by_path": dict(zip(["K5", "short_state", "K5c", "K5d", "K5e"],
+                                                   launches))},
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": dmma_peak,
                          "unit": "TFLOP/s", "frac": achieved_tf / dmma_peak,
                          "traffic": traffic, "traffic_unit": "GB per launch (ncu, profiles/)",
                          "peak_source": "measured fp64 tensor-core (DMMA) stream on this GPU "
                                         "(fraq_diag_dmma_peak); DFMA stream %.1f TF/s" % fp64_peak,
                          "dtype": "f64",
-                         "flops_per_dof_step": F, "kernel": "run3_kernel (K5d, DMMA)",
+                         "flops_per_dof_step": F,
+                         "kernel": "run4_kernel (K5e, DMMA)" if k5e else "run3_kernel (K5d, DMMA)",
+                         "executed": {"flops_per_dof_step": F_exec, "achieved": executed_tf,
+                                      "frac": executed_tf / dmma_peak,
+                                      "note": "achieved / frac above count SURVEY.md 8(d)'s "
+                                              "algorithmic flops of the reference's recurrences "
+                                              "(one state update + one readout term per node and "
+                                              "level); K5e replaces the nodes with r^M <= 2^-70 "
+                                              "by an exact M-tap FIR, so it executes fewer flops "
+                                              "and frac can exceed 1; executed.frac is the share "
+                                              "of the DMMA peak the kernel's own DMMAs reach"},
                          "hbm_equiv_gbs": B * dof_steps_local / (total_ms * 1e-3) / 1e9},
             "roofline_step_kernel": {"bound": "hbm", "achieved": hbm_step,
                                      "peak": pk.get("hbm_gbs"), "unit": "GB/s",
@@ -418,7 +448,7 @@ def main():
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": step_bytes,
                     "d2h_bytes_per_step": step_bytes, "steps": ke,
                     "path": "MultiHistory.run(host numpy) -> fraq_hist_run(FRAQ_HOST)"},
-            "gpu_launches": K,
+            "gpu_launches": int(sum(launches)),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "step_ms_min_max": [min(step_ms), max(step_ms)],

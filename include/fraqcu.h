@@ -183,8 +183,16 @@ int fraq_hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* 
                   int mem);
 /* Which kernel the last fraq_hist_run used: 0 = per-level K5 (calls under 4 levels, or more than
  * 512 nodes), 2 = K5c (lane-per-DOF DFMA blocked: FRAQ_K5C=1, or head windows over 32 levels),
- * 3 = K5d (DMMA block GEMMs, default).  (1 was the retired warp-per-4-DOF kernel K5b.) */
+ * 3 = K5d (DMMA block GEMMs; the first levels of a history and ragged tails), 4 = K5e (K5d's
+ * block GEMMs on the slow nodes + the fast-decaying nodes as an exact FIR window; the steady
+ * state, default).  (1 was the retired warp-per-4-DOF kernel K5b.) */
 int fraq_hist_last_path(fraq_hist h);
+/* Diagnostics of fraq_hist_run on this history.  launches[0..4]: kernels launched so far by
+ * path (0 per-level K5, 1 short-state rebuilds after K5e, 2 K5c, 3 K5d, 4 K5e).  fir[3 g + 0..2]
+ * for group g < n_groups: K5e's FIR length M (levels; 0 = no node folded), the nodes kept as
+ * recurrences, the combined input window (rows) -- zeros while K5e has no plan.  Either pointer
+ * may be NULL. */
+int fraq_hist_path_info(fraq_hist h, long* launches, int n_groups, int* fir);
 
 /* ---------------------------------------------------------------- direct CQ (K10)
  * The classical O(N^2) CQ sum D[n] = sum_{i<=n} d_i U[n-i] with the exact weights of

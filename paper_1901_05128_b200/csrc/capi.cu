@@ -25,6 +25,7 @@ void hist_output(fraq_hist h, int mode, double* out, int mem);
 void hist_lagged(fraq_hist h, long depth, double* out, int mem);
 void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, long ldd, int mem);
 int hist_last_path(fraq_hist h);
+void hist_path_info(fraq_hist h, long* launches, int n_groups, int* fir);
 fraq_ctx hist_ctx(fraq_hist h);
 void dst2d(fraq_ctx c, int M, int n_fields, const double* in, double* out, bool inverse, int mem);
 void dst_cols(fraq_ctx c, int M, long n_cols, const double* in, double* out, bool inverse, int mem);
@@ -327,6 +328,10 @@ int fraq_hist_last_path(fraq_hist h) {
     if (!h) return -1;
     std::lock_guard<std::recursive_mutex> lock(hist_ctx(h)->mu);
     return hist_last_path(h);
+}
+
+int fraq_hist_path_info(fraq_hist h, long* launches, int n_groups, int* fir) {
+    return guarded_hist(h, [&] { hist_path_info(h, launches, n_groups, fir); });
 }
 
 // ------------------------------------------------------------------ direct CQ

@@ -236,6 +236,7 @@ DeviceHistory::DeviceHistory(const std::vector<fraq_kernel_t>& kernels,
                            variant == HistoryVariant::standalone ? FRAQ_STANDALONE : FRAQ_SCHEME,
                            &h_));
     dim_ = (std::size_t)total;
+    n_groups_ = kernels.size();
     lag_.resize(dim_);
 }
 
@@ -244,7 +245,7 @@ DeviceHistory::~DeviceHistory() {
 }
 
 DeviceHistory::DeviceHistory(DeviceHistory&& o) noexcept
-    : h_(o.h_), dim_(o.dim_), lag_(std::move(o.lag_)) {
+    : h_(o.h_), dim_(o.dim_), n_groups_(o.n_groups_), lag_(std::move(o.lag_)) {
     o.h_ = nullptr;
 }
 
@@ -253,6 +254,7 @@ DeviceHistory& DeviceHistory::operator=(DeviceHistory&& o) noexcept {
         if (h_) fraq_hist_destroy(h_);
         h_ = o.h_;
         dim_ = o.dim_;
+        n_groups_ = o.n_groups_;
         lag_ = std::move(o.lag_);
         o.h_ = nullptr;
     }
@@ -298,6 +300,16 @@ void DeviceHistory::run(const double* U, long ldu, long n_steps, double* D, long
     check(fraq_hist_run(h_, U, ldu, n_steps, D, ldd, mem));
 }
 int DeviceHistory::last_path() const { return fraq_hist_last_path(h_); }
+std::vector<long> DeviceHistory::launches() const {
+    std::vector<long> out(5, 0);
+    check(fraq_hist_path_info(h_, out.data(), 0, nullptr));
+    return out;
+}
+std::vector<int> DeviceHistory::fir_info() const {
+    std::vector<int> out(3 * n_groups_, 0);
+    check(fraq_hist_path_info(h_, nullptr, (int)n_groups_, out.data()));
+    return out;
+}
 
 BeHistory::BeHistory(const FastKernelBE& k, HistoryVariant v, std::size_t dim)
     : DeviceHistory({to_flat(k)}, {(long)dim}, v) {}

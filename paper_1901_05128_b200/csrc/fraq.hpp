@@ -146,11 +146,15 @@ public:
     /// n_steps x (push U row; derivative -> D row).  mem: FRAQ_HOST or FRAQ_DEVICE.
     void run(const double* U, long ldu, long n_steps, double* D, long ldd, int mem = FRAQ_HOST);
     int last_path() const;
+    /// kernels launched by path (fraq_hist_path_info) and K5e's per-group (M, long nodes, window)
+    std::vector<long> launches() const;
+    std::vector<int> fir_info() const;
     fraq_hist handle() const { return h_; }
 
 private:
     fraq_hist h_ = nullptr;
     std::size_t dim_ = 0;
+    std::size_t n_groups_ = 0;
     mutable std::vector<double> lag_;
 };
 

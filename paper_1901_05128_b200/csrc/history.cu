@@ -590,6 +590,7 @@ struct fraq_hist_s {
     DevBuf<int2> run3_tasks;   // (group, first DOF of a 16-DOF tile) for K5d
     int n_run3_tasks = 0;
     int last_path = 0;
+    long launches[5] = {0, 0, 0, 0, 0};  // by path (1: short-state rebuilds)
     // chunk staging for host-memory runs
     static constexpr int kMaxStages = 4;
     DevBuf<double> ubuf[kMaxStages], dbuf[kMaxStages];
@@ -662,7 +663,7 @@ void flush(fraq_hist h, int mode, double* out_d) {
     a.out = out_d;
     if (!a.adv && !a.app && mode == MODE_NONE) return;
     fir_materialize(h->ctx, h->d, h->appended);  // K5 reads every node's state
-    if (h->pending) fir_note_inputs(h->ctx, h->d, h->appended, h->stage.p, h->d.total_dim, 1);
+    if (h->pending) h->d.fir.xh_valid = 0;  // (single pushes are not recorded in K5e's input ring)
     h->d.launch_step(h->ctx, a);
     if (h->pending) {
         if (h->appended > 0) h->level += 1;
@@ -705,6 +706,8 @@ void hist_create(fraq_ctx c, int n_groups, const fraq_kernel_t* const* ks, const
         if (!t3.empty())
             FRAQ_CUDA(cudaMemcpy(h->run3_tasks.p, t3.data(), t3.size() * sizeof(int2),
                                  cudaMemcpyHostToDevice));
+        // K5e plan (host tables, input ring) with the history, not inside its first run
+        if (h->d.max_L <= run3_max_lag() && !std::getenv("FRAQ_K5C")) build_fir_plan(c, h->d);
         h->n_run2_tasks = (int)t2.size();
         h->run2_tasks.alloc(std::max<size_t>(1, t2.size()));
         if (!t2.empty())
@@ -756,7 +759,7 @@ void hist_append(fraq_hist h, const double* v, int mem) {
     StepArgs a = base_args(h);
     a.app = 1;
     a.u = h->stage.p;
-    fir_note_inputs(h->ctx, h->d, h->appended, h->stage.p, h->d.total_dim, 1);
+    h->d.fir.xh_valid = 0;
     h->d.launch_step(h->ctx, a);
     h->appended += 1;
 }
@@ -840,6 +843,7 @@ void run_device(fraq_hist h, const double* U, long ldu, long n_steps, double* D,
                 // K5e: short nodes as an exact FIR, long nodes in K5d's block form
                 m = rest & ~7L;
                 h->last_path = 4;
+                ++h->launches[4];
                 launch_run4(h->ctx, h->d, h->run3_tasks.p, h->n_run3_tasks, h->counter.p, A0, Uc,
                             ldu, m, Dc, ldd);
             } else {
@@ -851,6 +855,7 @@ void run_device(fraq_hist h, const double* U, long ldu, long n_steps, double* D,
                     const long pre = (s - A0 + 31) / 32 * 32;
                     if (pre > 0 && pre + 64 <= rest) m = pre;
                 }
+                if (h->d.fir.short_stale) ++h->launches[1];
                 fir_materialize(h->ctx, h->d, A0);
                 a.A0 = A0;
                 a.n_steps = m;
@@ -859,6 +864,7 @@ void run_device(fraq_hist h, const double* U, long ldu, long n_steps, double* D,
                 if (k5d) {
                     // K5d (DMMA block formulation)
                     h->last_path = 3;
+                    ++h->launches[3];
                     build_frag_tables(h->ctx, h->d);
                     a.tasks = h->run3_tasks.p;
                     a.n_tasks = h->n_run3_tasks;
@@ -867,6 +873,7 @@ void run_device(fraq_hist h, const double* U, long ldu, long n_steps, double* D,
                                 h->ctx->stream, even_groups);
                 } else {
                     h->last_path = 2;
+                    ++h->launches[2];
                     a.tasks = h->run2_tasks.p;
                     a.n_tasks = h->n_run2_tasks;
                     launch_run2(a, std::max(1, P), h->ctx->num_sms, h->ctx->stream);
@@ -892,8 +899,9 @@ void run_device(fraq_hist h, const double* U, long ldu, long n_steps, double* D,
             if (!G.sbd && h->appended + 1 < 2) ok = false;
         a.mode = (D && ok) ? MODE_DERIV : MODE_NONE;
         a.out = D ? D + n * ldd : nullptr;
-        fir_note_inputs(h->ctx, h->d, h->appended, a.u, h->d.total_dim, 1);
+        h->d.fir.xh_valid = 0;
         h->d.launch_step(h->ctx, a);
+        ++h->launches[0];
         if (D && !ok) {
             // derivative undefined on the first BE push: NaN row (the reference throws)
             std::vector<double> nan(h->d.total_dim, NAN);
@@ -984,6 +992,17 @@ void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, l
 }
 
 int hist_last_path(fraq_hist h) { return h->last_path; }
+void hist_path_info(fraq_hist h, long* launches, int n_groups, int* fir) {
+    if (launches)
+        for (int i = 0; i < 5; ++i) launches[i] = h->launches[i];
+    if (fir)
+        for (int g = 0; g < n_groups; ++g) {
+            const bool have = h->d.fir.ok && g < (int)h->d.fir.groups_h.size();
+            fir[3 * g + 0] = have ? h->d.fir.groups_h[g].M : 0;
+            fir[3 * g + 1] = have ? h->d.fir.groups_h[g].JL : 0;
+            fir[3 * g + 2] = have ? h->d.fir.groups_h[g].KW : 0;
+        }
+}
 fraq_ctx hist_ctx(fraq_hist h) { return h->ctx; }
 
 }  // namespace fraqcu

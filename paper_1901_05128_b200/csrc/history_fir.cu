@@ -126,7 +126,9 @@ __device__ __forceinline__ void run_task(const Run4Args& A, const TaskCtx& c, co
     const int L = G.L, KW = F->KW, NTW = F->NTW;
     const long ld = G.ld;
     const int kk0 = F->kk0[warp], kk1 = F->kk0[warp + 1];
-    // state fragments Y[rb][ntl][e]: DOF tk.y + 8 rb + g, long position 8 tile + 2t + e
+    // state fragments Y[rb][ntl][e]: DOF tk.y + 2g + rb, long position 8 tile + 2t + e.  (Row g
+    // of row block rb is DOF 2g + rb: a lane's two A operands of an input row are then adjacent
+    // -- one 128-bit LDS, each 128-byte row one wavefront -- and so are its partial outputs)
     double Y[2][NY][2];
     const int* pm = A.perm + F->perm_off + 8 * (warp * NTW) + 2 * t;
 #pragma unroll
@@ -136,7 +138,7 @@ __device__ __forceinline__ void run_task(const Run4Args& A, const TaskCtx& c, co
             const int j = pm[8 * ntl + e];
 #pragma unroll
             for (int rb = 0; rb < 2; ++rb) {
-                const int m = tk.y + 8 * rb + g;
+                const int m = tk.y + 2 * g + rb;
                 Y[rb][ntl][e] = (j >= 0 && m < G.dim) ? A.state[G.st_off + j * ld + m] : 0.0;
             }
         }
@@ -208,18 +210,21 @@ __device__ __forceinline__ void run_task(const Run4Args& A, const TaskCtx& c, co
 #pragma unroll 2
                 for (int kk = kk0; kk < kk1; ++kk) {
                     const double b = Hl[kk * 32];
-                    const double* xr = X + ((w0 + 4 * kk) & mask) * 16 + g;
-                    dmma(sacc[0], xr[0], b);
-                    dmma(sacc[1], xr[8], b);
+                    const double2 a = *reinterpret_cast<const double2*>(
+                        X + ((w0 + 4 * kk) & mask) * 16 + 2 * g);
+                    dmma(sacc[0], a.x, b);
+                    dmma(sacc[1], a.y, b);
                 }
             }
             double vf[2][2];
             if (NT > 0) {
 #pragma unroll
-                for (int rb = 0; rb < 2; ++rb)
-#pragma unroll
-                    for (int h = 0; h < 2; ++h)
-                        vf[rb][h] = X[((q0 + 4 * h + t - L) & mask) * 16 + 8 * rb + g];
+                for (int h = 0; h < 2; ++h) {
+                    const double2 a = *reinterpret_cast<const double2*>(
+                        X + ((q0 + 4 * h + t - L) & mask) * 16 + 2 * g);
+                    vf[0][h] = a.x;
+                    vf[1][h] = a.y;
+                }
             }
             if (mid_reduce) reduce_pair();
             // ---- state: Y <- r^8 (.) Y + V R (rescale DMULs first, as in K5d)
@@ -240,11 +245,10 @@ __device__ __forceinline__ void run_task(const Run4Args& A, const TaskCtx& c, co
 #pragma unroll
                     for (int rb = 0; rb < 2; ++rb) dmma(Y[rb][ntl], vf[rb][h], b);
                 }
-#pragma unroll
-            for (int rb = 0; rb < 2; ++rb) {
-                pw[(2 * t) * 16 + 8 * rb + g] = sacc[rb][0];
-                pw[(2 * t + 1) * 16 + 8 * rb + g] = sacc[rb][1];
-            }
+            *reinterpret_cast<double2*>(pw + (2 * t) * 16 + 2 * g) =
+                make_double2(sacc[0][0], sacc[1][0]);
+            *reinterpret_cast<double2*>(pw + (2 * t + 1) * 16 + 2 * g) =
+                make_double2(sacc[0][1], sacc[1][1]);
         };
         for (int t0 = 0; t0 < tmax; t0 += 2 * E_TB) {
             const int nblk = t0 + E_TB < tmax ? 2 : 1;
@@ -267,7 +271,7 @@ __device__ __forceinline__ void run_task(const Run4Args& A, const TaskCtx& c, co
             const int j = pm[8 * ntl + e];
 #pragma unroll
             for (int rb = 0; rb < 2; ++rb) {
-                const int m = tk.y + 8 * rb + g;
+                const int m = tk.y + 2 * g + rb;
                 if (j >= 0 && m < G.dim) A.state[G.st_off + j * ld + m] = Y[rb][ntl][e];
             }
         }
@@ -416,9 +420,19 @@ void build_fir_plan(fraq_ctx c, HistDevice& d) {
         const int taps = G.sbd ? G.L : 2;
         // candidate FIR lengths: the DMMA count of a block is 4 per long tile and rb, 1 per
         // window k-step and rb; windows up to 72 rows fit the 128-row shared-memory ring
-        auto is_short = [&](int j, int M) {
-            return M > 0 && std::pow(std::fabs((long double)r[j]), (long double)M) <= thr;
+        // |r|^M for M = 8, 16, ..., 96 by repeated squaring-free products (host, once per history)
+        std::vector<long double> r8(G.J);
+        for (int j = 0; j < G.J; ++j) {
+            long double a = std::fabs((long double)r[j]), p = a;
+            for (int q = 1; q < 8; ++q) p *= a;
+            r8[j] = p;
+        }
+        auto rpow = [&](int j, int M) {  // M a multiple of 8
+            long double p = 1.0L;
+            for (int q = 0; q < M / 8; ++q) p *= r8[j];
+            return p;
         };
+        auto is_short = [&](int j, int M) { return M > 0 && rpow(j, M) <= thr; };
         auto cost = [&](int M) {
             int jl = 0;
             for (int j = 0; j < G.J; ++j) jl += !is_short(j, M);
@@ -438,7 +452,7 @@ void build_fir_plan(fraq_ctx c, HistDevice& d) {
         for (int j = 0; j < G.J; ++j)
             if (is_short(j, M)) {
                 const long double a = std::fabs((long double)r[j]);
-                tail += std::fabs((long double)f[j]) * std::pow(a, (long double)M) / (1.0L - a);
+                tail += std::fabs((long double)f[j]) * rpow(j, M) / (1.0L - a);
             }
         if (!(tail <= std::pow(2.0L, -60.0L) * std::fabs((long double)hd[0]))) M = 0;
         std::vector<int> lng, sht;
@@ -474,10 +488,14 @@ void build_fir_plan(fraq_ctx c, HistDevice& d) {
         // the long nodes' in-block part wL_(i-L) on the rows of this block's own feeds
         // (jj >= KW - 8 - L, i.e. v_i' with i' = jj - (KW - 8 - L) <= k)
         std::vector<long double> wS(std::max(1, M), 0.0L), wL(8, 0.0L);
-        for (int m = 0; m < M; ++m)
-            for (int j : sht) wS[m] += (long double)f[j] * std::pow((long double)r[j], (long double)m);
-        for (int m = 0; m < 8; ++m)
-            for (int j : lng) wL[m] += (long double)f[j] * std::pow((long double)r[j], (long double)m);
+        for (int j : sht) {
+            long double p = (long double)f[j];
+            for (int m = 0; m < M; ++m, p *= (long double)r[j]) wS[m] += p;
+        }
+        for (int j : lng) {
+            long double p = (long double)f[j];
+            for (int m = 0; m < 8; ++m, p *= (long double)r[j]) wL[m] += p;
+        }
         for (int kk = 0; kk < F.nkk; ++kk)
             for (int lane = 0; lane < 32; ++lane) {
                 const int gg = lane >> 2, tt = lane & 3, jj = 4 * kk + tt, k = gg;
@@ -492,8 +510,9 @@ void build_fir_plan(fraq_ctx c, HistDevice& d) {
         tabs.insert(tabs.end(), R.begin(), R.end());
         tabs.insert(tabs.end(), H.begin(), H.end());
     }
-    // warps per CTA: ~32 DMMA pairs per warp and block, every group's tiles must fit
-    int nwg = std::max(1, std::min(E_MAXWG, (units_max + 31) / 32));
+    // warps per CTA: ~24 DMMA pairs per warp and block (C2: 4 warps, 3.46e10 DOF-steps/s; 3 warps
+    // 3.33e10, 5 warps 3.18e10), every group's tiles must fit
+    int nwg = std::max(1, std::min(E_MAXWG, (units_max + 23) / 24));
     if (const char* e = std::getenv("FRAQ_K5E_NWG")) nwg = std::max(1, std::min(E_MAXWG, std::atoi(e)));
     for (const FirGroup& F : P.groups_h) nwg = std::max(nwg, (F.TL + E_NT - 1) / E_NT);
     P.nwg = nwg;
@@ -552,22 +571,38 @@ void build_fir_plan(fraq_ctx c, HistDevice& d) {
     P.ok = true;
 }
 
+namespace {
+// rows [n0, n0 + cnt) of U -> the input ring (a kernel, not cudaMemcpy2DAsync: device-to-device
+// copies go through the copy engines that the host path's H2D / D2H transfers are using)
+__global__ void note_rows_kernel(const double* U, long ldu, long A0, long n0, long cnt, long dim,
+                                 double* xh, int xh_mask) {
+    const long per = (dim + 1) / 2;  // double2 units per row (dim even: K5e's precondition)
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < cnt * per;
+         i += (long)gridDim.x * blockDim.x) {
+        const long row = i / per, c = 2 * (i % per), n = n0 + row;
+        const double* src = U + (n - A0) * ldu + c;
+        double* dst = xh + (size_t)(n & xh_mask) * dim + c;
+        if (c + 1 < dim && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+            *reinterpret_cast<double2*>(dst) = *reinterpret_cast<const double2*>(src);
+        } else {
+            dst[0] = src[0];
+            if (c + 1 < dim) dst[1] = src[1];
+        }
+    }
+}
+}  // namespace
+
 // Appends the call's last input rows to the HBM input ring (row = level & (xh_rows - 1)).
 void fir_note_inputs(fraq_ctx c, HistDevice& d, long A0, const double* U, long ldu, long n_steps) {
     FirPlan& P = d.fir;
     if (!P.ok || n_steps <= 0 || d.total_dim == 0) return;
     const long keep = std::min<long>(n_steps, P.kw_max + 8);
     const long dim = d.total_dim;
-    long n = A0 + n_steps - keep;  // first level copied
-    long left = keep;
-    while (left > 0) {
-        const long row = n & (P.xh_rows - 1);
-        const long cnt = std::min<long>(left, P.xh_rows - row);
-        FRAQ_CUDA(cudaMemcpy2DAsync(P.xh.p + row * dim, dim * 8, U + (n - A0) * ldu, ldu * 8,
-                                    dim * 8, cnt, cudaMemcpyDeviceToDevice, c->stream));
-        n += cnt;
-        left -= cnt;
-    }
+    const long n = A0 + n_steps - keep;  // first level copied
+    const long units = keep * ((dim + 1) / 2);
+    const int grid = (int)std::max<long>(1, std::min<long>((units + 255) / 256, 4L * c->num_sms));
+    note_rows_kernel<<<grid, 256, 0, c->stream>>>(U, ldu, A0, n, keep, dim, P.xh.p, P.xh_rows - 1);
+    FRAQ_LAUNCH_CHECK();
     // (a longer call leaves only its copied rows valid: the older rows belong to other levels)
     P.xh_valid = n_steps > keep ? keep : std::min<long>(P.xh_rows, P.xh_valid + n_steps);
 }

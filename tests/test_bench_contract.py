@@ -55,8 +55,13 @@ def test_gpu_arm_contract():
     assert KEYS <= set(d) and "impl" not in d
     assert d["value"] > 1e9 and d["n_gpus"] == 1 and d["scaling"] == "weak"
     rf = d["roofline"]
-    assert rf["bound"] in ("hbm", "tensor") and 0 < rf["frac"] <= 1.05
+    # frac counts SURVEY.md 8(d)'s algorithmic flops (the reference's recurrences), which K5e
+    # undercuts by folding the fast-decaying nodes into a FIR: only the executed share is <= 1
+    assert rf["bound"] in ("hbm", "tensor") and 0 < rf["frac"] <= 3.0
     assert rf["achieved"] == pytest.approx(rf["frac"] * rf["peak"], rel=1e-9)
+    ex = rf["executed"]
+    assert 0 < ex["frac"] <= 1.05 and ex["flops_per_dof_step"] <= rf["flops_per_dof_step"]
+    assert ex["achieved"] == pytest.approx(ex["frac"] * rf["peak"], rel=1e-9)
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] >= d["steps"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
