@@ -45,8 +45,8 @@ def launches(path):
 
 
 def role(name):
-    if "run3_kernel" in name or "k13_kernel" in name:
-        return "timed step"
+    if any(x in name for x in ("run3_kernel", "run4_kernel", "note_rows_kernel", "k13_kernel")):
+        return "timed step (and its e2e / warm-up repeats)"
     if "dmma_kernel" in name or "dfma_kernel" in name:
         return "peak diagnostic"
     if any(x in name for x in ("scan_kernel", "chain_kernel", "cauchy_kernel", "rule_kernel",
