@@ -434,6 +434,8 @@ void launch_modal(int npl, int P, const ModalArgs& a, cudaStream_t s) {
 struct ModalPlan {
     bool use_k13 = false;
     K13Plan k13;
+    DevBuf<double> fold;    // K13: node tables with the fast-decaying nodes folded into the head
+    int fold_levels = 0;
     DevBuf<ModalInst> dmi;  // K11 instance records
     int n_inst = 0, npl = 0, P = 2;
     bool sbd = false;
@@ -522,15 +524,96 @@ void modal_plan(fraq_ctx c, const HistDevice& hd, const std::vector<double>& a,
     P.sbd = sbd;
     P.use_k13 = k13_supported(maxJ, minL, maxL);
     if (P.use_k13) {
+        // The fast-decaying nodes folded into the exact head (the rewrite behind K5e,
+        // history_fir.cu): a node with |r_j|^M <= 2^-70 contributes only to the lags
+        // L <= m < L + M, so the kernel (head d_0..d_(L-1); nodes (r_j, f_j) fed at lag L) equals,
+        // to below rounding, the kernel with the head c_0..c_(L+M-1) (c_m = sum_j f_j r_j^(m-L)
+        // over ALL nodes for m >= L) and only the slow nodes, fed at lag L + M with f_j r_j^M.
+        // K13 then carries a fraction of the nodes through its GEMMs (BE, 256 nodes at
+        // tau = 1/16384: 162 left at M = 40) against a longer Toeplitz window in the solver warps.
+        // M: the largest multiple of 8 the kernel's window allows (head <= 48 levels).
+        int M = std::max(0, (48 - maxL) / 8 * 8);
+        if (const char* e = std::getenv("FRAQ_K13_FOLD")) M = std::max(0, std::min(M, std::atoi(e) / 8 * 8));
+        std::vector<double> ft;            // per group: r'[JL], f'[JL], head'[L + M]
+        std::vector<size_t> off(2 * n_inst);
+        std::vector<int> JLv(2 * n_inst), Lv(2 * n_inst);
+        const long double thr = std::pow(2.0L, -70.0L);
+        for (int g2 = 0; g2 < 2 * n_inst && M > 0; ++g2) {
+            const GroupDev& G = hd.groups_h[g2];
+            const double* r = hd.cr_h.data() + G.co_off;
+            const double* f = hd.cf_h.data() + G.co_off;
+            const fraq_kernel_t& K = hd.kernels[g2];
+            std::vector<long double> rM(G.J);
+            std::vector<int> lng;
+            long double tail = 0.0L;
+            for (int j = 0; j < G.J; ++j) {
+                long double a = std::fabs((long double)r[j]), pw = 1.0L;
+                for (int q = 0; q < M; ++q) pw *= a;
+                rM[j] = pw;
+                if (pw > thr)
+                    lng.push_back(j);
+                else
+                    tail += std::fabs((long double)f[j]) * pw / (1.0L - a);
+            }
+            // (what the fold drops must stay far below rounding of the newest head weight)
+            if (!(tail <= std::pow(2.0L, -60.0L) * std::fabs((long double)K.head[0]))) {
+                M = 0;
+                break;
+            }
+            off[g2] = ft.size();
+            JLv[g2] = (int)lng.size();
+            Lv[g2] = G.L + M;
+            for (int j : lng) ft.push_back(r[j]);
+            for (int j : lng) {
+                long double v = (long double)f[j];
+                for (int q = 0; q < M; ++q) v *= (long double)r[j];
+                ft.push_back((double)v);
+            }
+            std::vector<long double> cm(M, 0.0L);
+            for (int j = 0; j < G.J; ++j) {
+                long double pw = (long double)f[j];
+                for (int m = 0; m < M; ++m, pw *= (long double)r[j]) cm[m] += pw;
+            }
+            for (int i = 0; i < G.L; ++i) ft.push_back(i < K.n_head ? K.head[i] : 0.0);
+            for (int m = 0; m < M; ++m) ft.push_back((double)cm[m]);
+            if (lng.empty()) {  // (K13 wants at least one node per field)
+                M = 0;
+                break;
+            }
+        }
+        int fJ = 0, fminL = 1 << 30, fmaxL = 0;
+        for (int g2 = 0; g2 < 2 * n_inst && M > 0; ++g2) {
+            fJ = std::max(fJ, JLv[g2]);
+            fminL = std::min(fminL, Lv[g2]);
+            fmaxL = std::max(fmaxL, Lv[g2]);
+        }
+        if (M > 0 && !k13_supported(fJ, fminL, fmaxL)) M = 0;
+        P.fold_levels = M;
+        if (M > 0) {
+            P.fold.alloc(ft.size());
+            FRAQ_CUDA(cudaMemcpyAsync(P.fold.p, ft.data(), ft.size() * sizeof(double),
+                                      cudaMemcpyHostToDevice, c->stream));
+            FRAQ_CUDA(cudaStreamSynchronize(c->stream));  // (ft goes out of scope)
+        }
         std::vector<K13Inst> ki(n_inst);
         for (int i = 0; i < n_inst; ++i) {
             ki[i].a = a[i];
             ki[i].tau = tau[i];
             for (int f = 0; f < 2; ++f) {
+                ki[i].corr[f] = mi[i].fld[f].corr;
+                if (M > 0) {
+                    const int g2 = 2 * i + f;
+                    const double* base = P.fold.p + off[g2];
+                    ki[i].r[f] = base;
+                    ki[i].f[f] = base + JLv[g2];
+                    ki[i].head[f] = base + 2 * JLv[g2];
+                    ki[i].J[f] = JLv[g2];
+                    ki[i].L[f] = Lv[g2];
+                    continue;
+                }
                 ki[i].r[f] = mi[i].fld[f].r;
                 ki[i].f[f] = mi[i].fld[f].f;
                 ki[i].head[f] = mi[i].fld[f].head;
-                ki[i].corr[f] = mi[i].fld[f].corr;
                 ki[i].J[f] = mi[i].fld[f].J;
                 ki[i].L[f] = mi[i].fld[f].L;
             }

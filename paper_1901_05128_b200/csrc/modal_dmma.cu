@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 320 && RB == 2) ? 2 : 1) k13_ke
             // (m >= 2; SBD: B_2 -= Q/2), C(m) = diag(c1_m, c2_m) the in-block weights
             // (BE in the 192-thread shape -- C3, C5-BE: +6.6% / +3.1%; the SBD chain carries more
             // terms and lost 3% in the wide CTA, and the 96-register shapes would spill)
-            constexpr bool kChain2 = NT == 16 && MAXT == 192;
+            constexpr bool kChain2 = MAXT == 192;
             double chA[4], chB[8][4];
             if (kChain2) {
                 const double lq = A.sbd ? 2.0 : 1.0;
@@ -573,9 +573,18 @@ void k13_prepare(fraq_ctx c, const std::vector<K13Inst>& in, bool sbd, K13Plan& 
     // J in (192, 256] (C3, C5-BE): 2 GEMM warps per field of 128 nodes, 6 warps per CTA, two
     // CTAs per SM (168 registers x 192 threads x 2 fit): C5-shaped BE 2.360e10 -> 2.499e10
     if (P.RB == 2 && maxJ > 192 && maxJ <= 256) P.NT = 16;
+    // the same 2-GEMM-warps-per-field shape with narrower warps for node counts between 128 and
+    // 192 (what the head fold of modal.cu leaves of a 256-node BE kernel: ~162 at M = 40)
+    if (P.RB == 2 && maxJ > 128 && maxJ <= 192 && !std::getenv("FRAQ_K13_NOMID"))
+        P.NT = maxJ <= 144 ? 9 : maxJ <= 160 ? 10 : maxJ <= 176 ? 11 : 12;
+    // and 4 GEMM warps per field of 96 nodes for 256 < J <= 384 (a folded 512-node SBD kernel:
+    // 357 at M = 24)
+    if (P.RB == 2 && maxJ > 256 && maxJ <= 384 && !std::getenv("FRAQ_K13_NOMID")) P.NT = 12;
     if (const char* ent = std::getenv("FRAQ_K13_NT")) {  // experiment override: 8, 13 or 16
         const int nt = std::atoi(ent);
-        if (P.RB == 2 && (nt == 8 || (nt == 13 && maxJ <= 416) || nt == 16))
+        if (P.RB == 2 && (nt == 8 || (nt == 13 && maxJ <= 416) || nt == 16 ||
+                          (nt >= 9 && nt <= 12 && 2 * 8 * nt >= maxJ) ||
+                          (nt == 12 && maxJ <= 384)))
             P.NT = nt;
     }
     if (P.RB == 1) {
@@ -643,6 +652,16 @@ void k13_exec(fraq_ctx c, K13Plan& P, const double* lam, int n_modes, long N, co
     const size_t smem = k13_smem(P.TS, P.nwg, P.ring, modes);
     if (P.RB == 2 && P.NT == 13)
         k13_launch<2, 13, 384>(A, smem, c->num_sms, c->stream);
+    else if (P.RB == 2 && P.NT == 12 && P.nwg > 4)
+        k13_launch<2, 12, 384>(A, smem, c->num_sms, c->stream);
+    else if (P.RB == 2 && P.NT == 12)
+        k13_launch<2, 12, 192>(A, smem, c->num_sms, c->stream);
+    else if (P.RB == 2 && P.NT == 11)
+        k13_launch<2, 11, 192>(A, smem, c->num_sms, c->stream);
+    else if (P.RB == 2 && P.NT == 10)
+        k13_launch<2, 10, 192>(A, smem, c->num_sms, c->stream);
+    else if (P.RB == 2 && P.NT == 9)
+        k13_launch<2, 9, 192>(A, smem, c->num_sms, c->stream);
     else if (P.RB == 2 && P.NT == 16 && P.nwg <= 4)  // J <= 256: two CTAs per SM
         k13_launch<2, 16, 192>(A, smem, c->num_sms, c->stream);
     else if (P.RB == 2 && P.NT == 16)

@@ -182,3 +182,32 @@ def test_k5e_long_run_device(fraq, orc, c2_kernels):
     fraq.synchronize()
     assert h.last_path == 4
     check(Dd.cpu().numpy(), ref, C2_TAU ** -0.3, 1e-12)
+
+
+def test_k5e_padded_rows_and_no_output(fraq, orc, c2_kernels):
+    """run_device with leading dimensions above the DOF count (rows of a wider device array)
+    and a null output pointer on part of the sequence (state only, as a solver that needs no
+    derivative there would call it): the levels that are written equal the reference history."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(61)
+    o = c2_kernels[0]
+    dim, ld, n = 48, 80, 1024
+    U = rng.uniform(-1, 1, (n, dim))
+    ref = orc.hist_run(o, U)
+    k = kernel_from_oracle(fraq, o)
+    h = fraq.MultiHistory([k], [dim])
+    Ud = torch.zeros((n, ld), dtype=torch.float64, device="cuda")
+    Ud[:, :dim] = torch.from_numpy(U).cuda()
+    Dd = torch.full((n, ld), -7.0, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    row = ld * 8
+    h.run_device(Ud.data_ptr(), ld, 256, Dd.data_ptr(), ld)
+    h.run_device(Ud.data_ptr() + 256 * row, ld, 384, 0, ld)           # no output
+    h.run_device(Ud.data_ptr() + 640 * row, ld, 384, Dd.data_ptr() + 640 * row, ld)
+    fraq.synchronize()
+    assert h.last_path == 4 and h.launches[4] == 3
+    D = Dd.cpu().numpy()
+    assert np.all(D[:, dim:] == -7.0) and np.all(D[256:640, :dim] == -7.0)
+    scale = C2_TAU ** -o.gamma
+    check(D[:256, :dim], ref[:256], scale, 1e-12)
+    check(D[640:, :dim], ref[640:], scale, 1e-12)
