@@ -531,8 +531,11 @@ void modal_plan(fraq_ctx c, const HistDevice& hd, const std::vector<double>& a,
         // over ALL nodes for m >= L) and only the slow nodes, fed at lag L + M with f_j r_j^M.
         // K13 then carries a fraction of the nodes through its GEMMs (BE, 256 nodes at
         // tau = 1/16384: 162 left at M = 40) against a longer Toeplitz window in the solver warps.
-        // M: the largest multiple of 8 the kernel's window allows (head <= 48 levels).
-        int M = std::max(0, (48 - maxL) / 8 * 8);
+        // M: the largest multiple of 8 that keeps the head within `lcap` levels.
+        // (head caps swept on B200, profiles/r02/k13_fold3.sh: SBD best at 72-96 levels, BE at 64)
+        int lcap = sbd ? 72 : 64;
+        if (const char* e = std::getenv("FRAQ_K13_LCAP")) lcap = std::atoi(e);  // experiment
+        int M = std::max(0, (lcap - maxL) / 8 * 8);
         if (const char* e = std::getenv("FRAQ_K13_FOLD")) M = std::max(0, std::min(M, std::atoi(e) / 8 * 8));
         std::vector<double> ft;            // per group: r'[JL], f'[JL], head'[L + M]
         std::vector<size_t> off(2 * n_inst);

@@ -36,7 +36,7 @@ namespace fraqcu {
 
 namespace {
 
-constexpr int K13_CW = 64;  // combined weights c_m, m < 64
+constexpr int K13_CW = 128;  // combined weights c_m, m < 128
 
 struct K13Dev {
     double a, itau;
@@ -536,12 +536,12 @@ void k13_launch(const K13Args& a, size_t smem, int num_sms, cudaStream_t s) {
 
 }  // namespace
 
-// Can K13 run these kernels?  (J <= 512 per field, lag windows fit the 64-slot ring)
+// Can K13 run these kernels?  (J <= 512 per field, lag windows fit the 128-slot ring)
 bool k13_supported(int maxJ, int minL, int maxL) {
     if (std::getenv("FRAQ_MODAL_K11")) return false;
     if (maxJ > 512 || maxJ < 1 || minL < 2) return false;
     const int delta = minL >= 8 ? 0 : 1;
-    return 8 + 8 * delta + maxL + 8 <= 64 && 7 + 8 * delta + maxL < K13_CW;
+    return 8 + 8 * delta + maxL + 8 <= 128 && 7 + 8 * delta + maxL < K13_CW;
 }
 
 void k13_prepare(fraq_ctx c, const std::vector<K13Inst>& in, bool sbd, K13Plan& P) {
@@ -601,7 +601,7 @@ void k13_prepare(fraq_ctx c, const std::vector<K13Inst>& in, bool sbd, K13Plan& 
     P.nwg = 2 * P.nwf;
     P.TS = 17 * P.Jp + K13_CW;
     const int span = 8 + 8 * P.delta + maxL + 8;
-    P.ring = span <= 32 ? 32 : 64;
+    P.ring = span <= 32 ? 32 : span <= 64 ? 64 : 128;
     std::vector<K13TabSrc> src(2 * n_inst);
     std::vector<K13Dev> dv(n_inst);
     for (int i = 0; i < n_inst; ++i) {
