@@ -1,0 +1,78 @@
+"""The identity behind K5e (history_fir.cu) and the K13 head fold (modal.cu), checked on the CPU
+against the reference's own kernels (oracle): folding the fast-decaying nodes into the head does
+not change the convolution weights the compressed kernel stands for.
+
+A fast kernel (fast_kernel.cpp:54-124) with head d_0..d_(L-1) and nodes (r_j, f_j) fed at lag L
+represents the weights  w_i = d_i (i < L),  w_i = sum_j f_j r_j^(i-L) (i >= L)
+(fast_kernel.cpp:38-52, reconstruct).  With S = {j : |r_j|^M <= 2^-70}:
+
+  head'  c_i = d_i (i < L),  c_i = sum_{all j} f_j r_j^(i-L)  (L <= i < L + M)
+  nodes' (r_j, f_j r_j^M) for j not in S, fed at lag L + M
+
+represent  w'_i = w_i  for i < L + M  and  w'_i = w_i - sum_{j in S} f_j r_j^(i-L)  beyond, and
+the dropped sum is below 2^-70 sum_S |f_j|.
+"""
+import numpy as np
+import pytest
+
+
+@pytest.fixture(scope="module")
+def orc():
+    from oracle.oracle import Oracle, ref_available
+    return Oracle("reference" if ref_available() else "port")
+
+
+def weights(head, r, f, L, n):
+    w = np.zeros(n, dtype=np.longdouble)
+    w[:L] = head[:L]
+    p = f.astype(np.longdouble).copy()
+    rl = r.astype(np.longdouble)
+    for i in range(L, n):
+        w[i] = p.sum()
+        p *= rl
+    return w
+
+
+@pytest.mark.parametrize("sbd,g,tau,M", [(True, 0.7, 1.0 / 65536, 48), (True, 0.3, 1.0 / 65536, 48),
+                                          (True, 0.55, 1.0 / 16384, 24), (False, 0.5, 1.0 / 16384, 56),
+                                          (False, 0.9, 1.0 / 16384, 40)])
+def test_fold_preserves_weights(orc, sbd, g, tau, M):
+    k = orc.build_kernel_auto(sbd, g, tau, int(round(1 / tau)), 1e-12)
+    r = np.concatenate([k.r1, k.r2])
+    m = np.concatenate([k.m1, k.m2])
+    L = k.n_head if sbd else 2
+    # feeds: BE node weights; SBD mult * ratio^(n_head - 3) (fast_kernel.cpp:337-340)
+    f = m * r ** (k.n_head - 3) if sbd else m
+    n = 4096
+    w = weights(np.asarray(k.head), r, f, L, n)
+    short = np.abs(r.astype(np.longdouble)) ** M <= np.longdouble(2.0) ** -70
+    assert short.sum() >= 0.3 * len(r)  # the fold is worth something on the reference's tables
+    rl, fl = r.astype(np.longdouble), f.astype(np.longdouble)
+    head2 = np.zeros(L + M, dtype=np.longdouble)
+    head2[:L] = np.asarray(k.head)[:L]
+    p = fl.copy()
+    for i in range(M):
+        head2[L + i] = p.sum()
+        p *= rl
+    r2 = r[~short]
+    f2 = (fl[~short] * rl[~short] ** M).astype(np.float64)
+    w2 = weights(head2.astype(np.float64), r2, f2, L + M, n)
+    scale = abs(float(k.head[0]))
+    assert float(np.max(np.abs(w2 - w))) <= 1e-15 * scale
+    # what is dropped: bounded by 2^-70 sum |f_j| / (1 - |r_j|) over the folded nodes
+    bound = float(np.sum(np.abs(fl[short]) * np.abs(rl[short]) ** M / (1 - np.abs(rl[short]))))
+    assert bound <= 2.0 ** -60 * scale
+
+
+def test_fold_sbd_is_a_kernel_rewrite(orc):
+    """For the SBD families the folded kernel is again a reference-format kernel: the feed
+    convention mult * ratio^(n_head - 3) absorbs r^M when n_head grows by M, so the node tables
+    of the kept nodes are unchanged."""
+    k = orc.build_kernel_auto(True, 0.7, 1.0 / 65536, 65536, 1e-12)
+    r = np.concatenate([k.r1, k.r2])
+    m = np.concatenate([k.m1, k.m2])
+    M = 48
+    keep = np.abs(r) ** M > 2.0 ** -70
+    f_fold = (m * r ** (k.n_head - 3))[keep] * r[keep] ** M
+    f_rewritten = m[keep] * r[keep] ** (k.n_head + M - 3)
+    assert np.max(np.abs(f_fold - f_rewritten) / np.abs(f_rewritten)) <= 1e-13

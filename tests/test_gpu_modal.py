@@ -138,6 +138,33 @@ def test_k13_warp_shapes_agree(fraq, scheme, pts, monkeypatch):
             assert rel(np.array(getattr(r.final_state, g)), ref) <= 1e-12
 
 
+@pytest.mark.parametrize("scheme,pts", [("FastBE", 140), ("FastBE", 150), ("FastBE", 170),
+                                        ("FastBE", 190), ("FastSBD", 70), ("FastSBD", 150),
+                                        ("FastSBD", 190), ("FastBE", 256), ("FastSBD", 256)])
+def test_k13_head_fold_and_mid_shapes(fraq, scheme, pts, monkeypatch):
+    """The K13 head fold (modal_plan: fast-decaying nodes moved into a longer exact head) and the
+    9..12-tile GEMM-warp shapes it needs, on a ragged mode count (1000) and level count (200,
+    past every folded head): the default (fold up to 64 / 72 head levels), no fold (the node
+    counts 140 / 150 / 170 / 190 and 2 x 150 / 2 x 190 then hit the 72 / 80 / 88 / 96-node warps
+    directly), shorter and longer head caps, all against K11 on the original tables."""
+    spec = fraq.ProblemSpec(alpha1=0.35, alpha2=0.75, coupling_a=-2.5, grid_m=1000,
+                            t_final=200.0 / 16384, n_steps=200, initial="poly_sin")
+    kc = modal_kc(fraq, auto_size=False, be_points=pts, sbd_points_1=pts, sbd_points_2=pts)
+    sch = getattr(fraq.Scheme, scheme)
+    runs = [fraq.run(spec, sch, kc)]
+    for var, val in (("FRAQ_K13_FOLD", "0"), ("FRAQ_K13_FOLD", "16"), ("FRAQ_K13_LCAP", "40"),
+                     ("FRAQ_K13_LCAP", "104")):
+        monkeypatch.setenv(var, val)
+        runs.append(fraq.run(spec, sch, kc))
+        monkeypatch.delenv(var)
+    monkeypatch.setenv("FRAQ_MODAL_K11", "1")
+    ref = fraq.run(spec, sch, kc)
+    for g in ("g1", "g2"):
+        want = np.array(getattr(ref.final_state, g))
+        for r in runs:
+            assert rel(np.array(getattr(r.final_state, g)), want) <= 1e-12
+
+
 def test_k13_batch_mixed_instances(fraq, orc):
     """C5-like batch through K13 with per-instance kernels (different J and L per field)."""
     from workloads import c5_instances
