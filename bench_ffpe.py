@@ -288,7 +288,7 @@ def run_gpu(args, rank, world, local, pg, METRIC, Clocks, fraq, torch):
     def folded(ratios, L):
         # the head fold of modal_plan (modal.cu): M = 8 floor((cap - L) / 8) levels, nodes with
         # |r|^M <= 2^-70 move into the head window; executed flops 4 N_left + 2 (L + M)
-        M = max(0, (72 if sbd else 64) - L) // 8 * 8
+        M = max(0, 80 - L) // 8 * 8
         if os.environ.get("FRAQ_K13_FOLD") is not None:
             M = max(0, min(M, int(os.environ["FRAQ_K13_FOLD"]) // 8 * 8))
         left = int(np.sum(np.abs(np.asarray(ratios)) ** M > 2.0 ** -70)) if M else len(ratios)

@@ -532,8 +532,9 @@ void modal_plan(fraq_ctx c, const HistDevice& hd, const std::vector<double>& a,
         // K13 then carries a fraction of the nodes through its GEMMs (BE, 256 nodes at
         // tau = 1/16384: 162 left at M = 40) against a longer Toeplitz window in the solver warps.
         // M: the largest multiple of 8 that keeps the head within `lcap` levels.
-        // (head caps swept on B200, profiles/r02/k13_fold3.sh: SBD best at 72-96 levels, BE at 64)
-        int lcap = sbd ? 72 : 64;
+        // (head caps swept on B200 with the window rows split between GEMM and solver warps,
+        // profiles/r02/k13_split2.sh: 80 levels best for C3 / C5-BE / C5-BDF2, 72 for C4 by 1.4%)
+        int lcap = 80;
         if (const char* e = std::getenv("FRAQ_K13_LCAP")) lcap = std::atoi(e);  // experiment
         int M = std::max(0, (lcap - maxL) / 8 * 8);
         if (const char* e = std::getenv("FRAQ_K13_FOLD")) M = std::max(0, std::min(M, std::atoi(e) / 8 * 8));

@@ -53,6 +53,7 @@ struct K13Args {
     long n_tasks;
     long N;
     int sbd, delta, ring_mask;
+    int split;            // GEMM warps take the window rows older than the previous block
     const double* c0;     // [inst][2][modes]
     double* cN;
     int* counter;
@@ -237,6 +238,25 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 320 && RB == 2) ? 2 : 1) k13_ke
 #pragma unroll
                             for (int rb = 0; rb < RB; ++rb) dmma(sacc[rb][q % NACC], Y[rb][q][e], b);
                         }
+                    if (A.split) {
+                        // ---- the known part's older rows: the solved levels up to block i - 2
+                        // (lags >= 9 from block i's first level) are in the ring by now, so their
+                        // Toeplitz terms sum_q c_(n0+k-q) G^q join this readout, shared among the
+                        // field's GEMM warps; the solver warp's critical path keeps only the 8
+                        // levels of block i - 1.  A[mode g][row t] = G^lev, B[row t][level g] = c
+                        const int Lts = 8 * A.delta + Lf, n0 = 1 + 8 * (int)i;
+                        const double* CWf = f ? cwt[1] : cwt[0];
+#pragma unroll 2
+                        for (int j0 = 4 * sl; j0 < Lts - 8; j0 += 4 * nwf) {
+                            const int j = j0 + t, lev = n0 - Lts + j;
+                            const bool ok = j < Lts - 8;
+                            const double bv = ok ? CWf[g + Lts - j] : 0.0;
+                            const double* rr = rg + (lev & mask) * MODES + g;
+#pragma unroll
+                            for (int rb = 0; rb < RB; ++rb)
+                                dmma(sacc[rb][0], (ok && lev >= 1) ? rr[8 * rb] : 0.0, bv);
+                        }
+                    }
                     double* pw = part + ((size_t)(i & 1) * nwg + warp) * 8 * MODES;
 #pragma unroll
                     for (int rb = 0; rb < RB; ++rb)
@@ -350,7 +370,8 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 320 && RB == 2) ? 2 : 1) k13_ke
                         D[nt][1] = v.y;
 #endif
                     }
-                    for (int j0 = 0; j0 < Lts; j0 += 4) {
+                    // (with A.split only the previous block's 8 levels are left here)
+                    for (int j0 = A.split ? Lts - 8 : 0; j0 < Lts; j0 += 4) {
                         const int j = j0 + t, lev = n0 - Lts + j;
                         const bool ok = j < Lts;
                         const double av = ok ? CWs[g + Lts - j] : 0.0;
@@ -645,6 +666,7 @@ void k13_exec(fraq_ctx c, K13Plan& P, const double* lam, int n_modes, long N, co
     A.sbd = P.sbd ? 1 : 0;
     A.delta = P.delta;
     A.ring_mask = P.ring - 1;
+    A.split = std::getenv("FRAQ_K13_NOSPLIT") ? 0 : 1;
     A.c0 = c0;
     A.cN = cN;
     A.counter = P.counter.p;
@@ -666,6 +688,10 @@ void k13_exec(fraq_ctx c, K13Plan& P, const double* lam, int n_modes, long N, co
         k13_launch<2, 16, 192>(A, smem, c->num_sms, c->stream);
     else if (P.RB == 2 && P.NT == 16)
         k13_launch<2, 16, 384>(A, smem, c->num_sms, c->stream);
+    else if (P.RB == 2 && P.nwg <= 4 && !std::getenv("FRAQ_K13_NOMID"))
+        // J <= 128 (what the head fold leaves of most kernels): the 192-thread, 168-register
+        // shape (the 96-register instance below spills with the window rows on the GEMM warps)
+        k13_launch<2, 8, 192>(A, smem, c->num_sms, c->stream);
     else if (P.RB == 2 && P.nwg <= 8)
         k13_launch<2, 8, 320>(A, smem, c->num_sms, c->stream);
     else if (P.RB == 2)
