@@ -26,7 +26,8 @@ int run3_max_lag();
 // history_fir.cu (K5e)
 void build_fir_plan(fraq_ctx c, HistDevice& d);
 void fir_note_inputs(fraq_ctx c, HistDevice& d, long A0, const double* U, long ldu, long n_steps);
-bool fir_eligible(const HistDevice& d, long A0, const double* U, long ldu, long n_steps);
+bool fir_eligible(const HistDevice& d, long A0, const double* U, long ldu, long n_steps,
+                  const double* D, long ldd);
 void launch_run4(fraq_ctx c, HistDevice& d, const int2* tasks, int n_tasks, int* counter, long A0,
                  const double* U, long ldu, long n_steps, double* D, long ldd);
 void fir_materialize(fraq_ctx c, HistDevice& d, long A1);
@@ -839,7 +840,7 @@ void run_device(fraq_hist h, const double* U, long ldu, long n_steps, double* D,
             double* Dc = D ? D + done * ldd : nullptr;
             long m = rest;
             FRAQ_CUDA(cudaMemsetAsync(h->counter.p, 0, sizeof(int), h->ctx->stream));
-            if (k5d && even_groups && fir_eligible(h->d, A0, Uc, ldu, rest & ~7L)) {
+            if (k5d && even_groups && fir_eligible(h->d, A0, Uc, ldu, rest & ~7L, Dc, ldd)) {
                 // K5e: short nodes as an exact FIR, long nodes in K5d's block form
                 m = rest & ~7L;
                 h->last_path = 4;

@@ -164,17 +164,48 @@ __device__ __forceinline__ void run_task(const Run4Args& A, const TaskCtx& c, co
     const double* Hl = c.Hfr + lane;
     int p_row = 0, p_nb = 0, p_buf = 0;
     auto reduce_pair = [&]() {
-        for (int o = tid; o < 2 * E_TB * 16; o += blockDim.x) {
-            const int slot = o >> 7, k = (o >> 4) & 7, d = o & 15;
+#ifdef FRAQ_EXP_NOREDUCE  // (timing experiments only: profiles/r02/k5e_variants.sh)
+        return;
+#endif
+        // one item = two adjacent DOFs of one level: 128-bit loads of the warps' partial tiles, a
+        // two-level add tree (every DADD waits behind the DMMAs on the shared fp64 pipe, so the
+        // chain depth is what costs), one 128-bit store
+        for (int o = tid; o < 2 * E_TB * 8; o += blockDim.x) {
+            const int slot = o >> 6, k = (o >> 3) & 7, d = 2 * (o & 7);
             if (slot >= p_nb) continue;
             const double* pb = part + ((size_t)(p_buf * 2 + slot) * nwg) * 128 + k * 16 + d;
-            double s0 = 0.0, s1 = 0.0;
-            for (int w = 0; w + 1 < nwg; w += 2) {
-                s0 += pb[w * 128];
-                s1 += pb[(w + 1) * 128];
+            double2 s;
+            if (nwg == 4) {
+                const double2 a0 = *reinterpret_cast<const double2*>(pb);
+                const double2 a1 = *reinterpret_cast<const double2*>(pb + 128);
+                const double2 a2 = *reinterpret_cast<const double2*>(pb + 256);
+                const double2 a3 = *reinterpret_cast<const double2*>(pb + 384);
+                s.x = (a0.x + a1.x) + (a2.x + a3.x);
+                s.y = (a0.y + a1.y) + (a2.y + a3.y);
+            } else {
+                double2 s0 = *reinterpret_cast<const double2*>(pb), s1 = make_double2(0.0, 0.0);
+                for (int w = 1; w + 1 < nwg; w += 2) {
+                    const double2 a = *reinterpret_cast<const double2*>(pb + w * 128);
+                    const double2 b = *reinterpret_cast<const double2*>(pb + (w + 1) * 128);
+                    s1.x += a.x;
+                    s1.y += a.y;
+                    s0.x += b.x;
+                    s0.y += b.y;
+                }
+                if (!(nwg & 1)) {
+                    const double2 a = *reinterpret_cast<const double2*>(pb + (nwg - 1) * 128);
+                    s1.x += a.x;
+                    s1.y += a.y;
+                }
+                s.x = s0.x + s1.x;
+                s.y = s0.y + s1.y;
             }
-            if (nwg & 1) s0 += pb[(nwg - 1) * 128];
-            if (Db && tk.y + d < G.dim) Db[(size_t)(p_row + 8 * slot + k) * A.ldd + d] = s0 + s1;
+            if (!Db) continue;
+            double* dst = Db + (size_t)(p_row + 8 * slot + k) * A.ldd + d;
+            if (tk.y + d + 1 < G.dim)
+                *reinterpret_cast<double2*>(dst) = s;  // (D 16-byte aligned, ldd even: fir_eligible)
+            else if (tk.y + d < G.dim)
+                dst[0] = s.x;
         }
     };
     int buf = 0;
@@ -205,6 +236,7 @@ __device__ __forceinline__ void run_task(const Run4Args& A, const TaskCtx& c, co
 #pragma unroll
                     for (int rb = 0; rb < 2; ++rb) dmma(sacc[rb], Y[rb][ntl][e], b);
                 }
+#ifndef FRAQ_EXP_NOFIR
             {
                 const int w0 = q0 + E_TB - KW + t;
 #pragma unroll 2
@@ -216,6 +248,7 @@ __device__ __forceinline__ void run_task(const Run4Args& A, const TaskCtx& c, co
                     dmma(sacc[1], a.y, b);
                 }
             }
+#endif
             double vf[2][2];
             if (NT > 0) {
 #pragma unroll
@@ -231,11 +264,13 @@ __device__ __forceinline__ void run_task(const Run4Args& A, const TaskCtx& c, co
 #pragma unroll
             for (int ntl = 0; ntl < NT; ++ntl) {
                 const double ra = r8w[(ntl * 2) * 32], rbv = r8w[(ntl * 2 + 1) * 32];
+#ifndef FRAQ_EXP_NODMUL
 #pragma unroll
                 for (int rb = 0; rb < 2; ++rb) {
                     Y[rb][ntl][0] *= ra;
                     Y[rb][ntl][1] *= rbv;
                 }
+#endif
             }
 #pragma unroll
             for (int h = 0; h < 2; ++h)
@@ -256,7 +291,9 @@ __device__ __forceinline__ void run_task(const Run4Args& A, const TaskCtx& c, co
             if (nblk == 2) do_block(t0 + E_TB, 1, false);
             p_row = c0 + t0;
             p_nb = nblk;
+#ifndef FRAQ_EXP_NOSYNC
             __syncthreads();
+#endif
             p_buf = buf;
             pending = true;
             buf ^= 1;
@@ -608,13 +645,16 @@ void fir_note_inputs(fraq_ctx c, HistDevice& d, long A0, const double* U, long l
 }
 
 // Can [A0, A0 + n_steps) run on K5e?  (steady state, inputs of the last kw_max levels known)
-bool fir_eligible(const HistDevice& d, long A0, const double* U, long ldu, long n_steps) {
+bool fir_eligible(const HistDevice& d, long A0, const double* U, long ldu, long n_steps,
+                  const double* D, long ldd) {
     const FirPlan& P = d.fir;
     if (!P.ok || n_steps < 8 || (n_steps & 7) || n_steps >= (1L << 30)) return false;
     if (A0 < P.min_level || A0 < P.kw_max || P.xh_valid < P.kw_max) return false;
     if (reinterpret_cast<uintptr_t>(U) % 16 != 0 || (ldu % 2) != 0 || ldu < 16 ||
         ldu >= (1L << 31))
         return false;
+    // (outputs leave as 128-bit stores)
+    if (D && (reinterpret_cast<uintptr_t>(D) % 16 != 0 || (ldd % 2) != 0)) return false;
     return true;
 }
 
