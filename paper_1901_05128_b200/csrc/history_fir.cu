@@ -40,7 +40,11 @@ namespace fraqcu {
 
 namespace {
 
-constexpr int E_TC = 32;   // levels per staged chunk
+#ifndef FRAQ_K5E_TC
+#define FRAQ_K5E_TC 32
+#endif
+constexpr int E_TC = FRAQ_K5E_TC;  // levels per staged chunk (16 or 32)
+constexpr int E_KW_CAP = 128 - (2 * E_TC - 8);  // widest window the 128-row shared ring holds
 constexpr int E_TB = 8;    // levels per block
 constexpr int E_NT = 8;    // node tiles per warp at most (64 long nodes)
 
@@ -477,8 +481,8 @@ void build_fir_plan(fraq_ctx c, HistDevice& d) {
             return 4 * ((jl + 7) / 8) + kw / 4;
         };
         int M = 0, best = cost(0);
-        for (int cand = 8; cand <= 64; cand += 8) {
-            if ((G.L + cand + 7 + 3) / 4 * 4 > 72 && m_force < 0) break;
+        for (int cand = 8; cand <= 96; cand += 8) {
+            if ((G.L + cand + 7 + 3) / 4 * 4 > E_KW_CAP && m_force < 0) break;
             const int cc = cost(cand);
             if (cc < best) best = cc, M = cand;
         }
@@ -587,7 +591,7 @@ void build_fir_plan(fraq_ctx c, HistDevice& d) {
             std::fprintf(stderr, "\n");
         }
     P.ring_rows = 128;
-    while (P.ring_rows < P.kw_max + 56) P.ring_rows *= 2;
+    while (P.ring_rows < P.kw_max + 2 * E_TC - 8) P.ring_rows *= 2;
     P.xh_rows = 128;
     while (P.xh_rows < P.kw_max + 8) P.xh_rows *= 2;
     if (run4_smem(P) > 200 * 1024) return;

@@ -52,10 +52,11 @@ def test_gauss_jacobi_errors(fraq):
 def test_weights_match_oracle(fraq, orc, g, tau, n):
     be = np.array(fraq.be_weights(g, tau, n).weights)
     assert rel_linf(be, orc.be_weights(g, tau, n)) <= 1e-15
-    if n <= 5000:
-        sbd = np.array(fraq.sbd_weights(g, tau, n).weights)
-        ref = orc.sbd_weights(g, tau, n)
-        assert np.max(np.abs(sbd - ref) / np.maximum(np.abs(ref), 1e-300)) <= 1e-12
+    # (the 65536-long C2 table too: the device Cauchy product measured 2.9e-16 relative per
+    # entry against the reference's serial product, profiles/r02/sbdw_probe.py)
+    sbd = np.array(fraq.sbd_weights(g, tau, n).weights)
+    ref = orc.sbd_weights(g, tau, n)
+    assert np.max(np.abs(sbd - ref) / np.maximum(np.abs(ref), 1e-300)) <= 1e-12
 
 
 def test_weights_examples(fraq):
