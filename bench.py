@@ -365,6 +365,36 @@ def main():
     assert hs.last_path == 0
     step_level_ms = e0.elapsed_time(e1) / nstep
     hbm_step = B * NL / (step_level_ms * 1e-3) / 1e9
+    # the same per-level calls in the steady state: K5f (K5e's fold, per level: only the slow
+    # nodes keep a state in HBM, the fast-decaying ones are an exact FIR over the input ring)
+    fold = None
+    n0f = 3 + nstep
+    hs.run_device(U.data_ptr() + n0f * NL * 8, NL, 160, D.data_ptr() + n0f * NL * 8, NL)
+    n0f += 160
+    lf0 = list(hs.launches)
+    for n in range(n0f, n0f + 4):
+        hs.run_device(U.data_ptr() + n * NL * 8, NL, 1, D.data_ptr() + n * NL * 8, NL)
+    n0f += 4
+    e0.record(stream)
+    for n in range(n0f, n0f + nstep):
+        hs.run_device(U.data_ptr() + n * NL * 8, NL, 1, D.data_ptr() + n * NL * 8, NL)
+    e1.record(stream)
+    e1.synchronize()
+    lf1 = list(hs.launches)
+    if len(lf1) > 5 and lf1[5] - lf0[5] == nstep + 4:
+        fold_ms = e0.elapsed_time(e1) / nstep
+        fi = list(hs.fir_info)
+        # bytes K5f moves per DOF-step: the kept nodes' states read + written, the window rows
+        # (head + FIR taps, from the L2-resident input ring), input and output
+        Bf = 0.5 * sum(8 * (2 * fi[3 * g + 1] + (n_head[g] + fi[3 * g]) + 2) for g in range(2))
+        fold = {"kernel": "step_fir_kernel (K5f)", "ms_per_level": fold_ms,
+                "speedup_vs_K5": step_level_ms / fold_ms,
+                "bytes_per_dof_step_moved": Bf,
+                "moved_gbs": Bf * NL / (fold_ms * 1e-3) / 1e9,
+                "algorithmic_gbs": B * NL / (fold_ms * 1e-3) / 1e9,
+                "note": "algorithmic_gbs counts SURVEY.md 8(d)'s B (every node's state read and "
+                        "written per level) and can exceed the HBM peak: K5f keeps only the "
+                        "slow nodes' states"}
     del hs
 
     # e2e: the same metric through the C-ABI call with HOST buffers (pinned), copies inside
@@ -419,8 +449,8 @@ def main():
                                "as an exact FIR window; K5d on a history's first 96 levels)"
                                if k5e else "K5d (temporally blocked, fp64 tensor cores)"),
                       "k5e_groups": fir_groups,
-                      "launches_by_path": dict(zip(["K5", "short_state", "K5c", "K5d", "K5e"],
-                                                   launches))},
+                      "launches_by_path": dict(zip(["K5", "short_state", "K5c", "K5d", "K5e",
+                                                    "K5f"], launches))},
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": dmma_peak,
                          "unit": "TFLOP/s", "frac": achieved_tf / dmma_peak,
                          "traffic": traffic, "traffic_unit": "GB per launch (ncu, profiles/)",
@@ -444,7 +474,8 @@ def main():
                                      "frac": hbm_step / pk.get("hbm_gbs"),
                                      "bytes_per_dof_step": B, "kernel": "step_kernel (K5)",
                                      "ms_per_level": step_level_ms,
-                                     "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+                                     "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                                     "folded": fold},
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": step_bytes,
                     "d2h_bytes_per_step": step_bytes, "steps": ke,
                     "path": "MultiHistory.run(host numpy) -> fraq_hist_run(FRAQ_HOST)"},

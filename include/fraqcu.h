@@ -187,8 +187,10 @@ int fraq_hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* 
  * block GEMMs on the slow nodes + the fast-decaying nodes as an exact FIR window; the steady
  * state, default).  (1 was the retired warp-per-4-DOF kernel K5b.) */
 int fraq_hist_last_path(fraq_hist h);
-/* Diagnostics of fraq_hist_run on this history.  launches[0..4]: kernels launched so far by
- * path (0 per-level K5, 1 short-state rebuilds after K5e, 2 K5c, 3 K5d, 4 K5e).  fir[3 g + 0..2]
+/* Diagnostics of this history's kernels.  launches[0..5]: kernels launched so far by path
+ * (0 per-level K5, 1 short-state rebuilds after K5e / K5f, 2 K5c, 3 K5d, 4 K5e, 5 K5f: the
+ * per-level step in K5e's folded form -- push / derivative / history_sum in the steady state of
+ * a pure push sequence, FRAQ_NO_K5F=1 keeps them on K5).  fir[3 g + 0..2]
  * for group g < n_groups: K5e's FIR length M (levels; 0 = no node folded), the nodes kept as
  * recurrences, the combined input window (rows) -- zeros while K5e has no plan.  Either pointer
  * may be NULL. */

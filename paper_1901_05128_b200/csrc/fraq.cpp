@@ -301,7 +301,7 @@ void DeviceHistory::run(const double* U, long ldu, long n_steps, double* D, long
 }
 int DeviceHistory::last_path() const { return fraq_hist_last_path(h_); }
 std::vector<long> DeviceHistory::launches() const {
-    std::vector<long> out(5, 0);
+    std::vector<long> out(6, 0);
     check(fraq_hist_path_info(h_, out.data(), 0, nullptr));
     return out;
 }

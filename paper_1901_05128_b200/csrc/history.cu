@@ -31,6 +31,10 @@ bool fir_eligible(const HistDevice& d, long A0, const double* U, long ldu, long 
 void launch_run4(fraq_ctx c, HistDevice& d, const int2* tasks, int n_tasks, int* counter, long A0,
                  const double* U, long ldu, long n_steps, double* D, long ldd);
 void fir_materialize(fraq_ctx c, HistDevice& d, long A1);
+// history_fir.cu (K5f)
+bool step_fir_eligible(const HistDevice& d, long level, long appended, bool push);
+void launch_step_fir(fraq_ctx c, HistDevice& d, long appended, int push, int mode, const double* u,
+                     double* out);
 
 namespace {
 
@@ -591,7 +595,7 @@ struct fraq_hist_s {
     DevBuf<int2> run3_tasks;   // (group, first DOF of a 16-DOF tile) for K5d
     int n_run3_tasks = 0;
     int last_path = 0;
-    long launches[5] = {0, 0, 0, 0, 0};  // by path (1: short-state rebuilds)
+    long launches[6] = {0, 0, 0, 0, 0, 0};  // by path (1: short-state rebuilds, 5: K5f)
     // chunk staging for host-memory runs
     static constexpr int kMaxStages = 4;
     DevBuf<double> ubuf[kMaxStages], dbuf[kMaxStages];
@@ -652,6 +656,16 @@ void copy_out(fraq_hist h, double* dst, const double* src, int mem) {
     if (mem != FRAQ_DEVICE) FRAQ_CUDA(cudaStreamSynchronize(h->ctx->stream));
 }
 
+// A K5 push of `u` (device, user layout) at level h->appended, before the counters move: pure
+// push sequences keep K5e's / K5f's input ring current, anything else invalidates it.
+void note_push(fraq_hist h, const double* u) {
+    const bool pure = h->appended == 0 ? h->level == 0 : h->level == h->appended - 1;
+    if (pure && h->d.fir.ok)
+        fir_note_inputs(h->ctx, h->d, h->appended, u, std::max<long>(1, h->d.total_dim), 1);
+    else
+        h->d.fir.xh_valid = 0;
+}
+
 // Run a pending push (advance + append from the stage) fused with `mode` output into out_d.
 void flush(fraq_hist h, int mode, double* out_d) {
     StepArgs a = base_args(h);
@@ -663,9 +677,16 @@ void flush(fraq_hist h, int mode, double* out_d) {
     a.mode = mode;
     a.out = out_d;
     if (!a.adv && !a.app && mode == MODE_NONE) return;
-    fir_materialize(h->ctx, h->d, h->appended);  // K5 reads every node's state
-    if (h->pending) h->d.fir.xh_valid = 0;  // (single pushes are not recorded in K5e's input ring)
-    h->d.launch_step(h->ctx, a);
+    if (step_fir_eligible(h->d, h->level, h->appended, h->pending)) {
+        // K5f: the folded per-level step (steady state of a pure push sequence)
+        launch_step_fir(h->ctx, h->d, h->appended, h->pending ? 1 : 0, mode, h->stage.p, out_d);
+        ++h->launches[5];
+    } else {
+        fir_materialize(h->ctx, h->d, h->appended);  // K5 reads every node's state
+        h->d.launch_step(h->ctx, a);
+        ++h->launches[0];
+        if (h->pending) note_push(h, h->stage.p);
+    }
     if (h->pending) {
         if (h->appended > 0) h->level += 1;
         h->appended += 1;
@@ -760,8 +781,14 @@ void hist_append(fraq_hist h, const double* v, int mem) {
     StepArgs a = base_args(h);
     a.app = 1;
     a.u = h->stage.p;
-    h->d.fir.xh_valid = 0;
     h->d.launch_step(h->ctx, a);
+    ++h->launches[0];
+    // advance() then append() is a push: the input ring stays current (K5e / K5f can follow)
+    const bool pure = h->appended == 0 ? h->level == 0 : h->level == h->appended;
+    if (pure && h->d.fir.ok)
+        fir_note_inputs(h->ctx, h->d, h->appended, h->stage.p, std::max<long>(1, h->d.total_dim), 1);
+    else
+        h->d.fir.xh_valid = 0;
     h->appended += 1;
 }
 
@@ -888,7 +915,6 @@ void run_device(fraq_hist h, const double* U, long ldu, long n_steps, double* D,
         return;
     }
     h->last_path = 0;
-    fir_materialize(h->ctx, h->d, h->appended);
     for (long n = 0; n < n_steps; ++n) {
         if (h->appended > 0) check_advance(h);
         StepArgs a = base_args(h);
@@ -900,9 +926,15 @@ void run_device(fraq_hist h, const double* U, long ldu, long n_steps, double* D,
             if (!G.sbd && h->appended + 1 < 2) ok = false;
         a.mode = (D && ok) ? MODE_DERIV : MODE_NONE;
         a.out = D ? D + n * ldd : nullptr;
-        h->d.fir.xh_valid = 0;
-        h->d.launch_step(h->ctx, a);
-        ++h->launches[0];
+        if (step_fir_eligible(h->d, h->level, h->appended, true)) {
+            launch_step_fir(h->ctx, h->d, h->appended, 1, a.mode, a.u, a.out);
+            ++h->launches[5];
+        } else {
+            fir_materialize(h->ctx, h->d, h->appended);
+            h->d.launch_step(h->ctx, a);
+            ++h->launches[0];
+            note_push(h, a.u);
+        }
         if (D && !ok) {
             // derivative undefined on the first BE push: NaN row (the reference throws)
             std::vector<double> nan(h->d.total_dim, NAN);
@@ -995,7 +1027,7 @@ void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, l
 int hist_last_path(fraq_hist h) { return h->last_path; }
 void hist_path_info(fraq_hist h, long* launches, int n_groups, int* fir) {
     if (launches)
-        for (int i = 0; i < 5; ++i) launches[i] = h->launches[i];
+        for (int i = 0; i < 6; ++i) launches[i] = h->launches[i];
     if (fir)
         for (int g = 0; g < n_groups; ++g) {
             const bool have = h->d.fir.ok && g < (int)h->d.fir.groups_h.size();

@@ -92,6 +92,7 @@ struct FirGroup {
     long tab_off;            // tables: C[TL*64], R[TL*64], H[nkk*32] (doubles)
     int perm_off;            // original node index of long position p (-1: padding)
     int short_off, n_short;  // original node indices of the short nodes
+    long ws_off;             // tables: the short nodes' FIR taps wS_m = sum_j f_j r_j^m, m < M (K5f)
 };
 struct FirPlan {
     bool built = false, ok = false;

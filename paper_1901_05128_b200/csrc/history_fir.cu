@@ -550,6 +550,10 @@ void build_fir_plan(fraq_ctx c, HistDevice& d) {
         tabs.insert(tabs.end(), C.begin(), C.end());
         tabs.insert(tabs.end(), R.begin(), R.end());
         tabs.insert(tabs.end(), H.begin(), H.end());
+        while (tabs.size() % 4) tabs.push_back(0.0);
+        F.ws_off = (long)tabs.size();
+        for (int m = 0; m < M; ++m) tabs.push_back((double)wS[m]);
+        tabs.push_back(0.0);
     }
     // warps per CTA: ~24 DMMA pairs per warp and block (C2: 4 warps, 3.46e10 DOF-steps/s; 3 warps
     // 3.33e10, 5 warps 3.18e10), every group's tiles must fit
@@ -738,5 +742,239 @@ void fir_materialize(fraq_ctx c, HistDevice& d, long A1) {
         P.xh_rows - 1, A1, m_max, slices);
     FRAQ_LAUNCH_CHECK();
 }
+
+// ------------------------------------------------------------------------------------- K5f
+// The per-level step (K5's role: one push / advance + append + readout for every DOF,
+// fast_kernel.cpp:268-409) in K5e's folded form: only the slow ("long") nodes keep a state in
+// HBM -- y_j <- r_j y_j + f_j X(n - L), one 256-bit read and write per node and DOF quad -- and
+// the fast-decaying nodes are the exact FIR  sum_{m<M} wS_m X(n - L - m)  over the input ring
+// `xh` (L2-resident: 65 rows at C2), next to the exact head taps d_i X(n - i).  For the
+// reference's auto-sized C2 tables that is 151 of 512 states per level.  Steady state only
+// (step_fir_eligible); everything else stays on K5, after short_state_kernel rebuilt the short
+// states it reads.
+namespace {
+
+struct F4 {
+    double x, y, z, w;
+};
+__device__ __forceinline__ F4 ldg_stream4(const double* p) {
+    F4 v;
+    asm volatile("ld.global.L1::no_allocate.L2::evict_first.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void stg_stream4(double* p, const F4& v) {
+    asm volatile("st.global.L1::no_allocate.L2::evict_first.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p),
+                 "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w)
+                 : "memory");
+}
+// up to 4 consecutive doubles of a user-layout row (any alignment; nv valid)
+__device__ __forceinline__ F4 ld_row4(const double* p, int nv) {
+    F4 v = {0.0, 0.0, 0.0, 0.0};
+    if (nv == 4 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+        const double2 a = *reinterpret_cast<const double2*>(p);
+        const double2 b = *reinterpret_cast<const double2*>(p + 2);
+        v = {a.x, a.y, b.x, b.y};
+    } else {
+        if (nv > 0) v.x = p[0];
+        if (nv > 1) v.y = p[1];
+        if (nv > 2) v.z = p[2];
+        if (nv > 3) v.w = p[3];
+    }
+    return v;
+}
+__device__ __forceinline__ void st_row4(double* p, const F4& v, int nv) {
+    if (nv == 4 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+        *reinterpret_cast<double2*>(p) = make_double2(v.x, v.y);
+        *reinterpret_cast<double2*>(p + 2) = make_double2(v.z, v.w);
+    } else {
+        if (nv > 0) p[0] = v.x;
+        if (nv > 1) p[1] = v.y;
+        if (nv > 2) p[2] = v.z;
+        if (nv > 3) p[3] = v.w;
+    }
+}
+__device__ __forceinline__ void fma_f4(F4& acc, double c, const F4& x) {
+    acc.x = fma(c, x.x, acc.x);
+    acc.y = fma(c, x.y, acc.y);
+    acc.z = fma(c, x.z, acc.z);
+    acc.w = fma(c, x.w, acc.w);
+}
+__device__ __forceinline__ void add_f4(F4& acc, const F4& x) {
+    acc.x += x.x;
+    acc.y += x.y;
+    acc.z += x.z;
+    acc.w += x.w;
+}
+
+struct StepFirArgs {
+    const GroupDev* groups;
+    const FirGroup* fg;
+    const int2* tiles;   // K5's tiles: (group, first DOF quad)
+    double* state;
+    double* ring;
+    const double* cr;
+    const double* cf;
+    const double* head;
+    const int* perm;
+    const double* tabs;
+    double* xh;
+    long ldx;
+    int xh_mask;
+    long appended;       // values appended before this launch
+    int push;            // 1: advance + append u (level n = appended); 0: read-only, n = appended - 1
+    int mode;            // MODE_NONE / MODE_SUM / MODE_DERIV
+    const double* u;     // device, user layout
+    double* out;         // device, user layout
+};
+
+// CTA = LANES DOF quads x S slices; slice sl takes the long nodes p = sl, sl + S, ... and the
+// window taps i = i0 + sl, i0 + sl + S, ...; partial sums meet in shared memory and slice 0
+// finishes (lag ring, input ring, output), as in K5.
+template <int LANES, int S>
+__global__ void __launch_bounds__(LANES* S, 5) step_fir_kernel(StepFirArgs A) {
+    const int2 tile = A.tiles[blockIdx.x];
+    const GroupDev G = A.groups[tile.x];
+    const FirGroup* F = A.fg + tile.x;
+    const int lane = threadIdx.x % LANES;
+    const int sl = threadIdx.x / LANES;
+    const int m = 4 * (tile.y + lane);
+    const bool live = m < G.dim;
+    const int nv = live ? min(4, G.dim - m) : 0;
+    __shared__ F4 s_part[S][LANES];
+    const long n = A.push ? A.appended : A.appended - 1;  // level of the newest value
+    const int L = G.L, M = F->M, JL = F->JL;
+    const long ld = G.ld;
+    const double* xcol = A.xh + G.dof0 + m;
+    F4 acc = {0.0, 0.0, 0.0, 0.0};
+    F4 unew = {0.0, 0.0, 0.0, 0.0};
+    if (live) {
+        if (A.push) unew = ld_row4(A.u + G.dof0 + m, nv);
+        const int* pm = A.perm + F->perm_off;
+        const double* __restrict__ cr = A.cr + G.co_off;
+        const double* __restrict__ cf = A.cf + G.co_off;
+        double* base = A.state + G.st_off + m;
+        if (A.push) {
+            // feed of level n: X(n - L)  (steady state: n - L >= lo and still on record)
+            const F4 v = ld_row4(xcol + (size_t)((n - L) & A.xh_mask) * A.ldx, nv);
+            constexpr int NB = 4;  // independent 256-bit loads in flight before the first store
+            int p = sl;
+            for (; p + (NB - 1) * S < JL; p += NB * S) {
+                F4 y[NB];
+                int j[NB];
+#pragma unroll
+                for (int b = 0; b < NB; ++b) {
+                    j[b] = pm[p + b * S];
+                    y[b] = ldg_stream4(base + j[b] * ld);
+                }
+#pragma unroll
+                for (int b = 0; b < NB; ++b) {
+                    const double r = __ldg(cr + j[b]), f = __ldg(cf + j[b]);
+                    y[b].x = fma(r, y[b].x, f * v.x);
+                    y[b].y = fma(r, y[b].y, f * v.y);
+                    y[b].z = fma(r, y[b].z, f * v.z);
+                    y[b].w = fma(r, y[b].w, f * v.w);
+                    stg_stream4(base + j[b] * ld, y[b]);
+                    add_f4(acc, y[b]);
+                }
+            }
+            for (; p < JL; p += S) {
+                const int j = pm[p];
+                F4 y = ldg_stream4(base + j * ld);
+                const double r = __ldg(cr + j), f = __ldg(cf + j);
+                y.x = fma(r, y.x, f * v.x);
+                y.y = fma(r, y.y, f * v.y);
+                y.z = fma(r, y.z, f * v.z);
+                y.w = fma(r, y.w, f * v.w);
+                stg_stream4(base + j * ld, y);
+                add_f4(acc, y);
+            }
+        } else if (A.mode != MODE_NONE) {
+#pragma unroll 4
+            for (int p = sl; p < JL; p += S) add_f4(acc, ldg_stream4(base + pm[p] * ld));
+        }
+        if (A.mode != MODE_NONE) {
+            // window: exact head taps d_i (derivative only), then the short nodes' FIR
+            const double* hd = A.head + G.hd_off;
+            const double* ws = A.tabs + F->ws_off;
+            const int i0 = A.mode == MODE_DERIV ? 0 : L;
+#pragma unroll 4
+            for (int i = i0 + sl; i < L + M; i += S) {
+                const double c = i < L ? hd[i] : ws[i - L];
+                const F4 x = (i == 0 && A.push)
+                                 ? unew
+                                 : ld_row4(xcol + (size_t)((n - i) & A.xh_mask) * A.ldx, nv);
+                fma_f4(acc, c, x);
+            }
+        }
+    }
+    if (A.mode != MODE_NONE && S > 1) {
+        s_part[sl][lane] = acc;
+        __syncthreads();
+        if (sl == 0) {
+#pragma unroll
+            for (int q = 1; q < S; ++q) add_f4(acc, s_part[q][lane]);
+        }
+    }
+    if (sl != 0 || !live) return;
+    if (A.push) {
+        // (the feed X(n - L) was read from the input ring, so the lag ring slot n % L -- the
+        // one it sat in -- can be overwritten without a barrier)
+        double* rg = A.ring + G.ring_off + (n % L) * ld + m;
+        *reinterpret_cast<double2*>(rg) = make_double2(unew.x, unew.y);
+        *reinterpret_cast<double2*>(rg + 2) = make_double2(unew.z, unew.w);
+        st_row4(A.xh + (size_t)(n & A.xh_mask) * A.ldx + G.dof0 + m, unew, nv);
+    }
+    if (A.mode != MODE_NONE) st_row4(A.out + G.dof0 + m, acc, nv);
+}
+
+}  // namespace
+
+// Can the next per-level step run on K5f?  push: a pending push (advance + append) at level
+// `appended`; otherwise a read-only output at level appended - 1.
+bool step_fir_eligible(const HistDevice& d, long level, long appended, bool push) {
+    const FirPlan& P = d.fir;
+    if (!P.ok || std::getenv("FRAQ_NO_K5F")) return false;
+    if (appended < 1 || level != appended - 1) return false;  // pure push sequence
+    const long n = push ? appended : appended - 1;
+    if (n < P.min_level || n < P.kw_max || P.xh_valid < P.kw_max) return false;
+    return true;
+}
+
+void launch_step_fir(fraq_ctx c, HistDevice& d, long appended, int push, int mode, const double* u,
+                     double* out) {
+    FirPlan& P = d.fir;
+    if (d.n_tiles == 0) return;
+    StepFirArgs a{};
+    a.groups = d.groups.p;
+    a.fg = P.groups.p;
+    a.tiles = d.tiles.p;
+    a.state = d.state.p;
+    a.ring = d.ring.p;
+    a.cr = d.cr.p;
+    a.cf = d.cf.p;
+    a.head = d.head.p;
+    a.perm = P.perm.p;
+    a.tabs = P.tabs.p;
+    a.xh = P.xh.p;
+    a.ldx = d.total_dim;
+    a.xh_mask = P.xh_rows - 1;
+    a.appended = appended;
+    a.push = push;
+    a.mode = mode;
+    a.u = u;
+    a.out = out;
+    if (d.lanes == 32)
+        step_fir_kernel<32, 4><<<d.n_tiles, 128, 0, c->stream>>>(a);
+    else
+        step_fir_kernel<8, 16><<<d.n_tiles, 128, 0, c->stream>>>(a);
+    FRAQ_LAUNCH_CHECK();
+    if (push) {
+        P.xh_valid = std::min<long>(P.xh_rows, P.xh_valid + 1);
+        P.short_stale = true;  // the short nodes' states in HBM are not advanced
+    }
+}
+
 
 }  // namespace fraqcu

@@ -211,3 +211,107 @@ def test_k5e_padded_rows_and_no_output(fraq, orc, c2_kernels):
     scale = C2_TAU ** -o.gamma
     check(D[:256, :dim], ref[:256], scale, 1e-12)
     check(D[640:, :dim], ref[640:], scale, 1e-12)
+
+
+# ------------------------------------------------------------------------------------- K5f
+# The per-level step in K5e's folded form (history_fir.cu step_fir_kernel): push / derivative /
+# history_sum of a pure push sequence past the first levels.  launches[5] counts its launches.
+
+@pytest.mark.parametrize("sbd,variant", [(False, "standalone"), (True, "standalone"),
+                                         (True, "scheme"), (False, "scheme")])
+def test_k5f_pure_push_sequence(fraq, orc, sbd, variant):
+    """push + derivative level by level from a fresh history (the reference's own calling
+    pattern, fast_kernel.cpp:291-300, 317-325, 366-376, 397-409): K5 on the first levels (which
+    also records the inputs), K5f from the level its window is on record, equal to the reference
+    history throughout."""
+    rng = np.random.default_rng(71 + 2 * sbd + (variant == "scheme"))
+    tau = 1.0 / 16384
+    o = orc.build_kernel_auto(sbd, 0.45, tau, 16384, 1e-12)
+    dim, n = 22, 260
+    U = rng.uniform(-1, 1, (n, dim))
+    if variant == "scheme":
+        U[0] = 0.0  # (scheme histories start from the initial value G^0 = 0 convention of the tests)
+    ref = orc.hist_run(o, U, scheme_variant=variant == "scheme")
+    h = make(fraq, o, variant, dim)
+    out = np.full((n, dim), np.nan)
+    for i in range(n):
+        h.push(list(U[i]))
+        if sbd or i >= 1:
+            out[i] = h.derivative()
+    lz = list(h.launches)
+    assert lz[5] > 100 and lz[0] > 20
+    check(out, ref, tau ** -0.45, 1e-12)
+
+
+def test_k5f_mixed_with_runs_and_read_only_outputs(fraq, orc, c2_kernels, monkeypatch):
+    """Blocked runs (K5d / K5e) interleaved with single pushes on K5f, history_sum and repeated
+    derivative reads without a new push (read-only K5f), lagged values, and a separate
+    advance() / append() pair (K5, after the short states were rebuilt): the same sequence with
+    FRAQ_NO_K5F=1 (K5 for every per-level call) gives the same numbers, and both equal the
+    reference history."""
+    rng = np.random.default_rng(83)
+    o = c2_kernels[0]
+    dim, n = 20, 700
+    U = rng.uniform(-1, 1, (n, dim))
+    ref = orc.hist_run(o, U)
+
+    def sequence():
+        h = make(fraq, o, "standalone", dim)
+        D = np.full((n, dim), np.nan)
+        sums, lag = [], []
+        pos = 0
+        for ln in (208, -40, 136, -3, 99, -60, 154):
+            if ln > 0:
+                D[pos:pos + ln] = np.asarray(h.run(U[pos:pos + ln]), dtype=float)
+                pos += ln
+                continue
+            for q in range(-ln):
+                if q == 5:
+                    # the reference's split calls (fast_kernel.cpp:268-289, 343-365)
+                    h.advance()
+                    h.append(list(U[pos]))
+                else:
+                    h.push(list(U[pos]))
+                if q % 4 == 1:
+                    sums.append(np.array(h.history_sum()))
+                D[pos] = h.derivative()
+                if q % 7 == 2:
+                    assert np.array_equal(np.array(h.derivative()), D[pos])  # read-only repeat
+                    lag.append(np.array(h.lagged(3)))
+                pos += 1
+        assert pos == n
+        return h, D, np.array(sums), np.array(lag)
+
+    h1, D1, s1, l1 = sequence()
+    assert h1.launches[5] > 60
+    monkeypatch.setenv("FRAQ_NO_K5F", "1")
+    h2, D2, s2, l2 = sequence()
+    assert h2.launches[5] == 0
+    scale = C2_TAU ** -o.gamma
+    check(D1, ref, scale, 1e-12)
+    check(D2, ref, scale, 1e-12)
+    assert np.max(np.abs(s1 - s2)) <= 1e-12 * scale
+    assert np.array_equal(l1, l2)
+
+
+def test_k5f_ragged_groups_odd_starts(fraq, orc):
+    """Groups of ragged sizes with odd first DOFs (rows K5e cannot stage by TMA): the per-level
+    fold has no alignment precondition; every group equals its own reference history."""
+    rng = np.random.default_rng(89)
+    dims = [1, 3, 16, 17, 33, 6]
+    taus = [1e-3, 1e-4, 1e-5, 1e-3, 1e-5, 1e-4]
+    os_ = [orc.build_be_kernel(0.25 + 0.1 * i, taus[i], 24 + 37 * i) for i in range(len(dims))]
+    ks = [kernel_from_oracle(fraq, o) for o in os_]
+    h = fraq.MultiHistory(ks, dims)
+    n = 300
+    U = rng.uniform(-1, 1, (n, sum(dims)))
+    D = np.full((n, sum(dims)), np.nan)
+    D[:160] = np.asarray(h.run(U[:160]), dtype=float)
+    for i in range(160, n):
+        D[i] = np.asarray(h.run(U[i:i + 1]), dtype=float)[0]  # one-level calls
+    assert h.launches[5] == n - 160
+    c = 0
+    for o, dm, tau in zip(os_, dims, taus):
+        D_ref = orc.hist_run(o, np.ascontiguousarray(U[:, c:c + dm]))
+        check(D[:, c:c + dm], D_ref, tau ** -o.gamma, 1e-12)
+        c += dm
