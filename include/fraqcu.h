@@ -157,6 +157,18 @@ int fraq_reconstruct(fraq_ctx ctx, const fraq_kernel_t* k, long n, const long* i
 int fraq_kernel_error_report(fraq_ctx ctx, const fraq_kernel_t* k, long n_max, double* eps,
                              double* max_eps, long* argmax);
 
+/* The short-node fold as a kernel rewrite (host only; no reference counterpart -- it rewrites
+ * the reference's FastKernelBE / FastKernelSBD tables, fast_kernel.hpp:13-39, into an equivalent
+ * kernel): a node with |r_j|^M <= 2^-70 has forgotten everything older than M levels, so the
+ * kernel (head d_0..d_(L-1); nodes fed at lag L) equals, to below fp64 rounding, the kernel with
+ * the head c_0..c_(L+M-1), c_i = reconstruct(i) (fast_kernel.cpp:38-52) for i >= L, and only the
+ * slow nodes.  `out` is in the SBD table format (generic head; the feed convention
+ * mult * ratio^(n_head - 3), fast_kernel.cpp:337-340, absorbs r^M).  M is the multiple of 8 with
+ * L + M <= max_head that minimises the bytes a per-level history pass moves; *fold_levels = 0
+ * and `out` = *k when nothing folds.  The physical FFPE stepper builds its histories from such
+ * kernels; K5e / K5f / K13 use the same node split. */
+int fraq_fold_kernel(const fraq_kernel_t* k, int max_head, fraq_kernel_t* out, int* fold_levels);
+
 /* ---------------------------------------------------------------- L2 history states
  * BeHistory / SbdHistory (fast_kernel.hpp:87-146, fast_kernel.cpp:261-409) on the device.
  * A history holds n_groups contiguous DOF groups, group g having dims[g] DOFs and its own kernel

@@ -60,6 +60,7 @@ EXTRA = [
     "build_kernels_auto_sizes",
     "context_stream",
     "diag_dmma_peak",
+    "fold_kernel",
     "direct_cq",
     "direct_cq_device",
     "BenchRow",

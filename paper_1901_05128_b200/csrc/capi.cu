@@ -252,6 +252,22 @@ int fraq_build_sbd_kernel(fraq_ctx c, double g, double tau, int np1, int np2, in
 
 int fraq_default_sbd_head(double g) { return g <= 0.5 ? 15 : 17; }
 
+int fraq_fold_kernel(const fraq_kernel_t* k, int max_head, fraq_kernel_t* out, int* fold_levels) {
+    return guarded([&] {
+        if (!k || !out) fail(FRAQ_EINVAL, "fold_kernel: null kernel");
+        if (k->np1 < 0 || k->np2 < 0 || k->np1 > FRAQ_MAX_POINTS || k->np2 > FRAQ_MAX_POINTS ||
+            k->n_head < 2 || k->n_head > FRAQ_MAX_HEAD)
+            fail(FRAQ_EINVAL, "fold_kernel: malformed kernel tables");
+        fraq_kernel_t tmp;
+        const int M = fold_kernel(*k, max_head, &tmp);
+        if (M > 0)
+            *out = tmp;
+        else if (out != k)
+            *out = *k;
+        if (fold_levels) *fold_levels = M;
+    });
+}
+
 int fraq_build_be_kernel_auto(fraq_ctx c, double g, double tau, fraq_budget_t* b,
                               fraq_kernel_t* out) {
     return guarded(c, [&] {

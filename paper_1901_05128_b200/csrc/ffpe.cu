@@ -206,6 +206,8 @@ struct InstDev {
     int sys_main, sys_first;
     long g0_off;         // G^0 copies (2 * m doubles)
     long corr_off1, corr_off2;  // SBD correction sequences (index e)
+    int nh1, nh2;        // exact head lengths of the reference kernels (the history groups may
+                         // carry folded kernels with longer heads)
 };
 
 struct SolveArgs {
@@ -529,8 +531,8 @@ __global__ void __launch_bounds__(THREADS) solve_kernel(SolveArgs A) {
         q2 = r2 + ((n - 2) % G2.L) * ld;
         if (A.corr) {
             // (1/2) d_{n-1} G^0: exact head inside, reconstructed (running powers) beyond
-            c1 = (n - 1 < G1.L) ? A.head[G1.hd_off + n - 1] : A.corr[I.corr_off1 + (n - 4)];
-            c2 = (n - 1 < G2.L) ? A.head[G2.hd_off + n - 1] : A.corr[I.corr_off2 + (n - 4)];
+            c1 = (n - 1 < I.nh1) ? A.head[G1.hd_off + n - 1] : A.corr[I.corr_off1 + (n - 4)];
+            c2 = (n - 1 < I.nh2) ? A.head[G2.hd_off + n - 1] : A.corr[I.corr_off2 + (n - 4)];
         }
     }
     const double* g01 = A.g0 + I.g0_off;
@@ -780,6 +782,7 @@ void ffpe_run_modal(fraq_ctx c, const fraq_spec_t* specs, int n_inst, bool sbd,
 struct PhysStepper {
     fraq_ctx c = nullptr;
     int n_inst = 0, m = 0;
+    int fold_levels[2] = {0, 0};  // head levels the last instance's kernels were folded by
     long N = 0;        // horizon the kernels / classical tables are sized for
     bool sbd = false, fast = false;
     double tau = 0.0;
@@ -909,6 +912,8 @@ PhysStepper::PhysStepper(fraq_ctx c_, const fraq_spec_t* specs, int n_inst_, int
         I.g1 = 2 * i;
         I.g2 = 2 * i + 1;
         I.g0_off = (long)i * 2 * m;
+        I.nh1 = fast ? ks[2 * i].n_head : 2;
+        I.nh2 = fast ? ks[2 * i + 1].n_head : 2;
         if (sbd) {
             I.sys_main = 2 * i;
             I.sys_first = 2 * i + 1;
@@ -936,8 +941,24 @@ PhysStepper::PhysStepper(fraq_ctx c_, const fraq_spec_t* specs, int n_inst_, int
     std::vector<long> dims(2 * n_inst, m);
     std::vector<const fraq_kernel_t*> kp(2 * n_inst);
     std::vector<fraq_kernel_t> pseudo;  // classical: a 2-slot lag ring carrier (no nodes)
+    std::vector<fraq_kernel_t> folded;  // fast: kernels with the fast-decaying nodes in the head
     if (fast) {
         for (int t = 0; t < 2 * n_inst; ++t) kp[t] = &ks[t];
+        // The K5 pass streams every node's state once per level; the nodes that forget within M
+        // levels move into the exact head instead (fold_kernel, history_fir.cu: the rewrite
+        // K13 and K5e / K5f use), which leaves 16 bytes per kept node + 8 per head tap.
+        if (!std::getenv("FRAQ_NO_PHYS_FOLD")) {
+            int lcap = 96;
+            if (const char* e = std::getenv("FRAQ_PHYS_LCAP")) lcap = std::atoi(e);  // experiment
+            folded.resize(2 * n_inst);
+            for (int t = 0; t < 2 * n_inst; ++t) {
+                fold_levels[t % 2] = 0;
+                if (int M = fold_kernel(ks[t], lcap, &folded[t])) {
+                    kp[t] = &folded[t];
+                    fold_levels[t % 2] = M;
+                }
+            }
+        }
     } else {
         pseudo.resize(2 * n_inst);
         for (int t = 0; t < 2 * n_inst; ++t) {

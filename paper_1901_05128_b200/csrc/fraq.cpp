@@ -197,6 +197,27 @@ FastKernelSBD build_sbd_kernel(double alpha, double tau, int n1, int n2, int n_h
 }
 
 int default_sbd_head(double alpha) { return fraq_default_sbd_head(alpha); }
+namespace {
+FastKernelSBD fold_flat(const fraq_kernel_t& f, int max_head, int* levels) {
+    fraq_kernel_t o;
+    int M = 0;
+    check(fraq_fold_kernel(&f, max_head, &o, &M));
+    if (levels) *levels = M;
+    if (!o.sbd) {
+        // nothing folded in a BE kernel: the same kernel in the generic-head format
+        // (feed w = m' r^(n_head - 3) with n_head = 2: m' = w r)
+        o.sbd = 1;
+        for (int j = 0; j < o.np1; ++j) o.m1[j] *= o.r1[j];
+    }
+    return sbd_from_flat(o);
+}
+}  // namespace
+FastKernelSBD fold_kernel(const FastKernelBE& k, int max_head, int* levels) {
+    return fold_flat(to_flat(k), max_head, levels);
+}
+FastKernelSBD fold_kernel(const FastKernelSBD& k, int max_head, int* levels) {
+    return fold_flat(to_flat(k), max_head, levels);
+}
 
 KernelErrorReport kernel_error_report(const FastKernelBE& k, long n_max) {
     return report(to_flat(k), n_max);

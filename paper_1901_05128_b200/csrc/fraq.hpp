@@ -101,6 +101,10 @@ FastKernelBE build_be_kernel(double alpha, double tau, int n_points);
 FastKernelSBD build_sbd_kernel(double alpha, double tau, int n_points_1, int n_points_2,
                                int n_head);
 int default_sbd_head(double alpha);
+/// B200 addition (fraq_fold_kernel): the fast-decaying nodes folded into a longer exact head; the
+/// result is an SBD-format kernel equal to `k` below fp64 rounding (`levels`: head levels added).
+FastKernelSBD fold_kernel(const FastKernelBE& k, int max_head = 96, int* levels = nullptr);
+FastKernelSBD fold_kernel(const FastKernelSBD& k, int max_head = 96, int* levels = nullptr);
 KernelErrorReport kernel_error_report(const FastKernelBE& k, long n_max);
 KernelErrorReport kernel_error_report(const FastKernelSBD& k, long n_max);
 

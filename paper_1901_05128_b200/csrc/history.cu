@@ -151,6 +151,22 @@ __global__ void __launch_bounds__(LANES* S, 6) step_kernel(StepArgs A) {
             }
         }
     }
+    if (A.mode == MODE_FFPE && live) {
+        // FastStepper: s = history + sum_{i=first}^{top} d_i G^{n-i}, n = appended (G^n not yet
+        // in; the solve kernel appends it).  No append in this launch, so the taps are split
+        // over the node slices ahead of the barrier (folded kernels carry 60-80 of them).
+        const double* hd = A.head + G.hd_off;
+        const double* ring = A.ring + G.ring_off + m;
+        const long n = appended;
+        long top;
+        if (!G.sbd)
+            top = n >= 2 ? 1 : 0;
+        else
+            top = min((long)G.L - 1, n - 1);
+#pragma unroll 4
+        for (long i = (A.first_tap > 1 ? A.first_tap : 1) + sl; i <= top; i += S)
+            fma4(acc, hd[i], ld4(ring + ((n - i) % G.L) * ld));
+    }
     if (S > 1) {
         s_part[sl][lane] = acc;
         __syncthreads();
@@ -189,16 +205,6 @@ __global__ void __launch_bounds__(LANES* S, 6) step_kernel(StepArgs A) {
             top = min((long)G.L - 1, bound);
         }
         for (long i = 0; i <= top; ++i) fma4(acc, hd[i], ld4(ring + ((n - i) % G.L) * ld));
-    } else if (A.mode == MODE_FFPE) {
-        // FastStepper: s = history + sum_{i=1}^{top} d_i G^{n-i}, n = appended (G^n not yet in)
-        const long n = appended;
-        long top;
-        if (!G.sbd)
-            top = n >= 2 ? 1 : 0;
-        else
-            top = min((long)G.L - 1, n - 1);
-        for (long i = A.first_tap > 1 ? A.first_tap : 1; i <= top; ++i)
-            fma4(acc, hd[i], ld4(ring + ((n - i) % G.L) * ld));
     }
     double* o = A.out + G.dof0 + m;
     o[0] = acc.x;

@@ -112,6 +112,10 @@ struct FirPlan {
     bool short_stale = false;  // short-node states in `state` lag behind (rebuilt on demand)
 };
 
+// history_fir.cu: the fold as a kernel rewrite (longer exact head, only the slow nodes); returns
+// the number of head levels added (0: `out` untouched).
+int fold_kernel(const fraq_kernel_t& k, int lcap, fraq_kernel_t* out);
+
 // Device-resident tables + state of a set of groups.
 struct HistDevice {
     std::vector<GroupDev> groups_h;

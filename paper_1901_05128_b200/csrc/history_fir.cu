@@ -977,4 +977,78 @@ void launch_step_fir(fraq_ctx c, HistDevice& d, long appended, int push, int mod
 }
 
 
+// The fold as a kernel rewrite (tests/test_fold_identity.py): head c_0..c_(L+M-1) with c_i = d_i
+// for i < L and c_i = sum_{all j} f_j r_j^(i-L) beyond, and only the nodes with |r_j|^M > 2^-70,
+// fed at lag L + M with f_j r_j^M.  The result is a kernel in the generic-head (SBD) table
+// format, whose feed convention mult * ratio^(n_head - 3) (fast_kernel.cpp:337-340) absorbs r^M:
+// SBD families keep their multipliers, BE node weights become m' = w r.  M (a multiple of 8, head
+// at most `lcap` levels) minimises the bytes a per-level pass moves, 16 per kept node + 8 per
+// head tap.  Returns M (0: `out` untouched).
+int fold_kernel(const fraq_kernel_t& k, int lcap, fraq_kernel_t* out) {
+    const int L = k.sbd ? std::max(2, k.n_head) : 2;
+    const int J = k.np1 + k.np2;
+    if (J == 0) return 0;
+    std::vector<long double> r(J), f(J);
+    for (int j = 0; j < J; ++j) {
+        const double rj = j < k.np1 ? k.r1[j] : k.r2[j - k.np1];
+        const double mj = j < k.np1 ? k.m1[j] : k.m2[j - k.np1];
+        r[j] = rj;
+        long double v = mj;
+        if (k.sbd) v *= std::pow((long double)rj, (long double)(k.n_head - 3));
+        f[j] = v;
+    }
+    const long double thr = std::pow(2.0L, -70.0L);
+    auto n_long = [&](int M) {
+        int c = 0;
+        for (int j = 0; j < J; ++j) c += !(std::pow(std::fabs(r[j]), (long double)M) <= thr);
+        return c;
+    };
+    int M = 0;
+    long best = 16L * J + 8L * L;
+    for (int cand = 8; L + cand <= std::min(lcap, FRAQ_MAX_HEAD); cand += 8) {
+        const long cost = 16L * n_long(cand) + 8L * (L + cand);
+        if (cost < best) best = cost, M = cand;
+    }
+    if (M == 0) return 0;
+    long double tail = 0.0L;
+    for (int j = 0; j < J; ++j) {
+        const long double a = std::fabs(r[j]), pw = std::pow(a, (long double)M);
+        if (pw <= thr) tail += std::fabs(f[j]) * pw / (1.0L - a);
+    }
+    if (!(tail <= std::pow(2.0L, -60.0L) * std::fabs((long double)k.head[0]))) return 0;
+    fraq_kernel_t o;
+    std::memset(&o, 0, sizeof(o));
+    o.sbd = 1;
+    o.gamma = k.gamma;
+    o.tau = k.tau;
+    o.n_head = L + M;
+    for (int i = 0; i < L; ++i) o.head[i] = i < k.n_head ? k.head[i] : 0.0;
+    std::vector<long double> pw(f);
+    for (int m = 0; m < M; ++m) {
+        long double c = 0.0L;
+        for (int j = 0; j < J; ++j) {
+            c += pw[j];
+            pw[j] *= r[j];
+        }
+        o.head[L + m] = (double)c;
+    }
+    for (int j = 0; j < J; ++j) {
+        if (std::pow(std::fabs(r[j]), (long double)M) <= thr) continue;
+        const double rj = (double)r[j];
+        const double mj = j < k.np1 ? k.m1[j] : k.m2[j - k.np1];
+        const double mo = k.sbd ? mj : mj * rj;  // m' r^(L + M - 3) = f r^M
+        if (j < k.np1) {
+            o.m1[o.np1] = mo;
+            o.r1[o.np1++] = rj;
+        } else {
+            o.m2[o.np2] = mo;
+            o.r2[o.np2++] = rj;
+        }
+    }
+    if (o.np1 + o.np2 == 0) return 0;
+    *out = o;
+    return M;
+}
+
+
 }  // namespace fraqcu

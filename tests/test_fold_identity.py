@@ -76,3 +76,49 @@ def test_fold_sbd_is_a_kernel_rewrite(orc):
     f_fold = (m * r ** (k.n_head - 3))[keep] * r[keep] ** M
     f_rewritten = m[keep] * r[keep] ** (k.n_head + M - 3)
     assert np.max(np.abs(f_fold - f_rewritten) / np.abs(f_rewritten)) <= 1e-13
+
+
+# ---------------------------------------------------------------------------- fraq_fold_kernel
+# The product's own rewrite (history_fir.cu fold_kernel, C ABI fraq_fold_kernel; host only), on
+# the reference's kernels: the folded kernel is a reference-format SBD kernel that stands for the
+# same convolution weights.
+
+def _pkg_kernel(fraq, k):
+    if k.sbd:
+        return fraq.make_sbd_kernel(k.gamma, k.tau, list(k.head), list(k.m1), list(k.r1),
+                                    list(k.m2), list(k.r2))
+    return fraq.make_be_kernel(k.gamma, k.tau, list(k.head), list(k.m1), list(k.r1))
+
+
+@pytest.mark.parametrize("sbd,g,tau", [(True, 0.7, 1.0 / 65536), (True, 0.3, 1.0 / 65536),
+                                       (False, 0.6, 1.0 / 16384), (False, 0.2, 1.0 / 16384),
+                                       (True, 0.45, 1.0 / 16384), (False, 0.9, 1.0 / 16384)])
+def test_fold_kernel_abi_preserves_weights(orc, sbd, g, tau):
+    import paper_1901_05128_b200 as fraq
+    k = orc.build_kernel_auto(sbd, g, tau, int(round(1 / tau)), 1e-12)
+    folded, M = fraq.fold_kernel(_pkg_kernel(fraq, k), 96)
+    L = k.n_head if sbd else 2
+    assert M > 0 and M % 8 == 0 and folded.n_head == L + M <= 96
+    r = np.concatenate([k.r1, k.r2])
+    m = np.concatenate([k.m1, k.m2])
+    f = m * r ** (k.n_head - 3) if sbd else m
+    n = 4096
+    w = weights(np.asarray(k.head), r, f, L, n)
+    r2 = np.concatenate([folded.ratio1, folded.ratio2])
+    m2 = np.concatenate([folded.mult1, folded.mult2])
+    assert 0 < len(r2) < len(r)
+    assert set(r2.tolist()) <= set(r.tolist())  # kept nodes keep their ratios
+    if sbd:
+        assert set(m2.tolist()) <= set(m.tolist())  # ... and, for SBD families, their multipliers
+    f2 = m2 * r2 ** (folded.n_head - 3)  # the reference's feed convention, fast_kernel.cpp:337-340
+    w2 = weights(np.asarray(folded.head), r2, f2, folded.n_head, n)
+    scale = abs(float(k.head[0]))
+    assert float(np.max(np.abs(w2 - w))) <= 2e-15 * scale
+    # the bytes a per-level pass moves (16 per node state, 8 per head tap) went down
+    assert 16 * len(r2) + 8 * folded.n_head < 16 * len(r) + 8 * L
+    # a head cap below L + 8 leaves the kernel alone (returned in the generic-head format)
+    same, M0 = fraq.fold_kernel(_pkg_kernel(fraq, k), L + 7)
+    assert M0 == 0 and same.n_head == L and len(same.ratio1) + len(same.ratio2) == len(r)
+    f0 = np.concatenate([same.mult1, same.mult2]) * \
+        np.concatenate([same.ratio1, same.ratio2]) ** (same.n_head - 3)
+    assert np.max(np.abs(f0 - f) / np.abs(f)) <= 4e-16

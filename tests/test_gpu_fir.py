@@ -315,3 +315,30 @@ def test_k5f_ragged_groups_odd_starts(fraq, orc):
         D_ref = orc.hist_run(o, np.ascontiguousarray(U[:, c:c + dm]))
         check(D[:, c:c + dm], D_ref, tau ** -o.gamma, 1e-12)
         c += dm
+
+
+@pytest.mark.parametrize("sbd,max_head", [(False, 96), (True, 96), (True, 64), (False, 40)])
+def test_folded_kernel_history_equals_reference(fraq, orc, sbd, max_head, monkeypatch):
+    """fraq_fold_kernel's rewrite (longer exact head, only the slow nodes; the kernels the
+    physical FFPE stepper hands to its K5 pass) driven through the plain history kernels: an
+    SbdHistory over the folded kernel reproduces the reference history of the ORIGINAL kernel,
+    level by level (K5) and in one blocked run."""
+    monkeypatch.setenv("FRAQ_NO_K5F", "1")  # plain K5: every node of the folded kernel streamed
+    rng = np.random.default_rng(97 + sbd)
+    tau = 1.0 / 16384
+    o = orc.build_kernel_auto(sbd, 0.6, tau, 16384, 1e-12)
+    folded, M = fraq.fold_kernel(kernel_from_oracle(fraq, o), max_head)
+    assert M > 0
+    dim, n = 10, 320
+    U = rng.uniform(-1, 1, (n, dim))
+    ref = orc.hist_run(o, U)
+    h = fraq.SbdHistory(folded, fraq.HistoryVariant.standalone, dim)
+    out = np.full((n, dim), np.nan)
+    for i in range(n):
+        h.push(list(U[i]))
+        out[i] = h.derivative()
+    first = 0 if sbd else 1  # (the reference's BE derivative needs two pushed values)
+    check(out[first:], ref[first:], tau ** -0.6, 1e-12)
+    h2 = fraq.SbdHistory(folded, fraq.HistoryVariant.standalone, dim)
+    D = np.asarray(h2.run(U), dtype=float)
+    check(D[first:], ref[first:], tau ** -0.6, 1e-12)
