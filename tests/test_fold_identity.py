@@ -122,3 +122,27 @@ def test_fold_kernel_abi_preserves_weights(orc, sbd, g, tau):
     f0 = np.concatenate([same.mult1, same.mult2]) * \
         np.concatenate([same.ratio1, same.ratio2]) ** (same.n_head - 3)
     assert np.max(np.abs(f0 - f) / np.abs(f)) <= 4e-16
+
+
+@pytest.mark.parametrize("sbd,g", [(False, 0.6), (True, 0.7)])
+def test_reference_history_on_the_folded_kernel(orc, sbd, g):
+    """The rewrite is an algorithmic identity, not a property of the CUDA kernels: the
+    REFERENCE's own SbdHistory (fast_kernel.cpp:327-409), built from the folded kernel, reproduces
+    the reference history of the original kernel while carrying a fraction of the node states."""
+    import paper_1901_05128_b200 as fraq
+    from oracle.oracle import Kernel
+    tau = 1.0 / 16384
+    k = orc.build_kernel_auto(sbd, g, tau, 16384, 1e-12)
+    folded, M = fraq.fold_kernel(_pkg_kernel(fraq, k), 96)
+    assert M > 0
+    kf = Kernel(True, k.gamma, k.tau, np.array(folded.head), np.array(folded.mult1),
+                np.array(folded.ratio1), np.array(folded.mult2), np.array(folded.ratio2))
+    assert kf.np1 + kf.np2 <= 0.75 * (k.np1 + k.np2)
+    rng = np.random.default_rng(101 + sbd)
+    U = rng.uniform(-1, 1, (600, 6))
+    ref = orc.hist_run(k, U)
+    got = orc.hist_run(kf, U)
+    first = 0 if sbd else 1  # (BeHistory::derivative needs two pushed values)
+    scale = tau ** -g
+    err = np.max(np.abs(got[first:] - ref[first:]) / np.maximum(np.abs(ref[first:]), scale))
+    assert err <= 1e-13, err
