@@ -832,8 +832,11 @@ struct StepFirArgs {
 // CTA = LANES DOF quads x S slices; slice sl takes the long nodes p = sl, sl + S, ... and the
 // window taps i = i0 + sl, i0 + sl + S, ...; partial sums meet in shared memory and slice 0
 // finishes (lag ring, input ring, output), as in K5.
+#ifndef FRAQ_K5F_NB
+#define FRAQ_K5F_NB 6
+#endif
 template <int LANES, int S>
-__global__ void __launch_bounds__(LANES* S, 5) step_fir_kernel(StepFirArgs A) {
+__global__ void __launch_bounds__(LANES* S, 4) step_fir_kernel(StepFirArgs A) {
     const int2 tile = A.tiles[blockIdx.x];
     const GroupDev G = A.groups[tile.x];
     const FirGroup* F = A.fg + tile.x;
@@ -843,56 +846,54 @@ __global__ void __launch_bounds__(LANES* S, 5) step_fir_kernel(StepFirArgs A) {
     const bool live = m < G.dim;
     const int nv = live ? min(4, G.dim - m) : 0;
     __shared__ F4 s_part[S][LANES];
+    // the kept nodes' rows and coefficients, staged once per CTA: the state loads' addresses then
+    // hang on a shared-memory read instead of a dependent global load per batch
+    __shared__ int s_j[512];
+    __shared__ double s_r[512], s_f[512];
     const long n = A.push ? A.appended : A.appended - 1;  // level of the newest value
     const int L = G.L, M = F->M, JL = F->JL;
     const long ld = G.ld;
+    {
+        const int* pm = A.perm + F->perm_off;
+        for (int p = threadIdx.x; p < JL; p += LANES * S) {
+            const int j = pm[p];
+            s_j[p] = j;
+            s_r[p] = A.cr[G.co_off + j];
+            s_f[p] = A.cf[G.co_off + j];
+        }
+    }
+    __syncthreads();
     const double* xcol = A.xh + G.dof0 + m;
     F4 acc = {0.0, 0.0, 0.0, 0.0};
     F4 unew = {0.0, 0.0, 0.0, 0.0};
     if (live) {
         if (A.push) unew = ld_row4(A.u + G.dof0 + m, nv);
-        const int* pm = A.perm + F->perm_off;
-        const double* __restrict__ cr = A.cr + G.co_off;
-        const double* __restrict__ cf = A.cf + G.co_off;
         double* base = A.state + G.st_off + m;
         if (A.push) {
             // feed of level n: X(n - L)  (steady state: n - L >= lo and still on record)
             const F4 v = ld_row4(xcol + (size_t)((n - L) & A.xh_mask) * A.ldx, nv);
-            constexpr int NB = 4;  // independent 256-bit loads in flight before the first store
-            int p = sl;
-            for (; p + (NB - 1) * S < JL; p += NB * S) {
+            constexpr int NB = FRAQ_K5F_NB;  // independent 256-bit loads in flight per thread
+            // (the last batch is partial: predicated loads, no serial tail)
+            for (int p = sl; p < JL; p += NB * S) {
                 F4 y[NB];
-                int j[NB];
 #pragma unroll
-                for (int b = 0; b < NB; ++b) {
-                    j[b] = pm[p + b * S];
-                    y[b] = ldg_stream4(base + j[b] * ld);
-                }
+                for (int b = 0; b < NB; ++b)
+                    if (p + b * S < JL) y[b] = ldg_stream4(base + s_j[p + b * S] * ld);
 #pragma unroll
-                for (int b = 0; b < NB; ++b) {
-                    const double r = __ldg(cr + j[b]), f = __ldg(cf + j[b]);
-                    y[b].x = fma(r, y[b].x, f * v.x);
-                    y[b].y = fma(r, y[b].y, f * v.y);
-                    y[b].z = fma(r, y[b].z, f * v.z);
-                    y[b].w = fma(r, y[b].w, f * v.w);
-                    stg_stream4(base + j[b] * ld, y[b]);
-                    add_f4(acc, y[b]);
-                }
-            }
-            for (; p < JL; p += S) {
-                const int j = pm[p];
-                F4 y = ldg_stream4(base + j * ld);
-                const double r = __ldg(cr + j), f = __ldg(cf + j);
-                y.x = fma(r, y.x, f * v.x);
-                y.y = fma(r, y.y, f * v.y);
-                y.z = fma(r, y.z, f * v.z);
-                y.w = fma(r, y.w, f * v.w);
-                stg_stream4(base + j * ld, y);
-                add_f4(acc, y);
+                for (int b = 0; b < NB; ++b)
+                    if (p + b * S < JL) {
+                        const double r = s_r[p + b * S], f = s_f[p + b * S];
+                        y[b].x = fma(r, y[b].x, f * v.x);
+                        y[b].y = fma(r, y[b].y, f * v.y);
+                        y[b].z = fma(r, y[b].z, f * v.z);
+                        y[b].w = fma(r, y[b].w, f * v.w);
+                        stg_stream4(base + s_j[p + b * S] * ld, y[b]);
+                        add_f4(acc, y[b]);
+                    }
             }
         } else if (A.mode != MODE_NONE) {
 #pragma unroll 4
-            for (int p = sl; p < JL; p += S) add_f4(acc, ldg_stream4(base + pm[p] * ld));
+            for (int p = sl; p < JL; p += S) add_f4(acc, ldg_stream4(base + s_j[p] * ld));
         }
         if (A.mode != MODE_NONE) {
             // window: exact head taps d_i (derivative only), then the short nodes' FIR
