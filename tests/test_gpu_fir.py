@@ -342,3 +342,31 @@ def test_folded_kernel_history_equals_reference(fraq, orc, sbd, max_head, monkey
     h2 = fraq.SbdHistory(folded, fraq.HistoryVariant.standalone, dim)
     D = np.asarray(h2.run(U), dtype=float)
     check(D[first:], ref[first:], tau ** -0.6, 1e-12)
+
+
+def test_k5f_padded_rows_and_guard_bands(fraq, orc, c2_kernels):
+    """One-level run_device calls (K5f) on rows of wider device arrays, odd DOF count: the
+    padding columns and the rows around the call stay untouched, the written levels equal the
+    reference history."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(103)
+    o = c2_kernels[1]
+    dim, ld, n = 37, 64, 200
+    U = rng.uniform(-1, 1, (n, dim))
+    ref = orc.hist_run(o, U)
+    k = kernel_from_oracle(fraq, o)
+    h = fraq.MultiHistory([k], [dim])
+    Ud = torch.full((n, ld), 3.0, dtype=torch.float64, device="cuda")
+    Ud[:, :dim] = torch.from_numpy(U).cuda()
+    Dd = torch.full((n + 2, ld), -7.0, dtype=torch.float64, device="cuda")  # guard rows 0, n + 1
+    torch.cuda.synchronize()
+    row = ld * 8
+    h.run_device(Ud.data_ptr(), ld, 128, Dd.data_ptr() + row, ld)
+    for i in range(128, n):
+        h.run_device(Ud.data_ptr() + i * row, ld, 1, Dd.data_ptr() + (i + 1) * row, ld)
+    fraq.synchronize()
+    assert h.launches[5] == n - 128
+    D = Dd.cpu().numpy()
+    assert np.all(D[0] == -7.0) and np.all(D[n + 1] == -7.0) and np.all(D[:, dim:] == -7.0)
+    assert np.all(Ud.cpu().numpy()[:, dim:] == 3.0)
+    check(D[1:n + 1, :dim], ref, C2_TAU ** -o.gamma, 1e-12)
