@@ -970,11 +970,12 @@ void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, l
     // i (the kernels themselves are sequential: each chunk continues the history state).
     // Pinned host memory gives full overlap; pageable memory still works (staged copies).
     const long dim = std::max<long>(1, h->d.total_dim);
-    // chunk height: ~1/16 of the call in multiples of the kernel's 32-level staging chunk, so the
-    // pipeline fill (first H2D) and drain (last D2H) stay short, and at most ~16 MB per chunk
-    // (but 32 levels at least).  (C2, 65536 DOFs: 32-level chunks reach 87% of the measured
-    // concurrent PCIe bound; 64-level chunks 79%, 128-level chunks 72%.)
-    const long cap = std::max<long>(32, ((16L << 20) / (8 * dim)) / 32 * 32);
+    // chunk height: ~1/16 of the call in multiples of the kernel's 32-level staging chunk, at most
+    // ~32 MB per chunk (but 32 levels at least), with shorter chunks at both ends (below) so the
+    // pipeline fill (first H2D) and drain (last D2H) stay short.  (C2, 65536 DOFs, K5e, e2e in 1e9
+    // DOF-steps/s: uniform 32 / 64-level chunks 4.74 / 4.77; ramped 32 / 64 / 128: 4.68 / 5.02 /
+    // 4.91 -- profiles/r02/e2e_ramp.sh.)
+    const long cap = std::max<long>(32, ((32L << 20) / (8 * dim)) / 32 * 32);
     long rows = std::min<long>(cap, std::max<long>(32, ((n_steps / 16 + 31) / 32) * 32));
     const char* ce = std::getenv("FRAQ_HOST_CHUNK");  // experiment override (levels per chunk)
     if (ce && *ce) rows = std::max<long>(1, std::atol(ce));
@@ -1004,10 +1005,34 @@ void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, l
         FRAQ_CUDA(cudaEventRecord(h->ev_c[j], sc));
         FRAQ_CUDA(cudaEventRecord(h->ev_d[j], sc));
     }
+    // chunk schedule: `rows` per chunk, with shorter chunks at both ends of a long call (rows/4,
+    // rows/2, ..., rows/2, rows/4; multiples of 8, so they stay on K5e) -- the first H2D and the
+    // last D2H are the only copies nothing overlaps
+    std::vector<long> sched;
+    {
+        static const bool ramp_on = !std::getenv("FRAQ_HOST_NORAMP");
+        const long r4 = rows / 4 / 8 * 8, r2 = rows / 2 / 8 * 8;
+        long left = n_steps;
+        const bool ramp = ramp_on && r4 >= 8 && n_steps >= 6 * rows;
+        if (ramp) {
+            sched.push_back(r4);
+            sched.push_back(r2);
+            left -= r4 + r2 + r2 + r4;
+        }
+        while (left > 0) {
+            const long nr = (left - rows < 32) ? left : rows;
+            sched.push_back(nr);
+            left -= nr;
+        }
+        if (ramp) {
+            sched.push_back(r2);
+            sched.push_back(r4);
+        }
+    }
     long i = 0;
     for (long n0 = 0, nr = 0; n0 < n_steps; n0 += nr, ++i) {
         const int b = (int)(i % ns);
-        nr = (n_steps - n0 - rows < 32) ? n_steps - n0 : rows;
+        nr = sched[i];
         // H2D into ubuf[b] once the kernel that last read it (chunk i - ns) finished
         FRAQ_CUDA(cudaStreamWaitEvent(h->s_h2d, h->ev_c[b], 0));
         FRAQ_CUDA(cudaMemcpy2DAsync(h->ubuf[b].p, dim * 8, U + n0 * ldu, ldu * 8,
