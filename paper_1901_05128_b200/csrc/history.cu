@@ -1035,8 +1035,12 @@ void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, l
         nr = sched[i];
         // H2D into ubuf[b] once the kernel that last read it (chunk i - ns) finished
         FRAQ_CUDA(cudaStreamWaitEvent(h->s_h2d, h->ev_c[b], 0));
-        FRAQ_CUDA(cudaMemcpy2DAsync(h->ubuf[b].p, dim * 8, U + n0 * ldu, ldu * 8,
-                                    h->d.total_dim * 8, nr, cudaMemcpyHostToDevice, h->s_h2d));
+        if (ldu == dim)  // contiguous rows: one linear copy
+            FRAQ_CUDA(cudaMemcpyAsync(h->ubuf[b].p, U + n0 * ldu, (size_t)nr * dim * 8,
+                                      cudaMemcpyHostToDevice, h->s_h2d));
+        else
+            FRAQ_CUDA(cudaMemcpy2DAsync(h->ubuf[b].p, dim * 8, U + n0 * ldu, ldu * 8,
+                                        h->d.total_dim * 8, nr, cudaMemcpyHostToDevice, h->s_h2d));
         FRAQ_CUDA(cudaEventRecord(h->ev_u[b], h->s_h2d));
         // kernel on chunk i: needs its inputs and dbuf[b] drained by the D2H of chunk i - ns
         FRAQ_CUDA(cudaStreamWaitEvent(sc, h->ev_u[b], 0));
@@ -1045,8 +1049,13 @@ void hist_run(fraq_hist h, const double* U, long ldu, long n_steps, double* D, l
         FRAQ_CUDA(cudaEventRecord(h->ev_c[b], sc));
         if (D) {
             FRAQ_CUDA(cudaStreamWaitEvent(h->s_d2h, h->ev_c[b], 0));
-            FRAQ_CUDA(cudaMemcpy2DAsync(D + n0 * ldd, ldd * 8, h->dbuf[b].p, dim * 8,
-                                        h->d.total_dim * 8, nr, cudaMemcpyDeviceToHost, h->s_d2h));
+            if (ldd == dim)
+                FRAQ_CUDA(cudaMemcpyAsync(D + n0 * ldd, h->dbuf[b].p, (size_t)nr * dim * 8,
+                                          cudaMemcpyDeviceToHost, h->s_d2h));
+            else
+                FRAQ_CUDA(cudaMemcpy2DAsync(D + n0 * ldd, ldd * 8, h->dbuf[b].p, dim * 8,
+                                            h->d.total_dim * 8, nr, cudaMemcpyDeviceToHost,
+                                            h->s_d2h));
             FRAQ_CUDA(cudaEventRecord(h->ev_d[b], h->s_d2h));
         }
     }
