@@ -966,39 +966,13 @@ void launch_step_fir(fraq_ctx c, HistDevice& d, long appended, int push, int mod
     a.mode = mode;
     a.u = u;
     a.out = out;
-    // experiment (FRAQ_K5F_L2PERSIST=1): the input ring as a persisting L2 window of the launch
-    static const bool persist = std::getenv("FRAQ_K5F_L2PERSIST") != nullptr;
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)d.n_tiles);
-    cfg.blockDim = dim3(128);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = c->stream;
-    cudaLaunchAttribute attr[1];
-    if (persist) {
-        static bool limit_set = false;
-        if (!limit_set) {
-            cudaDeviceProp prop;
-            int dev = 0;
-            FRAQ_CUDA(cudaGetDevice(&dev));
-            FRAQ_CUDA(cudaGetDeviceProperties(&prop, dev));
-            FRAQ_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize,
-                                         (size_t)prop.persistingL2CacheMaxSize));
-            limit_set = true;
-        }
-        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr[0].val.accessPolicyWindow.base_ptr = P.xh.p;
-        attr[0].val.accessPolicyWindow.num_bytes =
-            std::min<size_t>(P.xh.n * sizeof(double), (size_t)128 << 20);
-        attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
-        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-    }
+    // (declaring the input ring a persisting L2 window of the launch made the step slower, 66 us
+    // against 36: the window's write-backs doubled the DRAM writes; profiles/r02/k5f_l2.sh ran
+    // the experiment on the tree of commit 6e10ee6)
     if (d.lanes == 32)
-        FRAQ_CUDA(cudaLaunchKernelEx(&cfg, step_fir_kernel<32, 4>, a));
+        step_fir_kernel<32, 4><<<d.n_tiles, 128, 0, c->stream>>>(a);
     else
-        FRAQ_CUDA(cudaLaunchKernelEx(&cfg, step_fir_kernel<8, 16>, a));
+        step_fir_kernel<8, 16><<<d.n_tiles, 128, 0, c->stream>>>(a);
     FRAQ_LAUNCH_CHECK();
     if (push) {
         P.xh_valid = std::min<long>(P.xh_rows, P.xh_valid + 1);
