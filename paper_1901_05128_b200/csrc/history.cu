@@ -191,6 +191,13 @@ __global__ void __launch_bounds__(LANES* S, 6) step_kernel(StepArgs A) {
         x.z = nv > 2 ? u[2] : 0.0;
         x.w = nv > 3 ? u[3] : 0.0;
         st4(ring + (appended % G.L) * ld, x);
+        if (A.xh) {
+            double* xr = A.xh + (size_t)(appended & A.xh_mask) * A.ldx + G.dof0 + m;
+            xr[0] = x.x;
+            if (nv > 1) xr[1] = x.y;
+            if (nv > 2) xr[2] = x.z;
+            if (nv > 3) xr[3] = x.w;
+        }
         ++appended;
     }
     if (A.mode == MODE_NONE) return;
@@ -662,14 +669,22 @@ void copy_out(fraq_hist h, double* dst, const double* src, int mem) {
     if (mem != FRAQ_DEVICE) FRAQ_CUDA(cudaStreamSynchronize(h->ctx->stream));
 }
 
-// A K5 push of `u` (device, user layout) at level h->appended, before the counters move: pure
-// push sequences keep K5e's / K5f's input ring current, anything else invalidates it.
-void note_push(fraq_hist h, const double* u) {
-    const bool pure = h->appended == 0 ? h->level == 0 : h->level == h->appended - 1;
-    if (pure && h->d.fir.ok)
-        fir_note_inputs(h->ctx, h->d, h->appended, u, std::max<long>(1, h->d.total_dim), 1);
-    else
-        h->d.fir.xh_valid = 0;
+// A K5 launch that appends a value at level h->appended (before the counters move): in a pure
+// push sequence (`pure`) the kernel also records the value in K5e's / K5f's input ring; anything
+// else invalidates the ring.
+void record_append(fraq_hist h, StepArgs& a, bool pure) {
+    FirPlan& P = h->d.fir;
+    if (pure && P.ok) {
+        a.xh = P.xh.p;
+        a.ldx = h->d.total_dim;
+        a.xh_mask = P.xh_rows - 1;
+        P.xh_valid = std::min<long>(P.xh_rows, P.xh_valid + 1);
+    } else {
+        P.xh_valid = 0;
+    }
+}
+bool pure_push(fraq_hist h) {
+    return h->appended == 0 ? h->level == 0 : h->level == h->appended - 1;
 }
 
 // Run a pending push (advance + append from the stage) fused with `mode` output into out_d.
@@ -689,9 +704,9 @@ void flush(fraq_hist h, int mode, double* out_d) {
         ++h->launches[5];
     } else {
         fir_materialize(h->ctx, h->d, h->appended);  // K5 reads every node's state
+        if (h->pending) record_append(h, a, pure_push(h));
         h->d.launch_step(h->ctx, a);
         ++h->launches[0];
-        if (h->pending) note_push(h, h->stage.p);
     }
     if (h->pending) {
         if (h->appended > 0) h->level += 1;
@@ -787,14 +802,10 @@ void hist_append(fraq_hist h, const double* v, int mem) {
     StepArgs a = base_args(h);
     a.app = 1;
     a.u = h->stage.p;
+    // advance() then append() is a push: the input ring stays current (K5e / K5f can follow)
+    record_append(h, a, h->appended == 0 ? h->level == 0 : h->level == h->appended);
     h->d.launch_step(h->ctx, a);
     ++h->launches[0];
-    // advance() then append() is a push: the input ring stays current (K5e / K5f can follow)
-    const bool pure = h->appended == 0 ? h->level == 0 : h->level == h->appended;
-    if (pure && h->d.fir.ok)
-        fir_note_inputs(h->ctx, h->d, h->appended, h->stage.p, std::max<long>(1, h->d.total_dim), 1);
-    else
-        h->d.fir.xh_valid = 0;
     h->appended += 1;
 }
 
@@ -937,9 +948,9 @@ void run_device(fraq_hist h, const double* U, long ldu, long n_steps, double* D,
             ++h->launches[5];
         } else {
             fir_materialize(h->ctx, h->d, h->appended);
+            record_append(h, a, pure_push(h));
             h->d.launch_step(h->ctx, a);
             ++h->launches[0];
-            note_push(h, a.u);
         }
         if (D && !ok) {
             // derivative undefined on the first BE push: NaN row (the reference throws)

@@ -47,6 +47,11 @@ struct StepArgs {
     const long* n_dev;
     int n_off;
     int first_tap;
+    // K5e / K5f input ring (null = off): the appended value is also recorded in row
+    // appended & xh_mask (leading dimension ldx, user layout)
+    double* xh;
+    long ldx;
+    int xh_mask;
 };
 
 enum { MODE_NONE = 0, MODE_SUM = 1, MODE_DERIV = 2, MODE_FFPE = 3 };
