@@ -5,8 +5,10 @@
 //                      One HBM pass over the state per level.  BeHistory/SbdHistory
 //                      advance/append/history_sum/derivative, fast_kernel.cpp:268-409.
 // K5c (run2_kernel)    temporally blocked evaluation, lane per DOF, DFMA (head windows over 32
-//                      levels); the default blocked path K5d (DMMA block GEMMs) is in
-//                      history_dmma.cu.
+//                      levels); the default blocked paths K5d / K5e (DMMA block GEMMs) are in
+//                      history_dmma.cu / history_fir.cu, and so is K5f, the per-level step on
+//                      K5e's node split that takes over from K5 in the steady state of a push
+//                      sequence (flush() / run_device() below pick per call).
 #include <cuda_runtime.h>
 
 #include <algorithm>

@@ -24,6 +24,11 @@
 // are not touched by K5e; short_state_kernel rebuilds them from the last M inputs
 // (y_j = sum_{m<M} f_j r_j^m v(n-m), the reference's recurrence started M levels back) before
 // any other path reads them.
+//
+// The same split serves the per-level calls (K5f, step_fir_kernel below: push / derivative /
+// history_sum in the steady state; K5 records its appended values in `xh`, so a history pushed
+// level by level gets there by itself) and, as a kernel-to-kernel rewrite (fold_kernel), the
+// physical FFPE stepper's history pass.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
