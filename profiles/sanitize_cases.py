@@ -12,7 +12,9 @@ TMA-staged), k5c (head window > 32 levels), k10 (direct CQ), host (chunked host-
 k13 (modal BE/SBD, two-CTA shape), k13w (wide CTA, J > 256), k11 (modal fallback), k6 (physical
 stepper), dst2d (2D DST + K13); round 2: graph (the physical stepper's 64-level CUDA graph, K5 and
 K6 on two streams), blocks (BlockSystem CR + Thomas + refinement, BandedLU, Laplacian), dsts
-(the skinny DST K12s against the tile DST K12).
+(the skinny DST K12s against the tile DST K12); session 5: k5e (FIR-folded blocked run against
+K5d), k5f (the per-level fold against plain K5, odd sizes), fold (fold_kernel's rewritten kernel
+through K5, and the physical stepper with and without folded kernels).
 """
 import os
 import sys
@@ -68,7 +70,13 @@ def _blocked(points, dim, levels):
 
 
 def case_k5d():
-    assert _blocked(64, 16, 96) == 3
+    # (K5d on the first chunks; since K5e exists the last 32-level chunk of this call is K5e's)
+    assert _blocked(64, 16, 96) in (3, 4)
+    os.environ["FRAQ_NO_K5E"] = "1"
+    try:
+        assert _blocked(64, 16, 96) == 3
+    finally:
+        del os.environ["FRAQ_NO_K5E"]
 
 
 def case_k5c():
@@ -208,6 +216,69 @@ def case_dsts():
         S = torch.sin(torch.outer(k, k) * torch.pi / (M + 1))
         ref = (2.0 / (M + 1)) * S @ x
         assert float((y - ref).abs().max() / ref.abs().max()) < 1e-13
+
+
+def case_k5e():
+    k = fraq.build_be_kernel(0.5, 1.0 / 4096, 144)
+    rng = np.random.default_rng(11)
+    U = rng.uniform(-1, 1, (264, 18))
+    h = fraq.BeHistory(k, fraq.HistoryVariant.standalone, 18)
+    D = h.run(U)
+    assert h.launches[4] >= 1, list(h.launches)
+    os.environ["FRAQ_NO_K5E"] = "1"
+    try:
+        h2 = fraq.BeHistory(k, fraq.HistoryVariant.standalone, 18)
+        D2 = h2.run(U)
+        assert h2.launches[4] == 0
+    finally:
+        del os.environ["FRAQ_NO_K5E"]
+    assert rel(D[1:], D2[1:]) <= 1e-12
+
+
+def case_k5f():
+    k = fraq.build_sbd_kernel(0.4, 1.0 / 4096, 60, 60, 15)
+    rng = np.random.default_rng(12)
+    dims = [1, 3, 14, 7]
+    U = rng.uniform(-1, 1, (220, sum(dims)))
+    outs = []
+    for no in (False, True):
+        if no:
+            os.environ["FRAQ_NO_K5F"] = "1"
+        try:
+            h = fraq.MultiHistory([k] * len(dims), dims)
+            D = [np.asarray(h.run(U[i:i + 1]), dtype=float)[0] for i in range(len(U))]
+            assert (h.launches[5] == 0) == no, list(h.launches)
+            outs.append(np.array(D))
+        finally:
+            os.environ.pop("FRAQ_NO_K5F", None)
+    assert rel(outs[0], outs[1]) <= 1e-12
+
+
+def case_fold():
+    k = fraq.build_be_kernel(0.6, 1.0 / 4096, 96)
+    kf, M = fraq.fold_kernel(k, 64)
+    assert M > 0
+    rng = np.random.default_rng(13)
+    U = rng.uniform(-1, 1, (150, 9))
+    h = fraq.BeHistory(k, fraq.HistoryVariant.standalone, 9)
+    hf = fraq.SbdHistory(kf, fraq.HistoryVariant.standalone, 9)
+    D, Df = h.run(U), hf.run(U)
+    assert rel(Df[1:], D[1:]) <= 1e-12
+    spec = fraq.ProblemSpec(alpha1=0.3, alpha2=0.6, coupling_a=2.0, grid_m=31, t_final=0.125,
+                            n_steps=128)
+    kc = fraq.KernelConfig()
+    kc.solver = fraq.SOLVER_PHYSICAL
+    res = []
+    for no in (False, True):
+        if no:
+            os.environ["FRAQ_NO_PHYS_FOLD"] = "1"
+        try:
+            for sch in (fraq.Scheme.FastBE, fraq.Scheme.FastSBD):
+                rr = fraq.run(spec, sch, kc)
+                res.append(np.concatenate([rr.final_state.g1, rr.final_state.g2]))
+        finally:
+            os.environ.pop("FRAQ_NO_PHYS_FOLD", None)
+    assert rel(res[0], res[2]) <= 1e-11 and rel(res[1], res[3]) <= 1e-11
 
 
 CASES = {n[5:]: f for n, f in globals().items() if n.startswith("case_")}
