@@ -66,3 +66,10 @@ def test_gpu_arm_contract():
     assert d["gpu_launches"] >= d["steps"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["value"] > 0
+    # the per-level lines: K5 against the HBM roofline, K5f (the same calls in the steady state)
+    rs = d["roofline_step_kernel"]
+    assert rs["bound"] == "hbm" and 0 < rs["frac"] <= 1.0
+    fo = rs["folded"]
+    assert fo is not None and 0 < fo["ms_per_level"] < rs["ms_per_level"]
+    assert fo["bytes_per_dof_step_moved"] < rs["bytes_per_dof_step"]
+    assert d["setup"]["launches_by_path"]["K5e"] >= d["steps"] - 1
